@@ -1,0 +1,196 @@
+/*
+ * splatfield_b200.h -- C ABI of the B200 (sm_100a) sparse-coefficient
+ * splatting + open-vocabulary query path.
+ *
+ * The reference package (splatfield, /root/reference/pkg/src/splatfield) is
+ * pure Python/numpy and has no FFI of its own; its drop-in boundary is the
+ * Python module API re-exported in splatfield/__init__.py:10-66.  Each entry
+ * point below replaces one of those functions (cited per function).  A
+ * maintainer binds them from splatfield with ctypes exactly as
+ * paper_2507_07136_b200/_native.py does.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers unless the name says host_.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*)
+ *    and re-entrant: all scratch comes from the caller's workspace, so
+ *    concurrent calls on different streams with different workspaces are
+ *    safe (the reference server calls the path from many threads,
+ *    server.py:11-13).
+ *  - Return value: SF_OK or an SF_ERR_* code; sf_last_error() gives text.
+ *    Input checks happen before any launch (the reference raises before any
+ *    work, sparse_splat.py:114-122).
+ */
+#ifndef SPLATFIELD_B200_H
+#define SPLATFIELD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SF_OK 0
+#define SF_ERR_VALIDATION 1   /* -> splatfield.errors.ValidationError */
+#define SF_ERR_RESOURCE 2     /* -> splatfield.errors.ResourceLimitError */
+#define SF_ERR_CUDA 3         /* -> splatfield.errors.SplatfieldError */
+#define SF_ERR_WORKSPACE 4    /* workspace smaller than sf_*_workspace_bytes */
+
+#define SF_TILE 16            /* projection.py:31 DEFAULT_TILE_SIZE; kernels are specialised */
+
+/* Pinhole camera, projection.py:37-65 (Camera).  R row-major world->camera. */
+typedef struct SfCamera {
+    double R[9];
+    double t[3];
+    double fx, fy, cx, cy;
+    double near_plane;
+    int32_t width, height;
+} SfCamera;
+
+/* Device-resident scene, core.py:256-279 (Scene, struct of arrays).
+ * Rows MUST be ordered by ascending id: the canonical (depth, id) order of
+ * projection.py:396 then needs only a stable sort on depth. */
+typedef struct SfScene {
+    int64_t num_gaussians;
+    int32_t num_levels, L, K, D;
+    const float* positions;        /* (G,3) */
+    const float* rotations;        /* (G,4) w,x,y,z */
+    const float* scales;           /* (G,3) */
+    const float* opacities;        /* (G,) */
+    const uint16_t* coeff_indices; /* (num_levels,G,K) */
+    const float* coeff_values;     /* (num_levels,G,K) */
+    const int64_t* ids;            /* (G,) ascending */
+    const float* codebooks;        /* (num_levels,L,D) row-major */
+} SfScene;
+
+/* One text query, query.py:22-37 + the canonical set, query.py:65-84. */
+typedef struct SfQuery {
+    const double* vector;      /* (D,) */
+    const double* canonicals;  /* (n_canonicals,D) */
+    int32_t n_canonicals;
+    int32_t window;            /* mean_filter window, odd >= 1 (query.py:89-90) */
+    int32_t fixed_level;       /* -1 = select_level (query.py:111-118) else block index */
+    double threshold;          /* segment threshold (query.py:136) */
+} SfQuery;
+
+/* What one frame computes and where it goes.  NULL outputs are skipped. */
+typedef struct SfFrame {
+    const int32_t* host_levels; /* HOST (n_levels,) semantic levels to splat, sparse_splat.py:103-120 */
+    int32_t n_levels;
+    int32_t early_exit;         /* rasterizer.py:174-177 */
+    int64_t pair_capacity;      /* size of the (tile, rank) pair buffer in the workspace */
+    /* outputs */
+    float* coeff_map;           /* (H,W,n_levels*L) fp32      CoefficientMap.data */
+    float* final_t;             /* (H,W) fp32                 RenderStats.final_transmittance */
+    float* features;            /* (n_levels,H,W,D) fp32      FeatureMapSet.maps */
+    double* relevancy_raw;      /* (n_levels,H,W) fp64        relevancy_map() per level */
+    double* relevancy_filtered; /* (n_levels,H,W) fp64        mean_filter() per level */
+    uint8_t* mask;              /* (H,W) u8                   segment(chosen).mask */
+    int64_t* stats_i64;         /* (16,) see SF_STAT_* */
+    double* stats_f64;          /* (8 + 2*n_levels,) see SF_STATF_* */
+    /* optional cudaEvent_t recorded at: frame start, after blend (render),
+     * after decode, after post -- the StageTimings of sparse_splat.py:202-215 */
+    void* events[4];
+} SfFrame;
+
+/* stats_i64 slots */
+#define SF_STAT_VISIBLE 0     /* ProjectedScene.count */
+#define SF_STAT_PAIRS 1       /* RenderStats.pairs_blended (sum of tile list lengths) */
+#define SF_STAT_OVERFLOW 2    /* 1 if pairs > pair_capacity: grow and re-run */
+#define SF_STAT_LEVEL 3       /* chosen level block index */
+#define SF_STAT_ROW 4         /* localize() row */
+#define SF_STAT_COL 5         /* localize() col */
+#define SF_STAT_DEGENERATE 6  /* segment().degenerate */
+#define SF_STAT_FIXUPS 7      /* q~9 fp64 re-evaluations (diagnostic) */
+/* stats_f64 slots */
+#define SF_STATF_MIN 0        /* chosen map min */
+#define SF_STATF_MAX 1        /* chosen map max */
+#define SF_STATF_LEVEL_MAX 8  /* + b: max of filtered map of block b */
+
+/* Scratch needed by sf_render_frame for this scene/frame shape. */
+int sf_frame_workspace_bytes(int64_t num_gaussians, int32_t width, int32_t height,
+                             int32_t n_levels, int32_t L, int32_t K, int64_t pair_capacity,
+                             size_t* bytes);
+
+/*
+ * One full frame: preprocess -> depth-rank sort -> tile binning -> blend
+ * (+ fused projected-codebook relevancy) -> codebook GEMM -> mean filter ->
+ * select_level / localize / segment.
+ * Replaces, end to end, splat_multilevel (sparse_splat.py:178-180) +
+ * decode (:183-199) + query_pipeline (:243-297) + segment (query.py:136-145).
+ * query may be NULL (pure feature splatting).
+ */
+int sf_render_frame(const SfScene* scene, const SfCamera* cam, const SfQuery* query,
+                    const SfFrame* frame, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * project_scene, projection.py:240-315: the same surviving set, in scene-row
+ * order, with bitwise-identical fp64 values.  Outputs sized for G rows;
+ * *count_out (device int64) receives N.  inv_covs is (N,2,2).
+ */
+int sf_project_workspace_bytes(int64_t num_gaussians, size_t* bytes);
+int sf_project(const SfScene* scene, const SfCamera* cam, double* means2d, double* inv_covs,
+               double* depths, double* opacities, int64_t* source_ids, int64_t* rows,
+               int64_t* count_out, void* workspace, size_t workspace_bytes, void* stream);
+/* Same, for a device scene whose rows were permuted into id order at upload:
+ * orig_rows[g] is the caller's row of device row g (output keeps caller order). */
+int sf_project_rows(const SfScene* scene, const SfCamera* cam, const int64_t* orig_rows,
+                    double* means2d, double* inv_covs, double* depths, double* opacities,
+                    int64_t* source_ids, int64_t* rows, int64_t* count_out, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/*
+ * bin_projected, projection.py:379-450, on arbitrary projected arrays
+ * (N rows; inv_covs (N,2,2)).  Produces the canonical (depth, id) order
+ * (order[k] = input row of canonical rank k) and CSR per-tile lists of
+ * canonical ranks, byte-identical to the reference's tile_lists.
+ * tile_offsets has n_tiles+1 entries; *stats_i64 gets SF_STAT_PAIRS/OVERFLOW.
+ */
+int sf_bin_workspace_bytes(int64_t n, int32_t width, int32_t height, int64_t pair_capacity,
+                           size_t* bytes);
+int sf_bin(int64_t n, const double* means2d, const double* inv_covs, const double* depths,
+           const int64_t* source_ids, int32_t width, int32_t height, int64_t pair_capacity,
+           int64_t* order, int64_t* tile_offsets, int32_t* tile_entries, int64_t* stats_i64,
+           void* workspace, size_t workspace_bytes, void* stream);
+
+/* decode, sparse_splat.py:183-199: one level block, (P,L) @ (L,D) -> (P,D) fp32,
+ * 3xTF32 on tcgen05 tensor cores.  w has row stride w_stride floats. */
+int sf_decode(int64_t n_pixels, int32_t L, int32_t D, const float* w, int64_t w_stride,
+              const float* codebook, float* out, void* stream);
+/* Plain fp32 FMA-chain decode on CUDA cores: the independent cross-check the
+ * parity tests hold the tensor-core kernel against (not used by any frame). */
+int sf_decode_simt(int64_t n_pixels, int32_t L, int32_t D, const float* w, int64_t w_stride,
+                   const float* codebook, float* out, void* stream);
+
+/* relevancy_map, query.py:65-84, on an (P,D) feature map (fp32 or fp64). */
+int sf_relevancy_f32(int64_t n_pixels, int32_t D, const float* feats, const double* q,
+                     const double* canonicals, int32_t n_canonicals, double* out, void* stream);
+int sf_relevancy_f64(int64_t n_pixels, int32_t D, const double* feats, const double* q,
+                     const double* canonicals, int32_t n_canonicals, double* out, void* stream);
+
+/* mean_filter, query.py:87-108 (edge-clamped box filter), fp64 (H,W). */
+int sf_mean_filter(int32_t height, int32_t width, const double* in, int32_t window, double* out,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* select_level / localize / segment, query.py:111-145 over n maps (H,W) fp64:
+ * stats_i64[SF_STAT_LEVEL/ROW/COL/DEGENERATE], stats_f64[MIN/MAX/LEVEL_MAX+b];
+ * mask may be NULL.  fixed_level >= 0 skips selection. */
+size_t sf_select_segment_workspace_bytes(int32_t n_maps, int32_t height, int32_t width);
+int sf_select_segment(int32_t n_maps, int32_t height, int32_t width, const double* maps,
+                      int32_t fixed_level, double threshold, uint8_t* mask, int64_t* stats_i64,
+                      double* stats_f64, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Timing-event helpers for SfFrame.events (cudaEventCreate / elapsed ms). */
+void* sf_event_create(void);
+void sf_event_destroy(void* ev);
+float sf_event_elapsed_ms(void* start, void* end);
+
+/* Human-readable text of the last error on this thread. */
+const char* sf_last_error(void);
+/* ABI version (bumped on any signature change). */
+int sf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLATFIELD_B200_H */

@@ -1,0 +1,293 @@
+// sf_binning.cu -- K2-K4: depth-rank sort, tile-key duplication, per-tile lists.
+//
+// Reference: bin_projected, projection.py:379-450.
+//  (1) canonical order lexsort((ids, depths))            projection.py:396
+//  (2) candidate tile rectangle from the +-3 sigma extent projection.py:406-418
+//  (3) exact ellipse/rectangle test q_min <= 9            projection.py:429-441
+//  (4) stable argsort by tile + searchsorted bounds       projection.py:443-449
+//
+// B200 design.  (1) is a device radix sort of the fp64 depth bits (positive
+// doubles order like their bit patterns) over rows already stored in id
+// order, so a stable sort gives the (depth, id) order exactly; the position
+// in that order is the Gaussian's depth rank r.  (2)+(3) run per rank with
+// the reference's fp64 arithmetic (this file is compiled with -fmad=false)
+// and emit (tile, r) pairs; a per-tile counting pass plus an atomic bucket
+// fill replaces the global pair sort, and a CTA-local sort of each tile's
+// ranks restores the canonical order.  The resulting key order is exactly
+// (tile id | depth rank), i.e. the reference's per-tile lists, bit for bit.
+#include <cub/cub.cuh>
+
+#include "sf_common.cuh"
+
+namespace sf {
+
+size_t depth_sort_cub_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 64);
+    return bytes;
+}
+size_t id_sort_cub_bytes(int64_t n) { return depth_sort_cub_bytes(n); }
+
+int depth_sort(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in,
+               uint32_t* vals_out, int64_t n, void* tmp, size_t tmp_bytes, cudaStream_t st) {
+    if (n == 0) return 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in,
+                                                    vals_out, (int)n, 0, 64, st);
+    return e == cudaSuccess ? 0 : -1;
+}
+
+// ---------------------------------------------------------------------------
+// rank gather: canonical-order copies of the projected record, the fp32 blend
+// record and the selected levels' top-K (channel, value) scatter plan
+// (sparse_splat.py:126-132 cat_idx / cat_vals).
+
+__global__ void __launch_bounds__(256) k_rank_gather(int64_t G, const uint32_t* __restrict__ sorted_rows,
+                                                     const int64_t* __restrict__ stats,
+                                                     const Proj64* __restrict__ proj_by_row,
+                                                     const float* __restrict__ opac_by_row,
+                                                     const uint16_t* __restrict__ cidx,
+                                                     const float* __restrict__ cval, int K, int L,
+                                                     LevelSelDev levels,
+                                                     Proj64* __restrict__ proj_rank,
+                                                     Blend32* __restrict__ b32,
+                                                     uint16_t* __restrict__ ch_idx,
+                                                     float* __restrict__ ch_val, int C) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t n = stats[SF_STAT_VISIBLE];
+    if (r >= n) return;
+    uint32_t row = sorted_rows[r];
+    Proj64 p = proj_by_row[row];
+    proj_rank[r] = p;
+    Blend32 q;
+    q.mx_hi = (float)p.mx;
+    q.mx_lo = (float)(p.mx - (double)q.mx_hi);
+    q.my_hi = (float)p.my;
+    q.my_lo = (float)(p.my - (double)q.my_hi);
+    q.a = (float)p.a;
+    q.b2 = (float)(2.0 * p.b);
+    q.c = (float)p.c;
+    q.opacity = opac_by_row[row];
+    b32[r] = q;
+    if (ch_idx) {
+        for (int b = 0; b < levels.n; ++b) {
+            int lv = levels.lv[b];
+            const uint16_t* ip = cidx + ((int64_t)lv * G + row) * K;
+            const float* vp = cval + ((int64_t)lv * G + row) * K;
+            for (int k = 0; k < K; ++k) {
+                ch_idx[r * C + b * K + k] = (uint16_t)(ip[k] + b * L);
+                ch_val[r * C + b * K + k] = vp[k];
+            }
+        }
+    }
+}
+
+void launch_rank_gather(int64_t G, const uint32_t* sorted_rows, const int64_t* stats,
+                        const Proj64* proj_by_row, const float* opac_by_row, const SfScene* s,
+                        const LevelSelDev& levels, Proj64* proj_rank, Blend32* b32,
+                        uint16_t* ch_idx, float* ch_val, int C, cudaStream_t st) {
+    if (G == 0) return;
+    k_rank_gather<<<ceil_div(G, 256), 256, 0, st>>>(
+        G, sorted_rows, stats, proj_by_row, opac_by_row, s ? s->coeff_indices : nullptr,
+        s ? s->coeff_values : nullptr, s ? s->K : 0, s ? s->L : 0, levels, proj_rank, b32,
+        ch_idx, ch_val, C);
+}
+
+// ---------------------------------------------------------------------------
+// candidate rectangle + exact tile test (reference fp64 order)
+
+struct TileGrid {
+    int W, H, tiles_x, tiles_y;
+};
+
+__device__ __forceinline__ void cand_rect(const Proj64& p, const TileGrid& g, int& tx0, int& tx1,
+                                          int& ty0, int& ty1) {
+    double den = p.a * p.c - p.b * p.b;  // inv00*inv11 - inv01**2
+    double cov_xx = p.c / den;
+    double cov_yy = p.a / den;
+    double rx = 3.0 * sqrt(np_maximum(cov_xx, 0.0));
+    double ry = 3.0 * sqrt(np_maximum(cov_yy, 0.0));
+    const double ts = (double)SF_TILE;
+    int64_t v;
+    v = np_to_i64(np_floor_divide(p.mx - rx, ts));
+    tx0 = (int)(v < 0 ? 0 : (v > g.tiles_x - 1 ? g.tiles_x - 1 : v));
+    v = np_to_i64(np_floor_divide(p.mx + rx, ts));
+    tx1 = (int)(v < 0 ? 0 : (v > g.tiles_x - 1 ? g.tiles_x - 1 : v));
+    v = np_to_i64(np_floor_divide(p.my - ry, ts));
+    ty0 = (int)(v < 0 ? 0 : (v > g.tiles_y - 1 ? g.tiles_y - 1 : v));
+    v = np_to_i64(np_floor_divide(p.my + ry, ts));
+    ty1 = (int)(v < 0 ? 0 : (v > g.tiles_y - 1 ? g.tiles_y - 1 : v));
+}
+
+__device__ __forceinline__ bool tile_hit(const Proj64& p, int tx, int ty, const TileGrid& g) {
+    double lx = (double)(tx * SF_TILE), ly = (double)(ty * SF_TILE);
+    double hx = np_minimum(lx + (double)SF_TILE, (double)g.W) - 1;
+    double hy = np_minimum(ly + (double)SF_TILE, (double)g.H) - 1;
+    return min_mahal_sq_to_rect(p.mx, p.my, p.a, p.b, p.c, lx, ly, hx, hy) <= SF_CUTOFF;
+}
+
+__global__ void __launch_bounds__(256) k_count_pairs(int64_t G, const int64_t* __restrict__ stats,
+                                                     const Proj64* __restrict__ proj_rank,
+                                                     TileGrid g, uint32_t* __restrict__ tile_counts) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= stats[SF_STAT_VISIBLE]) return;
+    Proj64 p = proj_rank[r];
+    int tx0, tx1, ty0, ty1;
+    cand_rect(p, g, tx0, tx1, ty0, ty1);
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx)
+            if (tile_hit(p, tx, ty, g)) atomicAdd(&tile_counts[ty * g.tiles_x + tx], 1u);
+}
+
+// Exclusive scan over tiles (single CTA): offsets, cursors, pair total.
+__global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t* __restrict__ counts,
+                                                    uint32_t* __restrict__ offsets,
+                                                    uint32_t* __restrict__ cursor,
+                                                    int64_t pair_capacity, int64_t* stats) {
+    typedef cub::BlockScan<unsigned long long, 1024> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n_tiles; base += 1024) {
+        int t = base + threadIdx.x;
+        unsigned long long c = (t < n_tiles) ? counts[t] : 0, ex, tot;
+        Scan(tmp).ExclusiveSum(c, ex, tot);
+        if (t < n_tiles) {
+            offsets[t] = (uint32_t)(carry + ex);
+            cursor[t] = (uint32_t)(carry + ex);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        offsets[n_tiles] = (uint32_t)carry;
+        stats[SF_STAT_PAIRS] = (int64_t)carry;
+        stats[SF_STAT_OVERFLOW] = ((int64_t)carry > pair_capacity) ? 1 : 0;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_emit_pairs(int64_t G, const int64_t* __restrict__ stats,
+                                                    const Proj64* __restrict__ proj_rank, TileGrid g,
+                                                    uint32_t* __restrict__ cursor,
+                                                    uint32_t* __restrict__ entries) {
+    if (stats[SF_STAT_OVERFLOW]) return;
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= stats[SF_STAT_VISIBLE]) return;
+    Proj64 p = proj_rank[r];
+    int tx0, tx1, ty0, ty1;
+    cand_rect(p, g, tx0, tx1, ty0, ty1);
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx)
+            if (tile_hit(p, tx, ty, g)) {
+                uint32_t pos = atomicAdd(&cursor[ty * g.tiles_x + tx], 1u);
+                entries[pos] = (uint32_t)r;
+            }
+}
+
+// ---------------------------------------------------------------------------
+// per-tile sort of depth ranks (restores canonical order inside each bucket)
+
+constexpr int kSortSmemElems = 8192;
+
+__device__ void block_bitonic_sort(uint32_t* s, int N) {
+    // N is a power of two; ascending.
+    for (int k = 2; k <= N; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int p = threadIdx.x; p < (N >> 1); p += blockDim.x) {
+                int i = 2 * j * (p / j) + (p % j);
+                int ixj = i + j;
+                bool up = ((i & k) == 0);
+                uint32_t a = s[i], b = s[ixj];
+                if ((a > b) == up) {
+                    s[i] = b;
+                    s[ixj] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// LSD 1-bit stable split sort through global scratch (rare, very long lists).
+__device__ void block_radix_split_global(uint32_t* a, uint32_t* b, int n, int nbits) {
+    typedef cub::BlockScan<int, 256> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int s_zero;
+    uint32_t* src = a;
+    uint32_t* dst = b;
+    for (int bit = 0; bit < nbits; ++bit) {
+        int z = 0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) z += !((src[i] >> bit) & 1u);
+        int zsum;
+        Scan(tmp).ExclusiveSum(z, z, zsum);
+        if (threadIdx.x == 0) s_zero = zsum;
+        __syncthreads();
+        int base0 = 0, base1 = s_zero;
+        for (int start = 0; start < n; start += blockDim.x) {
+            int i = start + threadIdx.x;
+            bool valid = i < n;
+            uint32_t v = valid ? src[i] : 0u;
+            int isz = (valid && !((v >> bit) & 1u)) ? 1 : 0;
+            int ex, tot;
+            Scan(tmp).ExclusiveSum(isz, ex, tot);
+            if (valid) dst[isz ? base0 + ex : base1 + ((int)threadIdx.x - ex)] = v;
+            int chunk = min((int)blockDim.x, n - start);
+            base0 += tot;
+            base1 += chunk - tot;
+            __syncthreads();
+        }
+        uint32_t* t = src;
+        src = dst;
+        dst = t;
+        __syncthreads();
+    }
+    if (src != a) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = src[i];
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ offsets,
+                                                   uint32_t* __restrict__ entries,
+                                                   uint32_t* __restrict__ scratch,
+                                                   const int64_t* __restrict__ stats) {
+    if (stats[SF_STAT_OVERFLOW]) return;
+    __shared__ uint32_t s[kSortSmemElems];
+    int t = blockIdx.x;
+    uint32_t beg = offsets[t], end = offsets[t + 1];
+    int n = (int)(end - beg);
+    if (n <= 1) return;
+    uint32_t* e = entries + beg;
+    if (n <= kSortSmemElems) {
+        int N = 2;
+        while (N < n) N <<= 1;
+        for (int i = threadIdx.x; i < N; i += blockDim.x) s[i] = (i < n) ? e[i] : 0xffffffffu;
+        __syncthreads();
+        block_bitonic_sort(s, N);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) e[i] = s[i];
+    } else {
+        int64_t nvis = stats[SF_STAT_VISIBLE];
+        int nbits = 1;
+        while (nbits < 32 && ((int64_t)1 << nbits) < nvis) ++nbits;
+        block_radix_split_global(e, scratch + beg, n, nbits);
+    }
+}
+
+void launch_binning(int64_t G, const int64_t* stats_n, const Proj64* proj_rank, int W, int H,
+                    int64_t pair_capacity, uint32_t* tile_counts, uint32_t* tile_offsets,
+                    uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
+                    int64_t* stats, cudaStream_t st) {
+    TileGrid g{W, H, (W + SF_TILE - 1) / SF_TILE, (H + SF_TILE - 1) / SF_TILE};
+    int n_tiles = g.tiles_x * g.tiles_y;
+    cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * n_tiles, st);
+    int blocks = G > 0 ? ceil_div(G, 256) : 0;
+    if (blocks) k_count_pairs<<<blocks, 256, 0, st>>>(G, stats_n, proj_rank, g, tile_counts);
+    k_tile_scan<<<1, 1024, 0, st>>>(n_tiles, tile_counts, tile_offsets, tile_cursor, pair_capacity,
+                                    stats);
+    if (blocks) k_emit_pairs<<<blocks, 256, 0, st>>>(G, stats_n, proj_rank, g, tile_cursor, entries);
+    k_tile_sort<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, stats);
+}
+
+}  // namespace sf

@@ -1,0 +1,461 @@
+// sf_capi.cu -- extern "C" entry points (include/splatfield_b200.h).
+//
+// Validation happens on the host before any launch, mirroring where the
+// reference raises (sparse_splat.py:114-122, query.py:73-90).  All scratch
+// is carved from the caller's workspace; nothing allocates.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <cub/cub.cuh>
+
+#include "sf_common.cuh"
+
+using namespace sf;
+
+static thread_local char g_err[512];
+
+static int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+static int check_cuda(const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SF_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+    return SF_OK;
+}
+
+extern "C" const char* sf_last_error(void) { return g_err; }
+
+extern "C" void* sf_event_create(void) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    return (void*)e;
+}
+extern "C" void sf_event_destroy(void* e) {
+    if (e) cudaEventDestroy((cudaEvent_t)e);
+}
+extern "C" float sf_event_elapsed_ms(void* a, void* b) {
+    float ms = -1.f;
+    if (cudaEventSynchronize((cudaEvent_t)b) != cudaSuccess) return -1.f;
+    if (cudaEventElapsedTime(&ms, (cudaEvent_t)a, (cudaEvent_t)b) != cudaSuccess) return -1.f;
+    return ms;
+}
+extern "C" int sf_abi_version(void) { return 1; }
+
+// ---------------------------------------------------------------------------
+// frame workspace layout
+
+struct FrameWs {
+    Proj64* proj_by_row;
+    uint64_t* keys_in;
+    uint64_t* keys_out;
+    uint32_t* vals_in;
+    uint32_t* vals_out;
+    void* cub_tmp;
+    size_t cub_bytes;
+    int64_t* stats;
+    double* stats_f;
+    Proj64* proj_rank;
+    Blend32* b32;
+    uint16_t* ch_idx;
+    float* ch_val;
+    uint32_t* tile_counts;
+    uint32_t* tile_offsets;
+    uint32_t* tile_cursor;
+    uint32_t* entries;
+    uint32_t* scratch;
+    double* proj_cb;
+    double* filter_tmp;
+    void* sel_ws;
+};
+
+static constexpr int kMaxCanon = 64;
+
+static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n_levels, int L,
+                          int K, int64_t pair_cap, FrameWs* ws) {
+    Carver c(base, cap);
+    int64_t Gp = G > 0 ? G : 1;
+    int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
+    int C = n_levels * K;
+    ws->proj_by_row = c.take<Proj64>(Gp);
+    ws->keys_in = c.take<uint64_t>(Gp);
+    ws->keys_out = c.take<uint64_t>(Gp);
+    ws->vals_in = c.take<uint32_t>(Gp);
+    ws->vals_out = c.take<uint32_t>(Gp);
+    ws->cub_bytes = depth_sort_cub_bytes(Gp);
+    ws->cub_tmp = c.take<char>(ws->cub_bytes);
+    ws->stats = c.take<int64_t>(16);
+    ws->stats_f = c.take<double>(8 + kMaxLevels);
+    ws->proj_rank = c.take<Proj64>(Gp);
+    ws->b32 = c.take<Blend32>(Gp);
+    ws->ch_idx = c.take<uint16_t>(Gp * C);
+    ws->ch_val = c.take<float>(Gp * C);
+    ws->tile_counts = c.take<uint32_t>(n_tiles);
+    ws->tile_offsets = c.take<uint32_t>(n_tiles + 1);
+    ws->tile_cursor = c.take<uint32_t>(n_tiles);
+    ws->entries = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
+    ws->scratch = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
+    ws->proj_cb = c.take<double>((size_t)n_levels * L * (1 + kMaxCanon));
+    ws->filter_tmp = c.take<double>((size_t)n_levels * W * H);
+    ws->sel_ws = c.take<char>(select_segment_ws_bytes(n_levels, H, W));
+    return c.off;
+}
+
+extern "C" int sf_frame_workspace_bytes(int64_t G, int32_t W, int32_t H, int32_t n_levels,
+                                        int32_t L, int32_t K, int64_t pair_cap, size_t* bytes) {
+    FrameWs ws;
+    *bytes = carve_frame(nullptr, 0, G, W, H, n_levels, L, K, pair_cap, &ws) + 256;
+    return SF_OK;
+}
+
+static int validate_scene_cam(const SfScene* s, const SfCamera* cam) {
+    if (!s || !cam) return fail(SF_ERR_VALIDATION, "null scene or camera");
+    if (cam->width < 1 || cam->height < 1) return fail(SF_ERR_VALIDATION, "image size must be >= 1 pixel");
+    if (!(cam->fx > 0) || !(cam->fy > 0)) return fail(SF_ERR_VALIDATION, "focal lengths must be > 0");
+    if (!(cam->near_plane > 0)) return fail(SF_ERR_VALIDATION, "near plane must be > 0");
+    if (s->num_gaussians < 0 || s->num_gaussians >= (int64_t)1 << 31)
+        return fail(SF_ERR_VALIDATION, "num_gaussians out of range");
+    return SF_OK;
+}
+
+extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
+                               const SfFrame* f, void* workspace, size_t workspace_bytes,
+                               void* stream_) {
+    cudaStream_t st = (cudaStream_t)stream_;
+    int rc = validate_scene_cam(s, cam);
+    if (rc) return rc;
+    if (!f || f->n_levels < 1 || f->n_levels > kMaxLevels)
+        return fail(SF_ERR_VALIDATION, "1..%d levels must be selected", kMaxLevels);
+    LevelSelDev lv;
+    lv.n = f->n_levels;
+    for (int b = 0; b < f->n_levels; ++b) {
+        int l = f->host_levels[b];
+        if (l < 0 || l >= s->num_levels)
+            return fail(SF_ERR_VALIDATION, "level %d out of range for %d levels", l, s->num_levels);
+        lv.lv[b] = l;
+    }
+    const int W = cam->width, H = cam->height;
+    const int L = s->L, K = s->K, D = s->D;
+    const int C = f->n_levels * K;
+    const int n_ch = f->n_levels * L;
+    if (C > 16) return fail(SF_ERR_VALIDATION, "levels*K = %d exceeds 16 channels per Gaussian", C);
+    if (n_ch > 65535) return fail(SF_ERR_VALIDATION, "too many channels");
+    if (q) {
+        if (q->n_canonicals < 1) return fail(SF_ERR_VALIDATION, "at least one canonical D-vector is required");
+        if (q->n_canonicals > kMaxCanon) return fail(SF_ERR_VALIDATION, "at most %d canonicals", kMaxCanon);
+        if (q->window < 1 || q->window % 2 == 0)
+            return fail(SF_ERR_VALIDATION, "filter window must be odd and >= 1, got %d", q->window);
+        if (q->fixed_level >= f->n_levels) return fail(SF_ERR_VALIDATION, "fixed level was not rendered");
+        if (!f->relevancy_raw || !f->relevancy_filtered)
+            return fail(SF_ERR_VALIDATION, "query frames need relevancy buffers");
+    }
+    bool need_cmap = (f->features != nullptr) || (q && n_ch > 192);
+    if (need_cmap && !f->coeff_map) return fail(SF_ERR_VALIDATION, "coefficient map buffer required");
+
+    FrameWs ws;
+    size_t need = carve_frame(workspace, workspace_bytes, s->num_gaussians, W, H, f->n_levels, L, K,
+                              f->pair_capacity, &ws);
+    if (need > workspace_bytes) return fail(SF_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, need);
+
+    const int64_t G = s->num_gaussians;
+    if (f->events[0]) cudaEventRecord((cudaEvent_t)f->events[0], st);
+    cudaMemsetAsync(ws.stats, 0, 16 * sizeof(int64_t), st);
+    cudaMemsetAsync(ws.stats_f, 0, (8 + kMaxLevels) * sizeof(double), st);
+    // K1
+    launch_preprocess(*s, *cam, ws.proj_by_row, ws.keys_in, ws.vals_in, ws.stats, st);
+    // K2
+    if (depth_sort(ws.keys_in, ws.keys_out, ws.vals_in, ws.vals_out, G, ws.cub_tmp, ws.cub_bytes, st))
+        return check_cuda("depth sort");
+    launch_rank_gather(G, ws.vals_out, ws.stats, ws.proj_by_row, s->opacities, s, lv, ws.proj_rank,
+                       ws.b32, ws.ch_idx, ws.ch_val, C, st);
+    // K3/K4
+    launch_binning(G, ws.stats, ws.proj_rank, W, H, f->pair_capacity, ws.tile_counts, ws.tile_offsets,
+                   ws.tile_cursor, ws.entries, ws.scratch, ws.stats, st);
+    if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
+                                   ws.proj_cb, st);
+    // K5/K6 (+ fused relevancy)
+    BlendArgs a;
+    memset(&a, 0, sizeof(a));
+    a.W = W;
+    a.H = H;
+    a.tiles_x = (W + SF_TILE - 1) / SF_TILE;
+    a.tiles_y = (H + SF_TILE - 1) / SF_TILE;
+    a.n_ch = n_ch;
+    a.C = C;
+    a.early_exit = f->early_exit;
+    a.tile_offsets = ws.tile_offsets;
+    a.entries = ws.entries;
+    a.b32 = ws.b32;
+    a.p64 = ws.proj_rank;
+    a.ch_idx = ws.ch_idx;
+    a.ch_val = ws.ch_val;
+    a.stats = ws.stats;
+    a.coeff_map = f->coeff_map;
+    a.final_t = f->final_t;
+    a.proj_cb = q ? ws.proj_cb : nullptr;
+    a.n_levels = f->n_levels;
+    a.L = L;
+    a.n_canon = q ? q->n_canonicals : 0;
+    a.relevancy_raw = q ? f->relevancy_raw : nullptr;
+    if (launch_blend(a, st)) return fail(SF_ERR_VALIDATION, "blend configuration unsupported");
+    if (f->events[1]) cudaEventRecord((cudaEvent_t)f->events[1], st);
+    // K7
+    if (f->features) {
+        const int64_t P = (int64_t)W * H;
+        for (int b = 0; b < f->n_levels; ++b) {
+            if (launch_decode(P, L, D, f->coeff_map + (size_t)b * L, n_ch,
+                              s->codebooks + (size_t)lv.lv[b] * L * D, f->features + (size_t)b * P * D, st))
+                return fail(SF_ERR_VALIDATION, "decode configuration unsupported (L=%d, D=%d)", L, D);
+        }
+    }
+    if (f->events[2]) cudaEventRecord((cudaEvent_t)f->events[2], st);
+    // K8-K10
+    if (q) {
+        launch_mean_filter(f->n_levels, H, W, f->relevancy_raw, q->window, ws.filter_tmp,
+                           f->relevancy_filtered, st);
+        launch_select_segment(f->n_levels, H, W, f->relevancy_filtered, q->fixed_level, q->threshold,
+                              f->mask, ws.stats, ws.stats_f, ws.sel_ws, st);
+    }
+    if (f->events[3]) cudaEventRecord((cudaEvent_t)f->events[3], st);
+    if (f->stats_i64) cudaMemcpyAsync(f->stats_i64, ws.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+    if (f->stats_f64)
+        cudaMemcpyAsync(f->stats_f64, ws.stats_f, (8 + f->n_levels) * sizeof(double),
+                        cudaMemcpyDeviceToDevice, st);
+    return check_cuda("sf_render_frame");
+}
+
+// ---------------------------------------------------------------------------
+// project_scene
+
+struct ProjWs {
+    Proj64* proj;
+    uint64_t* keys;
+    uint32_t* vals;
+    int64_t* stats;
+    int32_t* flags;
+    int32_t* scan;
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+
+static size_t carve_project(void* base, size_t cap, int64_t G, ProjWs* w) {
+    Carver c(base, cap);
+    int64_t Gp = G > 0 ? G : 1;
+    w->proj = c.take<Proj64>(Gp);
+    w->keys = c.take<uint64_t>(Gp);
+    w->vals = c.take<uint32_t>(Gp);
+    w->stats = c.take<int64_t>(16);
+    w->flags = c.take<int32_t>(Gp);
+    w->scan = c.take<int32_t>(Gp);
+    w->cub_bytes = project_compact_cub_bytes(Gp);
+    w->cub_tmp = c.take<char>(w->cub_bytes);
+    return c.off;
+}
+
+extern "C" int sf_project_workspace_bytes(int64_t G, size_t* bytes) {
+    ProjWs w;
+    *bytes = carve_project(nullptr, 0, G, &w) + 256;
+    return SF_OK;
+}
+
+extern "C" int sf_project(const SfScene* s, const SfCamera* cam, double* means2d, double* inv_covs,
+                          double* depths, double* opacities, int64_t* source_ids, int64_t* rows,
+                          int64_t* count_out, void* workspace, size_t workspace_bytes, void* stream_) {
+    return sf_project_rows(s, cam, nullptr, means2d, inv_covs, depths, opacities, source_ids, rows,
+                           count_out, workspace, workspace_bytes, stream_);
+}
+
+extern "C" int sf_project_rows(const SfScene* s, const SfCamera* cam, const int64_t* orig_rows,
+                               double* means2d, double* inv_covs, double* depths, double* opacities,
+                               int64_t* source_ids, int64_t* rows, int64_t* count_out,
+                               void* workspace, size_t workspace_bytes, void* stream_) {
+    cudaStream_t st = (cudaStream_t)stream_;
+    int rc = validate_scene_cam(s, cam);
+    if (rc) return rc;
+    ProjWs w;
+    size_t need = carve_project(workspace, workspace_bytes, s->num_gaussians, &w);
+    if (need > workspace_bytes) return fail(SF_ERR_WORKSPACE, "workspace too small");
+    cudaMemsetAsync(w.stats, 0, 16 * sizeof(int64_t), st);
+    launch_preprocess(*s, *cam, w.proj, w.keys, w.vals, w.stats, st);
+    launch_project_compact(*s, w.proj, w.keys, orig_rows, w.flags, w.scan, means2d, inv_covs, depths,
+                           opacities, source_ids, rows, count_out, w.cub_tmp, w.cub_bytes, st);
+    return check_cuda("sf_project");
+}
+
+// ---------------------------------------------------------------------------
+// bin_projected on arbitrary projected arrays
+
+__global__ void k_bin_prepare(int64_t n, const double* means2d, const double* inv_covs,
+                              const double* depths, const int64_t* source_ids, Proj64* proj,
+                              uint64_t* id_keys, uint32_t* idx) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Proj64 p;
+    p.mx = means2d[2 * i];
+    p.my = means2d[2 * i + 1];
+    p.a = inv_covs[4 * i];
+    p.b = inv_covs[4 * i + 1];
+    p.c = inv_covs[4 * i + 3];
+    proj[i] = p;
+    id_keys[i] = (uint64_t)source_ids[i] ^ 0x8000000000000000ull;  // signed -> monotone unsigned
+    idx[i] = (uint32_t)i;
+}
+
+__device__ __forceinline__ uint64_t depth_key(double d) {
+    if (d == 0.0) d = 0.0;  // -0.0 ties with +0.0 like numpy's comparison
+    uint64_t b = (uint64_t)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void k_bin_depth_keys(int64_t n, const double* depths, const uint32_t* idx_by_id,
+                                 uint64_t* keys) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = depth_key(depths[idx_by_id[i]]);
+}
+
+__global__ void k_bin_finish(int64_t n, const uint32_t* order32, const Proj64* proj, Proj64* proj_rank,
+                             int64_t* order, int64_t* stats) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) stats[SF_STAT_VISIBLE] = n;
+    if (i >= n) return;
+    uint32_t r = order32[i];
+    proj_rank[i] = proj[r];
+    order[i] = r;
+}
+
+__global__ void k_offsets_to_i64(int n, const uint32_t* o32, int64_t* o64) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i <= n) o64[i] = o32[i];
+}
+
+struct BinWs {
+    Proj64* proj;
+    Proj64* proj_rank;
+    uint64_t* k0;
+    uint64_t* k1;
+    uint32_t* v0;
+    uint32_t* v1;
+    void* cub_tmp;
+    size_t cub_bytes;
+    int64_t* stats;
+    uint32_t* counts;
+    uint32_t* offsets;
+    uint32_t* cursor;
+    uint32_t* scratch;
+};
+
+static size_t carve_bin(void* base, size_t cap, int64_t n, int W, int H, int64_t pair_cap, BinWs* w) {
+    Carver c(base, cap);
+    int64_t np = n > 0 ? n : 1;
+    int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
+    w->proj = c.take<Proj64>(np);
+    w->proj_rank = c.take<Proj64>(np);
+    w->k0 = c.take<uint64_t>(np);
+    w->k1 = c.take<uint64_t>(np);
+    w->v0 = c.take<uint32_t>(np);
+    w->v1 = c.take<uint32_t>(np);
+    w->cub_bytes = depth_sort_cub_bytes(np);
+    w->cub_tmp = c.take<char>(w->cub_bytes);
+    w->stats = c.take<int64_t>(16);
+    w->counts = c.take<uint32_t>(n_tiles);
+    w->offsets = c.take<uint32_t>(n_tiles + 1);
+    w->cursor = c.take<uint32_t>(n_tiles);
+    w->scratch = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
+    return c.off;
+}
+
+extern "C" int sf_bin_workspace_bytes(int64_t n, int32_t W, int32_t H, int64_t pair_cap, size_t* bytes) {
+    BinWs w;
+    *bytes = carve_bin(nullptr, 0, n, W, H, pair_cap, &w) + 256;
+    return SF_OK;
+}
+
+extern "C" int sf_bin(int64_t n, const double* means2d, const double* inv_covs, const double* depths,
+                      const int64_t* source_ids, int32_t W, int32_t H, int64_t pair_cap, int64_t* order,
+                      int64_t* tile_offsets, int32_t* tile_entries, int64_t* stats_i64, void* workspace,
+                      size_t workspace_bytes, void* stream_) {
+    cudaStream_t st = (cudaStream_t)stream_;
+    if (W < 1 || H < 1) return fail(SF_ERR_VALIDATION, "image size must be >= 1 pixel");
+    if (n < 0 || n >= (int64_t)1 << 31) return fail(SF_ERR_VALIDATION, "n out of range");
+    BinWs w;
+    size_t need = carve_bin(workspace, workspace_bytes, n, W, H, pair_cap, &w);
+    if (need > workspace_bytes) return fail(SF_ERR_WORKSPACE, "workspace too small");
+    int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
+    cudaMemsetAsync(w.stats, 0, 16 * sizeof(int64_t), st);
+    int blocks = n > 0 ? ceil_div(n, 256) : 1;
+    if (n > 0) {
+        k_bin_prepare<<<blocks, 256, 0, st>>>(n, means2d, inv_covs, depths, source_ids, w.proj, w.k0, w.v0);
+        // (depth, id) order = stable depth sort of the id-sorted sequence
+        depth_sort(w.k0, w.k1, w.v0, w.v1, n, w.cub_tmp, w.cub_bytes, st);
+        k_bin_depth_keys<<<blocks, 256, 0, st>>>(n, depths, w.v1, w.k0);
+        depth_sort(w.k0, w.k1, w.v1, w.v0, n, w.cub_tmp, w.cub_bytes, st);
+    }
+    k_bin_finish<<<blocks, 256, 0, st>>>(n, w.v0, w.proj, w.proj_rank, order, w.stats);
+    launch_binning(n, w.stats, w.proj_rank, W, H, pair_cap, w.counts, w.offsets, w.cursor,
+                   (uint32_t*)tile_entries, w.scratch, w.stats, st);
+    k_offsets_to_i64<<<ceil_div(n_tiles + 1, 256), 256, 0, st>>>(n_tiles, w.offsets, tile_offsets);
+    if (stats_i64) cudaMemcpyAsync(stats_i64, w.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+    return check_cuda("sf_bin");
+}
+
+// ---------------------------------------------------------------------------
+// standalone ops
+
+extern "C" int sf_decode(int64_t P, int32_t L, int32_t D, const float* w, int64_t w_stride,
+                         const float* cb, float* out, void* stream) {
+    if (launch_decode(P, L, D, w, w_stride, cb, out, (cudaStream_t)stream))
+        return fail(SF_ERR_VALIDATION, "decode configuration unsupported (L=%d, D=%d)", L, D);
+    return check_cuda("sf_decode");
+}
+
+extern "C" int sf_decode_simt(int64_t P, int32_t L, int32_t D, const float* w, int64_t w_stride,
+                              const float* cb, float* out, void* stream) {
+    if (launch_decode_simt(P, L, D, w, w_stride, cb, out, (cudaStream_t)stream))
+        return fail(SF_ERR_VALIDATION, "decode configuration unsupported (L=%d, D=%d)", L, D);
+    return check_cuda("sf_decode_simt");
+}
+
+extern "C" int sf_relevancy_f32(int64_t P, int32_t D, const float* f, const double* q, const double* c,
+                                int32_t nc, double* out, void* stream) {
+    if (nc < 1) return fail(SF_ERR_VALIDATION, "at least one canonical D-vector is required");
+    launch_relevancy_f32(P, D, f, q, c, nc, out, (cudaStream_t)stream);
+    return check_cuda("sf_relevancy_f32");
+}
+
+extern "C" int sf_relevancy_f64(int64_t P, int32_t D, const double* f, const double* q, const double* c,
+                                int32_t nc, double* out, void* stream) {
+    if (nc < 1) return fail(SF_ERR_VALIDATION, "at least one canonical D-vector is required");
+    launch_relevancy_f64(P, D, f, q, c, nc, out, (cudaStream_t)stream);
+    return check_cuda("sf_relevancy_f64");
+}
+
+extern "C" int sf_mean_filter(int32_t H, int32_t W, const double* in, int32_t window, double* out,
+                              void* ws, size_t ws_bytes, void* stream) {
+    if (window < 1 || window % 2 == 0)
+        return fail(SF_ERR_VALIDATION, "filter window must be odd and >= 1, got %d", window);
+    if (ws_bytes < (size_t)H * W * sizeof(double)) return fail(SF_ERR_WORKSPACE, "workspace too small");
+    launch_mean_filter(1, H, W, in, window, (double*)ws, out, (cudaStream_t)stream);
+    return check_cuda("sf_mean_filter");
+}
+
+extern "C" int sf_select_segment(int32_t n_maps, int32_t H, int32_t W, const double* maps,
+                                 int32_t fixed_level, double threshold, uint8_t* mask,
+                                 int64_t* stats_i64, double* stats_f64, void* ws, size_t ws_bytes,
+                                 void* stream) {
+    if (n_maps < 1 || n_maps > 32) return fail(SF_ERR_VALIDATION, "at least one level map is required");
+    if ((int64_t)H * W == 0) return fail(SF_ERR_VALIDATION, "cannot localize an empty map");
+    if (ws_bytes < select_segment_ws_bytes(n_maps, H, W)) return fail(SF_ERR_WORKSPACE, "workspace too small");
+    launch_select_segment(n_maps, H, W, maps, fixed_level, threshold, mask, stats_i64, stats_f64, ws,
+                          (cudaStream_t)stream);
+    return check_cuda("sf_select_segment");
+}
+
+extern "C" size_t sf_select_segment_workspace_bytes(int32_t n_maps, int32_t H, int32_t W) {
+    return select_segment_ws_bytes(n_maps, H, W);
+}

@@ -1,0 +1,196 @@
+// sf_common.cuh -- shared device helpers and internal launch interfaces.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "../../include/splatfield_b200.h"
+
+#define SF_CUTOFF 9.0          // projection.py:33 CUTOFF_MAHAL_SQ
+#define SF_LOWPASS 0.3         // projection.py:32 LOWPASS_FLOOR
+#define SF_ALPHA_CLAMP 0.99    // projection.py:34 ALPHA_CLAMP
+#define SF_EARLY_EXIT_T 1e-4   // rasterizer.py:45 EARLY_EXIT_T
+
+namespace sf {
+
+// numpy ufunc semantics (NaN-propagating) -- needed wherever the reference's
+// np.minimum / np.maximum / np.clip feed an integer or membership decision.
+__host__ __device__ __forceinline__ double np_minimum(double a, double b) {
+    if (a != a) return a;
+    if (b != b) return b;
+    return (a <= b) ? a : b;
+}
+__host__ __device__ __forceinline__ double np_maximum(double a, double b) {
+    if (a != a) return a;
+    if (b != b) return b;
+    return (a >= b) ? a : b;
+}
+__host__ __device__ __forceinline__ double np_clip(double x, double lo, double hi) {
+    return np_minimum(np_maximum(x, lo), hi);
+}
+// numpy float64 -> int64 cast on x86-64: NaN / out of range -> INT64_MIN.
+__host__ __device__ __forceinline__ int64_t np_to_i64(double v) {
+    if (!(v >= -9223372036854775808.0 && v < 9223372036854775808.0)) return INT64_MIN;
+    return (int64_t)v;
+}
+// numpy floor_divide(a, b) (npy_divmod) for the tile size.
+__host__ __device__ __forceinline__ double np_floor_divide(double a, double b) {
+    double mod = fmod(a, b);
+    double div = (a - mod) / b;
+    if (mod) {
+        if ((b < 0) != (mod < 0)) {
+            mod += b;
+            div -= 1.0;
+        }
+    }
+    double fl;
+    if (div) {
+        fl = floor(div);
+        if (div - fl > 0.5) fl += 1.0;
+    } else {
+        fl = copysign(0.0, a / b);
+    }
+    return fl;
+}
+
+// min_mahalanobis_sq_to_rect, projection.py:191-226, one (mean, A, rect).
+// Exact fp64 op order of the reference; callers compile with -fmad=false.
+__host__ __device__ __forceinline__ double min_mahal_sq_to_rect(double mx, double my, double a,
+                                                               double b, double c, double lx,
+                                                               double ly, double hx, double hy) {
+    double best = INFINITY;
+    {
+        double dx = lx - mx;
+        double ys = np_clip(my - (b / c) * dx, ly, hy);
+        double dy = ys - my;
+        best = np_minimum(best, (a * dx) * dx + ((2.0 * b) * dx) * dy + (c * dy) * dy);
+    }
+    {
+        double dx = hx - mx;
+        double ys = np_clip(my - (b / c) * dx, ly, hy);
+        double dy = ys - my;
+        best = np_minimum(best, (a * dx) * dx + ((2.0 * b) * dx) * dy + (c * dy) * dy);
+    }
+    {
+        double dy = ly - my;
+        double xs = np_clip(mx - (b / a) * dy, lx, hx);
+        double dx = xs - mx;
+        best = np_minimum(best, (a * dx) * dx + ((2.0 * b) * dx) * dy + (c * dy) * dy);
+    }
+    {
+        double dy = hy - my;
+        double xs = np_clip(mx - (b / a) * dy, lx, hx);
+        double dx = xs - mx;
+        best = np_minimum(best, (a * dx) * dx + ((2.0 * b) * dx) * dy + (c * dy) * dy);
+    }
+    if ((mx >= lx) && (mx <= hx) && (my >= ly) && (my <= hy)) best = 0.0;
+    return best;
+}
+
+// Projected record of one surviving Gaussian (fp64, the reference's values).
+struct __align__(8) Proj64 {
+    double mx, my;  // means2d
+    double a, b, c; // inv_cov2d [[a, b], [b, c]]
+};
+
+// Blend-side record in canonical rank order: fp32 reject test inputs.
+struct __align__(16) Blend32 {
+    float mx_hi, mx_lo, my_hi, my_lo;  // mean split so (px - hi) - lo is ~exact
+    float a, b2, c, opacity;           // conic (a, 2b, c) and opacity
+};
+
+// Workspace carving helper.
+struct Carver {
+    char* base;
+    size_t off, cap;
+    __host__ Carver(void* p, size_t c) : base((char*)p), off(0), cap(c) {}
+    template <typename T>
+    __host__ T* take(size_t n) {
+        off = (off + 255) & ~(size_t)255;
+        T* p = (T*)(base ? base + off : nullptr);
+        off += n * sizeof(T);
+        return p;
+    }
+    __host__ bool ok() const { return off <= cap; }
+};
+
+__host__ __device__ __forceinline__ int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// Selected semantic levels, passed by value (no host->device copy).
+constexpr int kMaxLevels = 8;
+struct LevelSelDev {
+    int n;
+    int lv[kMaxLevels];
+};
+
+// ---------------- internal launchers (one .cu each) ----------------
+
+// sf_preprocess.cu
+void launch_preprocess(const SfScene& s, const SfCamera& cam, Proj64* proj, uint64_t* keys,
+                       uint32_t* vals, int64_t* stats, cudaStream_t st);
+void launch_project_compact(const SfScene& s, const Proj64* proj, const uint64_t* keys,
+                            const int64_t* orig_rows_or_null, int32_t* flags, int32_t* scan,
+                            double* means2d, double* inv_covs, double* depths, double* opac,
+                            int64_t* source_ids, int64_t* rows, int64_t* count, void* cub_tmp,
+                            size_t cub_bytes, cudaStream_t st);
+size_t project_compact_cub_bytes(int64_t G);
+
+// sf_binning.cu
+size_t depth_sort_cub_bytes(int64_t n);
+int depth_sort(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in,
+               uint32_t* vals_out, int64_t n, void* tmp, size_t tmp_bytes, cudaStream_t st);
+size_t id_sort_cub_bytes(int64_t n);
+void launch_rank_gather(int64_t G, const uint32_t* sorted_rows, const int64_t* stats,
+                        const Proj64* proj_by_row, const float* opac_by_row, const SfScene* s,
+                        const LevelSelDev& levels, Proj64* proj_rank, Blend32* b32,
+                        uint16_t* ch_idx, float* ch_val, int C, cudaStream_t st);
+void launch_binning(int64_t G, const int64_t* stats_n, const Proj64* proj_rank, int W, int H,
+                    int64_t pair_capacity, uint32_t* tile_counts, uint32_t* tile_offsets,
+                    uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
+                    int64_t* stats, cudaStream_t st);
+
+// sf_blend.cu
+struct BlendArgs {
+    int W, H, tiles_x, tiles_y;
+    int n_ch;          // n_levels * L
+    int C;             // channels per Gaussian = n_levels * K
+    int early_exit;
+    const uint32_t* tile_offsets;
+    const uint32_t* entries;
+    const Blend32* b32;
+    const Proj64* p64;
+    const uint16_t* ch_idx;
+    const float* ch_val;
+    const int64_t* stats;  // overflow flag gate
+    float* coeff_map;      // (H,W,n_ch) or null
+    float* final_t;        // (H,W) or null
+    // fused projected-codebook relevancy (optional)
+    const double* proj_cb; // (n_levels, L, 1 + n_canon) or null
+    int n_levels, L, n_canon;
+    double* relevancy_raw; // (n_levels, H, W)
+    int64_t* fixups;
+};
+int launch_blend(const BlendArgs& a, cudaStream_t st);
+
+// sf_post.cu
+void launch_project_codebook(const float* codebooks, const LevelSelDev& levels, int L, int D,
+                             const double* q, const double* canon, int n_canon, double* out,
+                             cudaStream_t st);
+void launch_relevancy_f32(int64_t P, int D, const float* f, const double* q, const double* c,
+                          int nc, double* out, cudaStream_t st);
+void launch_relevancy_f64(int64_t P, int D, const double* f, const double* q, const double* c,
+                          int nc, double* out, cudaStream_t st);
+void launch_mean_filter(int n_maps, int H, int W, const double* in, int window, double* tmp,
+                        double* out, cudaStream_t st);
+size_t select_segment_ws_bytes(int n_maps, int H, int W);
+void launch_select_segment(int n_maps, int H, int W, const double* maps, int fixed_level,
+                           double threshold, uint8_t* mask, int64_t* stats_i64,
+                           double* stats_f64, void* ws, cudaStream_t st);
+
+// sf_decode.cu (SIMT cross-check) / sf_decode_tc.cu (tcgen05 3xTF32)
+int launch_decode_simt(int64_t P, int L, int D, const float* w, int64_t w_stride, const float* cb,
+                       float* out, cudaStream_t st);
+int launch_decode(int64_t P, int L, int D, const float* w, int64_t w_stride, const float* cb,
+                  float* out, cudaStream_t st);
+
+}  // namespace sf

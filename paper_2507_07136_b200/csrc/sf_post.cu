@@ -1,0 +1,216 @@
+// sf_post.cu -- K8-K10: relevancy, mean filter, level selection, argmax, mask.
+//
+// Reference: relevancy_map (query.py:65-84, raw dot products, two-branch
+// sigmoid), mean_filter (query.py:87-108, edge-clamped box filter),
+// select_level (:111-118, first argmax of maxima), localize (:121-126, first
+// row-major argmax), segment (:136-145, min-max normalised > threshold).
+// All fp64: the outputs feed discontinuous decisions (level, point, mask).
+#include <cub/cub.cuh>
+
+#include "sf_common.cuh"
+
+namespace sf {
+
+__device__ __forceinline__ double sigmoid2p(double x) {
+    if (x >= 0) return 1.0 / (1.0 + exp(-x));
+    double ex = exp(x);
+    return ex / (1.0 + ex);
+}
+
+// P[b][l][j] = atoms_{lv_b}[l] . v_j, v_0 = query, v_j = canonical j-1 (fp64).
+__global__ void k_project_codebook(const float* __restrict__ cb, LevelSelDev lv, int L, int D,
+                                   const double* __restrict__ q, const double* __restrict__ canon,
+                                   int n_canon, double* __restrict__ out) {
+    int nv = 1 + n_canon;
+    int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    int total = lv.n * L * nv;
+    if (idx >= total) return;
+    int j = idx % nv;
+    int l = (idx / nv) % L;
+    int b = idx / (nv * L);
+    const float* a = cb + ((size_t)lv.lv[b] * L + l) * D;
+    const double* v = (j == 0) ? q : canon + (size_t)(j - 1) * D;
+    double s = 0.0;
+    for (int d = 0; d < D; ++d) s = fma((double)a[d], v[d], s);
+    out[idx] = s;
+}
+
+void launch_project_codebook(const float* codebooks, const LevelSelDev& lv, int L, int D,
+                             const double* q, const double* canon, int n_canon, double* out,
+                             cudaStream_t st) {
+    int total = lv.n * L * (1 + n_canon);
+    k_project_codebook<<<ceil_div(total, 128), 128, 0, st>>>(codebooks, lv, L, D, q, canon,
+                                                             n_canon, out);
+}
+
+template <typename T>
+__global__ void k_relevancy(int64_t P, int D, const T* __restrict__ f, const double* __restrict__ q,
+                            const double* __restrict__ c, int nc, double* __restrict__ out) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const T* fp = f + (size_t)p * D;
+    double lq = 0.0;
+    for (int d = 0; d < D; ++d) lq = fma((double)fp[d], q[d], lq);
+    double best = INFINITY;
+    for (int j = 0; j < nc; ++j) {
+        double lc = 0.0;
+        const double* cj = c + (size_t)j * D;
+        for (int d = 0; d < D; ++d) lc = fma((double)fp[d], cj[d], lc);
+        best = np_minimum(best, sigmoid2p(lq - lc));
+    }
+    out[p] = best;
+}
+
+void launch_relevancy_f32(int64_t P, int D, const float* f, const double* q, const double* c,
+                          int nc, double* out, cudaStream_t st) {
+    if (P) k_relevancy<float><<<ceil_div(P, 128), 128, 0, st>>>(P, D, f, q, c, nc, out);
+}
+void launch_relevancy_f64(int64_t P, int D, const double* f, const double* q, const double* c,
+                          int nc, double* out, cudaStream_t st) {
+    if (P) k_relevancy<double><<<ceil_div(P, 128), 128, 0, st>>>(P, D, f, q, c, nc, out);
+}
+
+// Separable edge-clamped box filter.  Pass 1 sums rows, pass 2 columns.
+__global__ void k_box_rows(int n_maps, int H, int W, const double* __restrict__ in, int r,
+                           double* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = (int64_t)n_maps * H * W;
+    if (i >= total) return;
+    int x = (int)(i % W);
+    const double* row = in + (i - x);
+    double s = 0.0;
+    for (int d = -r; d <= r; ++d) {
+        int xx = min(max(x + d, 0), W - 1);
+        s += row[xx];
+    }
+    out[i] = s;
+}
+__global__ void k_box_cols(int n_maps, int H, int W, const double* __restrict__ in, int r,
+                           double inv_area, double* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = (int64_t)n_maps * H * W;
+    if (i >= total) return;
+    int64_t hw = (int64_t)H * W;
+    int64_t m = i / hw;
+    int64_t rem = i - m * hw;
+    int y = (int)(rem / W), x = (int)(rem % W);
+    const double* base = in + m * hw;
+    double s = 0.0;
+    for (int d = -r; d <= r; ++d) {
+        int yy = min(max(y + d, 0), H - 1);
+        s += base[(int64_t)yy * W + x];
+    }
+    out[i] = s / inv_area;
+}
+
+void launch_mean_filter(int n_maps, int H, int W, const double* in, int window, double* tmp,
+                        double* out, cudaStream_t st) {
+    int64_t total = (int64_t)n_maps * H * W;
+    if (total == 0) return;
+    if (window == 1) {
+        cudaMemcpyAsync(out, in, total * sizeof(double), cudaMemcpyDeviceToDevice, st);
+        return;
+    }
+    int r = window / 2;
+    k_box_rows<<<ceil_div(total, 256), 256, 0, st>>>(n_maps, H, W, in, r, tmp);
+    k_box_cols<<<ceil_div(total, 256), 256, 0, st>>>(n_maps, H, W, tmp, r,
+                                                     (double)window * (double)window, out);
+}
+
+// ---- select_level / localize / segment ----
+
+struct MaxMin {
+    double mx;
+    int64_t idx;  // first index of the maximum
+    double mn;
+};
+
+__device__ __forceinline__ MaxMin mm_combine(MaxMin a, MaxMin b) {
+    MaxMin r;
+    if (b.mx > a.mx || (b.mx == a.mx && b.idx < a.idx)) {
+        r.mx = b.mx;
+        r.idx = b.idx;
+    } else {
+        r.mx = a.mx;
+        r.idx = a.idx;
+    }
+    r.mn = fmin(a.mn, b.mn);
+    return r;
+}
+
+constexpr int kRedBlocks = 296;  // 2 x 148 SMs
+
+__global__ void __launch_bounds__(256) k_reduce_maps(int64_t hw, const double* __restrict__ maps,
+                                                     MaxMin* __restrict__ partial) {
+    int m = blockIdx.y;
+    const double* p = maps + (size_t)m * hw;
+    MaxMin acc{-INFINITY, INT64_MAX, INFINITY};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double v = p[i];
+        MaxMin x{v, i, v};
+        acc = mm_combine(acc, x);
+    }
+    typedef cub::BlockReduce<MaxMin, 256> Red;
+    __shared__ typename Red::TempStorage tmp;
+    struct Op {
+        __device__ MaxMin operator()(const MaxMin& a, const MaxMin& b) const { return mm_combine(a, b); }
+    };
+    MaxMin r = Red(tmp).Reduce(acc, Op());
+    if (threadIdx.x == 0) partial[(size_t)m * gridDim.x + blockIdx.x] = r;
+}
+
+__global__ void k_finalize_select(int n_maps, int nblk, int W, const MaxMin* __restrict__ partial,
+                                  int fixed_level, int64_t* stats_i64, double* stats_f64) {
+    __shared__ MaxMin per_map[32];
+    if (threadIdx.x < n_maps) {
+        MaxMin acc{-INFINITY, INT64_MAX, INFINITY};
+        for (int b = 0; b < nblk; ++b) acc = mm_combine(acc, partial[(size_t)threadIdx.x * nblk + b]);
+        per_map[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int lvl = fixed_level;
+        if (lvl < 0) {
+            lvl = 0;
+            for (int m = 1; m < n_maps; ++m)
+                if (per_map[m].mx > per_map[lvl].mx) lvl = m;  // ties -> lowest level
+        }
+        MaxMin c = per_map[lvl];
+        stats_i64[SF_STAT_LEVEL] = lvl;
+        stats_i64[SF_STAT_ROW] = c.idx / W;
+        stats_i64[SF_STAT_COL] = c.idx % W;
+        stats_i64[SF_STAT_DEGENERATE] = (c.mx <= c.mn) ? 1 : 0;
+        stats_f64[SF_STATF_MIN] = c.mn;
+        stats_f64[SF_STATF_MAX] = c.mx;
+        for (int m = 0; m < n_maps; ++m) stats_f64[SF_STATF_LEVEL_MAX + m] = per_map[m].mx;
+    }
+}
+
+__global__ void k_mask(int64_t hw, const double* __restrict__ maps, const int64_t* __restrict__ stats_i64,
+                       const double* __restrict__ stats_f64, double threshold, uint8_t* __restrict__ mask) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hw) return;
+    int lvl = (int)stats_i64[SF_STAT_LEVEL];
+    double lo = stats_f64[SF_STATF_MIN], hi = stats_f64[SF_STATF_MAX];
+    uint8_t v = 0;
+    if (!(hi <= lo)) v = ((maps[(size_t)lvl * hw + i] - lo) / (hi - lo)) > threshold;
+    mask[i] = v;
+}
+
+size_t select_segment_ws_bytes(int n_maps, int H, int W) {
+    return sizeof(MaxMin) * (size_t)kRedBlocks * (size_t)n_maps + 256;
+}
+
+void launch_select_segment(int n_maps, int H, int W, const double* maps, int fixed_level,
+                           double threshold, uint8_t* mask, int64_t* stats_i64, double* stats_f64,
+                           void* ws, cudaStream_t st) {
+    int64_t hw = (int64_t)H * W;
+    MaxMin* partial = (MaxMin*)ws;
+    k_reduce_maps<<<dim3(kRedBlocks, n_maps), 256, 0, st>>>(hw, maps, partial);
+    k_finalize_select<<<1, 32, 0, st>>>(n_maps, kRedBlocks, W, partial, fixed_level, stats_i64,
+                                        stats_f64);
+    if (mask) k_mask<<<ceil_div(hw, 256), 256, 0, st>>>(hw, maps, stats_i64, stats_f64, threshold, mask);
+}
+
+}  // namespace sf

@@ -1,0 +1,265 @@
+"""Device plumbing: resident scenes, workspaces and the per-frame launcher.
+
+PyTorch is used only for device memory, streams and copies.  All compute
+is the native library (``_native``); this module marshals pointers into the
+C structs of include/splatfield_b200.h.
+
+* ``DeviceScene`` -- the scene uploaded once to HBM in id order (the
+  canonical order tie-break of projection.py:396 then reduces to a stable
+  depth sort).  Cached per scene object (scenes are immutable by contract).
+* ``FrameEngine`` -- owns the per-shape workspace (grown on pair-buffer
+  overflow) and launches ``sf_render_frame`` on the current torch stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import SplatfieldError, ValidationError
+
+try:
+    import torch
+except ImportError as exc:  # pragma: no cover
+    raise SplatfieldError("PyTorch is required for device memory management") from exc
+
+
+def require_cuda() -> "torch.device":
+    if not torch.cuda.is_available():
+        raise SplatfieldError("a CUDA device is required: the sm_100a path has no CPU fallback")
+    N.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def camera_struct(cam) -> N.SfCamera:
+    c = N.SfCamera()
+    R = np.ascontiguousarray(np.asarray(cam.rotation, dtype=np.float64)).reshape(9)
+    t = np.asarray(cam.translation, dtype=np.float64).reshape(3)
+    for i in range(9):
+        c.R[i] = float(R[i])
+    for i in range(3):
+        c.t[i] = float(t[i])
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    c.near_plane = float(getattr(cam, "near", 0.01))
+    c.width, c.height = int(cam.width), int(cam.height)
+    return c
+
+
+def _dev(a: np.ndarray, device, dtype=None) -> "torch.Tensor":
+    a = np.ascontiguousarray(a if dtype is None else a.astype(dtype, copy=False))
+    return torch.from_numpy(a).to(device, non_blocking=False)
+
+
+class DeviceScene:
+    """A scene resident on the GPU, rows ordered by id (SfScene)."""
+
+    def __init__(self, scene, device=None):
+        device = device or require_cuda()
+        cfg = scene.config
+        g = int(np.asarray(scene.positions).shape[0])
+        ids = np.asarray(scene.ids, dtype=np.int64).reshape(g)
+        if g > 1 and np.any(ids[1:] < ids[:-1]):
+            perm = np.argsort(ids, kind="stable")
+        else:
+            perm = None
+        sel = (lambda a: a) if perm is None else (lambda a: a[perm])
+        ci = np.asarray(scene.coeff_indices, dtype=np.uint16).reshape(cfg.num_levels, g, cfg.K)
+        cv = np.asarray(scene.coeff_values, dtype=np.float32).reshape(cfg.num_levels, g, cfg.K)
+        if perm is not None:
+            ci, cv = ci[:, perm], cv[:, perm]
+        self.device = device
+        self.num_gaussians = g
+        self.config = cfg
+        self.bad_index = bool(g and np.any(ci >= cfg.L))
+        self.positions = _dev(sel(np.asarray(scene.positions)).reshape(g, 3), device, np.float32)
+        self.rotations = _dev(sel(np.asarray(scene.rotations)).reshape(g, 4), device, np.float32)
+        self.scales = _dev(sel(np.asarray(scene.scales)).reshape(g, 3), device, np.float32)
+        self.opacities = _dev(sel(np.asarray(scene.opacities)).reshape(g), device, np.float32)
+        self.coeff_indices = _dev(np.ascontiguousarray(ci).view(np.int16), device)
+        self.coeff_values = _dev(cv, device)
+        self.ids = _dev(sel(ids), device)
+        self.orig_rows = None if perm is None else _dev(perm.astype(np.int64), device)
+        atoms = np.stack([np.asarray(cb.atoms, dtype=np.float32) for cb in scene.codebooks]) \
+            if len(scene.codebooks) else np.zeros((0, cfg.L, cfg.D), np.float32)
+        self.codebooks = _dev(atoms, device)
+        self.struct = N.SfScene(
+            g, cfg.num_levels, cfg.L, cfg.K, cfg.D,
+            N.ptr(self.positions), N.ptr(self.rotations), N.ptr(self.scales), N.ptr(self.opacities),
+            N.ptr(self.coeff_indices), N.ptr(self.coeff_values), N.ptr(self.ids), N.ptr(self.codebooks))
+        self._engine = None
+        self._lock = threading.Lock()
+
+    @property
+    def engine(self) -> "FrameEngine":
+        if self._engine is None:
+            self._engine = FrameEngine(self)
+        return self._engine
+
+
+_scene_cache: dict = {}
+_cache_lock = threading.Lock()
+
+
+def device_scene(scene) -> DeviceScene:
+    """Upload ``scene`` once and return its cached device copy."""
+    if isinstance(scene, DeviceScene):
+        return scene
+    key = id(scene)
+    with _cache_lock:
+        hit = _scene_cache.get(key)
+        if hit is not None and hit[0]() is scene:
+            return hit[1]
+    ds = DeviceScene(scene)
+    with _cache_lock:
+        try:
+            ref = weakref.ref(scene, lambda _r, k=key: _scene_cache.pop(k, None))
+        except TypeError:  # not weak-referenceable: cache without eviction hook
+            ref = (lambda s=scene: s)
+        _scene_cache[key] = (ref, ds)
+    return ds
+
+
+@dataclass
+class QuerySpec:
+    vector: np.ndarray          # (D,) float64
+    canonicals: np.ndarray      # (n, D) float64
+    window: int = 11
+    fixed_level: int = -1       # block index or -1
+    threshold: float = 0.5
+
+
+@dataclass
+class FrameOutputs:
+    """Device tensors of one frame (views valid until the next run with reuse)."""
+
+    width: int
+    height: int
+    levels: tuple
+    coeff_map: "torch.Tensor | None"
+    final_t: "torch.Tensor | None"
+    features: "torch.Tensor | None"
+    relevancy_raw: "torch.Tensor | None"
+    relevancy_filtered: "torch.Tensor | None"
+    mask: "torch.Tensor | None"
+    stats_i64: "torch.Tensor"
+    stats_f64: "torch.Tensor"
+    events: tuple | None = None
+
+    def host_stats(self):
+        return self.stats_i64.cpu().numpy(), self.stats_f64.cpu().numpy()
+
+    def stage_ms(self):
+        if not self.events:
+            return None
+        lib = N.load()
+        e = self.events
+        return (lib.sf_event_elapsed_ms(e[0], e[1]), lib.sf_event_elapsed_ms(e[1], e[2]),
+                lib.sf_event_elapsed_ms(e[2], e[3]))
+
+
+class FrameEngine:
+    """Launches frames of one DeviceScene; owns a growable workspace."""
+
+    def __init__(self, dscene: DeviceScene):
+        self.ds = dscene
+        g = dscene.num_gaussians
+        self.pair_capacity = max(1 << 16, 6 * g)
+        self._ws = None
+        self._ws_key = None
+        self._lock = threading.Lock()
+        self._events = None
+
+    def workspace(self, W: int, H: int, n_levels: int) -> "torch.Tensor":
+        cfg = self.ds.config
+        key = (W, H, n_levels, self.pair_capacity)
+        if self._ws is None or self._ws_key != key:
+            nbytes = ctypes.c_size_t(0)
+            N.check(N.load().sf_frame_workspace_bytes(self.ds.num_gaussians, W, H, n_levels, cfg.L,
+                                                      cfg.K, self.pair_capacity, ctypes.byref(nbytes)))
+            if self._ws is None or self._ws.numel() < nbytes.value:
+                self._ws = None
+                self._ws = torch.empty(nbytes.value, dtype=torch.uint8, device=self.ds.device)
+            self._ws_key = key
+        return self._ws
+
+    def allocate(self, W, H, levels, *, coeff_map=True, final_t=False, features=False,
+                 query=False, mask=True) -> FrameOutputs:
+        cfg = self.ds.config
+        dev = self.ds.device
+        nl = len(levels)
+        f32, f64 = torch.float32, torch.float64
+        return FrameOutputs(
+            W, H, tuple(levels),
+            torch.empty((H, W, nl * cfg.L), dtype=f32, device=dev) if coeff_map else None,
+            torch.empty((H, W), dtype=f32, device=dev) if final_t else None,
+            torch.empty((nl, H, W, cfg.D), dtype=f32, device=dev) if features else None,
+            torch.empty((nl, H, W), dtype=f64, device=dev) if query else None,
+            torch.empty((nl, H, W), dtype=f64, device=dev) if query else None,
+            torch.empty((H, W), dtype=torch.uint8, device=dev) if (query and mask) else None,
+            torch.zeros(16, dtype=torch.int64, device=dev),
+            torch.zeros(8 + 8, dtype=torch.float64, device=dev),
+        )
+
+    def enqueue(self, cam, levels, out: FrameOutputs, *, query: QuerySpec | None = None,
+                early_exit: bool = True, qdev=None, timing: bool = False):
+        """Launch one frame on the current stream (no host synchronisation)."""
+        cfg = self.ds.config
+        camc = camera_struct(cam)
+        W, H = camc.width, camc.height
+        lv = (ctypes.c_int32 * len(levels))(*[int(x) for x in levels])
+        ws = self.workspace(W, H, len(levels))
+        fr = N.SfFrame()
+        fr.host_levels = ctypes.cast(lv, ctypes.c_void_p)
+        fr.n_levels = len(levels)
+        fr.early_exit = 1 if early_exit else 0
+        fr.pair_capacity = self.pair_capacity
+        fr.coeff_map = N.ptr(out.coeff_map)
+        fr.final_t = N.ptr(out.final_t)
+        fr.features = N.ptr(out.features)
+        fr.relevancy_raw = N.ptr(out.relevancy_raw)
+        fr.relevancy_filtered = N.ptr(out.relevancy_filtered)
+        fr.mask = N.ptr(out.mask)
+        fr.stats_i64 = N.ptr(out.stats_i64)
+        fr.stats_f64 = N.ptr(out.stats_f64)
+        if timing:
+            if self._events is None:
+                lib = N.load()
+                self._events = tuple(lib.sf_event_create() for _ in range(4))
+            for i in range(4):
+                fr.events[i] = self._events[i]
+            out.events = self._events
+        qs = None
+        keep = None
+        if query is not None:
+            if qdev is None:
+                qdev = (torch.from_numpy(np.ascontiguousarray(query.vector, dtype=np.float64)).to(self.ds.device),
+                        torch.from_numpy(np.ascontiguousarray(query.canonicals, dtype=np.float64)).to(self.ds.device))
+            keep = qdev
+            qs = N.SfQuery(N.ptr(qdev[0]), N.ptr(qdev[1]), int(query.canonicals.shape[0]),
+                           int(query.window), int(query.fixed_level), float(query.threshold))
+        rc = N.load().sf_render_frame(ctypes.byref(self.ds.struct), ctypes.byref(camc),
+                                      ctypes.byref(qs) if qs is not None else None, ctypes.byref(fr),
+                                      N.ptr(ws), ws.numel(), stream_ptr())
+        N.check(rc)
+        return keep
+
+    def run(self, cam, levels, out: FrameOutputs, **kw) -> FrameOutputs:
+        """Launch and synchronise; grows the pair buffer and re-runs on overflow."""
+        with self._lock:
+            for _ in range(4):
+                keep = self.enqueue(cam, levels, out, **kw)
+                st = out.stats_i64.cpu()
+                del keep
+                if int(st[N.STAT_OVERFLOW]) == 0:
+                    return out
+                self.pair_capacity = int(int(st[N.STAT_PAIRS]) * 1.25) + 1024
+            raise SplatfieldError("pair buffer overflow persisted after growing")

@@ -1,0 +1,238 @@
+"""Parity of the sm_100a path against the reference (golden fixtures) and the oracle.
+
+Tolerances:
+  * projection (means2d, inv_covs, depths, opacities, ids, rows): bitwise
+  * binning (per-tile source-id lists, offsets, canonical_bytes): bitwise
+  * coefficient map: max |dW| <= 2e-6 absolute (fp32 accumulation of fp64
+    weights; the reference values are in [0, 1]); final T <= 1e-6
+  * features: max |dF| <= 2e-5 * max |F_ref| per level (3xTF32 tensor cores)
+  * relevancy (raw and filtered): max abs <= 1e-5
+  * level, point, mask: identical
+"""
+
+import numpy as np
+import pytest
+
+import paper_2507_07136_b200 as sf
+from conftest import golden_names, load_golden, make_camera, random_scene
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+W_TOL = 2e-6
+T_TOL = 1e-6
+F_REL = 2e-5
+R_TOL = 1e-5
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_projection_bitwise_vs_reference(name):
+    scene, cam, z = load_golden(name)
+    p = sf.project_scene(scene, cam)
+    assert p.count == z["p_means2d"].shape[0]
+    for f in ("means2d", "inv_covs", "depths", "opacities", "source_ids", "rows"):
+        assert getattr(p, f).tobytes() == z["p_" + f].tobytes(), f
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_binning_bytes_vs_reference(name):
+    scene, cam, z = load_golden(name)
+    b = sf.bin_projected(sf.project_scene(scene, cam), cam)
+    np.testing.assert_array_equal(b.tile_offsets, z["b_offsets"])
+    assert b.canonical_bytes() == z["b_canonical_bytes"].tobytes()
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_splat_vs_reference(name):
+    scene, cam, z = load_golden(name)
+    cmap, st = sf.splat_multilevel(scene, cam, with_stats=True)
+    assert cmap.data.shape == z["cmap"].shape
+    assert np.abs(cmap.data - z["cmap"]).max(initial=0) <= W_TOL
+    assert np.abs(st.final_transmittance - z["final_t"]).max(initial=0) <= T_TOL
+    assert st.pairs_blended == int(z["pairs"])
+    assert st.channels_per_gaussian == int(z["channels"])
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_decode_vs_reference(name):
+    scene, cam, z = load_golden(name)
+    fms = sf.decode(sf.splat_multilevel(scene, cam), scene.codebooks)
+    for b in range(len(fms.maps)):
+        ref = z["features"][b]
+        scale = max(np.abs(ref).max(initial=0), 1e-30)
+        assert np.abs(fms.maps[b] - ref).max(initial=0) <= F_REL * scale + 1e-7
+
+
+@pytest.mark.parametrize("name", golden_names(require_query=True))
+def test_query_pipeline_vs_reference(name):
+    scene, cam, z = load_golden(name)
+    q = sf.QueryEmbedding("q", z["q_vector"])
+    res = sf.query_pipeline(scene, cam, q, z["q_canon"], window=int(z["q_window"]))
+    for b, m in enumerate(res.level_maps):
+        assert np.abs(m.data - z["q_filtered"][b]).max(initial=0) <= R_TOL
+    assert res.level == int(z["q_level"])
+    assert res.point == tuple(int(v) for v in z["q_point"])
+    seg = sf.segment(res.chosen)
+    assert seg.degenerate == bool(z["q_degenerate"])
+    np.testing.assert_array_equal(seg.mask, z["q_mask"])
+    np.testing.assert_array_equal(res.mask, z["q_mask"])
+    # the lazily decoded features are the same as an explicit decode
+    assert np.abs(res.feature_maps.maps[0] - z["features"][0]).max(initial=0) <= \
+        F_REL * max(np.abs(z["features"][0]).max(initial=0), 1e-30) + 1e-7
+
+
+@pytest.mark.parametrize("name", golden_names(require_query=True))
+def test_relevancy_ops_vs_reference(name):
+    scene, cam, z = load_golden(name)
+    q = sf.QueryEmbedding("q", z["q_vector"])
+    maps = []
+    for b in range(z["features"].shape[0]):
+        raw = sf.relevancy_map(z["features"][b], q, z["q_canon"], level=b)
+        assert np.abs(raw.data - z["q_raw"][b]).max(initial=0) <= 1e-12
+        filt = sf.mean_filter(raw, int(z["q_window"]))
+        assert np.abs(filt.data - z["q_filtered"][b]).max(initial=0) <= 1e-12
+        maps.append(filt)
+    if scene.num_gaussians:
+        lv, chosen = sf.select_level(maps)
+        assert lv == int(z["q_level"])
+        assert sf.localize(chosen) == tuple(int(v) for v in z["q_point"])
+
+
+def test_config_a_full_path():
+    """SURVEY 8(d) config A (10k G, 256x256, 3 levels, L=64, K=4, D=512)."""
+    import os
+    from conftest import GOLDEN
+    from paper_2507_07136_b200 import synthetic
+    z = np.load(os.path.join(GOLDEN, "configA_binning.npz"))
+    scene = synthetic.make_scene(10_000)
+    cam = synthetic.make_camera(256, 256)
+    p = sf.project_scene(scene, cam)
+    assert p.means2d.tobytes() == z["p_means2d"].tobytes()
+    assert p.inv_covs.tobytes() == z["p_inv_covs"].tobytes()
+    assert p.depths.tobytes() == z["p_depths"].tobytes()
+    b = sf.bin_projected(p, cam)
+    np.testing.assert_array_equal(b.tile_offsets, z["b_offsets"])
+    np.testing.assert_array_equal(b.projected.source_ids[b.tile_entries], z["b_source_ids"])
+    cmap, st = sf.splat_multilevel(scene, cam, with_stats=True)
+    assert st.pairs_blended == 175_770
+    assert np.abs(cmap.data[[5, 130]] - z["cmap_rows"]).max() <= W_TOL
+    assert np.abs(st.final_transmittance[::8] - z["final_t"]).max() <= 1e-6
+    # decode + query against the oracle (fp64) on the same inputs
+    ocm = O.splat_multilevel(scene, cam)
+    qv, canon = synthetic.make_query()
+    fms = sf.decode(cmap, scene.codebooks)
+    for lv in range(3):
+        ref = O.decode_level(ocm.level_view(lv), scene.codebooks[lv].atoms)
+        assert np.abs(fms.maps[lv] - ref).max() <= F_REL * np.abs(ref).max()
+    res = sf.query_pipeline(scene, cam, sf.QueryEmbedding("q", qv), canon)
+    ores = O.query_pipeline(scene, cam, qv, canon, window=11, keep_features=False)
+    for lv in range(3):
+        assert np.abs(res.level_maps[lv].data - ores.level_maps[lv]).max() <= R_TOL
+    assert res.level == ores.level
+    assert res.point == ores.point
+    np.testing.assert_array_equal(res.mask, O.segment(ores.level_maps[ores.level])[0])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_random_scenes_vs_oracle(seed):
+    rng = np.random.default_rng(seed)
+    scene = random_scene(rng, num_gaussians=4000, num_levels=3, L=32, K=4, D=64)
+    cam = make_camera(width=123, height=77)
+    b = sf.bin_projected(sf.project_scene(scene, cam), cam)
+    ob = O.bin_projected(O.project_scene(scene, cam), cam)
+    assert b.canonical_bytes() == ob.canonical_bytes()
+    cm, st = sf.splat_multilevel(scene, cam, with_stats=True)
+    ocm, ost = O.splat_multilevel(scene, cam, binning=ob, with_stats=True)
+    assert np.abs(cm.data - ocm.data).max() <= W_TOL
+    assert st.pairs_blended == ost.pairs_blended
+
+
+def test_permutation_invariance_byte_exact(rng):
+    scene = random_scene(rng, num_gaussians=500, num_levels=2)
+    cam = make_camera(48, 40)
+    base = sf.splat_multilevel(scene, cam).data
+    for _ in range(2):
+        again = sf.splat_multilevel(scene.permuted(rng.permutation(500)), cam).data
+        assert base.tobytes() == again.tobytes()
+
+
+def test_fused_equals_per_level_byte_exact(rng):
+    scene = random_scene(rng, num_gaussians=300, num_levels=3, L=16, K=4)
+    cam = make_camera()
+    fused = sf.splat_multilevel(scene, cam)
+    for lv in range(3):
+        single = sf.splat_sparse(scene, cam, lv)
+        assert fused.level_view(lv).tobytes() == single.level_view(lv).tobytes()
+
+
+def test_k_equals_l_and_one_hot(rng):
+    scene = random_scene(rng, num_gaussians=200, num_levels=1, L=8, K=8)
+    cam = make_camera()
+    ocm = O.splat_multilevel(scene, cam)
+    assert np.abs(sf.splat_multilevel(scene, cam).data - ocm.data).max() <= W_TOL
+
+
+def test_wide_channel_blocks_match(rng):
+    """L=256, 1 level -> the accumulator is split over two channel blocks."""
+    scene = random_scene(rng, num_gaussians=300, num_levels=1, L=256, K=4, D=16)
+    cam = make_camera(40, 36)
+    ocm = O.splat_multilevel(scene, cam)
+    cm = sf.splat_multilevel(scene, cam)
+    assert np.abs(cm.data - ocm.data).max() <= W_TOL
+
+
+def test_per_level_mass_equals_blended_opacity(rng):
+    scene = random_scene(rng, num_gaussians=600, num_levels=2, L=16, K=4)
+    cmap, stats = sf.splat_multilevel(scene, make_camera(), with_stats=True)
+    for lv in range(2):
+        np.testing.assert_allclose(cmap.level_view(lv).sum(axis=2), 1.0 - stats.final_transmittance,
+                                   atol=1e-5)
+
+
+def test_errors_raised_before_work(rng):
+    scene = random_scene(rng, num_gaussians=5, L=16, K=2)
+    bad = scene.permuted(np.arange(5))
+    bad.coeff_indices = bad.coeff_indices.copy()
+    bad.coeff_indices[0, 0, -1] = 40
+    with pytest.raises(sf.ValidationError):
+        sf.splat_sparse(bad, make_camera(), 0)
+    with pytest.raises(sf.ValidationError):
+        sf.splat_sparse(scene, make_camera(), 3)
+    with pytest.raises(sf.ResourceLimitError):
+        sf.splat_multilevel(scene, make_camera(), max_elements=100)
+    with pytest.raises(sf.ValidationError):
+        sf.splat_multilevel(scene, make_camera(), tile_size=8)
+    q = sf.QueryEmbedding("q", np.ones(8))
+    with pytest.raises(sf.ValidationError):
+        sf.query_pipeline(scene, make_camera(), q, np.zeros((0, 8)))
+    with pytest.raises(sf.ValidationError):
+        sf.query_pipeline(scene, make_camera(), q, np.zeros((2, 8)), window=4)
+    with pytest.raises(sf.ValidationError):
+        sf.query_pipeline(scene, make_camera(), q, np.zeros((2, 8)), level=2)
+
+
+def test_empty_scene(rng):
+    scene = random_scene(rng, num_gaussians=0)
+    cmap = sf.splat_multilevel(scene, make_camera())
+    assert not cmap.data.any()
+    b = sf.bin_projected(sf.project_scene(scene, make_camera()), make_camera())
+    assert all(lst.size == 0 for lst in b.tile_lists)
+
+
+def test_tensor_core_decode_matches_simt_crosscheck(rng):
+    """tcgen05 3xTF32 decode vs the plain fp32 FMA-chain kernel, on a map with ragged M."""
+    import torch
+    from paper_2507_07136_b200 import _native as N
+    from paper_2507_07136_b200.device import stream_ptr
+    dev = torch.device("cuda")
+    P, L, D = 128 * 37 + 5, 64, 512
+    w = torch.from_numpy(rng.random((P, 3 * L)).astype(np.float32) / 8).to(dev)
+    cb = torch.from_numpy(rng.standard_normal((L, D)).astype(np.float32)).to(dev)
+    a = torch.empty((P, D), dtype=torch.float32, device=dev)
+    s = torch.empty_like(a)
+    lib = N.load()
+    N.check(lib.sf_decode(P, L, D, N.ptr(w[:, L:]), 3 * L, N.ptr(cb), N.ptr(a), stream_ptr()))
+    N.check(lib.sf_decode_simt(P, L, D, N.ptr(w[:, L:]), 3 * L, N.ptr(cb), N.ptr(s), stream_ptr()))
+    ref = w[:, L:2 * L].double() @ cb.double()
+    assert (a.double() - ref).abs().max().item() <= F_REL * ref.abs().max().item()
+    assert (s.double() - ref).abs().max().item() <= F_REL * ref.abs().max().item()
