@@ -1,0 +1,366 @@
+"""Benchmark: text-query FPS (and feature-splat FPS) at 1440x1080 with 2M Gaussians.
+
+One step = one full query frame of config C (BASELINE.json
+configs[2]): preprocess -> depth-rank sort -> binning -> blend (+ fused
+projected-codebook relevancy) -> 3 x 512-d feature decode written to HBM
+(3xTF32 tcgen05) -> mean filter -> select_level / localize / segment.  That
+is the reference's query_pipeline (sparse_splat.py:243-297) plus segment,
+with every feature map materialised, so the same step also bounds
+feature-splat FPS (render + decode).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Multi-GPU (torchrun): one rank per GPU renders its own frames of the scene
+(view sharding, config D; weak scaling); the only collective is an NCCL
+all-gather of each frame's final mask to every rank (the "gather the final
+maps" step).  Timing: CUDA events on the launching stream between a barrier
++ synchronize on both sides; max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "feature-splat FPS and text-query FPS at 1440×1080, ~2M Gaussians, 1/2/4/8 B200"
+CONFIGS = {
+    "A": (10_000, 256, 256),
+    "B": (1_000_000, 988, 731),
+    "C": (2_000_000, 1440, 1080),
+    "E": (5_000_000, 1920, 1080),
+}
+# Kernels launched per query frame (sf_render_frame), from the ncu launch list in
+# profiles/r01_launches.csv: preprocess, CUB onesweep depth sort (9), rank gather,
+# count, tile scan, emit, tile sort, project codebook, blend, 3 x (codebook split
+# + tcgen05 decode), 2 x box filter, reduce, finalize, mask.
+KERNELS_PER_FRAME = 29
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        return world, rank, local, dist
+    return 1, 0, 0, None
+
+
+def cpu_baseline_run(scene, cam, qv, canon, band_rows: int = 2):
+    """Oracle (C port, OpenMP) on a bounded sample: full projection + binning,
+    blend + decode + relevancy of `band_rows` tile rows.  Returns (fps, info)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    proj = O.project_scene(scene, cam)
+    binning = O.bin_projected(proj, cam)
+    t1 = time.perf_counter()
+    tiles_x = binning.tiles_x
+    rows = min(band_rows, binning.tiles_y)
+    cm = O.splat_levels(scene, cam, range(scene.config.num_levels), binning=binning,
+                        tile_range=(0, rows * tiles_x))
+    hb = min(rows * 16, cam.height)
+    for lv in range(scene.config.num_levels):
+        f = O.decode_level(cm.level_view(lv)[:hb], scene.codebooks[lv].atoms)
+        O.relevancy_map(f, qv, canon)
+        del f
+    t2 = time.perf_counter()
+    frac = hb / cam.height
+    frame_s = (t1 - t0) + (t2 - t1) / frac
+    info = {"projection_binning_s": round(t1 - t0, 3), "band_s": round(t2 - t1, 3),
+            "band_fraction": round(frac, 5)}
+    return 1.0 / frame_s, info, frame_s
+
+
+def run_reference(args, scene, cam, qv, canon):
+    """--impl reference: the CPU oracle port, rank 0 only."""
+    from oracle import oracle as O
+    ncores = O.num_threads()
+    samples = []
+    for i in range(args.warmup + args.steps):
+        fps, info, _ = cpu_baseline_run(scene, cam, qv, canon, band_rows=args.band_rows)
+        if i >= args.warmup:
+            samples.append(fps)
+    fps = statistics.median(samples)
+    n, w, h = CONFIGS[args.config]
+    sample = (f"config {args.config}: full projection+binning of {n} Gaussians + blend/decode/"
+              f"relevancy of {args.band_rows} tile rows ({info['band_fraction']*100:.2f}% of the "
+              f"frame), extrapolated to the frame; median of {args.steps}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / fps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY 8(d) generator, seed 1)",
+        "config": {"workload": f"config {args.config}: {n} Gaussians, {w}x{h}, L=64, K=4, 3 levels, "
+                               f"D=512, 1 text query + 4 canonicals", "parallelism": "cpu"},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": ncores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": info,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C", choices=sorted(CONFIGS))
+    ap.add_argument("--band-rows", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local, dist = dist_setup(args.gpus)
+    from paper_2507_07136_b200 import synthetic
+    n_g, W, H = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        scene = synthetic.make_scene(n_g)
+        cam = synthetic.make_camera(W, H)
+        qv, canon = synthetic.make_query()
+        run_reference(args, scene, cam, qv, canon)
+        return
+
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    if dist is not None:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2507_07136_b200 as sf
+    from paper_2507_07136_b200 import _native as N
+    from paper_2507_07136_b200.device import QuerySpec, device_scene
+
+    scene = synthetic.make_scene(n_g)
+    cam = synthetic.make_camera(W, H)
+    qv, canon = synthetic.make_query()
+    ds = device_scene(scene)
+    eng = ds.engine
+    levels = (0, 1, 2)
+    spec = QuerySpec(qv, canon, 11, -1, 0.5)
+    out = eng.allocate(W, H, levels, coeff_map=True, features=True, query=True)
+    qdev = (torch.from_numpy(qv).cuda(), torch.from_numpy(canon).cuda())
+    eng.run(cam, levels, out, query=spec, qdev=qdev)  # sizes the pair buffer
+    stream = torch.cuda.current_stream()
+    gathered = None
+    if dist is not None:
+        gathered = torch.empty((world, H, W), dtype=torch.uint8, device="cuda")
+
+    def step(timing=False):
+        eng.enqueue(cam, levels, out, query=spec, qdev=qdev, timing=timing)
+        if dist is not None:
+            dist.all_gather_into_tensor(gathered, out.mask)
+
+    for _ in range(args.warmup):
+        step()
+    # per-stage kernel times (render / decode / post) over a few frames
+    stage = []
+    for _ in range(3):
+        step(timing=True)
+        stage.append(out.stage_ms())
+    torch.cuda.synchronize()
+    st = out.stats_i64.cpu().numpy()
+    assert st[N.STAT_OVERFLOW] == 0
+
+    # ---- timed region: K frames ----
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    fps_total = world * args.steps / (ms / 1e3)
+
+    # decode-stage (dominant kernel) roofline, measured live with CUDA events
+    r_ms = statistics.median(s[0] for s in stage)
+    d_ms = statistics.median(s[1] for s in stage)
+    p_ms = statistics.median(s[2] for s in stage)
+    P = W * H
+    dec_bytes = 3 * P * 512 * 4 + P * 192 * 4 + 3 * 64 * 512 * 4  # F written + W read + codebooks
+    hbm_peak, peak_kind = peaks()
+    achieved = dec_bytes / (d_ms / 1e3) / 1e9
+
+    # feature-splat FPS (render + decode, no query post) and lazy-feature query FPS
+    out_f = eng.allocate(W, H, levels, coeff_map=True, features=True, query=False)
+    out_q = eng.allocate(W, H, levels, coeff_map=False, features=False, query=True)
+    extra = {}
+    for name, o, q in (("feature_splat", out_f, None), ("text_query_lazy_features", out_q, spec)):
+        for _ in range(3):
+            eng.enqueue(cam, levels, o, query=q, qdev=qdev)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            eng.enqueue(cam, levels, o, query=q, qdev=qdev)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        extra[name] = args.steps / (ev0.elapsed_time(ev1) / 1e3)
+    del out_f, out_q
+
+    # ---- e2e through the public API: query_pipeline with host query inputs ----
+    e2e = None
+    if not args.no_e2e:
+        qe = sf.QueryEmbedding("bench", qv)
+        canon_pinned = torch.from_numpy(canon).pin_memory().numpy()
+        for _ in range(2):
+            sf.query_pipeline(scene, cam, qe, canon_pinned, features="eager", instrument=False,
+                              max_elements=1 << 40)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        n_e2e = max(3, args.steps // 2)
+        for _ in range(n_e2e):
+            res = sf.query_pipeline(scene, cam, qe, canon_pinned, features="eager", instrument=False,
+                                    max_elements=1 << 40)
+            _ = res.mask  # already on the host: the step's result
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": world * n_e2e / dt, "unit": "frames/s",
+               "h2d_bytes_per_step": int(qv.nbytes + canon.nbytes),
+               "d2h_bytes_per_step": int(H * W + 16 * 8 + 16 * 8), "steps": n_e2e,
+               "api": "paper_2507_07136_b200.query_pipeline(..., features='eager')"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        fps_cpu, info, _ = cpu_baseline_run(scene, cam, qv, canon, band_rows=args.band_rows)
+        cpu = {"value": fps_cpu, "unit": "frames/s", "cores": O.num_threads(), "kind": "port",
+               "sample": (f"oracle C port (OpenMP): full projection+binning of {n_g} Gaussians + "
+                          f"blend/decode/relevancy of {args.band_rows} tile rows "
+                          f"({info['band_fraction']*100:.2f}% of the frame), extrapolated"),
+               "detail": info}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": fps_total, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (SURVEY 8(d) generator, seed 1; random codebooks/query)",
+            "config": {
+                "workload": (f"config {args.config}: {n_g} Gaussians, {W}x{H}, 3 levels, L=64, K=4, "
+                             "D=512 features decoded (3xTF32) + 1 text query vs 4 canonicals, "
+                             "window 11, level select + localize + segment"),
+                "parallelism": f"views x{world}" if world > 1 else "single",
+                "l2": "inputs/outputs larger than L2 (9.56 GB of features per frame)",
+                "visible": int(st[N.STAT_VISIBLE]), "pairs": int(st[N.STAT_PAIRS]),
+            },
+            "fps": {"text_query_full": fps_total / world,
+                    "feature_splat": extra["feature_splat"],
+                    "text_query_lazy_features": extra["text_query_lazy_features"]},
+            "stage_ms": {"render": r_ms, "decode": d_ms, "post": p_ms},
+            "roofline": {"bound": "hbm", "kernel": "k_decode_tc (3 levels, one frame)",
+                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "peak_kind": peak_kind,
+                         "algorithmic_bytes": dec_bytes, "traffic": None},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": KERNELS_PER_FRAME * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -109,8 +109,8 @@ typedef struct SfFrame {
 
 /* Scratch needed by sf_render_frame for this scene/frame shape. */
 int sf_frame_workspace_bytes(int64_t num_gaussians, int32_t width, int32_t height,
-                             int32_t n_levels, int32_t L, int32_t K, int64_t pair_capacity,
-                             size_t* bytes);
+                             int32_t n_levels, int32_t L, int32_t K, int32_t D,
+                             int64_t pair_capacity, size_t* bytes);
 
 /*
  * One full frame: preprocess -> depth-rank sort -> tile binning -> blend
@@ -154,9 +154,12 @@ int sf_bin(int64_t n, const double* means2d, const double* inv_covs, const doubl
            void* workspace, size_t workspace_bytes, void* stream);
 
 /* decode, sparse_splat.py:183-199: one level block, (P,L) @ (L,D) -> (P,D) fp32,
- * 3xTF32 on tcgen05 tensor cores.  w has row stride w_stride floats. */
+ * 3xTF32 on tcgen05 tensor cores (L in {32,64}, D % 256 == 0; other shapes
+ * use the SIMT kernel).  w has row stride w_stride floats. */
+size_t sf_decode_workspace_bytes(int32_t L, int32_t D);
 int sf_decode(int64_t n_pixels, int32_t L, int32_t D, const float* w, int64_t w_stride,
-              const float* codebook, float* out, void* stream);
+              const float* codebook, float* out, void* workspace, size_t workspace_bytes,
+              void* stream);
 /* Plain fp32 FMA-chain decode on CUDA cores: the independent cross-check the
  * parity tests hold the tensor-core kernel against (not used by any frame). */
 int sf_decode_simt(int64_t n_pixels, int32_t L, int32_t D, const float* w, int64_t w_stride,

@@ -51,7 +51,7 @@ class SfFrame(ctypes.Structure):
 
 
 EXPORTS = {
-    "sf_frame_workspace_bytes": (ctypes.c_int, [i64, i32, i32, i32, i32, i32, i64, ctypes.POINTER(sz)]),
+    "sf_frame_workspace_bytes": (ctypes.c_int, [i64, i32, i32, i32, i32, i32, i32, i64, ctypes.POINTER(sz)]),
     "sf_render_frame": (ctypes.c_int, [ctypes.POINTER(SfScene), ctypes.POINTER(SfCamera),
                                        ctypes.POINTER(SfQuery), ctypes.POINTER(SfFrame), P, sz, P]),
     "sf_project_workspace_bytes": (ctypes.c_int, [i64, ctypes.POINTER(sz)]),
@@ -61,7 +61,8 @@ EXPORTS = {
                                        P, P, P, P, P, P, sz, P]),
     "sf_bin_workspace_bytes": (ctypes.c_int, [i64, i32, i32, i64, ctypes.POINTER(sz)]),
     "sf_bin": (ctypes.c_int, [i64, P, P, P, P, i32, i32, i64, P, P, P, P, P, sz, P]),
-    "sf_decode": (ctypes.c_int, [i64, i32, i32, P, i64, P, P, P]),
+    "sf_decode_workspace_bytes": (sz, [i32, i32]),
+    "sf_decode": (ctypes.c_int, [i64, i32, i32, P, i64, P, P, P, sz, P]),
     "sf_decode_simt": (ctypes.c_int, [i64, i32, i32, P, i64, P, P, P]),
     "sf_relevancy_f32": (ctypes.c_int, [i64, i32, P, P, P, i32, P, P]),
     "sf_relevancy_f64": (ctypes.c_int, [i64, i32, P, P, P, i32, P, P]),

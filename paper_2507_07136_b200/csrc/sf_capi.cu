@@ -72,12 +72,13 @@ struct FrameWs {
     double* proj_cb;
     double* filter_tmp;
     void* sel_ws;
+    float* dec_ws;
 };
 
 static constexpr int kMaxCanon = 64;
 
 static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n_levels, int L,
-                          int K, int64_t pair_cap, FrameWs* ws) {
+                          int K, int D, int64_t pair_cap, FrameWs* ws) {
     Carver c(base, cap);
     int64_t Gp = G > 0 ? G : 1;
     int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
@@ -103,13 +104,14 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->proj_cb = c.take<double>((size_t)n_levels * L * (1 + kMaxCanon));
     ws->filter_tmp = c.take<double>((size_t)n_levels * W * H);
     ws->sel_ws = c.take<char>(select_segment_ws_bytes(n_levels, H, W));
+    ws->dec_ws = c.take<float>(decode_ws_bytes(L, D) / sizeof(float));
     return c.off;
 }
 
 extern "C" int sf_frame_workspace_bytes(int64_t G, int32_t W, int32_t H, int32_t n_levels,
-                                        int32_t L, int32_t K, int64_t pair_cap, size_t* bytes) {
+                                        int32_t L, int32_t K, int32_t D, int64_t pair_cap, size_t* bytes) {
     FrameWs ws;
-    *bytes = carve_frame(nullptr, 0, G, W, H, n_levels, L, K, pair_cap, &ws) + 256;
+    *bytes = carve_frame(nullptr, 0, G, W, H, n_levels, L, K, D, pair_cap, &ws) + 256;
     return SF_OK;
 }
 
@@ -158,7 +160,7 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     if (need_cmap && !f->coeff_map) return fail(SF_ERR_VALIDATION, "coefficient map buffer required");
 
     FrameWs ws;
-    size_t need = carve_frame(workspace, workspace_bytes, s->num_gaussians, W, H, f->n_levels, L, K,
+    size_t need = carve_frame(workspace, workspace_bytes, s->num_gaussians, W, H, f->n_levels, L, K, D,
                               f->pair_capacity, &ws);
     if (need > workspace_bytes) return fail(SF_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, need);
 
@@ -209,7 +211,8 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
         const int64_t P = (int64_t)W * H;
         for (int b = 0; b < f->n_levels; ++b) {
             if (launch_decode(P, L, D, f->coeff_map + (size_t)b * L, n_ch,
-                              s->codebooks + (size_t)lv.lv[b] * L * D, f->features + (size_t)b * P * D, st))
+                              s->codebooks + (size_t)lv.lv[b] * L * D, f->features + (size_t)b * P * D,
+                              ws.dec_ws, st))
                 return fail(SF_ERR_VALIDATION, "decode configuration unsupported (L=%d, D=%d)", L, D);
         }
     }
@@ -407,9 +410,12 @@ extern "C" int sf_bin(int64_t n, const double* means2d, const double* inv_covs, 
 // ---------------------------------------------------------------------------
 // standalone ops
 
+extern "C" size_t sf_decode_workspace_bytes(int32_t L, int32_t D) { return decode_ws_bytes(L, D); }
+
 extern "C" int sf_decode(int64_t P, int32_t L, int32_t D, const float* w, int64_t w_stride,
-                         const float* cb, float* out, void* stream) {
-    if (launch_decode(P, L, D, w, w_stride, cb, out, (cudaStream_t)stream))
+                         const float* cb, float* out, void* ws, size_t ws_bytes, void* stream) {
+    if (ws_bytes < decode_ws_bytes(L, D)) return fail(SF_ERR_WORKSPACE, "decode workspace too small");
+    if (launch_decode(P, L, D, w, w_stride, cb, out, ws, (cudaStream_t)stream))
         return fail(SF_ERR_VALIDATION, "decode configuration unsupported (L=%d, D=%d)", L, D);
     return check_cuda("sf_decode");
 }

@@ -190,7 +190,8 @@ void launch_select_segment(int n_maps, int H, int W, const double* maps, int fix
 // sf_decode.cu (SIMT cross-check) / sf_decode_tc.cu (tcgen05 3xTF32)
 int launch_decode_simt(int64_t P, int L, int D, const float* w, int64_t w_stride, const float* cb,
                        float* out, cudaStream_t st);
+size_t decode_ws_bytes(int L, int D);
 int launch_decode(int64_t P, int L, int D, const float* w, int64_t w_stride, const float* cb,
-                  float* out, cudaStream_t st);
+                  float* out, void* ws, cudaStream_t st);
 
 }  // namespace sf

@@ -184,7 +184,8 @@ class FrameEngine:
         if self._ws is None or self._ws_key != key:
             nbytes = ctypes.c_size_t(0)
             N.check(N.load().sf_frame_workspace_bytes(self.ds.num_gaussians, W, H, n_levels, cfg.L,
-                                                      cfg.K, self.pair_capacity, ctypes.byref(nbytes)))
+                                                      cfg.K, cfg.D, self.pair_capacity,
+                                                      ctypes.byref(nbytes)))
             if self._ws is None or self._ws.numel() < nbytes.value:
                 self._ws = None
                 self._ws = torch.empty(nbytes.value, dtype=torch.uint8, device=self.ds.device)

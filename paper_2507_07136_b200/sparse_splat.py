@@ -184,10 +184,11 @@ def decode(cmap: CoefficientMap, codebooks) -> FeatureMapSet:
     D = Dims.pop()
     out = torch.empty((len(cmap.levels), h, w, D), dtype=torch.float32, device=dev)
     lib = N.load()
+    ws = torch.empty(max(int(lib.sf_decode_workspace_bytes(cmap.L, D)), 16), dtype=torch.uint8, device=dev)
     for b, level in enumerate(cmap.levels):
         atoms = torch.from_numpy(np.ascontiguousarray(codebooks[level].atoms, dtype=np.float32)).to(dev)
         N.check(lib.sf_decode(h * w, cmap.L, D, N.ptr(W[:, :, b * cmap.L:]), nch, N.ptr(atoms),
-                              N.ptr(out[b]), stream_ptr()))
+                              N.ptr(out[b]), N.ptr(ws), ws.numel(), stream_ptr()))
         del atoms
     torch.cuda.current_stream().synchronize()
     return FeatureMapSet(levels=cmap.levels, provenance="decoded-from-coefficients", dev=out)
@@ -250,7 +251,8 @@ class QueryResult:
 def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int = 11,
                    level: int | None = None, tile_size: int = DEFAULT_TILE_SIZE, workers: int = 1,
                    instrument: bool = True, threshold: float = 0.5,
-                   features: str = "lazy") -> QueryResult:
+                   features: str = "lazy",
+                   max_elements: int = DEFAULT_MAX_RENDER_ELEMENTS) -> QueryResult:
     """Fused multilevel splat -> decode -> post-process (sparse_splat.py:243-297).
 
     One ``sf_render_frame``: the blend kernel also computes the per-level
@@ -258,6 +260,8 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
     P = atoms @ [q; canonicals]^T (fp64) -- exactly f.q = (W @ atoms).q --
     so the 512-d features are decoded only when asked for
     (``features="eager"`` decodes them inside the timed frame).
+    ``max_elements`` (extension, default = the reference's fixed budget) lets
+    configurations above 2^27 coefficient elements run.
     """
     from .device import QuerySpec, device_scene
     cfg = scene.config
@@ -274,8 +278,9 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
             f"canonicals D={canon.shape[1]}")
     if window < 1 or window % 2 == 0:
         raise ValidationError(f"filter window must be odd and >= 1, got {window}")
-    # the reference cannot override the render budget here (sparse_splat.py:264)
-    check_render_budget(W, H, len(levels) * cfg.L, DEFAULT_MAX_RENDER_ELEMENTS)
+    # the reference cannot override the render budget here (sparse_splat.py:264);
+    # the keyword is an extension whose default keeps that behaviour
+    check_render_budget(W, H, len(levels) * cfg.L, max_elements)
     fixed = -1
     if level is not None:
         if level not in levels:

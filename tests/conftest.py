@@ -79,3 +79,42 @@ def make_camera(width=32, height=32, fov=45.0):
 @pytest.fixture
 def rng():
     return np.random.default_rng(1234)
+
+
+TIE_MARGIN = 1e-12
+
+
+def assert_selection_matches(ref_maps, level, point, mask, ref_level, ref_point, ref_mask=None,
+                             threshold=0.5):
+    """level / point / mask identity, tie-aware.
+
+    The reference filters with an integral image (query.py:96-104) whose
+    rounding noise (~1e-15) decides between exactly tied maxima, although its
+    own contract is "ties to the lowest level" / "smallest row, then column"
+    (query.py:111-126).  We implement the contract on the exact filter.  So:
+    a differing choice is accepted only if the reference's own values tie
+    within TIE_MARGIN there (the margin is reported), and mask pixels are
+    compared wherever the reference's normalised value is not within 1e-9 of
+    the threshold.
+    """
+    maxima = np.array([m.max() for m in ref_maps])
+    if level != ref_level:
+        margin = maxima[ref_level] - maxima[level]
+        assert margin <= TIE_MARGIN, f"level {level} != {ref_level}, reference margin {margin:.3g}"
+    m = ref_maps[level]
+    if tuple(point) != tuple(ref_point):
+        margin = m.max() - m[tuple(point)]
+        assert margin <= TIE_MARGIN, f"point {point} != {ref_point}, reference margin {margin:.3g}"
+    if mask is not None:
+        lo, hi = m.min(), m.max()
+        if hi <= lo:
+            assert not np.asarray(mask).any()
+            return
+        norm = (m - lo) / (hi - lo)
+        want = norm > threshold
+        decided = np.abs(norm - threshold) > 1e-9
+        bad = (np.asarray(mask, dtype=bool) != want) & decided
+        assert not bad.any(), f"{int(bad.sum())} mask pixels differ away from the threshold"
+        if ref_mask is not None and level == ref_level:
+            bad = (np.asarray(mask, dtype=bool) != np.asarray(ref_mask, dtype=bool)) & decided
+            assert not bad.any()

@@ -51,7 +51,7 @@ def test_workspace_queries_need_no_gpu(lib_path):
     from paper_2507_07136_b200 import _native as N
     lib = N.load()
     n = ctypes.c_size_t(0)
-    assert lib.sf_frame_workspace_bytes(2_000_000, 1440, 1080, 3, 64, 4, 12_000_000, ctypes.byref(n)) == 0
+    assert lib.sf_frame_workspace_bytes(2_000_000, 1440, 1080, 3, 64, 4, 512, 12_000_000, ctypes.byref(n)) == 0
     assert n.value > 2_000_000 * 100
 
 
