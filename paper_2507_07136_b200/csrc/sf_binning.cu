@@ -48,18 +48,14 @@ __global__ void __launch_bounds__(256) k_rank_gather(int64_t G, const uint32_t* 
                                                      const float* __restrict__ opac_by_row,
                                                      const uint16_t* __restrict__ cidx,
                                                      const float* __restrict__ cval, int K, int L,
-                                                     LevelSelDev levels,
-                                                     Proj64* __restrict__ proj_rank,
-                                                     Blend32* __restrict__ b32,
-                                                     uint16_t* __restrict__ ch_idx,
-                                                     float* __restrict__ ch_val, int C) {
+                                                     LevelSelDev levels, GeomRec* __restrict__ geom,
+                                                     unsigned char* __restrict__ chan, int C) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t n = stats[SF_STAT_VISIBLE];
     if (r >= n) return;
     uint32_t row = sorted_rows[r];
     Proj64 p = proj_by_row[row];
-    proj_rank[r] = p;
-    Blend32 q;
+    GeomRec q;
     q.mx_hi = (float)p.mx;
     q.mx_lo = (float)(p.mx - (double)q.mx_hi);
     q.my_hi = (float)p.my;
@@ -67,16 +63,27 @@ __global__ void __launch_bounds__(256) k_rank_gather(int64_t G, const uint32_t* 
     q.a = (float)p.a;
     q.b2 = (float)(2.0 * p.b);
     q.c = (float)p.c;
-    q.opacity = opac_by_row[row];
-    b32[r] = q;
-    if (ch_idx) {
+    q.opacity = opac_by_row ? opac_by_row[row] : 0.f;
+    q.mx = p.mx;
+    q.my = p.my;
+    q.a64 = p.a;
+    q.b64 = p.b;
+    q.c64 = p.c;
+    q.row = row;
+    q.pad = 0;
+    geom[r] = q;
+    if (chan) {
+        const int cs = chan_rec_bytes(C);
+        unsigned char* rec = chan + (size_t)r * cs;
+        uint16_t* ch = reinterpret_cast<uint16_t*>(rec);
+        float* val = reinterpret_cast<float*>(rec + chan_val_offset(C));
         for (int b = 0; b < levels.n; ++b) {
             int lv = levels.lv[b];
             const uint16_t* ip = cidx + ((int64_t)lv * G + row) * K;
             const float* vp = cval + ((int64_t)lv * G + row) * K;
             for (int k = 0; k < K; ++k) {
-                ch_idx[r * C + b * K + k] = (uint16_t)(ip[k] + b * L);
-                ch_val[r * C + b * K + k] = vp[k];
+                ch[b * K + k] = (uint16_t)(ip[k] + b * L);
+                val[b * K + k] = vp[k];
             }
         }
     }
@@ -84,13 +91,12 @@ __global__ void __launch_bounds__(256) k_rank_gather(int64_t G, const uint32_t* 
 
 void launch_rank_gather(int64_t G, const uint32_t* sorted_rows, const int64_t* stats,
                         const Proj64* proj_by_row, const float* opac_by_row, const SfScene* s,
-                        const LevelSelDev& levels, Proj64* proj_rank, Blend32* b32,
-                        uint16_t* ch_idx, float* ch_val, int C, cudaStream_t st) {
+                        const LevelSelDev& levels, GeomRec* geom, unsigned char* chan, int C,
+                        cudaStream_t st) {
     if (G == 0) return;
     k_rank_gather<<<ceil_div(G, 256), 256, 0, st>>>(
         G, sorted_rows, stats, proj_by_row, opac_by_row, s ? s->coeff_indices : nullptr,
-        s ? s->coeff_values : nullptr, s ? s->K : 0, s ? s->L : 0, levels, proj_rank, b32,
-        ch_idx, ch_val, C);
+        s ? s->coeff_values : nullptr, s ? s->K : 0, s ? s->L : 0, levels, geom, chan, C);
 }
 
 // ---------------------------------------------------------------------------
@@ -127,11 +133,11 @@ __device__ __forceinline__ bool tile_hit(const Proj64& p, int tx, int ty, const 
 }
 
 __global__ void __launch_bounds__(256) k_count_pairs(int64_t G, const int64_t* __restrict__ stats,
-                                                     const Proj64* __restrict__ proj_rank,
+                                                     const GeomRec* __restrict__ geom,
                                                      TileGrid g, uint32_t* __restrict__ tile_counts) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= stats[SF_STAT_VISIBLE]) return;
-    Proj64 p = proj_rank[r];
+    Proj64 p = geom_proj(geom[r]);
     int tx0, tx1, ty0, ty1;
     cand_rect(p, g, tx0, tx1, ty0, ty1);
     for (int ty = ty0; ty <= ty1; ++ty)
@@ -169,13 +175,13 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
 }
 
 __global__ void __launch_bounds__(256) k_emit_pairs(int64_t G, const int64_t* __restrict__ stats,
-                                                    const Proj64* __restrict__ proj_rank, TileGrid g,
+                                                    const GeomRec* __restrict__ geom, TileGrid g,
                                                     uint32_t* __restrict__ cursor,
                                                     uint32_t* __restrict__ entries) {
     if (stats[SF_STAT_OVERFLOW]) return;
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= stats[SF_STAT_VISIBLE]) return;
-    Proj64 p = proj_rank[r];
+    Proj64 p = geom_proj(geom[r]);
     int tx0, tx1, ty0, ty1;
     cand_rect(p, g, tx0, tx1, ty0, ty1);
     for (int ty = ty0; ty <= ty1; ++ty)
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ 
     }
 }
 
-void launch_binning(int64_t G, const int64_t* stats_n, const Proj64* proj_rank, int W, int H,
+void launch_binning(int64_t G, const int64_t* stats_n, const GeomRec* geom, int W, int H,
                     int64_t pair_capacity, uint32_t* tile_counts, uint32_t* tile_offsets,
                     uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
                     int64_t* stats, cudaStream_t st) {
@@ -283,10 +289,10 @@ void launch_binning(int64_t G, const int64_t* stats_n, const Proj64* proj_rank, 
     int n_tiles = g.tiles_x * g.tiles_y;
     cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * n_tiles, st);
     int blocks = G > 0 ? ceil_div(G, 256) : 0;
-    if (blocks) k_count_pairs<<<blocks, 256, 0, st>>>(G, stats_n, proj_rank, g, tile_counts);
+    if (blocks) k_count_pairs<<<blocks, 256, 0, st>>>(G, stats_n, geom, g, tile_counts);
     k_tile_scan<<<1, 1024, 0, st>>>(n_tiles, tile_counts, tile_offsets, tile_cursor, pair_capacity,
                                     stats);
-    if (blocks) k_emit_pairs<<<blocks, 256, 0, st>>>(G, stats_n, proj_rank, g, tile_cursor, entries);
+    if (blocks) k_emit_pairs<<<blocks, 256, 0, st>>>(G, stats_n, geom, g, tile_cursor, entries);
     k_tile_sort<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, stats);
 }
 

@@ -8,20 +8,27 @@
 //
 // B200 mapping.  One CTA per 16x16 tile (x channel block), one pixel per
 // thread; each warp owns an 8x4 pixel patch so the set of Gaussians live in
-// a warp stays small.  The tile's depth-ordered list is streamed through
-// shared memory in batches of 32 Gaussians.  Per (pixel, Gaussian) the
-// rejection test q > 9 runs in fp32 with a conservative guard band (|q32 -
-// q64| <= 1.5e-6 S, guard 1e-4 (1 + S), S = a dx^2 + c dy^2); survivors are
-// re-evaluated in fp64 with the reference's exact op order, so the q <= 9
-// membership decision is bit-exact and alpha / T carry fp64 accuracy (the
-// T >= 1e-4 early-exit decision therefore matches the fp64 reference).  The
-// coefficient accumulator is fp32 in shared memory, laid out
-// acc[channel][pixel-slot] with a 257-float row pitch: the K channel
-// indices of a Gaussian are warp-uniform, so every scatter is one
-// conflict-free wavefront; the pitch also makes the transposed read for the
-// channel-contiguous HBM write conflict-free.  A warp skips a Gaussian's
-// scatter unless some lane has e > 0 (__any_sync vote), and the CTA stops
-// streaming when every pixel is saturated (__syncthreads_and vote).
+// a warp stays small.  The tile's depth-ordered list streams through shared
+// memory in batches of 32 Gaussian records (80 B geometry + scatter plan),
+// double-buffered with cp.async so the next batch's L2/HBM gathers overlap
+// the current batch's math.  Per batch:
+//   phase A  every thread runs the q > 9 rejection in fp32 for all 32
+//            Gaussians (independent work, high ILP) with a conservative
+//            guard band (|q32 - q64| <= 1.5e-6 S, guard 1e-4 (1 + S),
+//            S = a dx^2 + c dy^2) -> a 32-bit candidate mask;
+//   phase B  the warp walks the union of its candidate masks in depth order;
+//            candidates are re-evaluated in fp64 with the reference's exact
+//            op order (bit-exact q <= 9 membership), alpha = o exp(-q/2) via
+//            a 1/128-step table times a degree-5 polynomial (~1e-16 rel.),
+//            and T / e carried in fp64, so the T >= 1e-4 early-exit decision
+//            matches the fp64 reference.
+// The coefficient accumulator is fp32 in shared memory, acc[channel][slot]
+// with a 257-float pitch: the K channel ids of a Gaussian are warp-uniform,
+// so every scatter is one conflict-free wavefront, and the transposed read
+// for the channel-contiguous HBM write is conflict-free too.  A warp skips
+// a Gaussian's scatter unless some lane has e > 0 (__any_sync), skips whole
+// batches once all its pixels saturated, and the CTA stops streaming when
+// every pixel is saturated (__syncthreads_and).
 //
 // Optional fused epilogue: per pixel and level, logits against the query and
 // the canonical phrases via the projected codebook P = atoms @ [q; c]^T
@@ -34,15 +41,23 @@ namespace sf {
 constexpr int kBlendThreads = 256;
 constexpr int kBatch = 32;
 constexpr int kAccPitch = 257;
-constexpr int kMaxC = 16;            // channels per Gaussian (levels*K) supported in one pass
+constexpr int kMaxC = 16;            // channels per Gaussian (levels*K) supported
+constexpr int kMaxChanRec = 96;      // chan_rec_bytes(16)
 constexpr int kChBlock = 192;        // accumulator channels per CTA (smem bound)
-constexpr uint32_t kInvalidOff = 0xffffffffu;
+constexpr int kExpSteps = 128;       // exp table resolution in y = q / 2
+constexpr int kExpTable = 577;       // y in [0, 4.5]
 
-struct BlendSmem {
-    Blend32 g32[kBatch];
-    Proj64 g64[kBatch];
+__constant__ double c_exp_table[kExpTable];
+
+struct __align__(16) BlendStage {
+    GeomRec g[kBatch];
+    unsigned char chan[kBatch * kMaxChanRec];
     uint32_t off[kBatch][kMaxC];
-    float val[kBatch][kMaxC];
+};
+
+struct __align__(16) BlendSmem {
+    BlendStage st[2];
+    double exp_tab[kExpTable + 1];
 };
 
 __device__ __forceinline__ double sigmoid2(double x) {
@@ -51,11 +66,53 @@ __device__ __forceinline__ double sigmoid2(double x) {
     return ex / (1.0 + ex);
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// exp(-y) for y in [0, 4.5]: table at k/128 times a degree-5 Taylor
+// polynomial on f in [0, 1/128) (truncation < 3.2e-16 relative).
+__device__ __forceinline__ double exp_neg(double y, const double* tab) {
+    int k = (int)(y * (double)kExpSteps);  // exact scaling, truncation = floor (y >= 0)
+    double f = fma(-(double)k, 1.0 / kExpSteps, y);  // exact: y - k/128
+    double p = fma(f, -1.0 / 120.0, 1.0 / 24.0);
+    p = fma(p, f, -1.0 / 6.0);
+    p = fma(p, f, 0.5);
+    p = fma(p, f, -1.0);
+    p = fma(p, f, 1.0);
+    return tab[k] * p;
+}
+
+// Issue the cp.async copies of one batch (nb records) into stage buffer S.
+__device__ __forceinline__ void stage_batch(BlendStage& S, const BlendArgs& A, uint32_t base, int nb, int cs) {
+    const int gchunks = (int)(sizeof(GeomRec) / 16);  // 5
+    const int cchunks = cs / 16;
+    const int per = gchunks + cchunks;
+    for (int idx = threadIdx.x; idx < nb * per; idx += kBlendThreads) {
+        int j = idx / per, c = idx - j * per;
+        uint32_t r = __ldg(A.entries + base + j);
+        if (c < gchunks) {
+            cp_async16(reinterpret_cast<char*>(&S.g[j]) + 16 * c,
+                       reinterpret_cast<const char*>(A.geom + r) + 16 * c);
+        } else {
+            c -= gchunks;
+            cp_async16(S.chan + j * kMaxChanRec + 16 * c, A.chan + (size_t)r * cs + 16 * c);
+        }
+    }
+}
+
+template <int CT, bool SINGLE>
 __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_block) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
     float* acc = reinterpret_cast<float*>(smem_raw + sizeof(BlendSmem));
-    __shared__ int s_done_all;
 
     if (A.stats[SF_STAT_OVERFLOW]) return;
     const int tile = blockIdx.x;
@@ -69,52 +126,70 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
     const int ly = (warp >> 1) * 4 + (lane >> 3);
     const int px = x0 + lx, py = y0 + ly;
     const bool inside = (px < A.W) && (py < A.H);
-
-    for (int i = threadIdx.x; i < nchb * kAccPitch; i += kBlendThreads) acc[i] = 0.f;
+    const int C = CT > 0 ? CT : A.C;
+    const int cs = chan_rec_bytes(C);
+    const int voff = chan_val_offset(C);
 
     const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
+    if (beg < end) stage_batch(S.st[0], A, beg, (int)min((uint32_t)kBatch, end - beg), cs);
+    cp_async_commit();
+    for (int i = threadIdx.x; i < kExpTable; i += kBlendThreads) S.exp_tab[i] = c_exp_table[i];
+    for (int i = threadIdx.x; i < nchb * kAccPitch; i += kBlendThreads) acc[i] = 0.f;
+
     const float pxf = (float)px, pyf = (float)py;
     const double pxd = (double)px, pyd = (double)py;
     double T = 1.0;
     bool done = !inside;
-    const int C = A.C;
 
-    for (uint32_t base = beg; base < end; base += kBatch) {
+    int bi = 0;
+    for (uint32_t base = beg; base < end; base += kBatch, ++bi) {
         const int nb = (int)min((uint32_t)kBatch, end - base);
-        __syncthreads();  // previous batch fully consumed
-        if (threadIdx.x < nb) {
-            uint32_t r = A.entries[base + threadIdx.x];
-            S.g32[threadIdx.x] = A.b32[r];
-            S.g64[threadIdx.x] = A.p64[r];
-        }
+        BlendStage& B = S.st[bi & 1];
+        // prefetch the next batch into the other buffer (freed by the previous iteration's barrier)
+        const uint32_t nbase = base + kBatch;
+        if (nbase < end) stage_batch(S.st[(bi + 1) & 1], A, nbase, (int)min((uint32_t)kBatch, end - nbase), cs);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        // channel ids -> accumulator offsets for this CTA's channel block
         for (int idx = threadIdx.x; idx < nb * C; idx += kBlendThreads) {
             int j = idx / C, k = idx - j * C;
-            uint32_t r = A.entries[base + j];
-            int ch = (int)A.ch_idx[(size_t)r * C + k] - ch0;
-            S.off[j][k] = (ch >= 0 && ch < nchb) ? (uint32_t)(ch * kAccPitch) : kInvalidOff;
-            S.val[j][k] = A.ch_val[(size_t)r * C + k];
+            int ch = (int)reinterpret_cast<const uint16_t*>(B.chan + j * kMaxChanRec)[k] - ch0;
+            B.off[j][k] = ((unsigned)ch < (unsigned)nchb) ? (uint32_t)(ch * kAccPitch) : 0xffffffffu;
         }
         __syncthreads();
 
-        for (int j = 0; j < nb; ++j) {
-            float ef = 0.f;
+        if (!__all_sync(0xffffffffu, done)) {
+            // ---- phase A: fp32 rejection, candidate mask ----
+            uint32_t cand = 0;
             if (!done) {
-                const Blend32 g = S.g32[j];
-                float dx = (pxf - g.mx_hi) - g.mx_lo;
-                float dy = (pyf - g.my_hi) - g.my_lo;
-                float adx = g.a * dx, cdy = g.c * dy;
-                float q32 = adx * dx + g.b2 * dx * dy + cdy * dy;
-                float s32 = adx * dx + cdy * dy;
-                if (q32 <= 9.0f + 1e-4f * (1.0f + s32)) {
-                    // exact reference evaluation (rasterizer.py:161-168)
-                    const Proj64 p = S.g64[j];
-                    double ddx = __dadd_rn(pxd, -p.mx), ddy = __dadd_rn(pyd, -p.my);
-                    double t1 = __dmul_rn(__dmul_rn(p.a, ddx), ddx);
-                    double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, p.b), ddx), ddy);
-                    double t3 = __dmul_rn(__dmul_rn(p.c, ddy), ddy);
+#pragma unroll 4
+                for (int j = 0; j < nb; ++j) {
+                    const float4 m4 = *reinterpret_cast<const float4*>(&B.g[j].mx_hi);
+                    const float4 c4 = *reinterpret_cast<const float4*>(&B.g[j].a);
+                    float dx = (pxf - m4.x) - m4.y;
+                    float dy = (pyf - m4.z) - m4.w;
+                    float adx = c4.x * dx, cdy = c4.z * dy;
+                    float q32 = fmaf(adx, dx, fmaf(c4.y * dx, dy, cdy * dy));
+                    float s32 = fmaf(adx, dx, cdy * dy);
+                    if (q32 <= fmaf(1e-4f, s32, 9.0001f)) cand |= 1u << j;
+                }
+            }
+            // ---- phase B: exact evaluation + scatter, depth order ----
+            uint32_t wmask = __reduce_or_sync(0xffffffffu, cand);
+            while (wmask) {
+                const int j = __ffs(wmask) - 1;
+                wmask &= wmask - 1;
+                float ef = 0.f;
+                if (((cand >> j) & 1u) && !done) {
+                    const GeomRec& g = B.g[j];
+                    double ddx = __dadd_rn(pxd, -g.mx), ddy = __dadd_rn(pyd, -g.my);
+                    double t1 = __dmul_rn(__dmul_rn(g.a64, ddx), ddx);
+                    double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, g.b64), ddx), ddy);
+                    double t3 = __dmul_rn(__dmul_rn(g.c64, ddy), ddy);
                     double q = __dadd_rn(__dadd_rn(t1, t2), t3);
                     if (q <= SF_CUTOFF) {
-                        double al = __dmul_rn((double)g.opacity, exp(__dmul_rn(-0.5, q)));
+                        double al = __dmul_rn((double)g.opacity, exp_neg(__dmul_rn(0.5, q), S.exp_tab));
                         al = np_minimum(al, SF_ALPHA_CLAMP);
                         double e = __dmul_rn(al, T);
                         T = __dmul_rn(T, __dadd_rn(1.0, -al));
@@ -122,49 +197,82 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
                         if (A.early_exit && T < SF_EARLY_EXIT_T) done = true;
                     }
                 }
-            }
-            if (__any_sync(0xffffffffu, ef > 0.f)) {
-#pragma unroll 4
-                for (int k = 0; k < C; ++k) {
-                    uint32_t off = S.off[j][k];
-                    if (off != kInvalidOff) acc[off + slot] += ef * S.val[j][k];
+                if (__any_sync(0xffffffffu, ef > 0.f)) {
+                    const float* val = reinterpret_cast<const float*>(B.chan + j * kMaxChanRec + voff);
+                    float* accs = acc + slot;
+                    if (CT > 0) {
+#pragma unroll
+                        for (int k = 0; k < (CT > 0 ? CT : 1); ++k) {
+                            const uint32_t off = B.off[j][k];
+                            if (SINGLE || off != 0xffffffffu) accs[off] = fmaf(ef, val[k], accs[off]);
+                        }
+                    } else {
+                        for (int k = 0; k < C; ++k) {
+                            const uint32_t off = B.off[j][k];
+                            if (off != 0xffffffffu) accs[off] = fmaf(ef, val[k], accs[off]);
+                        }
+                    }
                 }
             }
         }
         if (__syncthreads_and(done)) break;
     }
+    cp_async_wait<0>();
     __syncthreads();
 
     // ---- outputs ----
     if (blockIdx.y == 0 && A.final_t && inside) A.final_t[(size_t)py * A.W + px] = (float)T;
     if (A.coeff_map) {
+        // warp w writes pixels x = w, w + 8 of every tile row; lanes stride the
+        // pixel's channels (contiguous in HBM), the smem read is conflict-free
         const int tw = min(SF_TILE, A.W - x0), th = min(SF_TILE, A.H - y0);
         for (int r = 0; r < th; ++r) {
-            float* row = A.coeff_map + ((size_t)(y0 + r) * A.W + x0) * A.n_ch + ch0;
             const int wr = (r >> 2) * 2, lr = (r & 3) * 8;
-            for (int idx = threadIdx.x; idx < tw * nchb; idx += kBlendThreads) {
-                int x = idx / nchb, ch = idx - x * nchb;
-                int sl = (wr + (x >> 3)) * 32 + lr + (x & 7);
-                row[(size_t)x * A.n_ch + ch] = acc[ch * kAccPitch + sl];
+            for (int x = warp; x < tw; x += kBlendThreads / 32) {
+                const int sl = (wr + (x >> 3)) * 32 + lr + (x & 7);
+                float* dst = A.coeff_map + ((size_t)(y0 + r) * A.W + x0 + x) * A.n_ch + ch0;
+                for (int ch = lane; ch < nchb; ch += 32) __stcs(dst + ch, acc[ch * kAccPitch + sl]);
             }
         }
     }
-    if (A.proj_cb && inside && nchb == A.n_ch) {
-        // fused relevancy: logits_j = sum_l W[l] * P[b][l][j]  (fp64)
+    if (A.proj_cb && nchb == A.n_ch) {
+        // fused relevancy: logits_j = sum_l W[l] * P[b][l][j] in fp64; the
+        // projected codebook is staged in the idle batch buffers
         const int nv = 1 + A.n_canon;
-        for (int b = 0; b < A.n_levels; ++b) {
-            const double* P = A.proj_cb + (size_t)b * A.L * nv;
-            double lq = 0.0;
-            double best = INFINITY;
-            // query logit
-            for (int l = 0; l < A.L; ++l) lq = fma((double)acc[(b * A.L + l) * kAccPitch + slot], P[l * nv], lq);
-            for (int j = 1; j < nv; ++j) {
-                double lc = 0.0;
-                for (int l = 0; l < A.L; ++l)
-                    lc = fma((double)acc[(b * A.L + l) * kAccPitch + slot], P[l * nv + j], lc);
-                best = np_minimum(best, sigmoid2(lq - lc));
+        const int np = A.n_levels * A.L * nv;
+        double* Ps = reinterpret_cast<double*>(&S.st[0]);
+        const bool fits = np * (int)sizeof(double) <= (int)sizeof(S.st);
+        if (fits) {
+            for (int i = threadIdx.x; i < np; i += kBlendThreads) Ps[i] = A.proj_cb[i];
+            __syncthreads();
+        }
+        const double* Pb = fits ? Ps : A.proj_cb;
+        if (inside) {
+            constexpr int kV = 8;
+            for (int b = 0; b < A.n_levels; ++b) {
+                const double* P = Pb + (size_t)b * A.L * nv;
+                double lq = 0.0, best = INFINITY;
+                for (int j0 = 0; j0 < nv; j0 += kV) {
+                    double lg[kV];
+#pragma unroll
+                    for (int t = 0; t < kV; ++t) lg[t] = 0.0;
+                    const int nj = min(kV, nv - j0);
+                    for (int l = 0; l < A.L; ++l) {
+                        const double w = (double)acc[(b * A.L + l) * kAccPitch + slot];
+                        const double* Pl = P + l * nv + j0;
+#pragma unroll
+                        for (int t = 0; t < kV; ++t)
+                            if (t < nj) lg[t] = fma(w, Pl[t], lg[t]);
+                    }
+#pragma unroll
+                    for (int t = 0; t < kV; ++t) {
+                        if (t >= nj) break;
+                        if (j0 + t == 0) lq = lg[t];
+                        else best = np_minimum(best, sigmoid2(lq - lg[t]));
+                    }
+                }
+                A.relevancy_raw[(size_t)b * A.W * A.H + (size_t)py * A.W + px] = best;
             }
-            A.relevancy_raw[(size_t)b * A.W * A.H + (size_t)py * A.W + px] = best;
         }
     }
 }
@@ -192,18 +300,31 @@ __global__ void k_relevancy_from_cmap(int64_t P, int n_ch, const float* __restri
     }
 }
 
+static bool init_exp_table() {
+    static bool done = false;
+    if (done) return true;
+    double h[kExpTable];
+    for (int k = 0; k < kExpTable; ++k) h[k] = exp(-(double)k / kExpSteps);
+    if (cudaMemcpyToSymbol(c_exp_table, h, sizeof(h)) != cudaSuccess) return false;
+    done = true;
+    return true;
+}
+
 int launch_blend(const BlendArgs& a, cudaStream_t st) {
     if (a.C > kMaxC) return -2;
+    if (!init_exp_table()) return -3;
     int n_tiles = a.tiles_x * a.tiles_y;
     int ch_block = a.n_ch < kChBlock ? a.n_ch : kChBlock;
     int nblk = (a.n_ch + ch_block - 1) / ch_block;
     size_t smem = sizeof(BlendSmem) + (size_t)ch_block * kAccPitch * sizeof(float);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaFuncSetAttribute(k_blend, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
+    auto kern = (a.C == 12 && nblk == 1) ? k_blend<12, true> : k_blend<0, false>;
+    static size_t configured[2] = {0, 0};
+    const int ki = (a.C == 12 && nblk == 1) ? 0 : 1;
+    if (smem > configured[ki]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured[ki] = smem;
     }
-    if (n_tiles > 0) k_blend<<<dim3(n_tiles, nblk), kBlendThreads, smem, st>>>(a, ch_block);
+    if (n_tiles > 0) kern<<<dim3(n_tiles, nblk), kBlendThreads, smem, st>>>(a, ch_block);
     if (a.proj_cb && nblk > 1) {
         int64_t P = (int64_t)a.W * a.H;
         k_relevancy_from_cmap<<<ceil_div(P, 256), 256, 0, st>>>(P, a.n_ch, a.coeff_map, a.proj_cb,

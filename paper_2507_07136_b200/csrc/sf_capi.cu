@@ -60,10 +60,8 @@ struct FrameWs {
     size_t cub_bytes;
     int64_t* stats;
     double* stats_f;
-    Proj64* proj_rank;
-    Blend32* b32;
-    uint16_t* ch_idx;
-    float* ch_val;
+    GeomRec* geom;
+    unsigned char* chan;
     uint32_t* tile_counts;
     uint32_t* tile_offsets;
     uint32_t* tile_cursor;
@@ -92,10 +90,8 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->cub_tmp = c.take<char>(ws->cub_bytes);
     ws->stats = c.take<int64_t>(16);
     ws->stats_f = c.take<double>(8 + kMaxLevels);
-    ws->proj_rank = c.take<Proj64>(Gp);
-    ws->b32 = c.take<Blend32>(Gp);
-    ws->ch_idx = c.take<uint16_t>(Gp * C);
-    ws->ch_val = c.take<float>(Gp * C);
+    ws->geom = c.take<GeomRec>(Gp);
+    ws->chan = c.take<unsigned char>((size_t)Gp * chan_rec_bytes(C));
     ws->tile_counts = c.take<uint32_t>(n_tiles);
     ws->tile_offsets = c.take<uint32_t>(n_tiles + 1);
     ws->tile_cursor = c.take<uint32_t>(n_tiles);
@@ -173,10 +169,10 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     // K2
     if (depth_sort(ws.keys_in, ws.keys_out, ws.vals_in, ws.vals_out, G, ws.cub_tmp, ws.cub_bytes, st))
         return check_cuda("depth sort");
-    launch_rank_gather(G, ws.vals_out, ws.stats, ws.proj_by_row, s->opacities, s, lv, ws.proj_rank,
-                       ws.b32, ws.ch_idx, ws.ch_val, C, st);
+    launch_rank_gather(G, ws.vals_out, ws.stats, ws.proj_by_row, s->opacities, s, lv, ws.geom, ws.chan, C,
+                       st);
     // K3/K4
-    launch_binning(G, ws.stats, ws.proj_rank, W, H, f->pair_capacity, ws.tile_counts, ws.tile_offsets,
+    launch_binning(G, ws.stats, ws.geom, W, H, f->pair_capacity, ws.tile_counts, ws.tile_offsets,
                    ws.tile_cursor, ws.entries, ws.scratch, ws.stats, st);
     if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
                                    ws.proj_cb, st);
@@ -192,10 +188,8 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     a.early_exit = f->early_exit;
     a.tile_offsets = ws.tile_offsets;
     a.entries = ws.entries;
-    a.b32 = ws.b32;
-    a.p64 = ws.proj_rank;
-    a.ch_idx = ws.ch_idx;
-    a.ch_val = ws.ch_val;
+    a.geom = ws.geom;
+    a.chan = ws.chan;
     a.stats = ws.stats;
     a.coeff_map = f->coeff_map;
     a.final_t = f->final_t;
@@ -322,13 +316,21 @@ __global__ void k_bin_depth_keys(int64_t n, const double* depths, const uint32_t
     keys[i] = depth_key(depths[idx_by_id[i]]);
 }
 
-__global__ void k_bin_finish(int64_t n, const uint32_t* order32, const Proj64* proj, Proj64* proj_rank,
+__global__ void k_bin_finish(int64_t n, const uint32_t* order32, const Proj64* proj, GeomRec* geom,
                              int64_t* order, int64_t* stats) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) stats[SF_STAT_VISIBLE] = n;
     if (i >= n) return;
     uint32_t r = order32[i];
-    proj_rank[i] = proj[r];
+    Proj64 p = proj[r];
+    GeomRec g;
+    memset(&g, 0, sizeof(g));
+    g.mx = p.mx;
+    g.my = p.my;
+    g.a64 = p.a;
+    g.b64 = p.b;
+    g.c64 = p.c;
+    geom[i] = g;
     order[i] = r;
 }
 
@@ -339,7 +341,7 @@ __global__ void k_offsets_to_i64(int n, const uint32_t* o32, int64_t* o64) {
 
 struct BinWs {
     Proj64* proj;
-    Proj64* proj_rank;
+    GeomRec* geom;
     uint64_t* k0;
     uint64_t* k1;
     uint32_t* v0;
@@ -358,7 +360,7 @@ static size_t carve_bin(void* base, size_t cap, int64_t n, int W, int H, int64_t
     int64_t np = n > 0 ? n : 1;
     int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
     w->proj = c.take<Proj64>(np);
-    w->proj_rank = c.take<Proj64>(np);
+    w->geom = c.take<GeomRec>(np);
     w->k0 = c.take<uint64_t>(np);
     w->k1 = c.take<uint64_t>(np);
     w->v0 = c.take<uint32_t>(np);
@@ -399,8 +401,8 @@ extern "C" int sf_bin(int64_t n, const double* means2d, const double* inv_covs, 
         k_bin_depth_keys<<<blocks, 256, 0, st>>>(n, depths, w.v1, w.k0);
         depth_sort(w.k0, w.k1, w.v1, w.v0, n, w.cub_tmp, w.cub_bytes, st);
     }
-    k_bin_finish<<<blocks, 256, 0, st>>>(n, w.v0, w.proj, w.proj_rank, order, w.stats);
-    launch_binning(n, w.stats, w.proj_rank, W, H, pair_cap, w.counts, w.offsets, w.cursor,
+    k_bin_finish<<<blocks, 256, 0, st>>>(n, w.v0, w.proj, w.geom, order, w.stats);
+    launch_binning(n, w.stats, w.geom, W, H, pair_cap, w.counts, w.offsets, w.cursor,
                    (uint32_t*)tile_entries, w.scratch, w.stats, st);
     k_offsets_to_i64<<<ceil_div(n_tiles + 1, 256), 256, 0, st>>>(n_tiles, w.offsets, tile_offsets);
     if (stats_i64) cudaMemcpyAsync(stats_i64, w.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);

@@ -93,11 +93,30 @@ struct __align__(8) Proj64 {
     double a, b, c; // inv_cov2d [[a, b], [b, c]]
 };
 
-// Blend-side record in canonical rank order: fp32 reject test inputs.
-struct __align__(16) Blend32 {
+// Per-Gaussian record in canonical (depth, id) rank order, 80 bytes:
+// fp32 inputs of the blend's rejection test, then the reference's fp64
+// values (means2d, inv_cov2d) used by binning and by the exact alpha.
+struct __align__(16) GeomRec {
     float mx_hi, mx_lo, my_hi, my_lo;  // mean split so (px - hi) - lo is ~exact
     float a, b2, c, opacity;           // conic (a, 2b, c) and opacity
+    double mx, my;                     // means2d (fp64, bitwise the reference's)
+    double a64, b64;                   // inv_cov2d[0][0], inv_cov2d[0][1]
+    double c64;                        // inv_cov2d[1][1]
+    uint32_t row, pad;
 };
+__host__ __device__ __forceinline__ Proj64 geom_proj(const GeomRec& g) {
+    Proj64 p;
+    p.mx = g.mx;
+    p.my = g.my;
+    p.a = g.a64;
+    p.b = g.b64;
+    p.c = g.c64;
+    return p;
+}
+// Scatter plan of one Gaussian (sparse_splat.py:126-132): C channel ids
+// (level block * L + index) then C values, padded to 16 bytes.
+__host__ __device__ __forceinline__ int chan_rec_bytes(int C) { return ((2 * C + 3) / 4 * 4 + 4 * C + 15) / 16 * 16; }
+__host__ __device__ __forceinline__ int chan_val_offset(int C) { return (2 * C + 3) / 4 * 4; }
 
 // Workspace carving helper.
 struct Carver {
@@ -142,9 +161,9 @@ int depth_sort(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals
 size_t id_sort_cub_bytes(int64_t n);
 void launch_rank_gather(int64_t G, const uint32_t* sorted_rows, const int64_t* stats,
                         const Proj64* proj_by_row, const float* opac_by_row, const SfScene* s,
-                        const LevelSelDev& levels, Proj64* proj_rank, Blend32* b32,
-                        uint16_t* ch_idx, float* ch_val, int C, cudaStream_t st);
-void launch_binning(int64_t G, const int64_t* stats_n, const Proj64* proj_rank, int W, int H,
+                        const LevelSelDev& levels, GeomRec* geom, unsigned char* chan, int C,
+                        cudaStream_t st);
+void launch_binning(int64_t G, const int64_t* stats_n, const GeomRec* geom, int W, int H,
                     int64_t pair_capacity, uint32_t* tile_counts, uint32_t* tile_offsets,
                     uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
                     int64_t* stats, cudaStream_t st);
@@ -157,10 +176,8 @@ struct BlendArgs {
     int early_exit;
     const uint32_t* tile_offsets;
     const uint32_t* entries;
-    const Blend32* b32;
-    const Proj64* p64;
-    const uint16_t* ch_idx;
-    const float* ch_val;
+    const GeomRec* geom;
+    const unsigned char* chan;
     const int64_t* stats;  // overflow flag gate
     float* coeff_map;      // (H,W,n_ch) or null
     float* final_t;        // (H,W) or null

@@ -6,21 +6,23 @@
 // Precision.  TF32 keeps 10 mantissa bits; one TF32 product would miss the
 // 1e-4 feature tolerance (hard part 3).  Split both operands
 // x = hi + lo with hi = rna_tf32(x) and lo = x - hi (exact in fp32), then
-//     F ~= A_hi B_hi + A_hi B_lo + A_lo B_hi        (error ~2^-22 |A||B|)
+//     F ~= A_lo B_hi + A_hi B_lo + A_hi B_hi        (error ~2^-22 |A||B|)
 // accumulated in fp32 in TMEM.  B (the codebook) is split once per call by
 // a prep kernel; A is split in shared memory by converter warps right after
 // its TMA lands.
 //
-// Mapping.  Persistent grid of 148 CTAs (one per SM); CTA c owns output
-// columns [256 (c % nsplit), +256) and M tiles m = c / nsplit + k * groups.
-// The codebook slice for its 256 columns (hi + lo, K-major, 128B swizzle,
-// 2 x 64 KB) stays resident in SMEM for a whole level; W tiles
-// (128 pixels x L) stream in through a 2-stage TMA ring.  One elected
-// thread issues 3 x (L / 8) MMAs of 128 x 256 x 8 per tile into one of two
-// TMEM accumulators (2 x 256 columns = all 512), so the epilogue of tile t
-// overlaps the MMAs of tile t+1.  Epilogue warps drain TMEM with
-// tcgen05.ld.32x32b and stream rows to HBM.  The kernel is HBM-store bound:
-// 4 B written per output element (D = 512, 3 levels: 9.56 GB at 1440x1080).
+// Mapping.  Persistent grid of 148 CTAs (one per SM).  CTA c owns output
+// columns [128 (c % 4), +128) of D = 512 and M tiles m = c / 4 + k * 37, so
+// the four CTAs of a group walk the same W tiles together (L2 hits).  The
+// codebook slice (hi + lo, K-major, 128B swizzle, 64 KB) stays resident in
+// SMEM; W tiles (128 pixels x L) stream in through a 2-stage TMA ring.  One
+// elected thread issues 3 x (L / 8) MMAs of 128 x 128 x 8 per tile into one
+// of four TMEM accumulators (4 x 128 columns), so epilogues of earlier tiles
+// overlap the MMAs of later ones.  Eight epilogue warps drain TMEM with
+// tcgen05.ld.32x32b into 128B-swizzled SMEM boxes (128 rows x 32 columns)
+// that TMA bulk-stores to HBM (out-of-range rows are clipped by the TMA
+// unit).  The kernel is HBM-store bound: 4 B per output element (D = 512,
+// 3 levels: 9.56 GB per 1440x1080 frame).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -31,12 +33,16 @@ namespace sf {
 namespace tc {
 
 constexpr int BM = 128;           // pixels per tile (TMEM lanes)
-constexpr int BN = 256;           // output columns per CTA (one MMA, N = 256)
+constexpr int BN = 128;           // output columns per CTA (MMA N)
 constexpr int KBOX = 32;          // fp32 per 128-byte swizzle row
-constexpr int kThreads = 320;     // 10 warps
-constexpr int kEpiWarp0 = 2;      // warps 2..5 epilogue
-constexpr int kCvtWarp0 = 6;      // warps 6..9 A splitters
-constexpr int kStages = 2;
+constexpr int kThreads = 448;     // 14 warps
+constexpr int kEpiWarp0 = 2;      // warps 2..9 epilogue: 2 sets x 4 lane quarters
+constexpr int kEpiWarps = 8;
+constexpr int kCvtWarp0 = 10;     // warps 10..13 A splitters
+constexpr int kStages = 2;        // W tile ring
+constexpr int kAcc = 4;           // TMEM accumulators (4 x 128 columns)
+constexpr int kBoxes = BN / 32;   // output boxes per tile
+constexpr int kStageBuf = 2;      // staging boxes per epilogue set
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -69,6 +75,23 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
             smem_u32(dst)),
         "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"((uint64_t)map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -112,27 +135,27 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 struct Smem {
     // operand tiles (1024-byte aligned, SW128 atoms)
-    float b_hi[64 / KBOX][BN * KBOX];   // 2 x 32 KB
-    float b_lo[64 / KBOX][BN * KBOX];   // 2 x 32 KB
+    float b_hi[64 / KBOX][BN * KBOX];        // 2 x 16 KB
+    float b_lo[64 / KBOX][BN * KBOX];        // 2 x 16 KB
     float a[kStages][64 / KBOX][BM * KBOX];  // 2 x 2 x 16 KB (hi after split)
-    float a_lo[64 / KBOX][BM * KBOX];   // 2 x 16 KB
+    float a_lo[64 / KBOX][BM * KBOX];        // 2 x 16 KB
+    float out[2][kStageBuf][BM * 32];        // 2 sets x 2 x 16 KB output staging (SW128)
     uint64_t full[kStages];      // TMA landed
     uint64_t ready[kStages];     // A split done
     uint64_t empty[kStages];     // MMAs finished reading the stage
-    uint64_t acc_full[2];        // accumulator complete
-    uint64_t acc_empty[2];       // accumulator drained
+    uint64_t acc_full[kAcc];     // accumulator complete
+    uint64_t acc_empty[kAcc];    // accumulator drained
     uint64_t b_full;             // codebook slice landed
     uint32_t tmem_base;
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
-k_decode_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int64_t P,
-            int L, int D, float* __restrict__ out, int nsplit) {
+k_decode_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+            const __grid_constant__ CUtensorMap map_out, int64_t P, int L, int D, int nsplit) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkb = L / KBOX;              // 1 or 2 K boxes
-    const int ksteps = L / 8;              // MMAs per product
     const int split = blockIdx.x % nsplit;
     const int groups = gridDim.x / nsplit;
     const int group = blockIdx.x / nsplit;
@@ -145,9 +168,9 @@ k_decode_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             mbar_init(&S.ready[s], 128);
             mbar_init(&S.empty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kAcc; ++s) {
             mbar_init(&S.acc_full[s], 1);
-            mbar_init(&S.acc_empty[s], 128);
+            mbar_init(&S.acc_empty[s], kEpiWarps * 32);
         }
         mbar_init(&S.b_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -161,117 +184,128 @@ k_decode_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     tc_fence_after();
     const uint32_t tmem = S.tmem_base;
 
-    // idesc: D f32, A/B tf32, K-major both, N = 256, M = 128
+    // idesc: D f32, A/B tf32, K-major both, N = 128, M = 128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     const uint32_t a_tile_bytes = (uint32_t)(BM * KBOX * 4) * nkb;
-
-    // the number of tiles this CTA handles per level
     const int my_tiles = (group < n_mtiles) ? (n_mtiles - group + groups - 1) / groups : 0;
 
-    // iteration counters persist across levels so barrier phases stay consistent
-    for (int level_pass = 0; level_pass < 1; ++level_pass) {
-        if (warp == 0 && lane == 0) {
-            // ---------------- TMA producer ----------------
-            mbar_expect_tx(&S.b_full, (uint32_t)(2 * nkb * BN * KBOX * 4));
-            for (int kb = 0; kb < nkb; ++kb) {
-                tma_load_2d(S.b_hi[kb], &map_b, &S.b_full, kb * KBOX, n0);
-                tma_load_2d(S.b_lo[kb], &map_b, &S.b_full, kb * KBOX, D + n0);
-            }
-            for (int i = 0; i < my_tiles; ++i) {
-                const int s = i & 1;
-                if (i >= kStages) mbar_wait(&S.empty[s], ((i / kStages) - 1) & 1);
-                const int m = group + i * groups;
-                mbar_expect_tx(&S.full[s], a_tile_bytes);
-                for (int kb = 0; kb < nkb; ++kb) tma_load_2d(S.a[s][kb], &map_a, &S.full[s], kb * KBOX, m * BM);
-            }
-        } else if (warp == 1 && lane == 0) {
-            // ---------------- MMA issuer ----------------
-            mbar_wait(&S.b_full, 0);
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer ----------------
+        mbar_expect_tx(&S.b_full, (uint32_t)(2 * nkb * BN * KBOX * 4));
+        for (int kb = 0; kb < nkb; ++kb) {
+            tma_load_2d(S.b_hi[kb], &map_b, &S.b_full, kb * KBOX, n0);
+            tma_load_2d(S.b_lo[kb], &map_b, &S.b_full, kb * KBOX, D + n0);
+        }
+        for (int i = 0; i < my_tiles; ++i) {
+            const int s = i % kStages;
+            if (i >= kStages) mbar_wait(&S.empty[s], ((i / kStages) - 1) & 1);
+            const int m = group + i * groups;
+            mbar_expect_tx(&S.full[s], a_tile_bytes);
+            for (int kb = 0; kb < nkb; ++kb) tma_load_2d(S.a[s][kb], &map_a, &S.full[s], kb * KBOX, m * BM);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer ----------------
+        mbar_wait(&S.b_full, 0);
+        tc_fence_after();
+        for (int i = 0; i < my_tiles; ++i) {
+            const int s = i % kStages, as = i % kAcc;
+            mbar_wait(&S.ready[s], (i / kStages) & 1);
+            if (i >= kAcc) mbar_wait(&S.acc_empty[as], ((i / kAcc) - 1) & 1);
             tc_fence_after();
-            for (int i = 0; i < my_tiles; ++i) {
-                const int s = i & 1, as = i & 1;
-                mbar_wait(&S.ready[s], (i / kStages) & 1);
-                if (i >= 2) mbar_wait(&S.acc_empty[as], ((i / 2) - 1) & 1);
-                tc_fence_after();
-                const uint32_t d = tmem + (uint32_t)(as * BN);
-                uint32_t acc = 0;
-                for (int kb = 0; kb < nkb; ++kb) {
-                    const uint32_t ahi = smem_u32(S.a[s][kb]);
-                    const uint32_t alo = smem_u32(S.a_lo[kb]);
-                    const uint32_t bhi = smem_u32(S.b_hi[kb]);
-                    const uint32_t blo = smem_u32(S.b_lo[kb]);
+            const uint32_t d = tmem + (uint32_t)(as * BN);
+            uint32_t acc = 0;
+            for (int kb = 0; kb < nkb; ++kb) {
+                const uint32_t ahi = smem_u32(S.a[s][kb]);
+                const uint32_t alo = smem_u32(S.a_lo[kb]);
+                const uint32_t bhi = smem_u32(S.b_hi[kb]);
+                const uint32_t blo = smem_u32(S.b_lo[kb]);
 #pragma unroll
-                    for (int k = 0; k < KBOX / 8; ++k) {
-                        const uint32_t off = k * 32;  // 8 tf32 = 32 B along the swizzled row
-                        mma_tf32(d, sw128_desc(alo + off), sw128_desc(bhi + off), idesc, acc);
-                        acc = 1;
-                        mma_tf32(d, sw128_desc(ahi + off), sw128_desc(blo + off), idesc, 1);
-                        mma_tf32(d, sw128_desc(ahi + off), sw128_desc(bhi + off), idesc, 1);
-                    }
+                for (int k = 0; k < KBOX / 8; ++k) {
+                    const uint32_t off = k * 32;  // 8 tf32 = 32 B along the swizzled row
+                    mma_tf32(d, sw128_desc(alo + off), sw128_desc(bhi + off), idesc, acc);
+                    acc = 1;
+                    mma_tf32(d, sw128_desc(ahi + off), sw128_desc(blo + off), idesc, 1);
+                    mma_tf32(d, sw128_desc(ahi + off), sw128_desc(bhi + off), idesc, 1);
                 }
-                mma_commit(&S.empty[s]);
-                mma_commit(&S.acc_full[as]);
             }
-        } else if (warp >= kCvtWarp0) {
-            // ---------------- A splitters: hi = rna(x) in place, lo = x - hi ----------------
-            const int t = threadIdx.x - kCvtWarp0 * 32;  // 0..127
-            for (int i = 0; i < my_tiles; ++i) {
-                const int s = i & 1;
-                mbar_wait(&S.full[s], (i / kStages) & 1);
-                // the single lo buffer is free once the previous tile's MMAs completed
-                if (i >= 1) mbar_wait(&S.empty[(i - 1) & 1], ((i - 1) / kStages) & 1);
-                for (int kb = 0; kb < nkb; ++kb) {
-                    float4* av = reinterpret_cast<float4*>(S.a[s][kb]);
-                    float4* lv = reinterpret_cast<float4*>(S.a_lo[kb]);
+            mma_commit(&S.empty[s]);
+            mma_commit(&S.acc_full[as]);
+        }
+    } else if (warp >= kCvtWarp0) {
+        // ---------------- A splitters: hi = rna(x) in place, lo = x - hi ----------------
+        const int t = threadIdx.x - kCvtWarp0 * 32;  // 0..127
+        for (int i = 0; i < my_tiles; ++i) {
+            const int s = i % kStages;
+            mbar_wait(&S.full[s], (i / kStages) & 1);
+            // the single lo buffer is free once the previous tile's MMAs completed
+            if (i >= 1) mbar_wait(&S.empty[(i - 1) % kStages], ((i - 1) / kStages) & 1);
+            for (int kb = 0; kb < nkb; ++kb) {
+                float4* av = reinterpret_cast<float4*>(S.a[s][kb]);
+                float4* lv = reinterpret_cast<float4*>(S.a_lo[kb]);
 #pragma unroll 4
-                    for (int j = t; j < BM * KBOX / 4; j += 128) {
-                        float4 x = av[j];
-                        float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-                        av[j] = h;
-                        lv[j] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
-                    }
+                for (int j = t; j < BM * KBOX / 4; j += 128) {
+                    float4 x = av[j];
+                    float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+                    av[j] = h;
+                    lv[j] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+                }
+            }
+            fence_proxy_async();
+            mbar_arrive(&S.ready[s]);
+        }
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
+        // ---------------- epilogue: TMEM -> swizzled SMEM box -> TMA store ----------------
+        const int quarter = warp & 3;                     // TMEM lane quarter this warp may access
+        const int set = (warp - kEpiWarp0) >> 2;          // boxes {2 set, 2 set + 1} of every tile
+        const int r = quarter * 32 + lane;                // row within the tile
+        const bool issuer = (quarter == 0 && lane == 0);
+        const int bar_id = 1 + set;
+        int nstore = 0;
+        for (int i = 0; i < my_tiles; ++i) {
+            const int as = i % kAcc;
+            const int m = group + i * groups;
+            mbar_wait(&S.acc_full[as], (i / kAcc) & 1);
+            tc_fence_after();
+            for (int bx = 0; bx < kBoxes / 2; ++bx) {
+                const int box = set * (kBoxes / 2) + bx;
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(as * BN + box * 32);
+                uint32_t v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (bx == kBoxes / 2 - 1) {  // accumulator fully read: hand it back to the MMA warp
+                    tc_fence_before();
+                    mbar_arrive(&S.acc_empty[as]);
+                }
+                // staging slot must be drained by the TMA store issued two boxes ago
+                const int slot = nstore % kStageBuf;
+                if (issuer) bulk_wait_read<kStageBuf - 1>();
+                named_bar(bar_id, 128);
+                float* buf = S.out[set][slot];
+                unsigned char* rowp = reinterpret_cast<unsigned char*>(buf) + r * 128;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const int pc = c ^ (r & 7);
+                    *reinterpret_cast<uint4*>(rowp + pc * 16) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
                 }
                 fence_proxy_async();
-                mbar_arrive(&S.ready[s]);
-            }
-        } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-            // ---------------- epilogue: TMEM -> registers -> HBM ----------------
-            const int quarter = warp & 3;           // TMEM lane quarter this warp may access
-            const int row_in_tile = quarter * 32 + lane;
-            for (int i = 0; i < my_tiles; ++i) {
-                const int as = i & 1;
-                const int m = group + i * groups;
-                mbar_wait(&S.acc_full[as], (i / 2) & 1);
-                tc_fence_after();
-                const int64_t row = (int64_t)m * BM + row_in_tile;
-                float* dst = out + row * D + n0;
-                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(as * BN);
-#pragma unroll 1
-                for (int c = 0; c < BN; c += 32) {
-                    uint32_t r[32];
-                    asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-                        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-                          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-                          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-                          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                        : "r"(taddr + (uint32_t)c));
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (row < P) {
-                        float4* d4 = reinterpret_cast<float4*>(dst + c);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            __stcs(d4 + j, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                                       __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
-                    }
+                named_bar(bar_id, 128);
+                if (issuer) {
+                    tma_store_2d(&map_out, buf, n0 + box * 32, m * BM);
+                    bulk_commit();
                 }
-                tc_fence_before();
-                mbar_arrive(&S.acc_empty[as]);
+                ++nstore;
             }
         }
+        if (issuer) bulk_wait<0>();
     }
     tc_fence_before();
     __syncthreads();
@@ -322,21 +356,22 @@ static int make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint6
 
 size_t decode_ws_bytes(int L, int D) { return (size_t)2 * L * D * sizeof(float); }
 
-bool decode_tc_supported(int64_t P, int L, int D, const float* w, int64_t w_stride) {
+static bool decode_tc_supported(int64_t P, int L, int D, const float* w, int64_t w_stride, const float* out) {
     return (L == 32 || L == 64) && D % tc::BN == 0 && ((uintptr_t)w % 16) == 0 && (w_stride * 4) % 16 == 0 &&
-           P > 0;
+           ((uintptr_t)out % 16) == 0 && P > 0 && P < (int64_t)1 << 31;
 }
 
 int launch_decode(int64_t P, int L, int D, const float* w, int64_t w_stride, const float* cb, float* out,
                   void* ws, cudaStream_t st) {
     if (P == 0) return 0;
-    if (!decode_tc_supported(P, L, D, w, w_stride) || ws == nullptr)
+    if (!decode_tc_supported(P, L, D, w, w_stride, out) || ws == nullptr)
         return launch_decode_simt(P, L, D, w, w_stride, cb, out, st);
     float* bsplit = (float*)ws;
     tc::k_split_codebook<<<ceil_div((int64_t)L * D, 256), 256, 0, st>>>(cb, L, D, bsplit);
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, mo;
     if (make_map_2d(&ma, w, (uint64_t)L, (uint64_t)P, (uint64_t)w_stride * 4, tc::KBOX, tc::BM)) return -3;
     if (make_map_2d(&mb, bsplit, (uint64_t)L, (uint64_t)2 * D, (uint64_t)L * 4, tc::KBOX, tc::BN)) return -3;
+    if (make_map_2d(&mo, out, (uint64_t)D, (uint64_t)P, (uint64_t)D * 4, 32, tc::BM)) return -3;
     static int num_sms = 0;
     if (!num_sms) {
         int dev;
@@ -354,7 +389,7 @@ int launch_decode(int64_t P, int L, int D, const float* w, int64_t w_stride, con
         cudaFuncSetAttribute(tc::k_decode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    tc::k_decode_tc<<<groups * nsplit, tc::kThreads, smem, st>>>(ma, mb, P, L, D, out, nsplit);
+    tc::k_decode_tc<<<groups * nsplit, tc::kThreads, smem, st>>>(ma, mb, mo, P, L, D, nsplit);
     return 0;
 }
 
