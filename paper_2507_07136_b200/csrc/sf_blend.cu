@@ -108,7 +108,9 @@ __device__ __forceinline__ void stage_batch(BlendStage& S, const BlendArgs& A, u
     }
 }
 
-template <int CT, bool SINGLE>
+// CT: channels per Gaussian (0 = runtime), SINGLE: one channel block,
+// NV: fused relevancy vectors (0 = none, -1 = runtime count).
+template <int CT, bool SINGLE, int NV>
 __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_block) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
         for (int idx = threadIdx.x; idx < nb * C; idx += kBlendThreads) {
             int j = idx / C, k = idx - j * C;
             int ch = (int)reinterpret_cast<const uint16_t*>(B.chan + j * kMaxChanRec)[k] - ch0;
-            B.off[j][k] = ((unsigned)ch < (unsigned)nchb) ? (uint32_t)(ch * kAccPitch) : 0xffffffffu;
+            B.off[j][k] = ((unsigned)ch < (unsigned)nchb) ? (uint32_t)(ch * kAccPitch * 4) : 0xffffffffu;
         }
         __syncthreads();
 
@@ -199,17 +201,31 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
                 }
                 if (__any_sync(0xffffffffu, ef > 0.f)) {
                     const float* val = reinterpret_cast<const float*>(B.chan + j * kMaxChanRec + voff);
-                    float* accs = acc + slot;
-                    if (CT > 0) {
+                    char* accs = reinterpret_cast<char*>(acc + slot);
+                    if (CT > 0 && CT % 4 == 0) {
+                        const uint4* o4 = reinterpret_cast<const uint4*>(B.off[j]);
+                        const float4* v4 = reinterpret_cast<const float4*>(val);
 #pragma unroll
-                        for (int k = 0; k < (CT > 0 ? CT : 1); ++k) {
-                            const uint32_t off = B.off[j][k];
-                            if (SINGLE || off != 0xffffffffu) accs[off] = fmaf(ef, val[k], accs[off]);
+                        for (int q = 0; q < (CT > 0 ? CT : 4) / 4; ++q) {
+                            const uint4 o = o4[q];
+                            const float4 v = v4[q];
+                            const uint32_t oo[4] = {o.x, o.y, o.z, o.w};
+                            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                if (SINGLE || oo[e] != 0xffffffffu) {
+                                    float* a = reinterpret_cast<float*>(accs + oo[e]);
+                                    *a = fmaf(ef, vv[e], *a);
+                                }
+                            }
                         }
                     } else {
                         for (int k = 0; k < C; ++k) {
                             const uint32_t off = B.off[j][k];
-                            if (off != 0xffffffffu) accs[off] = fmaf(ef, val[k], accs[off]);
+                            if (off != 0xffffffffu) {
+                                float* a = reinterpret_cast<float*>(accs + off);
+                                *a = fmaf(ef, val[k], *a);
+                            }
                         }
                     }
                 }
@@ -235,10 +251,10 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
             }
         }
     }
-    if (A.proj_cb && nchb == A.n_ch) {
+    if (NV != 0 && A.proj_cb && nchb == A.n_ch) {
         // fused relevancy: logits_j = sum_l W[l] * P[b][l][j] in fp64; the
         // projected codebook is staged in the idle batch buffers
-        const int nv = 1 + A.n_canon;
+        const int nv = NV > 0 ? NV : 1 + A.n_canon;
         const int np = A.n_levels * A.L * nv;
         double* Ps = reinterpret_cast<double*>(&S.st[0]);
         const bool fits = np * (int)sizeof(double) <= (int)sizeof(S.st);
@@ -246,29 +262,30 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
             for (int i = threadIdx.x; i < np; i += kBlendThreads) Ps[i] = A.proj_cb[i];
             __syncthreads();
         }
-        const double* Pb = fits ? Ps : A.proj_cb;
         if (inside) {
-            constexpr int kV = 8;
             for (int b = 0; b < A.n_levels; ++b) {
-                const double* P = Pb + (size_t)b * A.L * nv;
-                double lq = 0.0, best = INFINITY;
-                for (int j0 = 0; j0 < nv; j0 += kV) {
-                    double lg[kV];
+                double best = INFINITY;
+                if (NV > 0 && fits) {
+                    const double* P = Ps + (size_t)b * A.L * nv;
+                    double lg[NV > 0 ? NV : 1];
 #pragma unroll
-                    for (int t = 0; t < kV; ++t) lg[t] = 0.0;
-                    const int nj = min(kV, nv - j0);
+                    for (int t = 0; t < (NV > 0 ? NV : 1); ++t) lg[t] = 0.0;
                     for (int l = 0; l < A.L; ++l) {
                         const double w = (double)acc[(b * A.L + l) * kAccPitch + slot];
-                        const double* Pl = P + l * nv + j0;
 #pragma unroll
-                        for (int t = 0; t < kV; ++t)
-                            if (t < nj) lg[t] = fma(w, Pl[t], lg[t]);
+                        for (int t = 0; t < (NV > 0 ? NV : 1); ++t) lg[t] = fma(w, P[l * (NV > 0 ? NV : 1) + t], lg[t]);
                     }
 #pragma unroll
-                    for (int t = 0; t < kV; ++t) {
-                        if (t >= nj) break;
-                        if (j0 + t == 0) lq = lg[t];
-                        else best = np_minimum(best, sigmoid2(lq - lg[t]));
+                    for (int t = 1; t < (NV > 0 ? NV : 1); ++t) best = np_minimum(best, sigmoid2(lg[0] - lg[t]));
+                } else {
+                    const double* P = (fits ? Ps : A.proj_cb) + (size_t)b * A.L * nv;
+                    double lq = 0.0;
+                    for (int l = 0; l < A.L; ++l) lq = fma((double)acc[(b * A.L + l) * kAccPitch + slot], P[l * nv], lq);
+                    for (int j = 1; j < nv; ++j) {
+                        double lc = 0.0;
+                        for (int l = 0; l < A.L; ++l)
+                            lc = fma((double)acc[(b * A.L + l) * kAccPitch + slot], P[l * nv + j], lc);
+                        best = np_minimum(best, sigmoid2(lq - lc));
                     }
                 }
                 A.relevancy_raw[(size_t)b * A.W * A.H + (size_t)py * A.W + px] = best;
@@ -277,27 +294,67 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
     }
 }
 
-// Relevancy from a coefficient map in HBM (used when the channel count does
-// not fit one blend CTA).  One thread per pixel.
-__global__ void k_relevancy_from_cmap(int64_t P, int n_ch, const float* __restrict__ cmap,
-                                      const double* __restrict__ proj_cb, int n_levels, int L,
-                                      int n_canon, double* __restrict__ out) {
+// Relevancy from a coefficient map in HBM (the map is written anyway when the
+// features are decoded, or the channel count exceeds one blend CTA).  One
+// thread per pixel; the projected codebook sits in shared memory.
+template <int NV>
+__global__ void __launch_bounds__(256) k_relevancy_from_cmap(int64_t P, int n_ch, const float* __restrict__ cmap,
+                                                             const double* __restrict__ proj_cb, int n_levels,
+                                                             int L, int n_canon, double* __restrict__ out) {
+    extern __shared__ double Ps[];
+    const int nv = NV > 0 ? NV : 1 + n_canon;
+    for (int i = threadIdx.x; i < n_levels * L * nv; i += blockDim.x) Ps[i] = proj_cb[i];
+    __syncthreads();
     int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P) return;
-    const int nv = 1 + n_canon;
     const float* w = cmap + (size_t)p * n_ch;
     for (int b = 0; b < n_levels; ++b) {
-        const double* Pm = proj_cb + (size_t)b * L * nv;
-        double lq = 0.0;
-        for (int l = 0; l < L; ++l) lq = fma((double)w[b * L + l], Pm[l * nv], lq);
+        const double* Pm = Ps + (size_t)b * L * nv;
         double best = INFINITY;
-        for (int j = 1; j < nv; ++j) {
-            double lc = 0.0;
-            for (int l = 0; l < L; ++l) lc = fma((double)w[b * L + l], Pm[l * nv + j], lc);
-            best = np_minimum(best, sigmoid2(lq - lc));
+        if (NV > 0) {
+            double lg[NV > 0 ? NV : 1];
+#pragma unroll
+            for (int t = 0; t < (NV > 0 ? NV : 1); ++t) lg[t] = 0.0;
+            for (int l0 = 0; l0 < L; l0 += 4) {
+                const float4 w4 = __ldcs(reinterpret_cast<const float4*>(w + b * L + l0));
+                const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const double wd = (double)wv[e];
+#pragma unroll
+                    for (int t = 0; t < (NV > 0 ? NV : 1); ++t) lg[t] = fma(wd, Pm[(l0 + e) * (NV > 0 ? NV : 1) + t], lg[t]);
+                }
+            }
+#pragma unroll
+            for (int t = 1; t < (NV > 0 ? NV : 1); ++t) best = np_minimum(best, sigmoid2(lg[0] - lg[t]));
+        } else {
+            double lq = 0.0;
+            for (int l = 0; l < L; ++l) lq = fma((double)w[b * L + l], Pm[l * nv], lq);
+            for (int j = 1; j < nv; ++j) {
+                double lc = 0.0;
+                for (int l = 0; l < L; ++l) lc = fma((double)w[b * L + l], Pm[l * nv + j], lc);
+                best = np_minimum(best, sigmoid2(lq - lc));
+            }
         }
         out[(size_t)b * P + p] = best;
     }
+}
+
+void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const double* proj_cb, int n_levels,
+                                int L, int n_canon, double* out, cudaStream_t st) {
+    if (P == 0) return;
+    const size_t smem = sizeof(double) * (size_t)n_levels * L * (1 + n_canon);
+    const bool vec = (L % 4 == 0) && (n_ch % 4 == 0) && ((uintptr_t)cmap % 16 == 0);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_relevancy_from_cmap<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_relevancy_from_cmap<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    if (vec && n_canon == 4)
+        k_relevancy_from_cmap<5><<<ceil_div(P, 256), 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out);
+    else
+        k_relevancy_from_cmap<0><<<ceil_div(P, 256), 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out);
 }
 
 static bool init_exp_table() {
@@ -317,20 +374,23 @@ int launch_blend(const BlendArgs& a, cudaStream_t st) {
     int ch_block = a.n_ch < kChBlock ? a.n_ch : kChBlock;
     int nblk = (a.n_ch + ch_block - 1) / ch_block;
     size_t smem = sizeof(BlendSmem) + (size_t)ch_block * kAccPitch * sizeof(float);
-    auto kern = (a.C == 12 && nblk == 1) ? k_blend<12, true> : k_blend<0, false>;
-    static size_t configured[2] = {0, 0};
-    const int ki = (a.C == 12 && nblk == 1) ? 0 : 1;
+    const bool fast = (a.C == 12 && nblk == 1);
+    const int nv = a.proj_cb ? 1 + a.n_canon : 0;
+    void (*kern)(BlendArgs, int);
+    int ki;
+    if (fast && nv == 0) { kern = k_blend<12, true, 0>; ki = 0; }
+    else if (fast && nv == 5) { kern = k_blend<12, true, 5>; ki = 1; }
+    else if (fast) { kern = k_blend<12, true, -1>; ki = 2; }
+    else { kern = k_blend<0, false, -1>; ki = 3; }
+    static size_t configured[4] = {0, 0, 0, 0};
     if (smem > configured[ki]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured[ki] = smem;
     }
     if (n_tiles > 0) kern<<<dim3(n_tiles, nblk), kBlendThreads, smem, st>>>(a, ch_block);
-    if (a.proj_cb && nblk > 1) {
-        int64_t P = (int64_t)a.W * a.H;
-        k_relevancy_from_cmap<<<ceil_div(P, 256), 256, 0, st>>>(P, a.n_ch, a.coeff_map, a.proj_cb,
-                                                               a.n_levels, a.L, a.n_canon,
-                                                               a.relevancy_raw);
-    }
+    if (a.proj_cb && nblk > 1)
+        launch_relevancy_from_cmap((int64_t)a.W * a.H, a.n_ch, a.coeff_map, a.proj_cb, a.n_levels, a.L,
+                                   a.n_canon, a.relevancy_raw, st);
     return 0;
 }
 

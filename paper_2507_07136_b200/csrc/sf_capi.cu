@@ -193,12 +193,18 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     a.stats = ws.stats;
     a.coeff_map = f->coeff_map;
     a.final_t = f->final_t;
-    a.proj_cb = q ? ws.proj_cb : nullptr;
+    // relevancy: from the coefficient map in HBM when it is written anyway
+    // (features decoded), else fused into the blend epilogue
+    const bool rel_from_map = q && f->coeff_map != nullptr;
+    a.proj_cb = (q && !rel_from_map) ? ws.proj_cb : nullptr;
     a.n_levels = f->n_levels;
     a.L = L;
     a.n_canon = q ? q->n_canonicals : 0;
     a.relevancy_raw = q ? f->relevancy_raw : nullptr;
     if (launch_blend(a, st)) return fail(SF_ERR_VALIDATION, "blend configuration unsupported");
+    if (rel_from_map)
+        launch_relevancy_from_cmap((int64_t)W * H, n_ch, f->coeff_map, ws.proj_cb, f->n_levels, L,
+                                   q->n_canonicals, f->relevancy_raw, st);
     if (f->events[1]) cudaEventRecord((cudaEvent_t)f->events[1], st);
     // K7
     if (f->features) {

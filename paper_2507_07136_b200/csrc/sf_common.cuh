@@ -113,10 +113,11 @@ __host__ __device__ __forceinline__ Proj64 geom_proj(const GeomRec& g) {
     p.c = g.c64;
     return p;
 }
-// Scatter plan of one Gaussian (sparse_splat.py:126-132): C channel ids
-// (level block * L + index) then C values, padded to 16 bytes.
-__host__ __device__ __forceinline__ int chan_rec_bytes(int C) { return ((2 * C + 3) / 4 * 4 + 4 * C + 15) / 16 * 16; }
-__host__ __device__ __forceinline__ int chan_val_offset(int C) { return (2 * C + 3) / 4 * 4; }
+// Scatter plan of one Gaussian (sparse_splat.py:126-132): C u16 channel ids
+// (level block * L + index), then at a 16-byte boundary C f32 values, padded
+// to 16 bytes (C = 12 -> 80 B).
+__host__ __device__ __forceinline__ int chan_val_offset(int C) { return (2 * C + 15) / 16 * 16; }
+__host__ __device__ __forceinline__ int chan_rec_bytes(int C) { return chan_val_offset(C) + (4 * C + 15) / 16 * 16; }
 
 // Workspace carving helper.
 struct Carver {
@@ -188,6 +189,9 @@ struct BlendArgs {
     int64_t* fixups;
 };
 int launch_blend(const BlendArgs& a, cudaStream_t st);
+// relevancy of every pixel/level from a coefficient map already in HBM
+void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const double* proj_cb,
+                                int n_levels, int L, int n_canon, double* out, cudaStream_t st);
 
 // sf_post.cu
 void launch_project_codebook(const float* codebooks, const LevelSelDev& levels, int L, int D,

@@ -36,13 +36,13 @@ constexpr int BM = 128;           // pixels per tile (TMEM lanes)
 constexpr int BN = 128;           // output columns per CTA (MMA N)
 constexpr int KBOX = 32;          // fp32 per 128-byte swizzle row
 constexpr int kThreads = 448;     // 14 warps
-constexpr int kEpiWarp0 = 2;      // warps 2..9 epilogue: 2 sets x 4 lane quarters
+constexpr int kEpiWarp0 = 2;      // warps 2..9 epilogue: 2 column halves x 4 lane quarters
 constexpr int kEpiWarps = 8;
 constexpr int kCvtWarp0 = 10;     // warps 10..13 A splitters
 constexpr int kStages = 2;        // W tile ring
 constexpr int kAcc = 4;           // TMEM accumulators (4 x 128 columns)
 constexpr int kBoxes = BN / 32;   // output boxes per tile
-constexpr int kStageBuf = 2;      // staging boxes per epilogue set
+constexpr int kStageBuf = 2;      // output staging boxes (double buffer)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -139,7 +139,7 @@ struct Smem {
     float b_lo[64 / KBOX][BN * KBOX];        // 2 x 16 KB
     float a[kStages][64 / KBOX][BM * KBOX];  // 2 x 2 x 16 KB (hi after split)
     float a_lo[64 / KBOX][BM * KBOX];        // 2 x 16 KB
-    float out[2][kStageBuf][BM * 32];        // 2 sets x 2 x 16 KB output staging (SW128)
+    float out[kStageBuf][BM * 32];           // 2 x 16 KB output staging (SW128)
     uint64_t full[kStages];      // TMA landed
     uint64_t ready[kStages];     // A split done
     uint64_t empty[kStages];     // MMAs finished reading the stage
@@ -255,51 +255,48 @@ k_decode_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
         // ---------------- epilogue: TMEM -> swizzled SMEM box -> TMA store ----------------
+        // warp (quarter, half) drains rows 32*quarter.. and columns 16*half.. of each 32-column box
         const int quarter = warp & 3;                     // TMEM lane quarter this warp may access
-        const int set = (warp - kEpiWarp0) >> 2;          // boxes {2 set, 2 set + 1} of every tile
+        const int half = (warp - kEpiWarp0) >> 2;
         const int r = quarter * 32 + lane;                // row within the tile
-        const bool issuer = (quarter == 0 && lane == 0);
-        const int bar_id = 1 + set;
+        const bool issuer = (warp == kEpiWarp0 && lane == 0);
+        const int bar_id = 1;
+        const int nthr = kEpiWarps * 32;
         int nstore = 0;
         for (int i = 0; i < my_tiles; ++i) {
             const int as = i % kAcc;
             const int m = group + i * groups;
             mbar_wait(&S.acc_full[as], (i / kAcc) & 1);
             tc_fence_after();
-            for (int bx = 0; bx < kBoxes / 2; ++bx) {
-                const int box = set * (kBoxes / 2) + bx;
-                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(as * BN + box * 32);
-                uint32_t v[32];
+            for (int box = 0; box < kBoxes; ++box) {
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(as * BN + box * 32 + half * 16);
+                uint32_t v[16];
                 asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
                       "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
-                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
-                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                      "=r"(v[14]), "=r"(v[15])
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (bx == kBoxes / 2 - 1) {  // accumulator fully read: hand it back to the MMA warp
+                if (box == kBoxes - 1) {  // accumulator fully read: hand it back to the MMA warp
                     tc_fence_before();
                     mbar_arrive(&S.acc_empty[as]);
                 }
                 // staging slot must be drained by the TMA store issued two boxes ago
                 const int slot = nstore % kStageBuf;
                 if (issuer) bulk_wait_read<kStageBuf - 1>();
-                named_bar(bar_id, 128);
-                float* buf = S.out[set][slot];
-                unsigned char* rowp = reinterpret_cast<unsigned char*>(buf) + r * 128;
+                named_bar(bar_id, nthr);
+                unsigned char* rowp = reinterpret_cast<unsigned char*>(S.out[slot]) + r * 128;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const int pc = c ^ (r & 7);
+                for (int c = 0; c < 4; ++c) {
+                    const int pc = (half * 4 + c) ^ (r & 7);
                     *reinterpret_cast<uint4*>(rowp + pc * 16) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
                 }
                 fence_proxy_async();
-                named_bar(bar_id, 128);
+                named_bar(bar_id, nthr);
                 if (issuer) {
-                    tma_store_2d(&map_out, buf, n0 + box * 32, m * BM);
+                    tma_store_2d(&map_out, S.out[slot], n0 + box * 32, m * BM);
                     bulk_commit();
                 }
                 ++nstore;

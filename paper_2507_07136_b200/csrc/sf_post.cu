@@ -160,13 +160,22 @@ __global__ void __launch_bounds__(256) k_reduce_maps(int64_t hw, const double* _
     if (threadIdx.x == 0) partial[(size_t)m * gridDim.x + blockIdx.x] = r;
 }
 
+// One warp per map reduces the per-block partials; thread 0 then selects.
 __global__ void k_finalize_select(int n_maps, int nblk, int W, const MaxMin* __restrict__ partial,
                                   int fixed_level, int64_t* stats_i64, double* stats_f64) {
     __shared__ MaxMin per_map[32];
-    if (threadIdx.x < n_maps) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp < n_maps) {
         MaxMin acc{-INFINITY, INT64_MAX, INFINITY};
-        for (int b = 0; b < nblk; ++b) acc = mm_combine(acc, partial[(size_t)threadIdx.x * nblk + b]);
-        per_map[threadIdx.x] = acc;
+        for (int b = lane; b < nblk; b += 32) acc = mm_combine(acc, partial[(size_t)warp * nblk + b]);
+        for (int o = 16; o > 0; o >>= 1) {
+            MaxMin other;
+            other.mx = __shfl_xor_sync(0xffffffffu, acc.mx, o);
+            other.idx = __shfl_xor_sync(0xffffffffu, acc.idx, o);
+            other.mn = __shfl_xor_sync(0xffffffffu, acc.mn, o);
+            acc = mm_combine(acc, other);
+        }
+        if (lane == 0) per_map[warp] = acc;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -208,8 +217,8 @@ void launch_select_segment(int n_maps, int H, int W, const double* maps, int fix
     int64_t hw = (int64_t)H * W;
     MaxMin* partial = (MaxMin*)ws;
     k_reduce_maps<<<dim3(kRedBlocks, n_maps), 256, 0, st>>>(hw, maps, partial);
-    k_finalize_select<<<1, 32, 0, st>>>(n_maps, kRedBlocks, W, partial, fixed_level, stats_i64,
-                                        stats_f64);
+    k_finalize_select<<<1, 32 * n_maps, 0, st>>>(n_maps, kRedBlocks, W, partial, fixed_level, stats_i64,
+                                                  stats_f64);
     if (mask) k_mask<<<ceil_div(hw, 256), 256, 0, st>>>(hw, maps, stats_i64, stats_f64, threshold, mask);
 }
 
