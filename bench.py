@@ -343,6 +343,7 @@ def main():
                 "parallelism": f"views x{world}" if world > 1 else "single",
                 "l2": "inputs/outputs larger than L2 (9.56 GB of features per frame)",
                 "visible": int(st[N.STAT_VISIBLE]), "pairs": int(st[N.STAT_PAIRS]),
+                "exact_fp64_fixup_pixels": int(st[7]),
             },
             "fps": {"text_query_full": fps_total / world,
                     "feature_splat": extra["feature_splat"],

@@ -101,7 +101,7 @@ typedef struct SfFrame {
 #define SF_STAT_ROW 4         /* localize() row */
 #define SF_STAT_COL 5         /* localize() col */
 #define SF_STAT_DEGENERATE 6  /* segment().degenerate */
-#define SF_STAT_FIXUPS 7      /* q~9 fp64 re-evaluations (diagnostic) */
+#define SF_STAT_FIXUPS 7      /* pixels replayed exactly in fp64 (ambiguous early exit) */
 /* stats_f64 slots */
 #define SF_STATF_MIN 0        /* chosen map min */
 #define SF_STATF_MAX 1        /* chosen map max */

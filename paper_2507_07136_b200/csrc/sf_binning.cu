@@ -61,8 +61,8 @@ __global__ void __launch_bounds__(256) k_rank_gather(int64_t G, const uint32_t* 
     q.my_hi = (float)p.my;
     q.my_lo = (float)(p.my - (double)q.my_hi);
     q.a = (float)p.a;
-    q.b2 = (float)(2.0 * p.b);
-    q.c = (float)p.c;
+    q.k = (float)(p.b / p.a);
+    q.d = (float)((p.a * p.c - p.b * p.b) / p.a);
     q.opacity = opac_by_row ? opac_by_row[row] : 0.f;
     q.mx = p.mx;
     q.my = p.my;
@@ -81,9 +81,23 @@ __global__ void __launch_bounds__(256) k_rank_gather(int64_t G, const uint32_t* 
             int lv = levels.lv[b];
             const uint16_t* ip = cidx + ((int64_t)lv * G + row) * K;
             const float* vp = cval + ((int64_t)lv * G + row) * K;
-            for (int k = 0; k < K; ++k) {
-                ch[b * K + k] = (uint16_t)(ip[k] + b * L);
-                val[b * K + k] = vp[k];
+            if (K == 4) {  // 8-byte index and 16-byte value loads
+                const uint2 i2 = __ldg(reinterpret_cast<const uint2*>(ip));
+                const float4 v4 = __ldg(reinterpret_cast<const float4*>(vp));
+                const uint16_t off = (uint16_t)(b * L);
+                ch[b * 4 + 0] = (uint16_t)((i2.x & 0xffffu) + off);
+                ch[b * 4 + 1] = (uint16_t)((i2.x >> 16) + off);
+                ch[b * 4 + 2] = (uint16_t)((i2.y & 0xffffu) + off);
+                ch[b * 4 + 3] = (uint16_t)((i2.y >> 16) + off);
+                val[b * 4 + 0] = v4.x;
+                val[b * 4 + 1] = v4.y;
+                val[b * 4 + 2] = v4.z;
+                val[b * 4 + 3] = v4.w;
+            } else {
+                for (int k = 0; k < K; ++k) {
+                    ch[b * K + k] = (uint16_t)(ip[k] + b * L);
+                    val[b * K + k] = vp[k];
+                }
             }
         }
     }
@@ -255,16 +269,52 @@ __device__ void block_radix_split_global(uint32_t* a, uint32_t* b, int n, int nb
     }
 }
 
-__global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ offsets,
-                                                   uint32_t* __restrict__ entries,
-                                                   uint32_t* __restrict__ scratch,
-                                                   const int64_t* __restrict__ stats) {
+__device__ __forceinline__ int rank_bits(const int64_t* stats) {
+    int64_t nvis = stats[SF_STAT_VISIBLE];
+    int nbits = 1;
+    while (nbits < 32 && ((int64_t)1 << nbits) < nvis) ++nbits;
+    return nbits;
+}
+
+// Tiles with n <= 256 * ITEMS: CUB block radix sort in registers/shared memory.
+template <int ITEMS>
+__global__ void __launch_bounds__(256) k_tile_sort_small(const uint32_t* __restrict__ offsets,
+                                                         uint32_t* __restrict__ entries, int lo_exclusive,
+                                                         const int64_t* __restrict__ stats) {
+    if (stats[SF_STAT_OVERFLOW]) return;
+    typedef cub::BlockRadixSort<uint32_t, 256, ITEMS> Sort;
+    __shared__ typename Sort::TempStorage tmp;
+    const int t = blockIdx.x;
+    const uint32_t beg = offsets[t], end = offsets[t + 1];
+    const int n = (int)(end - beg);
+    if (n <= lo_exclusive || n > 256 * ITEMS || n <= 1) return;
+    uint32_t keys[ITEMS];
+    uint32_t* e = entries + beg;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int idx = threadIdx.x * ITEMS + i;
+        keys[i] = (idx < n) ? e[idx] : 0xffffffffu;
+    }
+    Sort(tmp).Sort(keys, 0, rank_bits(stats));
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int idx = threadIdx.x * ITEMS + i;
+        if (idx < n) e[idx] = keys[i];
+    }
+}
+
+// Longer lists: bitonic sort in shared memory up to 8192 entries, else a
+// stable 1-bit LSD split through global scratch.
+__global__ void __launch_bounds__(256) k_tile_sort_large(const uint32_t* __restrict__ offsets,
+                                                         uint32_t* __restrict__ entries,
+                                                         uint32_t* __restrict__ scratch, int lo_exclusive,
+                                                         const int64_t* __restrict__ stats) {
     if (stats[SF_STAT_OVERFLOW]) return;
     __shared__ uint32_t s[kSortSmemElems];
     int t = blockIdx.x;
     uint32_t beg = offsets[t], end = offsets[t + 1];
     int n = (int)(end - beg);
-    if (n <= 1) return;
+    if (n <= lo_exclusive) return;
     uint32_t* e = entries + beg;
     if (n <= kSortSmemElems) {
         int N = 2;
@@ -274,10 +324,7 @@ __global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ 
         block_bitonic_sort(s, N);
         for (int i = threadIdx.x; i < n; i += blockDim.x) e[i] = s[i];
     } else {
-        int64_t nvis = stats[SF_STAT_VISIBLE];
-        int nbits = 1;
-        while (nbits < 32 && ((int64_t)1 << nbits) < nvis) ++nbits;
-        block_radix_split_global(e, scratch + beg, n, nbits);
+        block_radix_split_global(e, scratch + beg, n, rank_bits(stats));
     }
 }
 
@@ -293,7 +340,11 @@ void launch_binning(int64_t G, const int64_t* stats_n, const GeomRec* geom, int 
     k_tile_scan<<<1, 1024, 0, st>>>(n_tiles, tile_counts, tile_offsets, tile_cursor, pair_capacity,
                                     stats);
     if (blocks) k_emit_pairs<<<blocks, 256, 0, st>>>(G, stats_n, geom, g, tile_cursor, entries);
-    k_tile_sort<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, stats);
+    // per-tile canonical order: most lists fit one CUB block sort (<= 2048),
+    // the rest go to the larger-capacity kernels (each CTA skips other sizes)
+    k_tile_sort_small<8><<<n_tiles, 256, 0, st>>>(tile_offsets, entries, 1, stats);
+    k_tile_sort_small<24><<<n_tiles, 256, 0, st>>>(tile_offsets, entries, 256 * 8, stats);
+    k_tile_sort_large<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, 256 * 24, stats);
 }
 
 }  // namespace sf

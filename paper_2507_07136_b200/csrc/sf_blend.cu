@@ -34,6 +34,8 @@
 // the canonical phrases via the projected codebook P = atoms @ [q; c]^T
 // (fp64), then relevancy = min_j sigmoid(l_q - l_j) (query.py:65-84) -- the
 // coefficient tile never has to be re-read from HBM for the query.
+#include <algorithm>
+
 #include "sf_common.cuh"
 
 namespace sf {
@@ -44,10 +46,6 @@ constexpr int kAccPitch = 257;
 constexpr int kMaxC = 16;            // channels per Gaussian (levels*K) supported
 constexpr int kMaxChanRec = 96;      // chan_rec_bytes(16)
 constexpr int kChBlock = 192;        // accumulator channels per CTA (smem bound)
-constexpr int kExpSteps = 128;       // exp table resolution in y = q / 2
-constexpr int kExpTable = 577;       // y in [0, 4.5]
-
-__constant__ double c_exp_table[kExpTable];
 
 struct __align__(16) BlendStage {
     GeomRec g[kBatch];
@@ -57,7 +55,6 @@ struct __align__(16) BlendStage {
 
 struct __align__(16) BlendSmem {
     BlendStage st[2];
-    double exp_tab[kExpTable + 1];
 };
 
 __device__ __forceinline__ double sigmoid2(double x) {
@@ -77,19 +74,6 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// exp(-y) for y in [0, 4.5]: table at k/128 times a degree-5 Taylor
-// polynomial on f in [0, 1/128) (truncation < 3.2e-16 relative).
-__device__ __forceinline__ double exp_neg(double y, const double* tab) {
-    int k = (int)(y * (double)kExpSteps);  // exact scaling, truncation = floor (y >= 0)
-    double f = fma(-(double)k, 1.0 / kExpSteps, y);  // exact: y - k/128
-    double p = fma(f, -1.0 / 120.0, 1.0 / 24.0);
-    p = fma(p, f, -1.0 / 6.0);
-    p = fma(p, f, 0.5);
-    p = fma(p, f, -1.0);
-    p = fma(p, f, 1.0);
-    return tab[k] * p;
-}
-
 // Issue the cp.async copies of one batch (nb records) into stage buffer S.
 __device__ __forceinline__ void stage_batch(BlendStage& S, const BlendArgs& A, uint32_t base, int nb, int cs) {
     const int gchunks = (int)(sizeof(GeomRec) / 16);  // 5
@@ -106,6 +90,31 @@ __device__ __forceinline__ void stage_batch(BlendStage& S, const BlendArgs& A, u
             cp_async16(S.chan + j * kMaxChanRec + 16 * c, A.chan + (size_t)r * cs + 16 * c);
         }
     }
+}
+
+// alpha = min(o exp(-q/2), 0.99) with q <= 9 membership (0 if outside).
+// q is evaluated in fp32 as a (dx + k dy)^2 + d dy^2 (no cancellation); inside
+// the guard band around 9 the reference's fp64 q decides (rasterizer.py:161-168).
+__device__ __forceinline__ float blend_alpha(const GeomRec& g, float pxf, float pyf, double pxd, double pyd) {
+    constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 / ln 2
+    const float dx = (pxf - g.mx_hi) - g.mx_lo;
+    const float dy = (pyf - g.my_hi) - g.my_lo;
+    const float u = fmaf(g.k, dy, dx);
+    const float ddy = g.d * dy * dy;
+    float q32 = fmaf(g.a * u, u, ddy);
+    const float su = fabsf(dx) + fabsf(g.k * dy);
+    const float guard = fmaf(1e-5f, fmaf(g.a * su, su, ddy), 1e-5f);
+    if (q32 > 9.f + guard) return 0.f;
+    if (q32 > 9.f - guard) {
+        double ddx = __dadd_rn(pxd, -g.mx), ddyd = __dadd_rn(pyd, -g.my);
+        double t1 = __dmul_rn(__dmul_rn(g.a64, ddx), ddx);
+        double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, g.b64), ddx), ddyd);
+        double t3 = __dmul_rn(__dmul_rn(g.c64, ddyd), ddyd);
+        double q = __dadd_rn(__dadd_rn(t1, t2), t3);
+        if (!(q <= SF_CUTOFF)) return 0.f;
+        q32 = (float)q;
+    }
+    return fminf(g.opacity * exp2f(kNegHalfLog2e * q32), 0.99f);
 }
 
 // CT: channels per Gaussian (0 = runtime), SINGLE: one channel block,
@@ -135,12 +144,14 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
     const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
     if (beg < end) stage_batch(S.st[0], A, beg, (int)min((uint32_t)kBatch, end - beg), cs);
     cp_async_commit();
-    for (int i = threadIdx.x; i < kExpTable; i += kBlendThreads) S.exp_tab[i] = c_exp_table[i];
     for (int i = threadIdx.x; i < nchb * kAccPitch; i += kBlendThreads) acc[i] = 0.f;
 
     const float pxf = (float)px, pyf = (float)py;
     const double pxd = (double)px, pyd = (double)py;
-    double T = 1.0;
+    float T = 1.f;        // transmittance (fp32: |dT|/T <= eb * 3e-6 + n * 1.2e-7, see header)
+    float eb = 0.f;       // sum of alpha / (1 - alpha) over contributions (error-bound driver)
+    float Tprev = 1.f;    // T before the last contribution
+    int ncontrib = 0;
     bool done = !inside;
 
     int bi = 0;
@@ -153,7 +164,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
-        // channel ids -> accumulator offsets for this CTA's channel block
+        // channel ids -> accumulator byte offsets for this CTA's channel block
         for (int idx = threadIdx.x; idx < nb * C; idx += kBlendThreads) {
             int j = idx / C, k = idx - j * C;
             int ch = (int)reinterpret_cast<const uint16_t*>(B.chan + j * kMaxChanRec)[k] - ch0;
@@ -162,63 +173,67 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
         __syncthreads();
 
         if (!__all_sync(0xffffffffu, done)) {
-            // ---- phase A: fp32 rejection, candidate mask ----
+            // ---- phase A: fp32 rejection (q > 9 + guard) -> candidate mask ----
             uint32_t cand = 0;
             if (!done) {
 #pragma unroll 4
                 for (int j = 0; j < nb; ++j) {
                     const float4 m4 = *reinterpret_cast<const float4*>(&B.g[j].mx_hi);
                     const float4 c4 = *reinterpret_cast<const float4*>(&B.g[j].a);
-                    float dx = (pxf - m4.x) - m4.y;
-                    float dy = (pyf - m4.z) - m4.w;
-                    float adx = c4.x * dx, cdy = c4.z * dy;
-                    float q32 = fmaf(adx, dx, fmaf(c4.y * dx, dy, cdy * dy));
-                    float s32 = fmaf(adx, dx, cdy * dy);
-                    if (q32 <= fmaf(1e-4f, s32, 9.0001f)) cand |= 1u << j;
+                    const float dx = (pxf - m4.x) - m4.y;
+                    const float dy = (pyf - m4.z) - m4.w;
+                    const float u = fmaf(c4.y, dy, dx);
+                    const float ddy = c4.z * dy * dy;
+                    const float q32 = fmaf(c4.x * u, u, ddy);
+                    const float su = fabsf(dx) + fabsf(c4.y * dy);
+                    const float guard = fmaf(1e-5f, fmaf(c4.x * su, su, ddy), 1e-5f);
+                    if (q32 <= 9.f + guard) cand |= 1u << j;
                 }
             }
-            // ---- phase B: exact evaluation + scatter, depth order ----
+            // ---- phase B: alpha, transmittance, scatter -- depth order ----
+            // alpha of the next candidate is computed before the current scatter
+            // (it depends only on geometry), so its latency hides under the
+            // scatter's shared-memory traffic.
             uint32_t wmask = __reduce_or_sync(0xffffffffu, cand);
-            while (wmask) {
-                const int j = __ffs(wmask) - 1;
-                wmask &= wmask - 1;
+            int j = wmask ? __ffs(wmask) - 1 : -1;
+            if (j >= 0) wmask &= wmask - 1;
+            float al = (j >= 0 && ((cand >> j) & 1u)) ? blend_alpha(B.g[j], pxf, pyf, pxd, pyd) : 0.f;
+            while (j >= 0) {
                 float ef = 0.f;
-                if (((cand >> j) & 1u) && !done) {
-                    const GeomRec& g = B.g[j];
-                    double ddx = __dadd_rn(pxd, -g.mx), ddy = __dadd_rn(pyd, -g.my);
-                    double t1 = __dmul_rn(__dmul_rn(g.a64, ddx), ddx);
-                    double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, g.b64), ddx), ddy);
-                    double t3 = __dmul_rn(__dmul_rn(g.c64, ddy), ddy);
-                    double q = __dadd_rn(__dadd_rn(t1, t2), t3);
-                    if (q <= SF_CUTOFF) {
-                        double al = __dmul_rn((double)g.opacity, exp_neg(__dmul_rn(0.5, q), S.exp_tab));
-                        al = np_minimum(al, SF_ALPHA_CLAMP);
-                        double e = __dmul_rn(al, T);
-                        T = __dmul_rn(T, __dadd_rn(1.0, -al));
-                        ef = (float)e;
-                        if (A.early_exit && T < SF_EARLY_EXIT_T) done = true;
-                    }
+                if (al > 0.f && !done) {
+                    ef = al * T;
+                    Tprev = T;
+                    T = fmaf(-al, T, T);
+                    eb += __fdividef(al, 1.f - al);
+                    ++ncontrib;
+                    if (A.early_exit && T < (float)SF_EARLY_EXIT_T) done = true;
                 }
+                const int jn = wmask ? __ffs(wmask) - 1 : -1;
+                if (jn >= 0) wmask &= wmask - 1;
+                const float aln = (jn >= 0 && ((cand >> jn) & 1u) && !done) ? blend_alpha(B.g[jn], pxf, pyf, pxd, pyd) : 0.f;
                 if (__any_sync(0xffffffffu, ef > 0.f)) {
                     const float* val = reinterpret_cast<const float*>(B.chan + j * kMaxChanRec + voff);
                     char* accs = reinterpret_cast<char*>(acc + slot);
-                    if (CT > 0 && CT % 4 == 0) {
+                    if (CT > 0 && CT % 4 == 0 && SINGLE) {
+                        // a Gaussian's channel ids are distinct: all loads, then FMAs, then stores
+                        constexpr int NC = CT > 0 ? CT : 4;
                         const uint4* o4 = reinterpret_cast<const uint4*>(B.off[j]);
                         const float4* v4 = reinterpret_cast<const float4*>(val);
+                        uint32_t oo[NC];
+                        float vv[NC], av[NC];
 #pragma unroll
-                        for (int q = 0; q < (CT > 0 ? CT : 4) / 4; ++q) {
+                        for (int q = 0; q < NC / 4; ++q) {
                             const uint4 o = o4[q];
                             const float4 v = v4[q];
-                            const uint32_t oo[4] = {o.x, o.y, o.z, o.w};
-                            const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                if (SINGLE || oo[e] != 0xffffffffu) {
-                                    float* a = reinterpret_cast<float*>(accs + oo[e]);
-                                    *a = fmaf(ef, vv[e], *a);
-                                }
-                            }
+                            oo[4 * q] = o.x; oo[4 * q + 1] = o.y; oo[4 * q + 2] = o.z; oo[4 * q + 3] = o.w;
+                            vv[4 * q] = v.x; vv[4 * q + 1] = v.y; vv[4 * q + 2] = v.z; vv[4 * q + 3] = v.w;
                         }
+#pragma unroll
+                        for (int e = 0; e < NC; ++e) av[e] = *reinterpret_cast<const float*>(accs + oo[e]);
+#pragma unroll
+                        for (int e = 0; e < NC; ++e) av[e] = fmaf(ef, vv[e], av[e]);
+#pragma unroll
+                        for (int e = 0; e < NC; ++e) *reinterpret_cast<float*>(accs + oo[e]) = av[e];
                     } else {
                         for (int k = 0; k < C; ++k) {
                             const uint32_t off = B.off[j][k];
@@ -229,15 +244,28 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
                         }
                     }
                 }
+                j = jn;
+                al = aln;
             }
         }
         if (__syncthreads_and(done)) break;
+    }
+    // Early-exit decisions (counted iff T >= 1e-4) that fp32 T cannot certify
+    // are replayed exactly in fp64 by k_blend_fixup.
+    if (inside && A.early_exit && A.fixup_list && blockIdx.y == 0) {
+        const float tol = fmaf(4e-6f, eb, fmaf(3e-7f, (float)ncontrib, 2e-6f));
+        const float thr = (float)SF_EARLY_EXIT_T;
+        const bool amb = done ? (Tprev < thr * (1.f + tol) || T > thr * (1.f - tol)) : (T < thr * (1.f + tol));
+        if (amb) {
+            uint32_t k = atomicAdd(A.fixup_count, 1u);
+            if (k < A.fixup_capacity) A.fixup_list[k] = ((uint32_t)tile << 8) | (uint32_t)slot;
+        }
     }
     cp_async_wait<0>();
     __syncthreads();
 
     // ---- outputs ----
-    if (blockIdx.y == 0 && A.final_t && inside) A.final_t[(size_t)py * A.W + px] = (float)T;
+    if (blockIdx.y == 0 && A.final_t && inside) A.final_t[(size_t)py * A.W + px] = T;
     if (A.coeff_map) {
         // warp w writes pixels x = w, w + 8 of every tile row; lanes stride the
         // pixel's channels (contiguous in HBM), the smem read is conflict-free
@@ -296,80 +324,185 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
 
 // Relevancy from a coefficient map in HBM (the map is written anyway when the
 // features are decoded, or the channel count exceeds one blend CTA).  One
-// thread per pixel; the projected codebook sits in shared memory.
-template <int NV>
+// thread per pixel; shared memory holds the logit-difference vectors
+// Pd_j = P_q - P_cj (so l_q - l_j = W . Pd_j: nc dot products instead of
+// nc + 1), read as 16-byte broadcasts.
+template <int NC>
 __global__ void __launch_bounds__(256) k_relevancy_from_cmap(int64_t P, int n_ch, const float* __restrict__ cmap,
                                                              const double* __restrict__ proj_cb, int n_levels,
                                                              int L, int n_canon, double* __restrict__ out) {
-    extern __shared__ double Ps[];
-    const int nv = NV > 0 ? NV : 1 + n_canon;
-    for (int i = threadIdx.x; i < n_levels * L * nv; i += blockDim.x) Ps[i] = proj_cb[i];
+    extern __shared__ __align__(16) double Pd[];
+    const int nc = NC > 0 ? NC : n_canon;
+    const int nv = 1 + n_canon;
+    for (int i = threadIdx.x; i < n_levels * L * nc; i += blockDim.x) {
+        const int j = i % nc, bl = i / nc;  // bl = b * L + l
+        Pd[i] = proj_cb[(size_t)bl * nv] - proj_cb[(size_t)bl * nv + 1 + j];
+    }
     __syncthreads();
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P) return;
-    const float* w = cmap + (size_t)p * n_ch;
-    for (int b = 0; b < n_levels; ++b) {
-        const double* Pm = Ps + (size_t)b * L * nv;
-        double best = INFINITY;
-        if (NV > 0) {
-            double lg[NV > 0 ? NV : 1];
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+        const float* w = cmap + (size_t)p * n_ch;
+        for (int b = 0; b < n_levels; ++b) {
+            const double* Pb = Pd + (size_t)b * L * nc;
+            double best = INFINITY;
+            if (NC > 0) {
+                double d[NC > 0 ? NC : 1];
 #pragma unroll
-            for (int t = 0; t < (NV > 0 ? NV : 1); ++t) lg[t] = 0.0;
-            for (int l0 = 0; l0 < L; l0 += 4) {
-                const float4 w4 = __ldcs(reinterpret_cast<const float4*>(w + b * L + l0));
-                const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+                for (int j = 0; j < (NC > 0 ? NC : 1); ++j) d[j] = 0.0;
+                for (int l0 = 0; l0 < L; l0 += 4) {
+                    const float4 w4 = __ldcs(reinterpret_cast<const float4*>(w + b * L + l0));
+                    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const double wd = (double)wv[e];
+                    for (int e = 0; e < 4; ++e) {
+                        const double wd = (double)wv[e];
+                        const double* Pl = Pb + (l0 + e) * (NC > 0 ? NC : 1);
 #pragma unroll
-                    for (int t = 0; t < (NV > 0 ? NV : 1); ++t) lg[t] = fma(wd, Pm[(l0 + e) * (NV > 0 ? NV : 1) + t], lg[t]);
+                        for (int j = 0; j < (NC > 0 ? NC : 1); ++j) d[j] = fma(wd, Pl[j], d[j]);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < (NC > 0 ? NC : 1); ++j) best = np_minimum(best, sigmoid2(d[j]));
+            } else {
+                for (int j = 0; j < nc; ++j) {
+                    double dj = 0.0;
+                    for (int l = 0; l < L; ++l) dj = fma((double)w[b * L + l], Pb[l * nc + j], dj);
+                    best = np_minimum(best, sigmoid2(dj));
                 }
             }
-#pragma unroll
-            for (int t = 1; t < (NV > 0 ? NV : 1); ++t) best = np_minimum(best, sigmoid2(lg[0] - lg[t]));
-        } else {
-            double lq = 0.0;
-            for (int l = 0; l < L; ++l) lq = fma((double)w[b * L + l], Pm[l * nv], lq);
-            for (int j = 1; j < nv; ++j) {
-                double lc = 0.0;
-                for (int l = 0; l < L; ++l) lc = fma((double)w[b * L + l], Pm[l * nv + j], lc);
-                best = np_minimum(best, sigmoid2(lq - lc));
-            }
+            out[(size_t)b * P + p] = best;
         }
-        out[(size_t)b * P + p] = best;
     }
 }
 
 void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const double* proj_cb, int n_levels,
                                 int L, int n_canon, double* out, cudaStream_t st) {
     if (P == 0) return;
-    const size_t smem = sizeof(double) * (size_t)n_levels * L * (1 + n_canon);
+    const size_t smem = sizeof(double) * (size_t)n_levels * L * n_canon;
     const bool vec = (L % 4 == 0) && (n_ch % 4 == 0) && ((uintptr_t)cmap % 16 == 0);
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k_relevancy_from_cmap<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_relevancy_from_cmap<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_relevancy_from_cmap<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         configured = true;
     }
+    const int blocks = (int)std::min<int64_t>(ceil_div(P, 256), 148 * 8);
     if (vec && n_canon == 4)
-        k_relevancy_from_cmap<5><<<ceil_div(P, 256), 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out);
+        k_relevancy_from_cmap<4><<<blocks, 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out);
     else
-        k_relevancy_from_cmap<0><<<ceil_div(P, 256), 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out);
+        k_relevancy_from_cmap<0><<<blocks, 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out);
 }
 
-static bool init_exp_table() {
-    static bool done = false;
-    if (done) return true;
-    double h[kExpTable];
-    for (int k = 0; k < kExpTable; ++k) h[k] = exp(-(double)k / kExpSteps);
-    if (cudaMemcpyToSymbol(c_exp_table, h, sizeof(h)) != cudaSuccess) return false;
-    done = true;
-    return true;
+// Exact fp64 replay (rasterizer.py:161-177) of the pixels whose early-exit
+// decision the fp32 transmittance could not certify.  One warp per pixel:
+// lanes evaluate 32 list entries at once in fp64 (reference op order), a
+// warp prefix product gives T before each entry, counted iff T >= 1e-4.
+// W accumulates in fp64 in shared memory.
+constexpr int kFixWarps = 4;
+__global__ void __launch_bounds__(32 * kFixWarps) k_blend_fixup(BlendArgs A) {
+    __shared__ double wsm[kFixWarps][kChBlock];
+    const uint32_t count = min(*A.fixup_count, A.fixup_capacity);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        const_cast<int64_t*>(A.stats)[SF_STAT_FIXUPS] = (int64_t)*A.fixup_count;
+    const int C = A.C;
+    const int cs = chan_rec_bytes(C);
+    const int voff = chan_val_offset(C);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* wl = wsm[wid];
+    const bool local = A.n_ch <= kChBlock;
+    for (uint32_t idx = blockIdx.x * kFixWarps + wid; idx < count; idx += gridDim.x * kFixWarps) {
+        const uint32_t code = A.fixup_list[idx];
+        const int tile = (int)(code >> 8), slot = (int)(code & 255u);
+        const int w8 = slot >> 5, l8 = slot & 31;
+        const int px = (tile % A.tiles_x) * SF_TILE + (w8 & 1) * 8 + (l8 & 7);
+        const int py = (tile / A.tiles_x) * SF_TILE + (w8 >> 1) * 4 + (l8 >> 3);
+        const size_t pix = (size_t)py * A.W + px;
+        float* row = A.coeff_map ? A.coeff_map + pix * A.n_ch : nullptr;
+        for (int c = lane; c < A.n_ch; c += 32) {
+            if (local) wl[c] = 0.0;
+            else row[c] = 0.f;
+        }
+        __syncwarp();
+        double T = 1.0;  // transmittance before the current chunk
+        const double pxd = (double)px, pyd = (double)py;
+        const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
+        for (uint32_t i0 = beg; i0 < end && T >= SF_EARLY_EXIT_T; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            double al = 0.0;
+            uint32_t r = 0;
+            if (i < end) {
+                r = A.entries[i];
+                const GeomRec g = A.geom[r];
+                double ddx = __dadd_rn(pxd, -g.mx), ddy = __dadd_rn(pyd, -g.my);
+                double t1 = __dmul_rn(__dmul_rn(g.a64, ddx), ddx);
+                double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, g.b64), ddx), ddy);
+                double t3 = __dmul_rn(__dmul_rn(g.c64, ddy), ddy);
+                double q = __dadd_rn(__dadd_rn(t1, t2), t3);
+                if (q <= SF_CUTOFF)
+                    al = np_minimum(__dmul_rn((double)g.opacity, exp(__dmul_rn(-0.5, q))), SF_ALPHA_CLAMP);
+            }
+            // inclusive prefix product of (1 - alpha) -> T before each lane's entry
+            double f = __dadd_rn(1.0, -al);
+            double incl = f;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                double v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl = __dmul_rn(v, incl);
+            }
+            double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) excl = 1.0;
+            const double Tb = __dmul_rn(T, excl);
+            const bool counted = (i < end) && (Tb >= SF_EARLY_EXIT_T) && (al > 0.0);
+            if (counted) {
+                const double e = __dmul_rn(al, Tb);
+                const unsigned char* rec = A.chan + (size_t)r * cs;
+                const uint16_t* ch = reinterpret_cast<const uint16_t*>(rec);
+                const float* val = reinterpret_cast<const float*>(rec + voff);
+                for (int k = 0; k < C; ++k) {
+                    if (local) atomicAdd(&wl[ch[k]], e * (double)val[k]);
+                    else atomicAdd(&row[ch[k]], (float)(e * (double)val[k]));
+                }
+            }
+            T = __dmul_rn(T, __shfl_sync(0xffffffffu, incl, 31));
+            // stop at the first uncounted entry: T before later entries only shrinks
+            if (__any_sync(0xffffffffu, (i < end) && !(Tb >= SF_EARLY_EXIT_T))) T = 0.0;
+            const unsigned last_counted = __ballot_sync(0xffffffffu, (i < end) && (Tb >= SF_EARLY_EXIT_T));
+            if (T == 0.0) {
+                // final T = T after the last counted entry
+                const int lc = 31 - __clz(last_counted);
+                double Tl = __shfl_sync(0xffffffffu, __dmul_rn(Tb, f), lc < 0 ? 0 : lc);
+                T = (lc < 0) ? 0.0 : Tl;
+                break;
+            }
+        }
+        __syncwarp();
+        if (local && row)
+            for (int c = lane; c < A.n_ch; c += 32) row[c] = (float)wl[c];
+        if (lane == 0 && A.final_t) A.final_t[pix] = (float)T;
+        if (A.proj_cb && A.relevancy_raw && lane == 0) {
+            const int nv = 1 + A.n_canon;
+            for (int b = 0; b < A.n_levels; ++b) {
+                const double* P = A.proj_cb + (size_t)b * A.L * nv;
+                double lq = 0.0, best = INFINITY;
+                for (int l = 0; l < A.L; ++l) {
+                    const int c = b * A.L + l;
+                    lq = fma((double)(local ? (float)wl[c] : row[c]), P[l * nv], lq);
+                }
+                for (int j = 1; j < nv; ++j) {
+                    double lc = 0.0;
+                    for (int l = 0; l < A.L; ++l) {
+                        const int c = b * A.L + l;
+                        lc = fma((double)(local ? (float)wl[c] : row[c]), P[l * nv + j], lc);
+                    }
+                    best = np_minimum(best, sigmoid2(lq - lc));
+                }
+                A.relevancy_raw[(size_t)b * A.W * A.H + pix] = best;
+            }
+        }
+        __syncwarp();
+    }
 }
 
 int launch_blend(const BlendArgs& a, cudaStream_t st) {
     if (a.C > kMaxC) return -2;
-    if (!init_exp_table()) return -3;
     int n_tiles = a.tiles_x * a.tiles_y;
     int ch_block = a.n_ch < kChBlock ? a.n_ch : kChBlock;
     int nblk = (a.n_ch + ch_block - 1) / ch_block;
@@ -388,6 +521,7 @@ int launch_blend(const BlendArgs& a, cudaStream_t st) {
         configured[ki] = smem;
     }
     if (n_tiles > 0) kern<<<dim3(n_tiles, nblk), kBlendThreads, smem, st>>>(a, ch_block);
+    if (n_tiles > 0 && a.fixup_list && a.early_exit) k_blend_fixup<<<296, 32 * kFixWarps, 0, st>>>(a);
     if (a.proj_cb && nblk > 1)
         launch_relevancy_from_cmap((int64_t)a.W * a.H, a.n_ch, a.coeff_map, a.proj_cb, a.n_levels, a.L,
                                    a.n_canon, a.relevancy_raw, st);

@@ -71,7 +71,10 @@ struct FrameWs {
     double* filter_tmp;
     void* sel_ws;
     float* dec_ws;
+    uint32_t* fixup;  // [0] = count, then the list
 };
+
+static constexpr uint32_t kFixupCapacity = 1u << 20;
 
 static constexpr int kMaxCanon = 64;
 
@@ -101,6 +104,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->filter_tmp = c.take<double>((size_t)n_levels * W * H);
     ws->sel_ws = c.take<char>(select_segment_ws_bytes(n_levels, H, W));
     ws->dec_ws = c.take<float>(decode_ws_bytes(L, D) / sizeof(float));
+    ws->fixup = c.take<uint32_t>(kFixupCapacity + 1);
     return c.off;
 }
 
@@ -164,6 +168,7 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     if (f->events[0]) cudaEventRecord((cudaEvent_t)f->events[0], st);
     cudaMemsetAsync(ws.stats, 0, 16 * sizeof(int64_t), st);
     cudaMemsetAsync(ws.stats_f, 0, (8 + kMaxLevels) * sizeof(double), st);
+    cudaMemsetAsync(ws.fixup, 0, sizeof(uint32_t), st);
     // K1
     launch_preprocess(*s, *cam, ws.proj_by_row, ws.keys_in, ws.vals_in, ws.stats, st);
     // K2
@@ -190,6 +195,9 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     a.entries = ws.entries;
     a.geom = ws.geom;
     a.chan = ws.chan;
+    a.fixup_count = ws.fixup;
+    a.fixup_list = ws.fixup + 1;
+    a.fixup_capacity = kFixupCapacity;
     a.stats = ws.stats;
     a.coeff_map = f->coeff_map;
     a.final_t = f->final_t;

@@ -98,7 +98,7 @@ struct __align__(8) Proj64 {
 // values (means2d, inv_cov2d) used by binning and by the exact alpha.
 struct __align__(16) GeomRec {
     float mx_hi, mx_lo, my_hi, my_lo;  // mean split so (px - hi) - lo is ~exact
-    float a, b2, c, opacity;           // conic (a, 2b, c) and opacity
+    float a, k, d, opacity;            // q = a (dx + k dy)^2 + d dy^2, k = b/a, d = det/a
     double mx, my;                     // means2d (fp64, bitwise the reference's)
     double a64, b64;                   // inv_cov2d[0][0], inv_cov2d[0][1]
     double c64;                        // inv_cov2d[1][1]
@@ -180,6 +180,9 @@ struct BlendArgs {
     const GeomRec* geom;
     const unsigned char* chan;
     const int64_t* stats;  // overflow flag gate
+    uint32_t* fixup_list;  // (tile << 8 | pixel slot) of pixels whose early-exit decision is ambiguous
+    uint32_t* fixup_count;
+    uint32_t fixup_capacity;
     float* coeff_map;      // (H,W,n_ch) or null
     float* final_t;        // (H,W) or null
     // fused projected-codebook relevancy (optional)
