@@ -35,14 +35,15 @@ namespace tc {
 constexpr int BM = 128;           // pixels per tile (TMEM lanes)
 constexpr int BN = 128;           // output columns per CTA (MMA N)
 constexpr int KBOX = 32;          // fp32 per 128-byte swizzle row
-constexpr int kThreads = 448;     // 14 warps
+constexpr int kThreads = 576;     // 18 warps
 constexpr int kEpiWarp0 = 2;      // warps 2..9 epilogue: 2 column halves x 4 lane quarters
 constexpr int kEpiWarps = 8;
-constexpr int kCvtWarp0 = 10;     // warps 10..13 A splitters
-constexpr int kStages = 2;        // W tile ring
+constexpr int kCvtWarp0 = 10;     // warps 10..17 A splitters
+constexpr int kCvtThreads = 256;
+constexpr int kStages = 2;        // W tile ring; A_lo is double-buffered with it
 constexpr int kAcc = 4;           // TMEM accumulators (4 x 128 columns)
 constexpr int kBoxes = BN / 32;   // output boxes per tile
-constexpr int kStageBuf = 2;      // output staging boxes (double buffer)
+constexpr int kStageBuf = 2;      // output staging boxes in flight (TMA store ring)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -137,8 +138,8 @@ struct Smem {
     // operand tiles (1024-byte aligned, SW128 atoms)
     float b_hi[64 / KBOX][BN * KBOX];        // 2 x 16 KB
     float b_lo[64 / KBOX][BN * KBOX];        // 2 x 16 KB
-    float a[kStages][64 / KBOX][BM * KBOX];  // 2 x 2 x 16 KB (hi after split)
-    float a_lo[64 / KBOX][BM * KBOX];        // 2 x 16 KB
+    float a[kStages][64 / KBOX][BM * KBOX];     // 2 x 2 x 16 KB (hi after split)
+    float a_lo[kStages][64 / KBOX][BM * KBOX];  // 2 x 2 x 16 KB
     float out[kStageBuf][BM * 32];           // 2 x 16 KB output staging (SW128)
     uint64_t full[kStages];      // TMA landed
     uint64_t ready[kStages];     // A split done
@@ -165,7 +166,7 @@ k_decode_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&S.full[s], 1);
-            mbar_init(&S.ready[s], 128);
+            mbar_init(&S.ready[s], kCvtThreads);
             mbar_init(&S.empty[s], 1);
         }
         for (int s = 0; s < kAcc; ++s) {
@@ -216,7 +217,7 @@ k_decode_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             uint32_t acc = 0;
             for (int kb = 0; kb < nkb; ++kb) {
                 const uint32_t ahi = smem_u32(S.a[s][kb]);
-                const uint32_t alo = smem_u32(S.a_lo[kb]);
+                const uint32_t alo = smem_u32(S.a_lo[s][kb]);
                 const uint32_t bhi = smem_u32(S.b_hi[kb]);
                 const uint32_t blo = smem_u32(S.b_lo[kb]);
 #pragma unroll
@@ -233,21 +234,28 @@ k_decode_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
     } else if (warp >= kCvtWarp0) {
         // ---------------- A splitters: hi = rna(x) in place, lo = x - hi ----------------
-        const int t = threadIdx.x - kCvtWarp0 * 32;  // 0..127
+        // A_lo[s] is free whenever stage s has refilled: the producer only
+        // reloads stage s after the MMAs of the tile two back completed
+        const int t = threadIdx.x - kCvtWarp0 * 32;  // 0..255
         for (int i = 0; i < my_tiles; ++i) {
             const int s = i % kStages;
             mbar_wait(&S.full[s], (i / kStages) & 1);
-            // the single lo buffer is free once the previous tile's MMAs completed
-            if (i >= 1) mbar_wait(&S.empty[(i - 1) % kStages], ((i - 1) / kStages) & 1);
             for (int kb = 0; kb < nkb; ++kb) {
-                float4* av = reinterpret_cast<float4*>(S.a[s][kb]);
-                float4* lv = reinterpret_cast<float4*>(S.a_lo[kb]);
+                const uint32_t av = smem_u32(S.a[s][kb]);
+                const uint32_t lv = smem_u32(S.a_lo[s][kb]);
 #pragma unroll 4
-                for (int j = t; j < BM * KBOX / 4; j += 128) {
-                    float4 x = av[j];
+                for (int j = t; j < BM * KBOX / 4; j += kCvtThreads) {
+                    float4 x;
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                                 : "r"(av + 16 * j));
                     float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-                    av[j] = h;
-                    lv[j] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(av + 16 * j), "f"(h.x), "f"(h.y),
+                                 "f"(h.z), "f"(h.w)
+                                 : "memory");
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lv + 16 * j), "f"(x.x - h.x),
+                                 "f"(x.y - h.y), "f"(x.z - h.z), "f"(x.w - h.w)
+                                 : "memory");
                 }
             }
             fence_proxy_async();
@@ -287,11 +295,13 @@ k_decode_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 const int slot = nstore % kStageBuf;
                 if (issuer) bulk_wait_read<kStageBuf - 1>();
                 named_bar(bar_id, nthr);
-                unsigned char* rowp = reinterpret_cast<unsigned char*>(S.out[slot]) + r * 128;
+                const uint32_t rowp = smem_u32(S.out[slot]) + r * 128;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const int pc = (half * 4 + c) ^ (r & 7);
-                    *reinterpret_cast<uint4*>(rowp + pc * 16) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowp + pc * 16), "r"(v[4 * c]),
+                                 "r"(v[4 * c + 1]), "r"(v[4 * c + 2]), "r"(v[4 * c + 3])
+                                 : "memory");
                 }
                 fence_proxy_async();
                 named_bar(bar_id, nthr);
