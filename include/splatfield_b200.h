@@ -91,6 +91,9 @@ typedef struct SfFrame {
     /* optional cudaEvent_t recorded at: frame start, after blend (render),
      * after decode, after post -- the StageTimings of sparse_splat.py:202-215 */
     void* events[4];
+    /* optional cached per-row scatter plan of host_levels (sf_pack_channels);
+     * NULL = built inside the frame */
+    const unsigned char* chan_by_row;
 } SfFrame;
 
 /* stats_i64 slots */
@@ -106,6 +109,12 @@ typedef struct SfFrame {
 #define SF_STATF_MIN 0        /* chosen map min */
 #define SF_STATF_MAX 1        /* chosen map max */
 #define SF_STATF_LEVEL_MAX 8  /* + b: max of filtered map of block b */
+
+/* Per-row scatter plan (channel ids level*L+idx and values of the selected
+ * levels, sparse_splat.py:126-132) -- a scene constant worth caching. */
+size_t sf_channel_plan_bytes(int64_t num_gaussians, int32_t n_levels, int32_t K);
+int sf_pack_channels(const SfScene* scene, const int32_t* host_levels, int32_t n_levels, void* out,
+                     size_t out_bytes, void* stream);
 
 /* Scratch needed by sf_render_frame for this scene/frame shape. */
 int sf_frame_workspace_bytes(int64_t num_gaussians, int32_t width, int32_t height,

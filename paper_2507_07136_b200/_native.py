@@ -47,7 +47,7 @@ class SfFrame(ctypes.Structure):
     _fields_ = [("host_levels", P), ("n_levels", i32), ("early_exit", i32), ("pair_capacity", i64),
                 ("coeff_map", P), ("final_t", P), ("features", P), ("relevancy_raw", P),
                 ("relevancy_filtered", P), ("mask", P), ("stats_i64", P), ("stats_f64", P),
-                ("events", P * 4)]
+                ("events", P * 4), ("chan_by_row", P)]
 
 
 EXPORTS = {
@@ -61,6 +61,8 @@ EXPORTS = {
                                        P, P, P, P, P, P, sz, P]),
     "sf_bin_workspace_bytes": (ctypes.c_int, [i64, i32, i32, i64, ctypes.POINTER(sz)]),
     "sf_bin": (ctypes.c_int, [i64, P, P, P, P, i32, i32, i64, P, P, P, P, P, sz, P]),
+    "sf_channel_plan_bytes": (sz, [i64, i32, i32]),
+    "sf_pack_channels": (ctypes.c_int, [ctypes.POINTER(SfScene), P, i32, P, sz, P]),
     "sf_decode_workspace_bytes": (sz, [i32, i32]),
     "sf_decode": (ctypes.c_int, [i64, i32, i32, P, i64, P, P, P, sz, P]),
     "sf_decode_simt": (ctypes.c_int, [i64, i32, i32, P, i64, P, P, P]),

@@ -38,79 +38,65 @@ int depth_sort(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals
 }
 
 // ---------------------------------------------------------------------------
-// rank gather: canonical-order copies of the projected record, the fp32 blend
-// record and the selected levels' top-K (channel, value) scatter plan
-// (sparse_splat.py:126-132 cat_idx / cat_vals).
+// inverse of the depth order, and the per-row scatter plan
+// (sparse_splat.py:126-132 cat_idx / cat_vals)
 
-__global__ void __launch_bounds__(256) k_rank_gather(int64_t G, const uint32_t* __restrict__ sorted_rows,
+__global__ void __launch_bounds__(256) k_rank_of_row(int64_t G, const uint32_t* __restrict__ sorted_rows,
                                                      const int64_t* __restrict__ stats,
-                                                     const Proj64* __restrict__ proj_by_row,
-                                                     const float* __restrict__ opac_by_row,
-                                                     const uint16_t* __restrict__ cidx,
-                                                     const float* __restrict__ cval, int K, int L,
-                                                     LevelSelDev levels, GeomRec* __restrict__ geom,
-                                                     unsigned char* __restrict__ chan, int C) {
+                                                     uint32_t* __restrict__ rank_of_row) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t n = stats[SF_STAT_VISIBLE];
-    if (r >= n) return;
-    uint32_t row = sorted_rows[r];
-    Proj64 p = proj_by_row[row];
-    GeomRec q;
-    q.mx_hi = (float)p.mx;
-    q.mx_lo = (float)(p.mx - (double)q.mx_hi);
-    q.my_hi = (float)p.my;
-    q.my_lo = (float)(p.my - (double)q.my_hi);
-    q.a = (float)p.a;
-    q.k = (float)(p.b / p.a);
-    q.d = (float)((p.a * p.c - p.b * p.b) / p.a);
-    q.opacity = opac_by_row ? opac_by_row[row] : 0.f;
-    q.mx = p.mx;
-    q.my = p.my;
-    q.a64 = p.a;
-    q.b64 = p.b;
-    q.c64 = p.c;
-    q.row = row;
-    q.pad = 0;
-    geom[r] = q;
-    if (chan) {
-        const int cs = chan_rec_bytes(C);
-        unsigned char* rec = chan + (size_t)r * cs;
+    if (r >= G) return;
+    rank_of_row[sorted_rows[r]] = (r < stats[SF_STAT_VISIBLE]) ? (uint32_t)r : 0xffffffffu;
+}
+
+void launch_rank_of_row(int64_t G, const uint32_t* sorted_rows, const int64_t* stats, uint32_t* rank_of_row,
+                        cudaStream_t st) {
+    if (G) k_rank_of_row<<<ceil_div(G, 256), 256, 0, st>>>(G, sorted_rows, stats, rank_of_row);
+}
+
+__global__ void __launch_bounds__(256) k_pack_channels(int64_t G, const uint16_t* __restrict__ cidx,
+                                                       const float* __restrict__ cval, int K, int L,
+                                                       LevelSelDev levels, unsigned char* __restrict__ chan) {
+    int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= G) return;
+    const int C = levels.n * K;
+    const int cs = chan_rec_bytes(C);
+    if (C <= 16) {
+        // build the record in registers, write it with 16-byte stores
+        uint32_t rec[24];  // <= 96 bytes
+#pragma unroll
+        for (int i = 0; i < 24; ++i) rec[i] = 0;
         uint16_t* ch = reinterpret_cast<uint16_t*>(rec);
-        float* val = reinterpret_cast<float*>(rec + chan_val_offset(C));
+        float* val = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(rec) + chan_val_offset(C));
         for (int b = 0; b < levels.n; ++b) {
-            int lv = levels.lv[b];
+            const int lv = levels.lv[b];
             const uint16_t* ip = cidx + ((int64_t)lv * G + row) * K;
             const float* vp = cval + ((int64_t)lv * G + row) * K;
-            if (K == 4) {  // 8-byte index and 16-byte value loads
-                const uint2 i2 = __ldg(reinterpret_cast<const uint2*>(ip));
-                const float4 v4 = __ldg(reinterpret_cast<const float4*>(vp));
-                const uint16_t off = (uint16_t)(b * L);
-                ch[b * 4 + 0] = (uint16_t)((i2.x & 0xffffu) + off);
-                ch[b * 4 + 1] = (uint16_t)((i2.x >> 16) + off);
-                ch[b * 4 + 2] = (uint16_t)((i2.y & 0xffffu) + off);
-                ch[b * 4 + 3] = (uint16_t)((i2.y >> 16) + off);
-                val[b * 4 + 0] = v4.x;
-                val[b * 4 + 1] = v4.y;
-                val[b * 4 + 2] = v4.z;
-                val[b * 4 + 3] = v4.w;
-            } else {
-                for (int k = 0; k < K; ++k) {
-                    ch[b * K + k] = (uint16_t)(ip[k] + b * L);
-                    val[b * K + k] = vp[k];
-                }
+            for (int k = 0; k < K; ++k) {
+                ch[b * K + k] = (uint16_t)(__ldg(ip + k) + b * L);
+                val[b * K + k] = __ldg(vp + k);
             }
+        }
+        uint4* dst = reinterpret_cast<uint4*>(chan + (size_t)row * cs);
+        for (int q = 0; q < cs / 16; ++q) dst[q] = make_uint4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
+        return;
+    }
+    unsigned char* rp = chan + (size_t)row * cs;
+    uint16_t* ch = reinterpret_cast<uint16_t*>(rp);
+    float* val = reinterpret_cast<float*>(rp + chan_val_offset(C));
+    for (int b = 0; b < levels.n; ++b) {
+        const int lv = levels.lv[b];
+        for (int k = 0; k < K; ++k) {
+            ch[b * K + k] = (uint16_t)(cidx[((int64_t)lv * G + row) * K + k] + b * L);
+            val[b * K + k] = cval[((int64_t)lv * G + row) * K + k];
         }
     }
 }
 
-void launch_rank_gather(int64_t G, const uint32_t* sorted_rows, const int64_t* stats,
-                        const Proj64* proj_by_row, const float* opac_by_row, const SfScene* s,
-                        const LevelSelDev& levels, GeomRec* geom, unsigned char* chan, int C,
-                        cudaStream_t st) {
-    if (G == 0) return;
-    k_rank_gather<<<ceil_div(G, 256), 256, 0, st>>>(
-        G, sorted_rows, stats, proj_by_row, opac_by_row, s ? s->coeff_indices : nullptr,
-        s ? s->coeff_values : nullptr, s ? s->K : 0, s ? s->L : 0, levels, geom, chan, C);
+void launch_pack_channels(const SfScene& s, const LevelSelDev& levels, unsigned char* chan, cudaStream_t st) {
+    if (s.num_gaussians)
+        k_pack_channels<<<ceil_div(s.num_gaussians, 256), 256, 0, st>>>(s.num_gaussians, s.coeff_indices,
+                                                                        s.coeff_values, s.K, s.L, levels, chan);
 }
 
 // ---------------------------------------------------------------------------
@@ -146,17 +132,37 @@ __device__ __forceinline__ bool tile_hit(const Proj64& p, int tx, int ty, const 
     return min_mahal_sq_to_rect(p.mx, p.my, p.a, p.b, p.c, lx, ly, hx, hy) <= SF_CUTOFF;
 }
 
-__global__ void __launch_bounds__(256) k_count_pairs(int64_t G, const int64_t* __restrict__ stats,
+__device__ __forceinline__ bool item_rank(int64_t i, const int64_t* stats, const uint32_t* rank_of, uint32_t& r) {
+    if (rank_of) {
+        r = rank_of[i];
+        return r != 0xffffffffu;
+    }
+    r = (uint32_t)i;
+    return i < stats[SF_STAT_VISIBLE];
+}
+
+// Count pass: exact tests of every candidate tile; the hit pattern over the
+// candidate rectangle (row-major, <= 64 tiles) is kept for the emit pass.
+__global__ void __launch_bounds__(256) k_count_pairs(int64_t N, const int64_t* __restrict__ stats,
                                                      const GeomRec* __restrict__ geom,
-                                                     TileGrid g, uint32_t* __restrict__ tile_counts) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= stats[SF_STAT_VISIBLE]) return;
-    Proj64 p = geom_proj(geom[r]);
+                                                     const uint32_t* __restrict__ rank_of,
+                                                     TileGrid g, uint32_t* __restrict__ tile_counts,
+                                                     unsigned long long* __restrict__ hit_mask) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t r;
+    if (i >= N || !item_rank(i, stats, rank_of, r)) return;
+    Proj64 p = geom_proj(geom[i]);
     int tx0, tx1, ty0, ty1;
     cand_rect(p, g, tx0, tx1, ty0, ty1);
+    unsigned long long mask = 0;
+    int bit = 0;
     for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx)
-            if (tile_hit(p, tx, ty, g)) atomicAdd(&tile_counts[ty * g.tiles_x + tx], 1u);
+        for (int tx = tx0; tx <= tx1; ++tx, ++bit)
+            if (tile_hit(p, tx, ty, g)) {
+                atomicAdd(&tile_counts[ty * g.tiles_x + tx], 1u);
+                if (bit < 64) mask |= 1ull << bit;
+            }
+    if (hit_mask) hit_mask[i] = mask;
 }
 
 // Exclusive scan over tiles (single CTA): offsets, cursors, pair total.
@@ -188,16 +194,31 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
     }
 }
 
-__global__ void __launch_bounds__(256) k_emit_pairs(int64_t G, const int64_t* __restrict__ stats,
-                                                    const GeomRec* __restrict__ geom, TileGrid g,
+__global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __restrict__ stats,
+                                                    const GeomRec* __restrict__ geom,
+                                                    const uint32_t* __restrict__ rank_of, TileGrid g,
+                                                    const unsigned long long* __restrict__ hit_mask,
                                                     uint32_t* __restrict__ cursor,
                                                     uint32_t* __restrict__ entries) {
     if (stats[SF_STAT_OVERFLOW]) return;
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= stats[SF_STAT_VISIBLE]) return;
-    Proj64 p = geom_proj(geom[r]);
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t r;
+    if (i >= N || !item_rank(i, stats, rank_of, r)) return;
+    Proj64 p = geom_proj(geom[i]);
     int tx0, tx1, ty0, ty1;
     cand_rect(p, g, tx0, tx1, ty0, ty1);
+    const int w = tx1 - tx0 + 1;
+    if (hit_mask && w * (ty1 - ty0 + 1) <= 64) {
+        unsigned long long mask = hit_mask[i];
+        while (mask) {
+            const int bit = __ffsll((long long)mask) - 1;
+            mask &= mask - 1;
+            const int tx = tx0 + bit % w, ty = ty0 + bit / w;
+            uint32_t pos = atomicAdd(&cursor[ty * g.tiles_x + tx], 1u);
+            entries[pos] = (uint32_t)r;
+        }
+        return;
+    }
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx)
             if (tile_hit(p, tx, ty, g)) {
@@ -280,14 +301,15 @@ __device__ __forceinline__ int rank_bits(const int64_t* stats) {
 template <int ITEMS>
 __global__ void __launch_bounds__(256) k_tile_sort_small(const uint32_t* __restrict__ offsets,
                                                          uint32_t* __restrict__ entries, int lo_exclusive,
-                                                         const int64_t* __restrict__ stats) {
+                                                         const int64_t* __restrict__ stats,
+                                                         const uint32_t* __restrict__ rank_to_row) {
     if (stats[SF_STAT_OVERFLOW]) return;
     typedef cub::BlockRadixSort<uint32_t, 256, ITEMS> Sort;
     __shared__ typename Sort::TempStorage tmp;
     const int t = blockIdx.x;
     const uint32_t beg = offsets[t], end = offsets[t + 1];
     const int n = (int)(end - beg);
-    if (n <= lo_exclusive || n > 256 * ITEMS || n <= 1) return;
+    if (n <= lo_exclusive || n > 256 * ITEMS) return;
     uint32_t keys[ITEMS];
     uint32_t* e = entries + beg;
 #pragma unroll
@@ -299,7 +321,7 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const uint32_t* __restr
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int idx = threadIdx.x * ITEMS + i;
-        if (idx < n) e[idx] = keys[i];
+        if (idx < n) e[idx] = rank_to_row ? __ldg(rank_to_row + keys[i]) : keys[i];
     }
 }
 
@@ -308,7 +330,8 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const uint32_t* __restr
 __global__ void __launch_bounds__(256) k_tile_sort_large(const uint32_t* __restrict__ offsets,
                                                          uint32_t* __restrict__ entries,
                                                          uint32_t* __restrict__ scratch, int lo_exclusive,
-                                                         const int64_t* __restrict__ stats) {
+                                                         const int64_t* __restrict__ stats,
+                                                         const uint32_t* __restrict__ rank_to_row) {
     if (stats[SF_STAT_OVERFLOW]) return;
     __shared__ uint32_t s[kSortSmemElems];
     int t = blockIdx.x;
@@ -322,29 +345,32 @@ __global__ void __launch_bounds__(256) k_tile_sort_large(const uint32_t* __restr
         for (int i = threadIdx.x; i < N; i += blockDim.x) s[i] = (i < n) ? e[i] : 0xffffffffu;
         __syncthreads();
         block_bitonic_sort(s, N);
-        for (int i = threadIdx.x; i < n; i += blockDim.x) e[i] = s[i];
+        for (int i = threadIdx.x; i < n; i += blockDim.x) e[i] = rank_to_row ? rank_to_row[s[i]] : s[i];
     } else {
         block_radix_split_global(e, scratch + beg, n, rank_bits(stats));
+        if (rank_to_row)
+            for (int i = threadIdx.x; i < n; i += blockDim.x) e[i] = rank_to_row[e[i]];
     }
 }
 
-void launch_binning(int64_t G, const int64_t* stats_n, const GeomRec* geom, int W, int H,
-                    int64_t pair_capacity, uint32_t* tile_counts, uint32_t* tile_offsets,
-                    uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
-                    int64_t* stats, cudaStream_t st) {
+void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint32_t* rank_of,
+                    const uint32_t* rank_to_row, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
+                    uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
+                    unsigned long long* hit_mask, cudaStream_t st) {
     TileGrid g{W, H, (W + SF_TILE - 1) / SF_TILE, (H + SF_TILE - 1) / SF_TILE};
     int n_tiles = g.tiles_x * g.tiles_y;
     cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * n_tiles, st);
-    int blocks = G > 0 ? ceil_div(G, 256) : 0;
-    if (blocks) k_count_pairs<<<blocks, 256, 0, st>>>(G, stats_n, geom, g, tile_counts);
+    int blocks = n_items > 0 ? ceil_div(n_items, 256) : 0;
+    if (blocks) k_count_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, tile_counts, hit_mask);
     k_tile_scan<<<1, 1024, 0, st>>>(n_tiles, tile_counts, tile_offsets, tile_cursor, pair_capacity,
-                                    stats);
-    if (blocks) k_emit_pairs<<<blocks, 256, 0, st>>>(G, stats_n, geom, g, tile_cursor, entries);
+                                    const_cast<int64_t*>(stats));
+    if (blocks)
+        k_emit_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, hit_mask, tile_cursor, entries);
     // per-tile canonical order: most lists fit one CUB block sort (<= 2048),
     // the rest go to the larger-capacity kernels (each CTA skips other sizes)
-    k_tile_sort_small<8><<<n_tiles, 256, 0, st>>>(tile_offsets, entries, 1, stats);
-    k_tile_sort_small<24><<<n_tiles, 256, 0, st>>>(tile_offsets, entries, 256 * 8, stats);
-    k_tile_sort_large<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, 256 * 24, stats);
+    k_tile_sort_small<8><<<n_tiles, 256, 0, st>>>(tile_offsets, entries, 0, stats, rank_to_row);
+    k_tile_sort_small<24><<<n_tiles, 256, 0, st>>>(tile_offsets, entries, 256 * 8, stats, rank_to_row);
+    k_tile_sort_large<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, 256 * 24, stats, rank_to_row);
 }
 
 }  // namespace sf

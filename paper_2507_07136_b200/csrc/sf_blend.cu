@@ -118,8 +118,8 @@ __device__ __forceinline__ float blend_alpha(const GeomRec& g, float pxf, float 
 }
 
 // CT: channels per Gaussian (0 = runtime), SINGLE: one channel block,
-// NV: fused relevancy vectors (0 = none, -1 = runtime count).
-template <int CT, bool SINGLE, int NV>
+// NC: canonical phrases of the fused relevancy (0 = none, -1 = runtime count).
+template <int CT, bool SINGLE, int NC>
 __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_block) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
@@ -279,41 +279,50 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
             }
         }
     }
-    if (NV != 0 && A.proj_cb && nchb == A.n_ch) {
-        // fused relevancy: logits_j = sum_l W[l] * P[b][l][j] in fp64; the
-        // projected codebook is staged in the idle batch buffers
-        const int nv = NV > 0 ? NV : 1 + A.n_canon;
-        const int np = A.n_levels * A.L * nv;
-        double* Ps = reinterpret_cast<double*>(&S.st[0]);
+    if (NC != 0 && A.proj_cb && nchb == A.n_ch) {
+        // fused relevancy (query.py:65-84): l_q - l_j = W . Pd_j with the
+        // logit-difference vectors Pd_j = P_q - P_cj of the projected codebook
+        // P = atoms @ [q; c]^T, fp64, staged in the idle batch buffers
+        const int nc = NC > 0 ? NC : A.n_canon;
+        const int nv = 1 + A.n_canon;
+        const int np = A.n_levels * A.L * nc;
+        double* Pd = reinterpret_cast<double*>(&S.st[0]);
         const bool fits = np * (int)sizeof(double) <= (int)sizeof(S.st);
         if (fits) {
-            for (int i = threadIdx.x; i < np; i += kBlendThreads) Ps[i] = A.proj_cb[i];
+            for (int i = threadIdx.x; i < np; i += kBlendThreads) {
+                const int j = i % nc, bl = i / nc;
+                Pd[i] = A.proj_cb[(size_t)bl * nv] - A.proj_cb[(size_t)bl * nv + 1 + j];
+            }
             __syncthreads();
         }
         if (inside) {
             for (int b = 0; b < A.n_levels; ++b) {
                 double best = INFINITY;
-                if (NV > 0 && fits) {
-                    const double* P = Ps + (size_t)b * A.L * nv;
-                    double lg[NV > 0 ? NV : 1];
-#pragma unroll
-                    for (int t = 0; t < (NV > 0 ? NV : 1); ++t) lg[t] = 0.0;
+                const float* wb = acc + (b * A.L) * kAccPitch + slot;
+                if (NC == 4 && fits) {
+                    const double* Pb = Pd + (size_t)b * A.L * 4;
+                    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll 4
                     for (int l = 0; l < A.L; ++l) {
-                        const double w = (double)acc[(b * A.L + l) * kAccPitch + slot];
-#pragma unroll
-                        for (int t = 0; t < (NV > 0 ? NV : 1); ++t) lg[t] = fma(w, P[l * (NV > 0 ? NV : 1) + t], lg[t]);
+                        const double w = (double)wb[l * kAccPitch];
+                        const double2 p01 = *reinterpret_cast<const double2*>(Pb + 4 * l);
+                        const double2 p23 = *reinterpret_cast<const double2*>(Pb + 4 * l + 2);
+                        d0 = fma(w, p01.x, d0);
+                        d1 = fma(w, p01.y, d1);
+                        d2 = fma(w, p23.x, d2);
+                        d3 = fma(w, p23.y, d3);
                     }
-#pragma unroll
-                    for (int t = 1; t < (NV > 0 ? NV : 1); ++t) best = np_minimum(best, sigmoid2(lg[0] - lg[t]));
+                    best = np_minimum(np_minimum(sigmoid2(d0), sigmoid2(d1)), np_minimum(sigmoid2(d2), sigmoid2(d3)));
                 } else {
-                    const double* P = (fits ? Ps : A.proj_cb) + (size_t)b * A.L * nv;
-                    double lq = 0.0;
-                    for (int l = 0; l < A.L; ++l) lq = fma((double)acc[(b * A.L + l) * kAccPitch + slot], P[l * nv], lq);
-                    for (int j = 1; j < nv; ++j) {
-                        double lc = 0.0;
-                        for (int l = 0; l < A.L; ++l)
-                            lc = fma((double)acc[(b * A.L + l) * kAccPitch + slot], P[l * nv + j], lc);
-                        best = np_minimum(best, sigmoid2(lq - lc));
+                    for (int j = 0; j < nc; ++j) {
+                        double dj = 0.0;
+                        for (int l = 0; l < A.L; ++l) {
+                            const double pd = fits ? Pd[((size_t)b * A.L + l) * nc + j]
+                                                   : A.proj_cb[((size_t)b * A.L + l) * nv] -
+                                                         A.proj_cb[((size_t)b * A.L + l) * nv + 1 + j];
+                            dj = fma((double)wb[l * kAccPitch], pd, dj);
+                        }
+                        best = np_minimum(best, sigmoid2(dj));
                     }
                 }
                 A.relevancy_raw[(size_t)b * A.W * A.H + (size_t)py * A.W + px] = best;
@@ -481,18 +490,14 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_blend_fixup(BlendArgs A) {
             const int nv = 1 + A.n_canon;
             for (int b = 0; b < A.n_levels; ++b) {
                 const double* P = A.proj_cb + (size_t)b * A.L * nv;
-                double lq = 0.0, best = INFINITY;
-                for (int l = 0; l < A.L; ++l) {
-                    const int c = b * A.L + l;
-                    lq = fma((double)(local ? (float)wl[c] : row[c]), P[l * nv], lq);
-                }
+                double best = INFINITY;
                 for (int j = 1; j < nv; ++j) {
-                    double lc = 0.0;
+                    double dj = 0.0;
                     for (int l = 0; l < A.L; ++l) {
                         const int c = b * A.L + l;
-                        lc = fma((double)(local ? (float)wl[c] : row[c]), P[l * nv + j], lc);
+                        dj = fma((double)(local ? (float)wl[c] : row[c]), P[l * nv] - P[l * nv + j], dj);
                     }
-                    best = np_minimum(best, sigmoid2(lq - lc));
+                    best = np_minimum(best, sigmoid2(dj));
                 }
                 A.relevancy_raw[(size_t)b * A.W * A.H + pix] = best;
             }
@@ -508,11 +513,11 @@ int launch_blend(const BlendArgs& a, cudaStream_t st) {
     int nblk = (a.n_ch + ch_block - 1) / ch_block;
     size_t smem = sizeof(BlendSmem) + (size_t)ch_block * kAccPitch * sizeof(float);
     const bool fast = (a.C == 12 && nblk == 1);
-    const int nv = a.proj_cb ? 1 + a.n_canon : 0;
+    const int nc = a.proj_cb ? a.n_canon : 0;
     void (*kern)(BlendArgs, int);
     int ki;
-    if (fast && nv == 0) { kern = k_blend<12, true, 0>; ki = 0; }
-    else if (fast && nv == 5) { kern = k_blend<12, true, 5>; ki = 1; }
+    if (fast && !a.proj_cb) { kern = k_blend<12, true, 0>; ki = 0; }
+    else if (fast && nc == 4) { kern = k_blend<12, true, 4>; ki = 1; }
     else if (fast) { kern = k_blend<12, true, -1>; ki = 2; }
     else { kern = k_blend<0, false, -1>; ki = 3; }
     static size_t configured[4] = {0, 0, 0, 0};

@@ -51,7 +51,8 @@ extern "C" int sf_abi_version(void) { return 1; }
 // frame workspace layout
 
 struct FrameWs {
-    Proj64* proj_by_row;
+    uint32_t* rank_of_row;
+    unsigned long long* hit_mask;
     uint64_t* keys_in;
     uint64_t* keys_out;
     uint32_t* vals_in;
@@ -84,7 +85,8 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     int64_t Gp = G > 0 ? G : 1;
     int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
     int C = n_levels * K;
-    ws->proj_by_row = c.take<Proj64>(Gp);
+    ws->rank_of_row = c.take<uint32_t>(Gp);
+    ws->hit_mask = c.take<unsigned long long>(Gp);
     ws->keys_in = c.take<uint64_t>(Gp);
     ws->keys_out = c.take<uint64_t>(Gp);
     ws->vals_in = c.take<uint32_t>(Gp);
@@ -170,15 +172,21 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     cudaMemsetAsync(ws.stats_f, 0, (8 + kMaxLevels) * sizeof(double), st);
     cudaMemsetAsync(ws.fixup, 0, sizeof(uint32_t), st);
     // K1
-    launch_preprocess(*s, *cam, ws.proj_by_row, ws.keys_in, ws.vals_in, ws.stats, st);
+    launch_preprocess(*s, *cam, ws.geom, ws.keys_in, ws.vals_in, ws.stats, st);
+    // per-row scatter plan: a scene constant for a level selection, so callers
+    // may pass a cached copy (sf_pack_channels)
+    const unsigned char* chan = f->chan_by_row;
+    if (!chan) {
+        launch_pack_channels(*s, lv, ws.chan, st);
+        chan = ws.chan;
+    }
     // K2
     if (depth_sort(ws.keys_in, ws.keys_out, ws.vals_in, ws.vals_out, G, ws.cub_tmp, ws.cub_bytes, st))
         return check_cuda("depth sort");
-    launch_rank_gather(G, ws.vals_out, ws.stats, ws.proj_by_row, s->opacities, s, lv, ws.geom, ws.chan, C,
-                       st);
-    // K3/K4
-    launch_binning(G, ws.stats, ws.geom, W, H, f->pair_capacity, ws.tile_counts, ws.tile_offsets,
-                   ws.tile_cursor, ws.entries, ws.scratch, ws.stats, st);
+    launch_rank_of_row(G, ws.vals_out, ws.stats, ws.rank_of_row, st);
+    // K3/K4: (tile, depth rank) lists, stored as scene rows
+    launch_binning(G, ws.stats, ws.geom, ws.rank_of_row, ws.vals_out, W, H, f->pair_capacity, ws.tile_counts,
+                   ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.hit_mask, st);
     if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
                                    ws.proj_cb, st);
     // K5/K6 (+ fused relevancy)
@@ -194,16 +202,17 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     a.tile_offsets = ws.tile_offsets;
     a.entries = ws.entries;
     a.geom = ws.geom;
-    a.chan = ws.chan;
+    a.chan = chan;
     a.fixup_count = ws.fixup;
     a.fixup_list = ws.fixup + 1;
     a.fixup_capacity = kFixupCapacity;
     a.stats = ws.stats;
     a.coeff_map = f->coeff_map;
     a.final_t = f->final_t;
-    // relevancy: from the coefficient map in HBM when it is written anyway
-    // (features decoded), else fused into the blend epilogue
-    const bool rel_from_map = q && f->coeff_map != nullptr;
+    // relevancy: fused into the blend epilogue while the coefficient tile is
+    // in shared memory; from the map in HBM only when the channels span
+    // several blend CTAs
+    const bool rel_from_map = q && n_ch > 192;
     a.proj_cb = (q && !rel_from_map) ? ws.proj_cb : nullptr;
     a.n_levels = f->n_levels;
     a.L = L;
@@ -244,7 +253,7 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
 // project_scene
 
 struct ProjWs {
-    Proj64* proj;
+    GeomRec* geom;
     uint64_t* keys;
     uint32_t* vals;
     int64_t* stats;
@@ -257,7 +266,7 @@ struct ProjWs {
 static size_t carve_project(void* base, size_t cap, int64_t G, ProjWs* w) {
     Carver c(base, cap);
     int64_t Gp = G > 0 ? G : 1;
-    w->proj = c.take<Proj64>(Gp);
+    w->geom = c.take<GeomRec>(Gp);
     w->keys = c.take<uint64_t>(Gp);
     w->vals = c.take<uint32_t>(Gp);
     w->stats = c.take<int64_t>(16);
@@ -292,8 +301,8 @@ extern "C" int sf_project_rows(const SfScene* s, const SfCamera* cam, const int6
     size_t need = carve_project(workspace, workspace_bytes, s->num_gaussians, &w);
     if (need > workspace_bytes) return fail(SF_ERR_WORKSPACE, "workspace too small");
     cudaMemsetAsync(w.stats, 0, 16 * sizeof(int64_t), st);
-    launch_preprocess(*s, *cam, w.proj, w.keys, w.vals, w.stats, st);
-    launch_project_compact(*s, w.proj, w.keys, orig_rows, w.flags, w.scan, means2d, inv_covs, depths,
+    launch_preprocess(*s, *cam, w.geom, w.keys, w.vals, w.stats, st);
+    launch_project_compact(*s, w.geom, w.keys, orig_rows, w.flags, w.scan, means2d, inv_covs, depths,
                            opacities, source_ids, rows, count_out, w.cub_tmp, w.cub_bytes, st);
     return check_cuda("sf_project");
 }
@@ -416,8 +425,8 @@ extern "C" int sf_bin(int64_t n, const double* means2d, const double* inv_covs, 
         depth_sort(w.k0, w.k1, w.v1, w.v0, n, w.cub_tmp, w.cub_bytes, st);
     }
     k_bin_finish<<<blocks, 256, 0, st>>>(n, w.v0, w.proj, w.geom, order, w.stats);
-    launch_binning(n, w.stats, w.geom, W, H, pair_cap, w.counts, w.offsets, w.cursor,
-                   (uint32_t*)tile_entries, w.scratch, w.stats, st);
+    launch_binning(n, w.stats, w.geom, nullptr, nullptr, W, H, pair_cap, w.counts, w.offsets, w.cursor,
+                   (uint32_t*)tile_entries, w.scratch, nullptr, st);
     k_offsets_to_i64<<<ceil_div(n_tiles + 1, 256), 256, 0, st>>>(n_tiles, w.offsets, tile_offsets);
     if (stats_i64) cudaMemcpyAsync(stats_i64, w.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
     return check_cuda("sf_bin");
@@ -434,6 +443,27 @@ extern "C" int sf_decode(int64_t P, int32_t L, int32_t D, const float* w, int64_
     if (launch_decode(P, L, D, w, w_stride, cb, out, ws, (cudaStream_t)stream))
         return fail(SF_ERR_VALIDATION, "decode configuration unsupported (L=%d, D=%d)", L, D);
     return check_cuda("sf_decode");
+}
+
+extern "C" size_t sf_channel_plan_bytes(int64_t G, int32_t n_levels, int32_t K) {
+    return (size_t)(G > 0 ? G : 1) * chan_rec_bytes(n_levels * K);
+}
+
+extern "C" int sf_pack_channels(const SfScene* s, const int32_t* host_levels, int32_t n_levels,
+                                void* out, size_t out_bytes, void* stream) {
+    if (!s || n_levels < 1 || n_levels > kMaxLevels) return fail(SF_ERR_VALIDATION, "bad level selection");
+    if (n_levels * s->K > 16) return fail(SF_ERR_VALIDATION, "levels*K exceeds 16 channels per Gaussian");
+    if (out_bytes < sf_channel_plan_bytes(s->num_gaussians, n_levels, s->K))
+        return fail(SF_ERR_WORKSPACE, "channel plan buffer too small");
+    LevelSelDev lv;
+    lv.n = n_levels;
+    for (int b = 0; b < n_levels; ++b) {
+        if (host_levels[b] < 0 || host_levels[b] >= s->num_levels)
+            return fail(SF_ERR_VALIDATION, "level %d out of range", host_levels[b]);
+        lv.lv[b] = host_levels[b];
+    }
+    launch_pack_channels(*s, lv, (unsigned char*)out, (cudaStream_t)stream);
+    return check_cuda("sf_pack_channels");
 }
 
 extern "C" int sf_decode_simt(int64_t P, int32_t L, int32_t D, const float* w, int64_t w_stride,

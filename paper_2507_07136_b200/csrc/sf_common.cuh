@@ -146,9 +146,9 @@ struct LevelSelDev {
 // ---------------- internal launchers (one .cu each) ----------------
 
 // sf_preprocess.cu
-void launch_preprocess(const SfScene& s, const SfCamera& cam, Proj64* proj, uint64_t* keys,
+void launch_preprocess(const SfScene& s, const SfCamera& cam, GeomRec* geom, uint64_t* keys,
                        uint32_t* vals, int64_t* stats, cudaStream_t st);
-void launch_project_compact(const SfScene& s, const Proj64* proj, const uint64_t* keys,
+void launch_project_compact(const SfScene& s, const GeomRec* geom, const uint64_t* keys,
                             const int64_t* orig_rows_or_null, int32_t* flags, int32_t* scan,
                             double* means2d, double* inv_covs, double* depths, double* opac,
                             int64_t* source_ids, int64_t* rows, int64_t* count, void* cub_tmp,
@@ -160,14 +160,18 @@ size_t depth_sort_cub_bytes(int64_t n);
 int depth_sort(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in,
                uint32_t* vals_out, int64_t n, void* tmp, size_t tmp_bytes, cudaStream_t st);
 size_t id_sort_cub_bytes(int64_t n);
-void launch_rank_gather(int64_t G, const uint32_t* sorted_rows, const int64_t* stats,
-                        const Proj64* proj_by_row, const float* opac_by_row, const SfScene* s,
-                        const LevelSelDev& levels, GeomRec* geom, unsigned char* chan, int C,
-                        cudaStream_t st);
-void launch_binning(int64_t G, const int64_t* stats_n, const GeomRec* geom, int W, int H,
-                    int64_t pair_capacity, uint32_t* tile_counts, uint32_t* tile_offsets,
-                    uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
-                    int64_t* stats, cudaStream_t st);
+// rank_of_row[row] = canonical rank, ~0 for culled rows
+void launch_rank_of_row(int64_t G, const uint32_t* sorted_rows, const int64_t* stats,
+                        uint32_t* rank_of_row, cudaStream_t st);
+// per-row scatter plan (channel ids + values) of the selected levels
+void launch_pack_channels(const SfScene& s, const LevelSelDev& levels, unsigned char* chan, cudaStream_t st);
+// Binning over n_items geometry records.  rank_of == null: record i has
+// canonical rank i (i < stats[VISIBLE]); else rank_of[i] (~0 = culled).
+// rank_to_row != null: the sorted per-tile ranks are replaced by rows.
+void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint32_t* rank_of,
+                    const uint32_t* rank_to_row, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
+                    uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
+                    unsigned long long* hit_mask, cudaStream_t st);
 
 // sf_blend.cu
 struct BlendArgs {

@@ -9,15 +9,16 @@
 // makes means2d / inv_covs / depths bitwise equal to the reference.
 //
 // HBM layout: one thread per scene row (rows ordered by id).  Reads 44 B of
-// geometry per Gaussian (pos 12 + quat 16 + scale 12 + opacity 4), writes a
-// 40 B Proj64 record, an 8 B depth key and a 4 B row index.
+// geometry per Gaussian (pos 12 + quat 16 + scale 12 + opacity 4), writes the
+// row's 80 B blend record (GeomRec: fp32 rejection inputs + the fp64
+// projected values), an 8 B depth key and a 4 B row index.
 #include <cub/cub.cuh>
 
 #include "sf_common.cuh"
 
 namespace sf {
 
-__global__ void __launch_bounds__(256) k_preprocess(SfScene s, SfCamera cam, Proj64* __restrict__ proj,
+__global__ void __launch_bounds__(256) k_preprocess(SfScene s, SfCamera cam, GeomRec* __restrict__ geom,
                                                     uint64_t* __restrict__ keys,
                                                     uint32_t* __restrict__ vals,
                                                     unsigned long long* __restrict__ n_visible) {
@@ -96,13 +97,24 @@ __global__ void __launch_bounds__(256) k_preprocess(SfScene s, SfCamera cam, Pro
                                                    (double)(cam.width - 1), (double)(cam.height - 1));
                 if (qmin <= SF_CUTOFF) {
                     vis = true;
-                    Proj64 p;
-                    p.mx = m0;
-                    p.my = m1;
-                    p.a = i00;
-                    p.b = off;
-                    p.c = i11;
-                    proj[g] = p;
+                    // blend record of this row: fp32 rejection inputs + the fp64 values
+                    GeomRec q;
+                    q.mx_hi = (float)m0;
+                    q.mx_lo = (float)(m0 - (double)q.mx_hi);
+                    q.my_hi = (float)m1;
+                    q.my_lo = (float)(m1 - (double)q.my_hi);
+                    q.a = (float)i00;
+                    q.k = (float)(off / i00);
+                    q.d = (float)((i00 * i11 - off * off) / i00);
+                    q.opacity = s.opacities[g];
+                    q.mx = m0;
+                    q.my = m1;
+                    q.a64 = i00;
+                    q.b64 = off;
+                    q.c64 = i11;
+                    q.row = (uint32_t)g;
+                    q.pad = 0;
+                    geom[g] = q;
                     keys[g] = (uint64_t)__double_as_longlong(z);  // z > near > 0: bits are monotone
                 }
             }
@@ -119,11 +131,11 @@ __global__ void k_zero_i64(int64_t* p, int n) {
     if (i < n) p[i] = 0;
 }
 
-void launch_preprocess(const SfScene& s, const SfCamera& cam, Proj64* proj, uint64_t* keys,
+void launch_preprocess(const SfScene& s, const SfCamera& cam, GeomRec* geom, uint64_t* keys,
                        uint32_t* vals, int64_t* stats, cudaStream_t st) {
     if (s.num_gaussians == 0) return;
     int blocks = ceil_div(s.num_gaussians, 256);
-    k_preprocess<<<blocks, 256, 0, st>>>(s, cam, proj, keys, vals,
+    k_preprocess<<<blocks, 256, 0, st>>>(s, cam, geom, keys, vals,
                                          (unsigned long long*)(stats + SF_STAT_VISIBLE));
 }
 
@@ -136,7 +148,7 @@ __global__ void k_flags(int64_t G, const uint64_t* keys, const int64_t* orig_row
     flags[r] = keys[g] != ~0ull;
 }
 
-__global__ void k_compact(SfScene s, const Proj64* proj, const uint64_t* keys,
+__global__ void k_compact(SfScene s, const GeomRec* geom, const uint64_t* keys,
                           const int64_t* orig_rows, const int32_t* flags, const int32_t* scan,
                           double* means2d, double* inv_covs, double* depths, double* opac,
                           int64_t* source_ids, int64_t* rows, int64_t* count) {
@@ -147,7 +159,7 @@ __global__ void k_compact(SfScene s, const Proj64* proj, const uint64_t* keys,
     if (r == G - 1) *count = (int64_t)scan[r] + flags[r];
     if (keys[g] == ~0ull) return;
     int64_t o = scan[r];
-    Proj64 p = proj[g];
+    Proj64 p = geom_proj(geom[g]);
     means2d[2 * o] = p.mx;
     means2d[2 * o + 1] = p.my;
     inv_covs[4 * o] = p.a;
@@ -166,7 +178,7 @@ size_t project_compact_cub_bytes(int64_t G) {
     return bytes;
 }
 
-void launch_project_compact(const SfScene& s, const Proj64* proj, const uint64_t* keys,
+void launch_project_compact(const SfScene& s, const GeomRec* geom, const uint64_t* keys,
                             const int64_t* orig_rows, int32_t* flags, int32_t* scan,
                             double* means2d, double* inv_covs, double* depths, double* opac,
                             int64_t* source_ids, int64_t* rows, int64_t* count, void* cub_tmp,
@@ -179,7 +191,7 @@ void launch_project_compact(const SfScene& s, const Proj64* proj, const uint64_t
     int blocks = ceil_div(G, 256);
     k_flags<<<blocks, 256, 0, st>>>(G, keys, orig_rows, flags);
     cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, flags, scan, (int)G, st);
-    k_compact<<<blocks, 256, 0, st>>>(s, proj, keys, orig_rows, flags, scan, means2d, inv_covs,
+    k_compact<<<blocks, 256, 0, st>>>(s, geom, keys, orig_rows, flags, scan, means2d, inv_covs,
                                       depths, opac, source_ids, rows, count);
 }
 

@@ -177,6 +177,22 @@ class FrameEngine:
         self._ws_key = None
         self._lock = threading.Lock()
         self._events = None
+        self._plans = {}
+
+    def channel_plan(self, levels) -> "torch.Tensor":
+        """Cached per-row scatter plan of a level selection (a scene constant)."""
+        key = tuple(int(x) for x in levels)
+        plan = self._plans.get(key)
+        if plan is None:
+            lib = N.load()
+            cfg = self.ds.config
+            nbytes = int(lib.sf_channel_plan_bytes(self.ds.num_gaussians, len(key), cfg.K))
+            plan = torch.empty(nbytes, dtype=torch.uint8, device=self.ds.device)
+            lv = (ctypes.c_int32 * len(key))(*key)
+            N.check(lib.sf_pack_channels(ctypes.byref(self.ds.struct), ctypes.cast(lv, ctypes.c_void_p), len(key),
+                                         N.ptr(plan), nbytes, stream_ptr()))
+            self._plans[key] = plan
+        return plan
 
     def workspace(self, W: int, H: int, n_levels: int) -> "torch.Tensor":
         cfg = self.ds.config
@@ -231,6 +247,8 @@ class FrameEngine:
         fr.mask = N.ptr(out.mask)
         fr.stats_i64 = N.ptr(out.stats_i64)
         fr.stats_f64 = N.ptr(out.stats_f64)
+        if len(levels) * cfg.K <= 16:
+            fr.chan_by_row = N.ptr(self.channel_plan(levels))
         if timing:
             if self._events is None:
                 lib = N.load()
