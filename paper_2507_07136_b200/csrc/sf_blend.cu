@@ -40,7 +40,11 @@
 
 namespace sf {
 
-constexpr int kBlendThreads = 256;
+constexpr int kBlendThreads = 256;  // consumer threads: one per pixel
+constexpr int kConsumerWarps = kBlendThreads / 32;
+constexpr int kCTAThreads = kBlendThreads + 32;  // + one producer warp
+constexpr int kTilePixels = 256;
+constexpr int kStages = 3;          // batch ring between the producer and the consumer warps
 constexpr int kBatch = 32;
 constexpr int kAccPitch = 257;
 constexpr int kMaxC = 16;            // channels per Gaussian (levels*K) supported
@@ -54,8 +58,31 @@ struct __align__(16) BlendStage {
 };
 
 struct __align__(16) BlendSmem {
-    BlendStage st[2];
+    BlendStage st[kStages];
+    uint64_t full[kStages];   // producer -> consumers: batch staged (count 1)
+    uint64_t empty[kStages];  // consumers -> producer: batch consumed (one arrival per consumer warp)
+    int nb[kStages];          // batch size; 0 = end of the tile's stream
+    int n_done_warps;         // consumer warps whose pixels all saturated
 };
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
 
 __device__ __forceinline__ double sigmoid2(double x) {
     if (x >= 0) return 1.0 / (1.0 + exp(-x));
@@ -74,12 +101,13 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Issue the cp.async copies of one batch (nb records) into stage buffer S.
+// Issue the cp.async copies of one batch (nb records) into stage buffer S
+// (called by the 32 lanes of the producer warp).
 __device__ __forceinline__ void stage_batch(BlendStage& S, const BlendArgs& A, uint32_t base, int nb, int cs) {
     const int gchunks = (int)(sizeof(GeomRec) / 16);  // 5
     const int cchunks = cs / 16;
     const int per = gchunks + cchunks;
-    for (int idx = threadIdx.x; idx < nb * per; idx += kBlendThreads) {
+    for (int idx = (int)(threadIdx.x & 31); idx < nb * per; idx += 32) {
         int j = idx / per, c = idx - j * per;
         uint32_t r = __ldg(A.entries + base + j);
         if (c < gchunks) {
@@ -120,7 +148,7 @@ __device__ __forceinline__ float blend_alpha(const GeomRec& g, float pxf, float 
 // CT: channels per Gaussian (0 = runtime), SINGLE: one channel block,
 // NC: canonical phrases of the fused relevancy (0 = none, -1 = runtime count).
 template <int CT, bool SINGLE, int NC>
-__global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_block) {
+__global__ void __launch_bounds__(kCTAThreads, 1) k_blend(BlendArgs A, int ch_block) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
     float* acc = reinterpret_cast<float*>(smem_raw + sizeof(BlendSmem));
@@ -131,20 +159,29 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
     const int nchb = min(ch_block, A.n_ch - ch0);
     const int tx = tile % A.tiles_x, ty = tile / A.tiles_x;
     const int x0 = tx * SF_TILE, y0 = ty * SF_TILE;
-    const int slot = threadIdx.x;
+    const int slot = threadIdx.x & (kTilePixels - 1);
     const int warp = slot >> 5, lane = slot & 31;
+    const int cw = threadIdx.x >> 5;  // warp index within the CTA (0..15)
     const int lx = (warp & 1) * 8 + (lane & 7);
     const int ly = (warp >> 1) * 4 + (lane >> 3);
     const int px = x0 + lx, py = y0 + ly;
-    const bool inside = (px < A.W) && (py < A.H);
+    const bool inside = (threadIdx.x < kBlendThreads) && (px < A.W) && (py < A.H);
     const int C = CT > 0 ? CT : A.C;
     const int cs = chan_rec_bytes(C);
     const int voff = chan_val_offset(C);
 
     const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
-    if (beg < end) stage_batch(S.st[0], A, beg, (int)min((uint32_t)kBatch, end - beg), cs);
-    cp_async_commit();
-    for (int i = threadIdx.x; i < nchb * kAccPitch; i += kBlendThreads) acc[i] = 0.f;
+    const bool consumer = threadIdx.x < kBlendThreads;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kStages; ++st) {
+            bar_init(&S.full[st], 1);
+            bar_init(&S.empty[st], kConsumerWarps);
+        }
+        S.n_done_warps = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = threadIdx.x; i < nchb * kAccPitch; i += kCTAThreads) acc[i] = 0.f;
+    __syncthreads();
 
     const float pxf = (float)px, pyf = (float)py;
     const double pxd = (double)px, pyd = (double)py;
@@ -154,25 +191,46 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
     int ncontrib = 0;
     bool done = !inside;
 
-    int bi = 0;
-    for (uint32_t base = beg; base < end; base += kBatch, ++bi) {
-        const int nb = (int)min((uint32_t)kBatch, end - base);
-        BlendStage& B = S.st[bi & 1];
-        // prefetch the next batch into the other buffer (freed by the previous iteration's barrier)
-        const uint32_t nbase = base + kBatch;
-        if (nbase < end) stage_batch(S.st[(bi + 1) & 1], A, nbase, (int)min((uint32_t)kBatch, end - nbase), cs);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-        // channel ids -> accumulator byte offsets for this CTA's channel block
-        for (int idx = threadIdx.x; idx < nb * C; idx += kBlendThreads) {
-            int j = idx / C, k = idx - j * C;
-            int ch = (int)reinterpret_cast<const uint16_t*>(B.chan + j * kMaxChanRec)[k] - ch0;
-            B.off[j][k] = ((unsigned)ch < (unsigned)nchb) ? (uint32_t)(ch * kAccPitch * 4) : 0xffffffffu;
+    if (!consumer) {
+        // ---------------- producer warp: stream the tile's list through the ring ----------------
+        const int pl = threadIdx.x & 31;
+        for (int bi = 0;; ++bi) {
+            const int st = bi % kStages;
+            if (bi >= kStages) bar_wait(&S.empty[st], ((bi / kStages) - 1) & 1);
+            const uint32_t base = beg + (uint32_t)bi * kBatch;
+            const bool all_done = *reinterpret_cast<volatile int*>(&S.n_done_warps) == kConsumerWarps;
+            const int nb = (base < end && !all_done) ? (int)min((uint32_t)kBatch, end - base) : 0;
+            BlendStage& B = S.st[st];
+            if (nb) {
+                stage_batch(B, A, base, nb, cs);
+                cp_async_commit();
+                cp_async_wait<0>();
+                __syncwarp();
+                // channel ids -> accumulator byte offsets for this CTA's channel block
+                for (int idx = pl; idx < nb * C; idx += 32) {
+                    int j = idx / C, k = idx - j * C;
+                    int ch = (int)reinterpret_cast<const uint16_t*>(B.chan + j * kMaxChanRec)[k] - ch0;
+                    B.off[j][k] = ((unsigned)ch < (unsigned)nchb) ? (uint32_t)(ch * kAccPitch * 4) : 0xffffffffu;
+                }
+                __syncwarp();
+            }
+            if (pl == 0) {
+                S.nb[st] = nb;
+                bar_arrive(&S.full[st]);
+            }
+            if (nb == 0) break;
         }
-        __syncthreads();
-
-        if (!__all_sync(0xffffffffu, done)) {
+    } else {
+        // ---------------- consumer warps: progress independently through the ring ----------------
+        bool warp_done = __all_sync(0xffffffffu, done);
+        if (warp_done && lane == 0) atomicAdd(&S.n_done_warps, 1);
+        for (int bi = 0;; ++bi) {
+            const int st = bi % kStages;
+            bar_wait(&S.full[st], (bi / kStages) & 1);
+            const int nb = *reinterpret_cast<volatile int*>(&S.nb[st]);
+            if (nb == 0) break;
+            BlendStage& B = S.st[st];
+            if (!warp_done) {
             // ---- phase A: fp32 rejection (q > 9 + guard) -> candidate mask ----
             uint32_t cand = 0;
             if (!done) {
@@ -216,24 +274,22 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
                     char* accs = reinterpret_cast<char*>(acc + slot);
                     if (CT > 0 && CT % 4 == 0 && SINGLE) {
                         // a Gaussian's channel ids are distinct: all loads, then FMAs, then stores
-                        constexpr int NC = CT > 0 ? CT : 4;
-                        const uint4* o4 = reinterpret_cast<const uint4*>(B.off[j]);
-                        const float4* v4 = reinterpret_cast<const float4*>(val);
-                        uint32_t oo[NC];
-                        float vv[NC], av[NC];
+                        constexpr int NH = CT > 0 ? CT : 4;
+                        const uint32_t* oh = B.off[j];
+                        const float* vh = val;
+                        uint32_t oo[NH];
+                        float vv[NH], av[NH];
 #pragma unroll
-                        for (int q = 0; q < NC / 4; ++q) {
-                            const uint4 o = o4[q];
-                            const float4 v = v4[q];
-                            oo[4 * q] = o.x; oo[4 * q + 1] = o.y; oo[4 * q + 2] = o.z; oo[4 * q + 3] = o.w;
-                            vv[4 * q] = v.x; vv[4 * q + 1] = v.y; vv[4 * q + 2] = v.z; vv[4 * q + 3] = v.w;
+                        for (int e = 0; e < NH; ++e) {
+                            oo[e] = oh[e];
+                            vv[e] = vh[e];
                         }
 #pragma unroll
-                        for (int e = 0; e < NC; ++e) av[e] = *reinterpret_cast<const float*>(accs + oo[e]);
+                        for (int e = 0; e < NH; ++e) av[e] = *reinterpret_cast<const float*>(accs + oo[e]);
 #pragma unroll
-                        for (int e = 0; e < NC; ++e) av[e] = fmaf(ef, vv[e], av[e]);
+                        for (int e = 0; e < NH; ++e) av[e] = fmaf(ef, vv[e], av[e]);
 #pragma unroll
-                        for (int e = 0; e < NC; ++e) *reinterpret_cast<float*>(accs + oo[e]) = av[e];
+                        for (int e = 0; e < NH; ++e) *reinterpret_cast<float*>(accs + oo[e]) = av[e];
                     } else {
                         for (int k = 0; k < C; ++k) {
                             const uint32_t off = B.off[j][k];
@@ -247,9 +303,17 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
                 j = jn;
                 al = aln;
             }
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(&S.empty[st]);
+            if (!warp_done && __all_sync(0xffffffffu, done)) {
+                warp_done = true;
+                if (lane == 0) atomicAdd(&S.n_done_warps, 1);
+            }
         }
-        if (__syncthreads_and(done)) break;
     }
+    __syncthreads();
+
     // Early-exit decisions (counted iff T >= 1e-4) that fp32 T cannot certify
     // are replayed exactly in fp64 by k_blend_fixup.
     if (inside && A.early_exit && A.fixup_list && blockIdx.y == 0) {
@@ -261,9 +325,6 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
             if (k < A.fixup_capacity) A.fixup_list[k] = ((uint32_t)tile << 8) | (uint32_t)slot;
         }
     }
-    cp_async_wait<0>();
-    __syncthreads();
-
     // ---- outputs ----
     if (blockIdx.y == 0 && A.final_t && inside) A.final_t[(size_t)py * A.W + px] = T;
     if (A.coeff_map) {
@@ -272,7 +333,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
         const int tw = min(SF_TILE, A.W - x0), th = min(SF_TILE, A.H - y0);
         for (int r = 0; r < th; ++r) {
             const int wr = (r >> 2) * 2, lr = (r & 3) * 8;
-            for (int x = warp; x < tw; x += kBlendThreads / 32) {
+            for (int x = cw; x < tw; x += kConsumerWarps) {
                 const int sl = (wr + (x >> 3)) * 32 + lr + (x & 7);
                 float* dst = A.coeff_map + ((size_t)(y0 + r) * A.W + x0 + x) * A.n_ch + ch0;
                 for (int ch = lane; ch < nchb; ch += 32) __stcs(dst + ch, acc[ch * kAccPitch + sl]);
@@ -289,7 +350,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1) k_blend(BlendArgs A, int ch_
         double* Pd = reinterpret_cast<double*>(&S.st[0]);
         const bool fits = np * (int)sizeof(double) <= (int)sizeof(S.st);
         if (fits) {
-            for (int i = threadIdx.x; i < np; i += kBlendThreads) {
+            for (int i = threadIdx.x; i < np; i += kCTAThreads) {
                 const int j = i % nc, bl = i / nc;
                 Pd[i] = A.proj_cb[(size_t)bl * nv] - A.proj_cb[(size_t)bl * nv + 1 + j];
             }
@@ -525,7 +586,7 @@ int launch_blend(const BlendArgs& a, cudaStream_t st) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured[ki] = smem;
     }
-    if (n_tiles > 0) kern<<<dim3(n_tiles, nblk), kBlendThreads, smem, st>>>(a, ch_block);
+    if (n_tiles > 0) kern<<<dim3(n_tiles, nblk), kCTAThreads, smem, st>>>(a, ch_block);
     if (n_tiles > 0 && a.fixup_list && a.early_exit) k_blend_fixup<<<296, 32 * kFixWarps, 0, st>>>(a);
     if (a.proj_cb && nblk > 1)
         launch_relevancy_from_cmap((int64_t)a.W * a.H, a.n_ch, a.coeff_map, a.proj_cb, a.n_levels, a.L,
