@@ -39,10 +39,11 @@ CONFIGS = {
     "E": (5_000_000, 1920, 1080),
 }
 # Kernels launched per query frame (sf_render_frame), from the ncu launch list in
-# profiles/r01_launches.csv: preprocess, CUB onesweep depth sort (9), rank gather,
-# count, tile scan, emit, tile sort, project codebook, blend, 3 x (codebook split
-# + tcgen05 decode), 2 x box filter, reduce, finalize, mask.
-KERNELS_PER_FRAME = 29
+# profiles/r01_launches_latest.csv: preprocess, CUB onesweep depth sort (10),
+# rank_of_row, count, tile scan, emit, 3 tile-sort kernels, project codebook,
+# blend, blend fixup, 3 x (codebook split + tcgen05 decode), 2 x box filter,
+# reduce, finalize, mask.
+KERNELS_PER_FRAME = 32
 
 
 def peaks():
