@@ -46,6 +46,25 @@ CONFIGS = {
 KERNELS_PER_FRAME = 32
 
 
+def ncu_traffic(kernel: str = "decode"):
+    """dram read+write bytes per launch of `kernel` from the committed ncu summary."""
+    try:
+        cur, rd, wr = None, None, None
+        for ln in open(os.path.join(ROOT, "profiles", "r01_ncu_summary.txt")):
+            ln = ln.strip()
+            if ln.startswith("kernel:"):
+                cur = ln.split(":", 1)[1].strip()
+            elif cur == kernel and ln.startswith("dram__bytes_read.sum"):
+                v, u = ln.split("=")[1].split()
+                rd = float(v) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}[u]
+            elif cur == kernel and ln.startswith("dram__bytes_write.sum"):
+                v, u = ln.split("=")[1].split()
+                wr = float(v) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}[u]
+        return None if rd is None or wr is None else rd + wr
+    except OSError:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -276,28 +295,14 @@ def main():
     hbm_peak, peak_kind = peaks()
     achieved = dec_bytes / (d_ms / 1e3) / 1e9
 
-    # feature-splat FPS (render + decode, no query post) and lazy-feature query FPS
-    out_f = eng.allocate(W, H, levels, coeff_map=True, features=True, query=False)
-    out_q = eng.allocate(W, H, levels, coeff_map=False, features=False, query=True)
-    extra = {}
-    for name, o, q in (("feature_splat", out_f, None), ("text_query_lazy_features", out_q, spec)):
-        for _ in range(3):
-            eng.enqueue(cam, levels, o, query=q, qdev=qdev)
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            eng.enqueue(cam, levels, o, query=q, qdev=qdev)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        extra[name] = args.steps / (ev0.elapsed_time(ev1) / 1e3)
-    del out_f, out_q
-
     # ---- e2e through the public API: query_pipeline with host query inputs ----
     e2e = None
     if not args.no_e2e:
+        del out  # release the device-loop buffers; the API allocates its own results
+        torch.cuda.empty_cache()
         qe = sf.QueryEmbedding("bench", qv)
         canon_pinned = torch.from_numpy(canon).pin_memory().numpy()
-        for _ in range(2):
+        for _ in range(3):
             sf.query_pipeline(scene, cam, qe, canon_pinned, features="eager", instrument=False,
                               max_elements=1 << 40)
         torch.cuda.synchronize()
@@ -319,6 +324,23 @@ def main():
                "h2d_bytes_per_step": int(qv.nbytes + canon.nbytes),
                "d2h_bytes_per_step": int(H * W + 16 * 8 + 16 * 8), "steps": n_e2e,
                "api": "paper_2507_07136_b200.query_pipeline(..., features='eager')"}
+
+    # feature-splat FPS (render + decode, no query post) and lazy-feature query FPS
+    out_f = eng.allocate(W, H, levels, coeff_map=True, features=True, query=False)
+    out_q = eng.allocate(W, H, levels, coeff_map=False, features=False, query=True)
+    extra = {}
+    for name, o, q in (("feature_splat", out_f, None), ("text_query_lazy_features", out_q, spec)):
+        for _ in range(3):
+            eng.enqueue(cam, levels, o, query=q, qdev=qdev)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            eng.enqueue(cam, levels, o, query=q, qdev=qdev)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        extra[name] = args.steps / (ev0.elapsed_time(ev1) / 1e3)
+    del out_f, out_q
+    torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -353,7 +375,9 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "k_decode_tc (3 levels, one frame)",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                         "algorithmic_bytes": dec_bytes, "traffic": None},
+                         "algorithmic_bytes": dec_bytes,
+                         "traffic": (3 * ncu_traffic("decode")) if ncu_traffic("decode") else None,
+                         "traffic_source": "profiles/r01_ncu_summary.txt (ncu --set full, per launch x 3 levels)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": KERNELS_PER_FRAME * args.steps,

@@ -155,7 +155,9 @@ class FrameOutputs:
     events: tuple | None = None
 
     def host_stats(self):
-        return self.stats_i64.cpu().numpy(), self.stats_f64.cpu().numpy()
+        if getattr(self, "_host", None) is None:
+            self._host = (self.stats_i64.cpu().numpy(), self.stats_f64.cpu().numpy())
+        return self._host
 
     def stage_ms(self):
         if not self.events:
@@ -276,7 +278,8 @@ class FrameEngine:
         with self._lock:
             for _ in range(4):
                 keep = self.enqueue(cam, levels, out, **kw)
-                st = out.stats_i64.cpu()
+                out._host = None
+                st = out.host_stats()[0]
                 del keep
                 if int(st[N.STAT_OVERFLOW]) == 0:
                     return out
