@@ -314,6 +314,7 @@ def main():
             res = sf.query_pipeline(scene, cam, qe, canon_pinned, features="eager", instrument=False,
                                     max_elements=1 << 40)
             _ = res.mask  # already on the host: the step's result
+            del res  # one frame's results alive at a time (the allocator reuses the block)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if dist is not None:

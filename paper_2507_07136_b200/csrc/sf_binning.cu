@@ -141,31 +141,56 @@ __device__ __forceinline__ bool item_rank(int64_t i, const int64_t* stats, const
     return i < stats[SF_STAT_VISIBLE];
 }
 
-// Count pass: exact tests of every candidate tile; the hit pattern over the
-// candidate rectangle (row-major, <= 64 tiles) is kept for the emit pass.
+// Count pass: exact tests of every candidate tile.  The first kBinSlots hits
+// of an item take their in-tile position from the counter (atomic with
+// return) and remember it, so the emit pass stores without atomics; later
+// hits count in a second counter bank and claim positions in the emit pass.
+// The hit pattern over the candidate rectangle (row-major, <= 64 tiles) is
+// kept too, so the emit pass repeats no fp64 arithmetic.
 __global__ void __launch_bounds__(256) k_count_pairs(int64_t N, const int64_t* __restrict__ stats,
                                                      const GeomRec* __restrict__ geom,
                                                      const uint32_t* __restrict__ rank_of,
                                                      TileGrid g, uint32_t* __restrict__ tile_counts,
-                                                     unsigned long long* __restrict__ hit_mask) {
+                                                     BinAux* __restrict__ aux) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t r;
     if (i >= N || !item_rank(i, stats, rank_of, r)) return;
     Proj64 p = geom_proj(geom[i]);
     int tx0, tx1, ty0, ty1;
     cand_rect(p, g, tx0, tx1, ty0, ty1);
-    unsigned long long mask = 0;
-    int bit = 0;
+    const int n_tiles = g.tiles_x * g.tiles_y;
+    BinAux a;
+    a.mask = 0;
+    a.tx0 = (uint16_t)tx0;
+    a.ty0 = (uint16_t)ty0;
+    a.w = (uint16_t)(tx1 - tx0 + 1);
+    a.h = (uint16_t)(ty1 - ty0 + 1);
+#pragma unroll
+    for (int k = 0; k < kBinSlots; ++k) a.pos[k] = 0;
+    int bit = 0, nh = 0;
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx, ++bit)
             if (tile_hit(p, tx, ty, g)) {
-                atomicAdd(&tile_counts[ty * g.tiles_x + tx], 1u);
-                if (bit < 64) mask |= 1ull << bit;
+                const int t = ty * g.tiles_x + tx;
+                if (nh < kBinSlots) {
+                    const uint32_t pos = atomicAdd(&tile_counts[t], 1u);
+#pragma unroll
+                    for (int k = 0; k < kBinSlots; ++k)
+                        if (k == nh) a.pos[k] = pos;
+                } else {
+                    atomicAdd(&tile_counts[n_tiles + t], 1u);
+                }
+                ++nh;
+                if (bit < 64) a.mask |= 1ull << bit;
             }
-    if (hit_mask) hit_mask[i] = mask;
+    const uint4* src = reinterpret_cast<const uint4*>(&a);
+    uint4* dst = reinterpret_cast<uint4*>(aux + i);
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(BinAux) / 16); ++k) dst[k] = src[k];
 }
 
-// Exclusive scan over tiles (single CTA): offsets, cursors, pair total.
+// Exclusive scan over tiles (single CTA): offsets, emit cursors (past the
+// slot-positioned entries), pair total.
 __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t* __restrict__ counts,
                                                     uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ cursor,
@@ -177,11 +202,12 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
     __syncthreads();
     for (int base = 0; base < n_tiles; base += 1024) {
         int t = base + threadIdx.x;
-        unsigned long long c = (t < n_tiles) ? counts[t] : 0, ex, tot;
+        unsigned long long c0 = (t < n_tiles) ? counts[t] : 0;
+        unsigned long long c = (t < n_tiles) ? c0 + counts[n_tiles + t] : 0, ex, tot;
         Scan(tmp).ExclusiveSum(c, ex, tot);
         if (t < n_tiles) {
             offsets[t] = (uint32_t)(carry + ex);
-            cursor[t] = (uint32_t)(carry + ex);
+            cursor[t] = (uint32_t)(carry + ex + c0);
         }
         __syncthreads();
         if (threadIdx.x == 0) carry += tot;
@@ -194,43 +220,66 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
     }
 }
 
+__device__ __forceinline__ void emit_one(int j, int t, uint32_t r, const BinAux& a,
+                                         const uint32_t* __restrict__ offsets, uint32_t* __restrict__ cursor,
+                                         uint32_t* __restrict__ entries) {
+    uint32_t pos;
+    if (j < kBinSlots) {
+        uint32_t slot = a.pos[0];
+#pragma unroll
+        for (int k = 1; k < kBinSlots; ++k)
+            if (k == j) slot = a.pos[k];
+        pos = __ldg(offsets + t) + slot;
+    } else {
+        pos = atomicAdd(&cursor[t], 1u);
+    }
+    entries[pos] = r;
+}
+
 __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __restrict__ stats,
                                                     const GeomRec* __restrict__ geom,
                                                     const uint32_t* __restrict__ rank_of, TileGrid g,
-                                                    const unsigned long long* __restrict__ hit_mask,
+                                                    const BinAux* __restrict__ aux,
+                                                    const uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ cursor,
                                                     uint32_t* __restrict__ entries) {
     if (stats[SF_STAT_OVERFLOW]) return;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t r;
     if (i >= N || !item_rank(i, stats, rank_of, r)) return;
-    Proj64 p = geom_proj(geom[i]);
-    int tx0, tx1, ty0, ty1;
-    cand_rect(p, g, tx0, tx1, ty0, ty1);
-    const int w = tx1 - tx0 + 1;
-    if (hit_mask && w * (ty1 - ty0 + 1) <= 64) {
-        unsigned long long mask = hit_mask[i];
+    BinAux a;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(aux + i);
+        uint4* dst = reinterpret_cast<uint4*>(&a);
+#pragma unroll
+        for (int k = 0; k < (int)(sizeof(BinAux) / 16); ++k) dst[k] = src[k];
+    }
+    const int w = a.w;
+    int j = 0;
+    if (w * (int)a.h <= 64) {
+        unsigned long long mask = a.mask;
         while (mask) {
             const int bit = __ffsll((long long)mask) - 1;
             mask &= mask - 1;
-            const int tx = tx0 + bit % w, ty = ty0 + bit / w;
-            uint32_t pos = atomicAdd(&cursor[ty * g.tiles_x + tx], 1u);
-            entries[pos] = (uint32_t)r;
+            const int tx = a.tx0 + bit % w, ty = a.ty0 + bit / w;
+            emit_one(j++, ty * g.tiles_x + tx, r, a, offsets, cursor, entries);
         }
         return;
     }
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx)
-            if (tile_hit(p, tx, ty, g)) {
-                uint32_t pos = atomicAdd(&cursor[ty * g.tiles_x + tx], 1u);
-                entries[pos] = (uint32_t)r;
-            }
+    // rectangles over 64 tiles: repeat the exact tests (same row-major hit order)
+    Proj64 p = geom_proj(geom[i]);
+    for (int ty = a.ty0; ty < a.ty0 + (int)a.h; ++ty)
+        for (int tx = a.tx0; tx < a.tx0 + w; ++tx)
+            if (tile_hit(p, tx, ty, g)) emit_one(j++, ty * g.tiles_x + tx, r, a, offsets, cursor, entries);
 }
 
 // ---------------------------------------------------------------------------
 // per-tile sort of depth ranks (restores canonical order inside each bucket)
 
 constexpr int kSortSmemElems = 8192;
+#ifndef SF_TILE_SORT_BITS
+#define SF_TILE_SORT_BITS 6  // radix digit width of the per-tile block sort (21-bit ranks: 4 passes)
+#endif
 
 __device__ void block_bitonic_sort(uint32_t* s, int N) {
     // N is a power of two; ascending.
@@ -304,7 +353,7 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const uint32_t* __restr
                                                          const int64_t* __restrict__ stats,
                                                          const uint32_t* __restrict__ rank_to_row) {
     if (stats[SF_STAT_OVERFLOW]) return;
-    typedef cub::BlockRadixSort<uint32_t, 256, ITEMS> Sort;
+    typedef cub::BlockRadixSort<uint32_t, 256, ITEMS, cub::NullType, SF_TILE_SORT_BITS> Sort;
     __shared__ typename Sort::TempStorage tmp;
     const int t = blockIdx.x;
     const uint32_t beg = offsets[t], end = offsets[t + 1];
@@ -356,16 +405,17 @@ __global__ void __launch_bounds__(256) k_tile_sort_large(const uint32_t* __restr
 void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint32_t* rank_of,
                     const uint32_t* rank_to_row, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
                     uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
-                    unsigned long long* hit_mask, cudaStream_t st) {
+                    BinAux* aux, cudaStream_t st) {
     TileGrid g{W, H, (W + SF_TILE - 1) / SF_TILE, (H + SF_TILE - 1) / SF_TILE};
     int n_tiles = g.tiles_x * g.tiles_y;
-    cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * n_tiles, st);
+    cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * 2 * n_tiles, st);
     int blocks = n_items > 0 ? ceil_div(n_items, 256) : 0;
-    if (blocks) k_count_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, tile_counts, hit_mask);
+    if (blocks) k_count_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, tile_counts, aux);
     k_tile_scan<<<1, 1024, 0, st>>>(n_tiles, tile_counts, tile_offsets, tile_cursor, pair_capacity,
                                     const_cast<int64_t*>(stats));
     if (blocks)
-        k_emit_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, hit_mask, tile_cursor, entries);
+        k_emit_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, aux, tile_offsets, tile_cursor,
+                                             entries);
     // per-tile canonical order: most lists fit one CUB block sort (<= 2048),
     // the rest go to the larger-capacity kernels (each CTA skips other sizes)
     k_tile_sort_small<8><<<n_tiles, 256, 0, st>>>(tile_offsets, entries, 0, stats, rank_to_row);

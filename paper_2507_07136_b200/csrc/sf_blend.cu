@@ -145,6 +145,36 @@ __device__ __forceinline__ float blend_alpha(const GeomRec& g, float pxf, float 
     return fminf(g.opacity * exp2f(kNegHalfLog2e * q32), 0.99f);
 }
 
+// Conservative patch culling: may any pixel of the 8x4 patch with corner
+// (x0, y0) have q <= 9?  q = a (dx + k dy)^2 + d dy^2 is convex, so its
+// minimum over the pixel-centre rectangle is 0 when the mean lies inside,
+// else on one of the four edges (1-D minimisation with clamping).  fp32 with
+// the same relative guard as blend_alpha; false positives only cost work,
+// blend_alpha still decides every pixel (exactly, inside the guard band).
+__device__ __forceinline__ bool patch_may_hit(const GeomRec& g, float x0, float y0) {
+    const float dx0 = (x0 - g.mx_hi) - g.mx_lo, dx1 = dx0 + 7.f;
+    const float dy0 = (y0 - g.my_hi) - g.my_lo, dy1 = dy0 + 3.f;
+    if (dx0 <= 0.f && dx1 >= 0.f && dy0 <= 0.f && dy1 >= 0.f) return true;
+    const float a = g.a, k = g.k, d = g.d;
+    const float c = fmaf(a * k, k, d);
+    const float s = -(a * k) / c;  // dy* = s * dx on an x edge
+    float best = INFINITY, bs = 0.f;
+    auto eval = [&](float dx, float dy) {
+        const float u = fmaf(k, dy, dx);
+        const float q = fmaf(a * u, u, d * dy * dy);
+        if (q < best) {
+            best = q;
+            const float su = fabsf(dx) + fabsf(k * dy);
+            bs = fmaf(a * su, su, d * dy * dy);
+        }
+    };
+    eval(dx0, fminf(fmaxf(s * dx0, dy0), dy1));
+    eval(dx1, fminf(fmaxf(s * dx1, dy0), dy1));
+    eval(fminf(fmaxf(-k * dy0, dx0), dx1), dy0);
+    eval(fminf(fmaxf(-k * dy1, dx0), dx1), dy1);
+    return best <= 9.f + fmaf(1e-4f, bs, 1e-4f);
+}
+
 // CT: channels per Gaussian (0 = runtime), SINGLE: one channel block,
 // NC: canonical phrases of the fused relevancy (0 = none, -1 = runtime count).
 template <int CT, bool SINGLE, int NC>
@@ -184,6 +214,7 @@ __global__ void __launch_bounds__(kCTAThreads, 1) k_blend(BlendArgs A, int ch_bl
     __syncthreads();
 
     const float pxf = (float)px, pyf = (float)py;
+    const float pdx0 = (float)(x0 + (warp & 1) * 8), pdy0 = (float)(y0 + (warp >> 1) * 4);  // patch corner
     const double pxd = (double)px, pyd = (double)py;
     float T = 1.f;        // transmittance (fp32: |dT|/T <= eb * 3e-6 + n * 1.2e-7, see header)
     float eb = 0.f;       // sum of alpha / (1 - alpha) over contributions (error-bound driver)
@@ -231,31 +262,17 @@ __global__ void __launch_bounds__(kCTAThreads, 1) k_blend(BlendArgs A, int ch_bl
             if (nb == 0) break;
             BlendStage& B = S.st[st];
             if (!warp_done) {
-            // ---- phase A: fp32 rejection (q > 9 + guard) -> candidate mask ----
-            uint32_t cand = 0;
-            if (!done) {
-#pragma unroll 4
-                for (int j = 0; j < nb; ++j) {
-                    const float4 m4 = *reinterpret_cast<const float4*>(&B.g[j].mx_hi);
-                    const float4 c4 = *reinterpret_cast<const float4*>(&B.g[j].a);
-                    const float dx = (pxf - m4.x) - m4.y;
-                    const float dy = (pyf - m4.z) - m4.w;
-                    const float u = fmaf(c4.y, dy, dx);
-                    const float ddy = c4.z * dy * dy;
-                    const float q32 = fmaf(c4.x * u, u, ddy);
-                    const float su = fabsf(dx) + fabsf(c4.y * dy);
-                    const float guard = fmaf(1e-5f, fmaf(c4.x * su, su, ddy), 1e-5f);
-                    if (q32 <= 9.f + guard) cand |= 1u << j;
-                }
-            }
+            // ---- phase A: lane j tests record j against the warp's 8x4 patch ----
+            // (conservative fp32 minimum of q over the patch rectangle, see patch_may_hit)
+            const uint32_t wcand = __ballot_sync(0xffffffffu, lane < nb && patch_may_hit(B.g[lane], pdx0, pdy0));
             // ---- phase B: alpha, transmittance, scatter -- depth order ----
             // alpha of the next candidate is computed before the current scatter
             // (it depends only on geometry), so its latency hides under the
             // scatter's shared-memory traffic.
-            uint32_t wmask = __reduce_or_sync(0xffffffffu, cand);
+            uint32_t wmask = wcand;
             int j = wmask ? __ffs(wmask) - 1 : -1;
             if (j >= 0) wmask &= wmask - 1;
-            float al = (j >= 0 && ((cand >> j) & 1u)) ? blend_alpha(B.g[j], pxf, pyf, pxd, pyd) : 0.f;
+            float al = (j >= 0 && !done) ? blend_alpha(B.g[j], pxf, pyf, pxd, pyd) : 0.f;
             while (j >= 0) {
                 float ef = 0.f;
                 if (al > 0.f && !done) {
@@ -268,21 +285,23 @@ __global__ void __launch_bounds__(kCTAThreads, 1) k_blend(BlendArgs A, int ch_bl
                 }
                 const int jn = wmask ? __ffs(wmask) - 1 : -1;
                 if (jn >= 0) wmask &= wmask - 1;
-                const float aln = (jn >= 0 && ((cand >> jn) & 1u) && !done) ? blend_alpha(B.g[jn], pxf, pyf, pxd, pyd) : 0.f;
+                const float aln = (jn >= 0 && !done) ? blend_alpha(B.g[jn], pxf, pyf, pxd, pyd) : 0.f;
                 if (__any_sync(0xffffffffu, ef > 0.f)) {
                     const float* val = reinterpret_cast<const float*>(B.chan + j * kMaxChanRec + voff);
                     char* accs = reinterpret_cast<char*>(acc + slot);
                     if (CT > 0 && CT % 4 == 0 && SINGLE) {
                         // a Gaussian's channel ids are distinct: all loads, then FMAs, then stores
                         constexpr int NH = CT > 0 ? CT : 4;
-                        const uint32_t* oh = B.off[j];
-                        const float* vh = val;
+                        const uint4* oh = reinterpret_cast<const uint4*>(B.off[j]);
+                        const float4* vh = reinterpret_cast<const float4*>(val);
                         uint32_t oo[NH];
                         float vv[NH], av[NH];
 #pragma unroll
-                        for (int e = 0; e < NH; ++e) {
-                            oo[e] = oh[e];
-                            vv[e] = vh[e];
+                        for (int e = 0; e < NH / 4; ++e) {
+                            const uint4 o4 = oh[e];
+                            const float4 v4 = vh[e];
+                            oo[4 * e] = o4.x, oo[4 * e + 1] = o4.y, oo[4 * e + 2] = o4.z, oo[4 * e + 3] = o4.w;
+                            vv[4 * e] = v4.x, vv[4 * e + 1] = v4.y, vv[4 * e + 2] = v4.z, vv[4 * e + 3] = v4.w;
                         }
 #pragma unroll
                         for (int e = 0; e < NH; ++e) av[e] = *reinterpret_cast<const float*>(accs + oo[e]);

@@ -52,7 +52,7 @@ extern "C" int sf_abi_version(void) { return 1; }
 
 struct FrameWs {
     uint32_t* rank_of_row;
-    unsigned long long* hit_mask;
+    BinAux* aux;
     uint64_t* keys_in;
     uint64_t* keys_out;
     uint32_t* vals_in;
@@ -86,7 +86,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
     int C = n_levels * K;
     ws->rank_of_row = c.take<uint32_t>(Gp);
-    ws->hit_mask = c.take<unsigned long long>(Gp);
+    ws->aux = c.take<BinAux>(Gp);
     ws->keys_in = c.take<uint64_t>(Gp);
     ws->keys_out = c.take<uint64_t>(Gp);
     ws->vals_in = c.take<uint32_t>(Gp);
@@ -97,7 +97,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->stats_f = c.take<double>(8 + kMaxLevels);
     ws->geom = c.take<GeomRec>(Gp);
     ws->chan = c.take<unsigned char>((size_t)Gp * chan_rec_bytes(C));
-    ws->tile_counts = c.take<uint32_t>(n_tiles);
+    ws->tile_counts = c.take<uint32_t>(2 * n_tiles);
     ws->tile_offsets = c.take<uint32_t>(n_tiles + 1);
     ws->tile_cursor = c.take<uint32_t>(n_tiles);
     ws->entries = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
@@ -186,7 +186,7 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     launch_rank_of_row(G, ws.vals_out, ws.stats, ws.rank_of_row, st);
     // K3/K4: (tile, depth rank) lists, stored as scene rows
     launch_binning(G, ws.stats, ws.geom, ws.rank_of_row, ws.vals_out, W, H, f->pair_capacity, ws.tile_counts,
-                   ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.hit_mask, st);
+                   ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, st);
     if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
                                    ws.proj_cb, st);
     // K5/K6 (+ fused relevancy)
@@ -376,6 +376,7 @@ struct BinWs {
     uint32_t* offsets;
     uint32_t* cursor;
     uint32_t* scratch;
+    BinAux* aux;
 };
 
 static size_t carve_bin(void* base, size_t cap, int64_t n, int W, int H, int64_t pair_cap, BinWs* w) {
@@ -391,7 +392,8 @@ static size_t carve_bin(void* base, size_t cap, int64_t n, int W, int H, int64_t
     w->cub_bytes = depth_sort_cub_bytes(np);
     w->cub_tmp = c.take<char>(w->cub_bytes);
     w->stats = c.take<int64_t>(16);
-    w->counts = c.take<uint32_t>(n_tiles);
+    w->counts = c.take<uint32_t>(2 * n_tiles);
+    w->aux = c.take<BinAux>(np);
     w->offsets = c.take<uint32_t>(n_tiles + 1);
     w->cursor = c.take<uint32_t>(n_tiles);
     w->scratch = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
@@ -426,7 +428,7 @@ extern "C" int sf_bin(int64_t n, const double* means2d, const double* inv_covs, 
     }
     k_bin_finish<<<blocks, 256, 0, st>>>(n, w.v0, w.proj, w.geom, order, w.stats);
     launch_binning(n, w.stats, w.geom, nullptr, nullptr, W, H, pair_cap, w.counts, w.offsets, w.cursor,
-                   (uint32_t*)tile_entries, w.scratch, nullptr, st);
+                   (uint32_t*)tile_entries, w.scratch, w.aux, st);
     k_offsets_to_i64<<<ceil_div(n_tiles + 1, 256), 256, 0, st>>>(n_tiles, w.offsets, tile_offsets);
     if (stats_i64) cudaMemcpyAsync(stats_i64, w.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
     return check_cuda("sf_bin");

@@ -168,10 +168,17 @@ void launch_pack_channels(const SfScene& s, const LevelSelDev& levels, unsigned 
 // Binning over n_items geometry records.  rank_of == null: record i has
 // canonical rank i (i < stats[VISIBLE]); else rank_of[i] (~0 = culled).
 // rank_to_row != null: the sorted per-tile ranks are replaced by rows.
+// tile_counts holds 2 * n_tiles counters; aux one BinAux per item.
+constexpr int kBinSlots = 8;
+struct __align__(16) BinAux {
+    unsigned long long mask;     // hits over the candidate rectangle, row-major (<= 64 tiles)
+    uint16_t tx0, ty0, w, h;     // candidate rectangle
+    uint32_t pos[kBinSlots];     // in-tile position of the first kBinSlots hits
+};
 void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint32_t* rank_of,
                     const uint32_t* rank_to_row, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
                     uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
-                    unsigned long long* hit_mask, cudaStream_t st);
+                    BinAux* aux, cudaStream_t st);
 
 // sf_blend.cu
 struct BlendArgs {

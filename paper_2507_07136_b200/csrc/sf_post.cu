@@ -18,29 +18,34 @@ __device__ __forceinline__ double sigmoid2p(double x) {
 }
 
 // P[b][l][j] = atoms_{lv_b}[l] . v_j, v_0 = query, v_j = canonical j-1 (fp64).
-__global__ void k_project_codebook(const float* __restrict__ cb, LevelSelDev lv, int L, int D,
-                                   const double* __restrict__ q, const double* __restrict__ canon,
-                                   int n_canon, double* __restrict__ out) {
-    int nv = 1 + n_canon;
-    int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    int total = lv.n * L * nv;
+// One warp per (b, l, j) dot product of length D, shuffle-reduced.
+__global__ void __launch_bounds__(256) k_project_codebook(const float* __restrict__ cb, LevelSelDev lv, int L, int D,
+                                                          const double* __restrict__ q,
+                                                          const double* __restrict__ canon, int n_canon,
+                                                          double* __restrict__ out) {
+    const int nv = 1 + n_canon;
+    const int lane = threadIdx.x & 31;
+    const int idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int total = lv.n * L * nv;
     if (idx >= total) return;
-    int j = idx % nv;
-    int l = (idx / nv) % L;
-    int b = idx / (nv * L);
+    const int j = idx % nv;
+    const int l = (idx / nv) % L;
+    const int b = idx / (nv * L);
     const float* a = cb + ((size_t)lv.lv[b] * L + l) * D;
     const double* v = (j == 0) ? q : canon + (size_t)(j - 1) * D;
     double s = 0.0;
-    for (int d = 0; d < D; ++d) s = fma((double)a[d], v[d], s);
-    out[idx] = s;
+    for (int d = lane; d < D; d += 32) s = fma((double)a[d], v[d], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[idx] = s;
 }
 
 void launch_project_codebook(const float* codebooks, const LevelSelDev& lv, int L, int D,
                              const double* q, const double* canon, int n_canon, double* out,
                              cudaStream_t st) {
     int total = lv.n * L * (1 + n_canon);
-    k_project_codebook<<<ceil_div(total, 128), 128, 0, st>>>(codebooks, lv, L, D, q, canon,
-                                                             n_canon, out);
+    k_project_codebook<<<ceil_div((int64_t)total * 32, 256), 256, 0, st>>>(codebooks, lv, L, D, q, canon,
+                                                                          n_canon, out);
 }
 
 template <typename T>
