@@ -40,13 +40,16 @@
 
 namespace sf {
 
-constexpr int kBlendThreads = 256;  // consumer threads: one per pixel
+// One CTA per half tile (16x8 pixels = 4 warp patches of 8x4): ~110 KB of
+// shared memory, so two CTAs share an SM and one's list start-up and
+// epilogue overlap the other's blending.
+constexpr int kBlendThreads = 128;  // consumer threads: one per pixel
 constexpr int kConsumerWarps = kBlendThreads / 32;
 constexpr int kCTAThreads = kBlendThreads + 32;  // + one producer warp
-constexpr int kTilePixels = 256;
-constexpr int kStages = 3;          // batch ring between the producer and the consumer warps
+constexpr int kTilePixels = 128;    // pixels per CTA (half a 16x16 tile)
+constexpr int kStages = 2;          // batch ring between the producer and the consumer warps
 constexpr int kBatch = 32;
-constexpr int kAccPitch = 257;
+constexpr int kAccPitch = 129;
 constexpr int kMaxC = 16;            // channels per Gaussian (levels*K) supported
 constexpr int kMaxChanRec = 96;      // chan_rec_bytes(16)
 constexpr int kChBlock = 192;        // accumulator channels per CTA (smem bound)
@@ -178,20 +181,21 @@ __device__ __forceinline__ bool patch_may_hit(const GeomRec& g, float x0, float 
 // CT: channels per Gaussian (0 = runtime), SINGLE: one channel block,
 // NC: canonical phrases of the fused relevancy (0 = none, -1 = runtime count).
 template <int CT, bool SINGLE, int NC>
-__global__ void __launch_bounds__(kCTAThreads, 1) k_blend(BlendArgs A, int ch_block) {
+__global__ void __launch_bounds__(kCTAThreads, 2) k_blend(BlendArgs A, int ch_block) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
     float* acc = reinterpret_cast<float*>(smem_raw + sizeof(BlendSmem));
 
     if (A.stats[SF_STAT_OVERFLOW]) return;
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x >> 1, half = blockIdx.x & 1;
     const int ch0 = blockIdx.y * ch_block;
     const int nchb = min(ch_block, A.n_ch - ch0);
     const int tx = tile % A.tiles_x, ty = tile / A.tiles_x;
     const int x0 = tx * SF_TILE, y0 = ty * SF_TILE;
-    const int slot = threadIdx.x & (kTilePixels - 1);
-    const int warp = slot >> 5, lane = slot & 31;
-    const int cw = threadIdx.x >> 5;  // warp index within the CTA (0..15)
+    const int slot = threadIdx.x & (kTilePixels - 1);  // pixel slot within the CTA
+    const int lane = slot & 31;
+    const int cw = threadIdx.x >> 5;                  // warp index within the CTA
+    const int warp = half * kConsumerWarps + (slot >> 5);  // patch index within the tile (0..7)
     const int lx = (warp & 1) * 8 + (lane & 7);
     const int ly = (warp >> 1) * 4 + (lane >> 3);
     const int px = x0 + lx, py = y0 + ly;
@@ -341,17 +345,19 @@ __global__ void __launch_bounds__(kCTAThreads, 1) k_blend(BlendArgs A, int ch_bl
         const bool amb = done ? (Tprev < thr * (1.f + tol) || T > thr * (1.f - tol)) : (T < thr * (1.f + tol));
         if (amb) {
             uint32_t k = atomicAdd(A.fixup_count, 1u);
-            if (k < A.fixup_capacity) A.fixup_list[k] = ((uint32_t)tile << 8) | (uint32_t)slot;
+            if (k < A.fixup_capacity) A.fixup_list[k] = ((uint32_t)tile << 8) | (uint32_t)(half * kTilePixels + slot);
         }
     }
     // ---- outputs ----
     if (blockIdx.y == 0 && A.final_t && inside) A.final_t[(size_t)py * A.W + px] = T;
     if (A.coeff_map) {
-        // warp w writes pixels x = w, w + 8 of every tile row; lanes stride the
-        // pixel's channels (contiguous in HBM), the smem read is conflict-free
-        const int tw = min(SF_TILE, A.W - x0), th = min(SF_TILE, A.H - y0);
-        for (int r = 0; r < th; ++r) {
-            const int wr = (r >> 2) * 2, lr = (r & 3) * 8;
+        // warp w writes pixels x = w, w + 4, ... of every row of the half
+        // tile; lanes stride the pixel's channels (contiguous in HBM), the
+        // smem read is conflict-free
+        const int tw = min(SF_TILE, A.W - x0), th = min(SF_TILE / 2, A.H - y0 - half * (SF_TILE / 2));
+        for (int rr = 0; rr < th; ++rr) {
+            const int r = half * (SF_TILE / 2) + rr;
+            const int wr = (rr >> 2) * 2, lr = (r & 3) * 8;
             for (int x = cw; x < tw; x += kConsumerWarps) {
                 const int sl = (wr + (x >> 3)) * 32 + lr + (x & 7);
                 float* dst = A.coeff_map + ((size_t)(y0 + r) * A.W + x0 + x) * A.n_ch + ch0;
@@ -392,7 +398,8 @@ __global__ void __launch_bounds__(kCTAThreads, 1) k_blend(BlendArgs A, int ch_bl
                         d2 = fma(w, p23.x, d2);
                         d3 = fma(w, p23.y, d3);
                     }
-                    best = np_minimum(np_minimum(sigmoid2(d0), sigmoid2(d1)), np_minimum(sigmoid2(d2), sigmoid2(d3)));
+                    // sigmoid is monotone: min_j sigmoid(d_j) = sigmoid(min_j d_j)
+                    best = sigmoid2(np_minimum(np_minimum(d0, d1), np_minimum(d2, d3)));
                 } else {
                     for (int j = 0; j < nc; ++j) {
                         double dj = 0.0;
@@ -605,7 +612,7 @@ int launch_blend(const BlendArgs& a, cudaStream_t st) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured[ki] = smem;
     }
-    if (n_tiles > 0) kern<<<dim3(n_tiles, nblk), kCTAThreads, smem, st>>>(a, ch_block);
+    if (n_tiles > 0) kern<<<dim3(2 * n_tiles, nblk), kCTAThreads, smem, st>>>(a, ch_block);
     if (n_tiles > 0 && a.fixup_list && a.early_exit) k_blend_fixup<<<296, 32 * kFixWarps, 0, st>>>(a);
     if (a.proj_cb && nblk > 1)
         launch_relevancy_from_cmap((int64_t)a.W * a.H, a.n_ch, a.coeff_map, a.proj_cb, a.n_levels, a.L,
