@@ -351,17 +351,29 @@ __global__ void __launch_bounds__(kCTAThreads, 2) k_blend(BlendArgs A, int ch_bl
     // ---- outputs ----
     if (blockIdx.y == 0 && A.final_t && inside) A.final_t[(size_t)py * A.W + px] = T;
     if (A.coeff_map) {
-        // warp w writes pixels x = w, w + 4, ... of every row of the half
-        // tile; lanes stride the pixel's channels (contiguous in HBM), the
-        // smem read is conflict-free
-        const int tw = min(SF_TILE, A.W - x0), th = min(SF_TILE / 2, A.H - y0 - half * (SF_TILE / 2));
-        for (int rr = 0; rr < th; ++rr) {
-            const int r = half * (SF_TILE / 2) + rr;
-            const int wr = (rr >> 2) * 2, lr = (r & 3) * 8;
-            for (int x = cw; x < tw; x += kConsumerWarps) {
-                const int sl = (wr + (x >> 3)) * 32 + lr + (x & 7);
-                float* dst = A.coeff_map + ((size_t)(y0 + r) * A.W + x0 + x) * A.n_ch + ch0;
-                for (int ch = lane; ch < nchb; ch += 32) __stcs(dst + ch, acc[ch * kAccPitch + sl]);
+        // Each warp instruction writes 4 pixels x 32 channels as float4:
+        // lane = (pixel p = lane / 8, channel quad q = lane % 8); the four
+        // scalar smem reads hit bank (4q + e + slot) mod 32 -- conflict-free
+        // with the 129-word pitch -- and the 16-byte stores of a pixel form
+        // one 128-byte line.  Slots past the image edge are skipped.
+        const int q = lane & 7, pl = lane >> 3;
+        const bool vec = (nchb % 32 == 0) && (A.n_ch % 4 == 0) && (ch0 % 4 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(A.coeff_map) & 15) == 0);
+        for (int sg = cw * 4; sg < kTilePixels; sg += 4 * kConsumerWarps) {
+            const int sl = sg + pl;                      // this lane's pixel slot
+            const int w8 = half * kConsumerWarps + (sl >> 5), l8 = sl & 31;
+            const int gx = x0 + (w8 & 1) * 8 + (l8 & 7), gy = y0 + (w8 >> 1) * 4 + (l8 >> 3);
+            const bool ok = gx < A.W && gy < A.H;
+            float* dst = A.coeff_map + ((size_t)gy * A.W + gx) * A.n_ch + ch0;
+            if (vec) {
+                for (int c0 = 0; c0 < nchb; c0 += 32) {
+                    const int c = c0 + 4 * q;
+                    const float* src = acc + c * kAccPitch + sl;
+                    const float4 v = make_float4(src[0], src[kAccPitch], src[2 * kAccPitch], src[3 * kAccPitch]);
+                    if (ok) __stcs(reinterpret_cast<float4*>(dst + c), v);
+                }
+            } else if (ok) {
+                for (int c = q; c < nchb; c += 8) __stcs(dst + c, acc[c * kAccPitch + sl]);
             }
         }
     }
