@@ -147,7 +147,7 @@ __device__ __forceinline__ bool item_rank(int64_t i, const int64_t* stats, const
 // hits count in a second counter bank and claim positions in the emit pass.
 // The hit pattern over the candidate rectangle (row-major, <= 64 tiles) is
 // kept too, so the emit pass repeats no fp64 arithmetic.
-__global__ void __launch_bounds__(256) k_count_pairs(int64_t N, const int64_t* __restrict__ stats,
+__global__ void __launch_bounds__(256, 4) k_count_pairs(int64_t N, const int64_t* __restrict__ stats,
                                                      const GeomRec* __restrict__ geom,
                                                      const uint32_t* __restrict__ rank_of,
                                                      TileGrid g, uint32_t* __restrict__ tile_counts,
@@ -374,6 +374,118 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const uint32_t* __restr
     }
 }
 
+// Per-tile sort of unique depth ranks, n <= CAP: MSD bucket sort in shared
+// memory.  Keys are distinct, so placement may use atomics (no stability is
+// needed): bucket = (key - min) * NB / (max - min + 1), histogram, scan,
+// scatter, then an insertion sort inside each bucket (a few keys on average).
+// A tile whose largest bucket exceeds kMaxBucket (strongly clustered ranks)
+// is bitonic-sorted instead.  The sorted ranks are written back as rows.
+constexpr int kMaxBucket = 48;
+template <int CAP, int NB>
+__global__ void __launch_bounds__(256) k_tile_sort_bucket(const uint32_t* __restrict__ offsets,
+                                                          uint32_t* __restrict__ entries, int lo_exclusive,
+                                                          const int64_t* __restrict__ stats,
+                                                          const uint32_t* __restrict__ rank_to_row) {
+    if (stats[SF_STAT_OVERFLOW]) return;
+    extern __shared__ __align__(16) uint32_t sort_smem[];
+    uint32_t* keys = sort_smem;         // CAP
+    uint32_t* outk = sort_smem + CAP;   // CAP
+    __shared__ uint32_t start[NB + 1];
+    __shared__ uint32_t cursor[NB];
+    __shared__ uint32_t s_min, s_max, s_big;
+    const int t = blockIdx.x;
+    const uint32_t beg = offsets[t], end = offsets[t + 1];
+    const int n = (int)(end - beg);
+    if (n <= lo_exclusive || n > CAP) return;
+    uint32_t* e = entries + beg;
+    if (threadIdx.x == 0) {
+        s_min = 0xffffffffu;
+        s_max = 0;
+        s_big = 0;
+    }
+    for (int b = threadIdx.x; b < NB; b += blockDim.x) cursor[b] = 0;
+    __syncthreads();
+    uint32_t mn = 0xffffffffu, mx = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t k = e[i];
+        keys[i] = k;
+        mn = min(mn, k);
+        mx = max(mx, k);
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&s_min, mn);
+        atomicMax(&s_max, mx);
+    }
+    __syncthreads();
+    const uint32_t kmin = s_min;
+    const uint64_t span = (uint64_t)(s_max - kmin) + 1;
+    // histogram
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int b = (int)(((uint64_t)(keys[i] - kmin) * NB) / span);
+        atomicAdd(&cursor[b], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the NB bucket counts (NB / 256 per thread)
+    {
+        typedef cub::BlockScan<uint32_t, 256> Scan;
+        __shared__ typename Scan::TempStorage tmp;
+        constexpr int PER = NB / 256;
+        uint32_t c[PER], sum = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            c[j] = cursor[threadIdx.x * PER + j];
+            sum += c[j];
+        }
+        uint32_t ex;
+        Scan(tmp).ExclusiveSum(sum, ex);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int b = threadIdx.x * PER + j;
+            start[b] = ex;
+            cursor[b] = ex;
+            if (c[j] > (uint32_t)kMaxBucket) s_big = 1;
+            ex += c[j];
+        }
+        if (threadIdx.x == 255) start[NB] = ex;
+    }
+    __syncthreads();
+    if (s_big) {
+        // clustered ranks: bitonic sort of the whole list
+        int N = 2;
+        while (N < n) N <<= 1;
+        for (int i = n + threadIdx.x; i < N; i += blockDim.x) keys[i] = 0xffffffffu;
+        __syncthreads();
+        block_bitonic_sort(keys, N);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) e[i] = rank_to_row ? __ldg(rank_to_row + keys[i]) : keys[i];
+        return;
+    }
+    // scatter into buckets
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t k = keys[i];
+        const int b = (int)(((uint64_t)(k - kmin) * NB) / span);
+        outk[atomicAdd(&cursor[b], 1u)] = k;
+    }
+    __syncthreads();
+    // insertion sort inside each bucket
+    for (int b = threadIdx.x; b < NB; b += blockDim.x) {
+        const int b0 = (int)start[b], b1 = (int)start[b + 1];
+        for (int i = b0 + 1; i < b1; ++i) {
+            const uint32_t k = outk[i];
+            int j = i - 1;
+            while (j >= b0 && outk[j] > k) {
+                outk[j + 1] = outk[j];
+                --j;
+            }
+            outk[j + 1] = k;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) e[i] = rank_to_row ? __ldg(rank_to_row + outk[i]) : outk[i];
+}
+
 // Longer lists: bitonic sort in shared memory up to 8192 entries, else a
 // stable 1-bit LSD split through global scratch.
 __global__ void __launch_bounds__(256) k_tile_sort_large(const uint32_t* __restrict__ offsets,
@@ -418,9 +530,16 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
                                              entries);
     // per-tile canonical order: most lists fit one CUB block sort (<= 2048),
     // the rest go to the larger-capacity kernels (each CTA skips other sizes)
-    k_tile_sort_small<8><<<n_tiles, 256, 0, st>>>(tile_offsets, entries, 0, stats, rank_to_row);
-    k_tile_sort_small<24><<<n_tiles, 256, 0, st>>>(tile_offsets, entries, 256 * 8, stats, rank_to_row);
-    k_tile_sort_large<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, 256 * 24, stats, rank_to_row);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_tile_sort_bucket<8192, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             2 * 8192 * 4);
+        configured = true;
+    }
+    k_tile_sort_bucket<2048, 512><<<n_tiles, 256, 2 * 2048 * 4, st>>>(tile_offsets, entries, 0, stats, rank_to_row);
+    k_tile_sort_bucket<8192, 1024><<<n_tiles, 256, 2 * 8192 * 4, st>>>(tile_offsets, entries, 2048, stats,
+                                                                       rank_to_row);
+    k_tile_sort_large<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192, stats, rank_to_row);
 }
 
 }  // namespace sf

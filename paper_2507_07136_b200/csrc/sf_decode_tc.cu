@@ -77,6 +77,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"((uint64_t)map), "r"(c0), "r"(c1)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"((uint64_t)map),
                  "r"(smem_u32(src)), "r"(c0), "r"(c1)
@@ -197,8 +201,15 @@ k_decode_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             tma_load_2d(S.b_hi[kb], &map_b, &S.b_full, kb * KBOX, n0);
             tma_load_2d(S.b_lo[kb], &map_b, &S.b_full, kb * KBOX, D + n0);
         }
+        constexpr int kPrefetch = 4;  // W tiles warmed into L2 ahead of their TMA load
+        if (split == 0)
+            for (int i = 0; i < kPrefetch && i < my_tiles; ++i)
+                for (int kb = 0; kb < nkb; ++kb) tma_prefetch_2d(&map_a, kb * KBOX, (group + i * groups) * BM);
         for (int i = 0; i < my_tiles; ++i) {
             const int s = i % kStages;
+            if (split == 0 && i + kPrefetch < my_tiles)
+                for (int kb = 0; kb < nkb; ++kb)
+                    tma_prefetch_2d(&map_a, kb * KBOX, (group + (i + kPrefetch) * groups) * BM);
             if (i >= kStages) mbar_wait(&S.empty[s], ((i / kStages) - 1) & 1);
             const int m = group + i * groups;
             mbar_expect_tx(&S.full[s], a_tile_bytes);
