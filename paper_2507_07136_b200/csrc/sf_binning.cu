@@ -21,6 +21,9 @@
 
 namespace sf {
 
+constexpr int kCountCTAs = 296;      // CTAs of the aggregated count pass (2 per SM)
+constexpr int kAggMaxTiles = 16384;  // shared-memory tile histogram limit (64 KB)
+
 size_t depth_sort_cub_bytes(int64_t n) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
@@ -28,6 +31,10 @@ size_t depth_sort_cub_bytes(int64_t n) {
     return bytes;
 }
 size_t id_sort_cub_bytes(int64_t n) { return depth_sort_cub_bytes(n); }
+size_t bin_cta_base_elems(int W, int H) {
+    const int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
+    return (size_t)kCountCTAs * (size_t)n_tiles;
+}
 
 int depth_sort(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in,
                uint32_t* vals_out, int64_t n, void* tmp, size_t tmp_bytes, cudaStream_t st) {
@@ -189,6 +196,65 @@ __global__ void __launch_bounds__(256, 4) k_count_pairs(int64_t N, const int64_t
     for (int k = 0; k < (int)(sizeof(BinAux) / 16); ++k) dst[k] = src[k];
 }
 
+// Aggregated count pass (n_tiles <= kAggMaxTiles): CTA c owns items
+// [c * per, (c + 1) * per) and counts its slot hits in a shared-memory tile
+// histogram (the in-CTA position comes from the shared atomic); one global
+// atomic per (CTA, tile) then reserves the CTA's range inside the tile and
+// its base is kept in cta_base[c][tile].  4x fewer global atomics than one
+// per pair, with the same emit-time arithmetic.
+__global__ void __launch_bounds__(512) k_count_pairs_agg(int64_t N, int64_t per, const int64_t* __restrict__ stats,
+                                                         const GeomRec* __restrict__ geom,
+                                                         const uint32_t* __restrict__ rank_of, TileGrid g,
+                                                         uint32_t* __restrict__ tile_counts, BinAux* __restrict__ aux,
+                                                         uint32_t* __restrict__ cta_base) {
+    extern __shared__ uint32_t hist[];
+    const int n_tiles = g.tiles_x * g.tiles_y;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) hist[t] = 0;
+    __syncthreads();
+    const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(N, i0 + per);
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        uint32_t r;
+        if (!item_rank(i, stats, rank_of, r)) continue;
+        Proj64 p = geom_proj(geom[i]);
+        int tx0, tx1, ty0, ty1;
+        cand_rect(p, g, tx0, tx1, ty0, ty1);
+        BinAux a;
+        a.mask = 0;
+        a.tx0 = (uint16_t)tx0;
+        a.ty0 = (uint16_t)ty0;
+        a.w = (uint16_t)(tx1 - tx0 + 1);
+        a.h = (uint16_t)(ty1 - ty0 + 1);
+#pragma unroll
+        for (int k = 0; k < kBinSlots; ++k) a.pos[k] = 0;
+        int bit = 0, nh = 0;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx, ++bit)
+                if (tile_hit(p, tx, ty, g)) {
+                    const int t = ty * g.tiles_x + tx;
+                    if (nh < kBinSlots) {
+                        const uint32_t pos = atomicAdd(&hist[t], 1u);
+#pragma unroll
+                        for (int k = 0; k < kBinSlots; ++k)
+                            if (k == nh) a.pos[k] = pos;
+                    } else {
+                        atomicAdd(&tile_counts[n_tiles + t], 1u);
+                    }
+                    ++nh;
+                    if (bit < 64) a.mask |= 1ull << bit;
+                }
+        const uint4* src = reinterpret_cast<const uint4*>(&a);
+        uint4* dst = reinterpret_cast<uint4*>(aux + i);
+#pragma unroll
+        for (int k = 0; k < (int)(sizeof(BinAux) / 16); ++k) dst[k] = src[k];
+    }
+    __syncthreads();
+    uint32_t* base = cta_base + (size_t)blockIdx.x * n_tiles;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint32_t c = hist[t];
+        base[t] = c ? atomicAdd(&tile_counts[t], c) : 0u;
+    }
+}
+
 // Exclusive scan over tiles (single CTA): offsets, emit cursors (past the
 // slot-positioned entries), pair total.
 __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t* __restrict__ counts,
@@ -221,15 +287,15 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
 }
 
 __device__ __forceinline__ void emit_one(int j, int t, uint32_t r, const BinAux& a,
-                                         const uint32_t* __restrict__ offsets, uint32_t* __restrict__ cursor,
-                                         uint32_t* __restrict__ entries) {
+                                         const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ base,
+                                         uint32_t* __restrict__ cursor, uint32_t* __restrict__ entries) {
     uint32_t pos;
     if (j < kBinSlots) {
         uint32_t slot = a.pos[0];
 #pragma unroll
         for (int k = 1; k < kBinSlots; ++k)
             if (k == j) slot = a.pos[k];
-        pos = __ldg(offsets + t) + slot;
+        pos = __ldg(offsets + t) + (base ? __ldg(base + t) : 0u) + slot;
     } else {
         pos = atomicAdd(&cursor[t], 1u);
     }
@@ -242,7 +308,8 @@ __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __
                                                     const BinAux* __restrict__ aux,
                                                     const uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ cursor,
-                                                    uint32_t* __restrict__ entries) {
+                                                    uint32_t* __restrict__ entries,
+                                                    const uint32_t* __restrict__ cta_base, int64_t per) {
     if (stats[SF_STAT_OVERFLOW]) return;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t r;
@@ -256,13 +323,14 @@ __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __
     }
     const int w = a.w;
     int j = 0;
+    const uint32_t* base = cta_base ? cta_base + (size_t)(i / per) * (g.tiles_x * g.tiles_y) : nullptr;
     if (w * (int)a.h <= 64) {
         unsigned long long mask = a.mask;
         while (mask) {
             const int bit = __ffsll((long long)mask) - 1;
             mask &= mask - 1;
             const int tx = a.tx0 + bit % w, ty = a.ty0 + bit / w;
-            emit_one(j++, ty * g.tiles_x + tx, r, a, offsets, cursor, entries);
+            emit_one(j++, ty * g.tiles_x + tx, r, a, offsets, base, cursor, entries);
         }
         return;
     }
@@ -270,7 +338,7 @@ __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __
     Proj64 p = geom_proj(geom[i]);
     for (int ty = a.ty0; ty < a.ty0 + (int)a.h; ++ty)
         for (int tx = a.tx0; tx < a.tx0 + w; ++tx)
-            if (tile_hit(p, tx, ty, g)) emit_one(j++, ty * g.tiles_x + tx, r, a, offsets, cursor, entries);
+            if (tile_hit(p, tx, ty, g)) emit_one(j++, ty * g.tiles_x + tx, r, a, offsets, base, cursor, entries);
 }
 
 // ---------------------------------------------------------------------------
@@ -517,17 +585,30 @@ __global__ void __launch_bounds__(256) k_tile_sort_large(const uint32_t* __restr
 void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint32_t* rank_of,
                     const uint32_t* rank_to_row, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
                     uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
-                    BinAux* aux, cudaStream_t st) {
+                    BinAux* aux, uint32_t* cta_base, cudaStream_t st) {
     TileGrid g{W, H, (W + SF_TILE - 1) / SF_TILE, (H + SF_TILE - 1) / SF_TILE};
     int n_tiles = g.tiles_x * g.tiles_y;
     cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * 2 * n_tiles, st);
     int blocks = n_items > 0 ? ceil_div(n_items, 256) : 0;
-    if (blocks) k_count_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, tile_counts, aux);
+    const bool agg = cta_base && n_tiles <= kAggMaxTiles && n_items > 0;
+    const int64_t per = agg ? (n_items + kCountCTAs - 1) / kCountCTAs : 1;
+    if (agg) {
+        static size_t configured = 0;
+        const size_t smem = sizeof(uint32_t) * n_tiles;
+        if (smem > configured) {
+            cudaFuncSetAttribute(k_count_pairs_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured = smem;
+        }
+        k_count_pairs_agg<<<kCountCTAs, 512, smem, st>>>(n_items, per, stats, geom, rank_of, g, tile_counts, aux,
+                                                         cta_base);
+    } else if (blocks) {
+        k_count_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, tile_counts, aux);
+    }
     k_tile_scan<<<1, 1024, 0, st>>>(n_tiles, tile_counts, tile_offsets, tile_cursor, pair_capacity,
                                     const_cast<int64_t*>(stats));
     if (blocks)
         k_emit_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, aux, tile_offsets, tile_cursor,
-                                             entries);
+                                             entries, agg ? cta_base : nullptr, per);
     // per-tile canonical order: most lists fit one CUB block sort (<= 2048),
     // the rest go to the larger-capacity kernels (each CTA skips other sizes)
     static bool configured = false;

@@ -53,6 +53,7 @@ extern "C" int sf_abi_version(void) { return 1; }
 struct FrameWs {
     uint32_t* rank_of_row;
     BinAux* aux;
+    uint32_t* cta_base;
     uint64_t* keys_in;
     uint64_t* keys_out;
     uint32_t* vals_in;
@@ -87,6 +88,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     int C = n_levels * K;
     ws->rank_of_row = c.take<uint32_t>(Gp);
     ws->aux = c.take<BinAux>(Gp);
+    ws->cta_base = c.take<uint32_t>(bin_cta_base_elems(W, H));
     ws->keys_in = c.take<uint64_t>(Gp);
     ws->keys_out = c.take<uint64_t>(Gp);
     ws->vals_in = c.take<uint32_t>(Gp);
@@ -186,7 +188,7 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     launch_rank_of_row(G, ws.vals_out, ws.stats, ws.rank_of_row, st);
     // K3/K4: (tile, depth rank) lists, stored as scene rows
     launch_binning(G, ws.stats, ws.geom, ws.rank_of_row, ws.vals_out, W, H, f->pair_capacity, ws.tile_counts,
-                   ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, st);
+                   ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, ws.cta_base, st);
     if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
                                    ws.proj_cb, st);
     // K5/K6 (+ fused relevancy)
@@ -377,6 +379,7 @@ struct BinWs {
     uint32_t* cursor;
     uint32_t* scratch;
     BinAux* aux;
+    uint32_t* cta_base;
 };
 
 static size_t carve_bin(void* base, size_t cap, int64_t n, int W, int H, int64_t pair_cap, BinWs* w) {
@@ -394,6 +397,7 @@ static size_t carve_bin(void* base, size_t cap, int64_t n, int W, int H, int64_t
     w->stats = c.take<int64_t>(16);
     w->counts = c.take<uint32_t>(2 * n_tiles);
     w->aux = c.take<BinAux>(np);
+    w->cta_base = c.take<uint32_t>(bin_cta_base_elems(W, H));
     w->offsets = c.take<uint32_t>(n_tiles + 1);
     w->cursor = c.take<uint32_t>(n_tiles);
     w->scratch = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
@@ -428,7 +432,7 @@ extern "C" int sf_bin(int64_t n, const double* means2d, const double* inv_covs, 
     }
     k_bin_finish<<<blocks, 256, 0, st>>>(n, w.v0, w.proj, w.geom, order, w.stats);
     launch_binning(n, w.stats, w.geom, nullptr, nullptr, W, H, pair_cap, w.counts, w.offsets, w.cursor,
-                   (uint32_t*)tile_entries, w.scratch, w.aux, st);
+                   (uint32_t*)tile_entries, w.scratch, w.aux, w.cta_base, st);
     k_offsets_to_i64<<<ceil_div(n_tiles + 1, 256), 256, 0, st>>>(n_tiles, w.offsets, tile_offsets);
     if (stats_i64) cudaMemcpyAsync(stats_i64, w.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
     return check_cuda("sf_bin");

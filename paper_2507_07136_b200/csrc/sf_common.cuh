@@ -178,7 +178,9 @@ struct __align__(16) BinAux {
 void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint32_t* rank_of,
                     const uint32_t* rank_to_row, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
                     uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
-                    BinAux* aux, cudaStream_t st);
+                    BinAux* aux, uint32_t* cta_base, cudaStream_t st);
+// per-(count CTA, tile) range bases of the aggregated count pass
+size_t bin_cta_base_elems(int W, int H);
 
 // sf_blend.cu
 struct BlendArgs {
