@@ -120,23 +120,24 @@ __device__ __forceinline__ void cand_rect(const Proj64& p, const TileGrid& g, in
     double cov_yy = p.a / den;
     double rx = 3.0 * sqrt(np_maximum(cov_xx, 0.0));
     double ry = 3.0 * sqrt(np_maximum(cov_yy, 0.0));
-    const double ts = (double)SF_TILE;
+    static_assert((SF_TILE & (SF_TILE - 1)) == 0, "tile size must be a power of two");
+    const double inv_ts = 1.0 / (double)SF_TILE;
     int64_t v;
-    v = np_to_i64(np_floor_divide(p.mx - rx, ts));
+    v = np_to_i64(np_floor_divide_pow2(p.mx - rx, inv_ts));
     tx0 = (int)(v < 0 ? 0 : (v > g.tiles_x - 1 ? g.tiles_x - 1 : v));
-    v = np_to_i64(np_floor_divide(p.mx + rx, ts));
+    v = np_to_i64(np_floor_divide_pow2(p.mx + rx, inv_ts));
     tx1 = (int)(v < 0 ? 0 : (v > g.tiles_x - 1 ? g.tiles_x - 1 : v));
-    v = np_to_i64(np_floor_divide(p.my - ry, ts));
+    v = np_to_i64(np_floor_divide_pow2(p.my - ry, inv_ts));
     ty0 = (int)(v < 0 ? 0 : (v > g.tiles_y - 1 ? g.tiles_y - 1 : v));
-    v = np_to_i64(np_floor_divide(p.my + ry, ts));
+    v = np_to_i64(np_floor_divide_pow2(p.my + ry, inv_ts));
     ty1 = (int)(v < 0 ? 0 : (v > g.tiles_y - 1 ? g.tiles_y - 1 : v));
 }
 
-__device__ __forceinline__ bool tile_hit(const Proj64& p, int tx, int ty, const TileGrid& g) {
+__device__ __forceinline__ bool tile_hit(const MahalPre& p, int tx, int ty, const TileGrid& g) {
     double lx = (double)(tx * SF_TILE), ly = (double)(ty * SF_TILE);
     double hx = np_minimum(lx + (double)SF_TILE, (double)g.W) - 1;
     double hy = np_minimum(ly + (double)SF_TILE, (double)g.H) - 1;
-    return min_mahal_sq_to_rect(p.mx, p.my, p.a, p.b, p.c, lx, ly, hx, hy) <= SF_CUTOFF;
+    return min_mahal_sq_to_rect_pre(p, lx, ly, hx, hy) <= SF_CUTOFF;
 }
 
 __device__ __forceinline__ bool item_rank(int64_t i, const int64_t* stats, const uint32_t* rank_of, uint32_t& r) {
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(256, 4) k_count_pairs(int64_t N, const int64_t
     Proj64 p = geom_proj(geom[i]);
     int tx0, tx1, ty0, ty1;
     cand_rect(p, g, tx0, tx1, ty0, ty1);
+    const MahalPre mp = mahal_pre(p.mx, p.my, p.a, p.b, p.c);
     const int n_tiles = g.tiles_x * g.tiles_y;
     BinAux a;
     a.mask = 0;
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(256, 4) k_count_pairs(int64_t N, const int64_t
     int bit = 0, nh = 0;
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx, ++bit)
-            if (tile_hit(p, tx, ty, g)) {
+            if (tile_hit(mp, tx, ty, g)) {
                 const int t = ty * g.tiles_x + tx;
                 if (nh < kBinSlots) {
                     const uint32_t pos = atomicAdd(&tile_counts[t], 1u);
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(512) k_count_pairs_agg(int64_t N, int64_t per,
         Proj64 p = geom_proj(geom[i]);
         int tx0, tx1, ty0, ty1;
         cand_rect(p, g, tx0, tx1, ty0, ty1);
+        const MahalPre mp = mahal_pre(p.mx, p.my, p.a, p.b, p.c);
         BinAux a;
         a.mask = 0;
         a.tx0 = (uint16_t)tx0;
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(512) k_count_pairs_agg(int64_t N, int64_t per,
         int bit = 0, nh = 0;
         for (int ty = ty0; ty <= ty1; ++ty)
             for (int tx = tx0; tx <= tx1; ++tx, ++bit)
-                if (tile_hit(p, tx, ty, g)) {
+                if (tile_hit(mp, tx, ty, g)) {
                     const int t = ty * g.tiles_x + tx;
                     if (nh < kBinSlots) {
                         const uint32_t pos = atomicAdd(&hist[t], 1u);
@@ -336,9 +339,10 @@ __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __
     }
     // rectangles over 64 tiles: repeat the exact tests (same row-major hit order)
     Proj64 p = geom_proj(geom[i]);
+    const MahalPre mp = mahal_pre(p.mx, p.my, p.a, p.b, p.c);
     for (int ty = a.ty0; ty < a.ty0 + (int)a.h; ++ty)
         for (int tx = a.tx0; tx < a.tx0 + w; ++tx)
-            if (tile_hit(p, tx, ty, g)) emit_one(j++, ty * g.tiles_x + tx, r, a, offsets, base, cursor, entries);
+            if (tile_hit(mp, tx, ty, g)) emit_one(j++, ty * g.tiles_x + tx, r, a, offsets, base, cursor, entries);
 }
 
 // ---------------------------------------------------------------------------

@@ -87,6 +87,12 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ double sigmoid2(double x) {
     if (x >= 0) return 1.0 / (1.0 + exp(-x));
     double ex = exp(x);
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(kCTAThreads, 2) k_blend(BlendArgs A, int ch_bl
                     ef = al * T;
                     Tprev = T;
                     T = fmaf(-al, T, T);
-                    eb += __fdividef(al, 1.f - al);
+                    eb = fmaf(al, rcp_approx(1.f - al), eb);  // 1 - al in [0.01, 1]: no denormals
                     ++ncontrib;
                     if (A.early_exit && T < (float)SF_EARLY_EXIT_T) done = true;
                 }

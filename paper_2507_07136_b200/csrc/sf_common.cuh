@@ -87,6 +87,56 @@ __host__ __device__ __forceinline__ double min_mahal_sq_to_rect(double mx, doubl
     return best;
 }
 
+// numpy floor_divide(a, 2^k) for the power-of-two tile size: a * 2^-k is
+// exact (no rounding above the subnormal range), so npy_divmod's
+// fmod/(a - mod)/b/floor sequence reduces to floor(a * 2^-k); a negative
+// subnormal that underflows to -0 still floors to -1 as npy_divmod does.
+__host__ __device__ __forceinline__ double np_floor_divide_pow2(double a, double inv_b) {
+    const double q = a * inv_b;
+    if (q == 0.0 && a < 0.0) return -1.0;
+    return floor(q);
+}
+
+// min_mahal_sq_to_rect with the per-Gaussian quotients hoisted: the same
+// IEEE operations in the same order (b / c, b / a and 2 b are computed once
+// per Gaussian instead of once per rectangle), so the result is identical.
+struct MahalPre {
+    double mx, my, a, b, c, boc, boa, twob;
+};
+__host__ __device__ __forceinline__ MahalPre mahal_pre(double mx, double my, double a, double b, double c) {
+    return MahalPre{mx, my, a, b, c, b / c, b / a, 2.0 * b};
+}
+__host__ __device__ __forceinline__ double min_mahal_sq_to_rect_pre(const MahalPre& p, double lx, double ly,
+                                                                    double hx, double hy) {
+    if ((p.mx >= lx) && (p.mx <= hx) && (p.my >= ly) && (p.my <= hy)) return 0.0;
+    double best = INFINITY;
+    {
+        double dx = lx - p.mx;
+        double ys = np_clip(p.my - p.boc * dx, ly, hy);
+        double dy = ys - p.my;
+        best = np_minimum(best, (p.a * dx) * dx + (p.twob * dx) * dy + (p.c * dy) * dy);
+    }
+    {
+        double dx = hx - p.mx;
+        double ys = np_clip(p.my - p.boc * dx, ly, hy);
+        double dy = ys - p.my;
+        best = np_minimum(best, (p.a * dx) * dx + (p.twob * dx) * dy + (p.c * dy) * dy);
+    }
+    {
+        double dy = ly - p.my;
+        double xs = np_clip(p.mx - p.boa * dy, lx, hx);
+        double dx = xs - p.mx;
+        best = np_minimum(best, (p.a * dx) * dx + (p.twob * dx) * dy + (p.c * dy) * dy);
+    }
+    {
+        double dy = hy - p.my;
+        double xs = np_clip(p.mx - p.boa * dy, lx, hx);
+        double dx = xs - p.mx;
+        best = np_minimum(best, (p.a * dx) * dx + (p.twob * dx) * dy + (p.c * dy) * dy);
+    }
+    return best;
+}
+
 // Projected record of one surviving Gaussian (fp64, the reference's values).
 struct __align__(8) Proj64 {
     double mx, my;  // means2d
