@@ -94,6 +94,18 @@ typedef struct SfFrame {
     /* optional cached per-row scatter plan of host_levels (sf_pack_channels);
      * NULL = built inside the frame */
     const unsigned char* chan_by_row;
+    /* Tile-band mode: pixel rows [band_y0, band_y1)
+     * are owned by this call; both 0 = the whole image.  The frame renders the
+     * tile rows covering the owned rows plus the mean-filter halo (window/2
+     * rows each side, clipped to the image) -- every rendered tile is
+     * identical to the full-frame one -- decodes and filters only those rows,
+     * and reduces select/localize/segment statistics over the owned rows
+     * (SF_STAT_LEVEL_ARGMAX / SF_STATF_LEVEL_MIN / LEVEL_MAX per level) for a
+     * cross-rank max-all-reduce; sf_mask_rows then applies the global
+     * normalisation.  Output buffers stay full-image sized; rows outside the
+     * rendered / owned range are not written. */
+    int32_t band_y0;
+    int32_t band_y1;
 } SfFrame;
 
 /* stats_i64 slots */
@@ -105,10 +117,12 @@ typedef struct SfFrame {
 #define SF_STAT_COL 5         /* localize() col */
 #define SF_STAT_DEGENERATE 6  /* segment().degenerate */
 #define SF_STAT_FIXUPS 7      /* pixels replayed exactly in fp64 (ambiguous early exit) */
+#define SF_STAT_LEVEL_ARGMAX 8 /* + b: first row-major argmax (flat, whole image) of block b over the owned rows */
 /* stats_f64 slots */
 #define SF_STATF_MIN 0        /* chosen map min */
 #define SF_STATF_MAX 1        /* chosen map max */
-#define SF_STATF_LEVEL_MAX 8  /* + b: max of filtered map of block b */
+#define SF_STATF_LEVEL_MAX 8  /* + b: max of filtered map of block b (owned rows) */
+/* stats_f64[8 + n_levels + b]: min of filtered map of block b (owned rows) */
 
 /* Per-row scatter plan (channel ids level*L+idx and values of the selected
  * levels, sparse_splat.py:126-132) -- a scene constant worth caching. */
@@ -191,6 +205,12 @@ size_t sf_select_segment_workspace_bytes(int32_t n_maps, int32_t height, int32_t
 int sf_select_segment(int32_t n_maps, int32_t height, int32_t width, const double* maps,
                       int32_t fixed_level, double threshold, uint8_t* mask, int64_t* stats_i64,
                       double* stats_f64, void* workspace, size_t workspace_bytes, void* stream);
+/* segment().mask rows [y0, y1) of map `level` of (n_maps,H,W) fp64 maps with
+ * the given (global) min/max: mask = (m - lo)/(hi - lo) > threshold, all zero
+ * when hi <= lo (query.py:136-145).  The band-mode step after the cross-rank
+ * reduction of the per-band statistics. */
+int sf_mask_rows(const double* maps, int32_t height, int32_t width, int32_t level, double lo, double hi,
+                 double threshold, int32_t y0, int32_t y1, uint8_t* mask, void* stream);
 
 /* Timing-event helpers for SfFrame.events (cudaEventCreate / elapsed ms). */
 void* sf_event_create(void);
@@ -200,7 +220,7 @@ float sf_event_elapsed_ms(void* start, void* end);
 /* Human-readable text of the last error on this thread. */
 const char* sf_last_error(void);
 /* ABI version (bumped on any signature change). */
-int sf_abi_version(void);
+int sf_abi_version(void); /* 2: SfFrame band fields */
 
 #ifdef __cplusplus
 }

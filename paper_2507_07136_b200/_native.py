@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(_HERE, "libsplatfield_b200.so")
 
 SF_OK, SF_ERR_VALIDATION, SF_ERR_RESOURCE, SF_ERR_CUDA, SF_ERR_WORKSPACE = 0, 1, 2, 3, 4
 STAT_VISIBLE, STAT_PAIRS, STAT_OVERFLOW, STAT_LEVEL, STAT_ROW, STAT_COL, STAT_DEGENERATE = range(7)
-STATF_MIN, STATF_MAX, STATF_LEVEL_MAX = 0, 1, 8
+STAT_FIXUPS, STAT_LEVEL_ARGMAX = 7, 8  # STAT_LEVEL_ARGMAX + b: band-owned first argmax of block b
+STATF_MIN, STATF_MAX, STATF_LEVEL_MAX = 0, 1, 8  # STATF_LEVEL_MAX + n_levels + b: block b min
 
 P = ctypes.c_void_p
 i32 = ctypes.c_int32
@@ -47,7 +48,7 @@ class SfFrame(ctypes.Structure):
     _fields_ = [("host_levels", P), ("n_levels", i32), ("early_exit", i32), ("pair_capacity", i64),
                 ("coeff_map", P), ("final_t", P), ("features", P), ("relevancy_raw", P),
                 ("relevancy_filtered", P), ("mask", P), ("stats_i64", P), ("stats_f64", P),
-                ("events", P * 4), ("chan_by_row", P)]
+                ("events", P * 4), ("chan_by_row", P), ("band_y0", i32), ("band_y1", i32)]
 
 
 EXPORTS = {
@@ -71,6 +72,8 @@ EXPORTS = {
     "sf_mean_filter": (ctypes.c_int, [i32, i32, P, i32, P, P, sz, P]),
     "sf_select_segment_workspace_bytes": (sz, [i32, i32, i32]),
     "sf_select_segment": (ctypes.c_int, [i32, i32, i32, P, i32, f64, P, P, P, P, sz, P]),
+    "sf_mask_rows": (ctypes.c_int, [P, i32, i32, i32, ctypes.c_double, ctypes.c_double, ctypes.c_double, i32,
+                                    i32, P, P]),
     "sf_event_create": (P, []),
     "sf_event_destroy": (None, [P]),
     "sf_event_elapsed_ms": (ctypes.c_float, [P, P]),

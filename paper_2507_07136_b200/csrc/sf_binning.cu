@@ -111,6 +111,7 @@ void launch_pack_channels(const SfScene& s, const LevelSelDev& levels, unsigned 
 
 struct TileGrid {
     int W, H, tiles_x, tiles_y;
+    int ty_lo, ty_hi;  // tile rows binned: [ty_lo, ty_hi] (band mode; else 0 .. tiles_y - 1)
 };
 
 __device__ __forceinline__ void cand_rect(const Proj64& p, const TileGrid& g, int& tx0, int& tx1,
@@ -131,6 +132,9 @@ __device__ __forceinline__ void cand_rect(const Proj64& p, const TileGrid& g, in
     ty0 = (int)(v < 0 ? 0 : (v > g.tiles_y - 1 ? g.tiles_y - 1 : v));
     v = np_to_i64(np_floor_divide_pow2(p.my + ry, inv_ts));
     ty1 = (int)(v < 0 ? 0 : (v > g.tiles_y - 1 ? g.tiles_y - 1 : v));
+    // band mode: only the band's tile rows (each tile's test is independent)
+    ty0 = max(ty0, g.ty_lo);
+    ty1 = min(ty1, g.ty_hi);
 }
 
 __device__ __forceinline__ bool tile_hit(const MahalPre& p, int tx, int ty, const TileGrid& g) {
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(256, 4) k_count_pairs(int64_t N, const int64_t
     a.tx0 = (uint16_t)tx0;
     a.ty0 = (uint16_t)ty0;
     a.w = (uint16_t)(tx1 - tx0 + 1);
-    a.h = (uint16_t)(ty1 - ty0 + 1);
+    a.h = (uint16_t)max(0, ty1 - ty0 + 1);
 #pragma unroll
     for (int k = 0; k < kBinSlots; ++k) a.pos[k] = 0;
     int bit = 0, nh = 0;
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(512) k_count_pairs_agg(int64_t N, int64_t per,
         a.tx0 = (uint16_t)tx0;
         a.ty0 = (uint16_t)ty0;
         a.w = (uint16_t)(tx1 - tx0 + 1);
-        a.h = (uint16_t)(ty1 - ty0 + 1);
+        a.h = (uint16_t)max(0, ty1 - ty0 + 1);
 #pragma unroll
         for (int k = 0; k < kBinSlots; ++k) a.pos[k] = 0;
         int bit = 0, nh = 0;
@@ -589,8 +593,10 @@ __global__ void __launch_bounds__(256) k_tile_sort_large(const uint32_t* __restr
 void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint32_t* rank_of,
                     const uint32_t* rank_to_row, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
                     uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
-                    BinAux* aux, uint32_t* cta_base, cudaStream_t st) {
-    TileGrid g{W, H, (W + SF_TILE - 1) / SF_TILE, (H + SF_TILE - 1) / SF_TILE};
+                    BinAux* aux, uint32_t* cta_base, int tile_row0, int tile_row1, cudaStream_t st) {
+    TileGrid g{W, H, (W + SF_TILE - 1) / SF_TILE, (H + SF_TILE - 1) / SF_TILE, 0, 0};
+    g.ty_lo = tile_row0;
+    g.ty_hi = (tile_row1 > tile_row0 ? tile_row1 : g.tiles_y) - 1;
     int n_tiles = g.tiles_x * g.tiles_y;
     cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * 2 * n_tiles, st);
     int blocks = n_items > 0 ? ceil_div(n_items, 256) : 0;

@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kCTAThreads, 2) k_blend(BlendArgs A, int ch_bl
     float* acc = reinterpret_cast<float*>(smem_raw + sizeof(BlendSmem));
 
     if (A.stats[SF_STAT_OVERFLOW]) return;
-    const int tile = blockIdx.x >> 1, half = blockIdx.x & 1;
+    const int tile = A.tile0 + (blockIdx.x >> 1), half = blockIdx.x & 1;
     const int ch0 = blockIdx.y * ch_block;
     const int nchb = min(ch_block, A.n_ch - ch0);
     const int tx = tile % A.tiles_x, ty = tile / A.tiles_x;
@@ -444,7 +444,8 @@ __global__ void __launch_bounds__(kCTAThreads, 2) k_blend(BlendArgs A, int ch_bl
 template <int NC>
 __global__ void __launch_bounds__(256) k_relevancy_from_cmap(int64_t P, int n_ch, const float* __restrict__ cmap,
                                                              const double* __restrict__ proj_cb, int n_levels,
-                                                             int L, int n_canon, double* __restrict__ out) {
+                                                             int L, int n_canon, double* __restrict__ out,
+                                                             int64_t out_stride) {
     extern __shared__ __align__(16) double Pd[];
     const int nc = NC > 0 ? NC : n_canon;
     const int nv = 1 + n_canon;
@@ -482,13 +483,13 @@ __global__ void __launch_bounds__(256) k_relevancy_from_cmap(int64_t P, int n_ch
                     best = np_minimum(best, sigmoid2(dj));
                 }
             }
-            out[(size_t)b * P + p] = best;
+            out[(size_t)b * out_stride + p] = best;
         }
     }
 }
 
 void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const double* proj_cb, int n_levels,
-                                int L, int n_canon, double* out, cudaStream_t st) {
+                                int L, int n_canon, double* out, int64_t out_stride, cudaStream_t st) {
     if (P == 0) return;
     const size_t smem = sizeof(double) * (size_t)n_levels * L * n_canon;
     const bool vec = (L % 4 == 0) && (n_ch % 4 == 0) && ((uintptr_t)cmap % 16 == 0);
@@ -500,9 +501,11 @@ void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const do
     }
     const int blocks = (int)std::min<int64_t>(ceil_div(P, 256), 148 * 8);
     if (vec && n_canon == 4)
-        k_relevancy_from_cmap<4><<<blocks, 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out);
+        k_relevancy_from_cmap<4><<<blocks, 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out,
+                                                            out_stride);
     else
-        k_relevancy_from_cmap<0><<<blocks, 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out);
+        k_relevancy_from_cmap<0><<<blocks, 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out,
+                                                            out_stride);
 }
 
 // Exact fp64 replay (rasterizer.py:161-177) of the pixels whose early-exit
@@ -613,7 +616,8 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_blend_fixup(BlendArgs A) {
 
 int launch_blend(const BlendArgs& a, cudaStream_t st) {
     if (a.C > kMaxC) return -2;
-    int n_tiles = a.tiles_x * a.tiles_y;
+    if (a.proj_cb && a.n_ch > kChBlock) return -3;  // fused relevancy needs every channel in one CTA
+    int n_tiles = a.n_band_tiles;
     int ch_block = a.n_ch < kChBlock ? a.n_ch : kChBlock;
     int nblk = (a.n_ch + ch_block - 1) / ch_block;
     size_t smem = sizeof(BlendSmem) + (size_t)ch_block * kAccPitch * sizeof(float);
@@ -632,10 +636,7 @@ int launch_blend(const BlendArgs& a, cudaStream_t st) {
     }
     if (n_tiles > 0) kern<<<dim3(2 * n_tiles, nblk), kCTAThreads, smem, st>>>(a, ch_block);
     if (n_tiles > 0 && a.fixup_list && a.early_exit) k_blend_fixup<<<296, 32 * kFixWarps, 0, st>>>(a);
-    if (a.proj_cb && nblk > 1)
-        launch_relevancy_from_cmap((int64_t)a.W * a.H, a.n_ch, a.coeff_map, a.proj_cb, a.n_levels, a.L,
-                                   a.n_canon, a.relevancy_raw, st);
-    return 0;
+    return 0;  // (relevancy for n_ch > one channel block: launch_relevancy_from_cmap by the caller)
 }
 
 }  // namespace sf

@@ -45,7 +45,7 @@ extern "C" float sf_event_elapsed_ms(void* a, void* b) {
     if (cudaEventElapsedTime(&ms, (cudaEvent_t)a, (cudaEvent_t)b) != cudaSuccess) return -1.f;
     return ms;
 }
-extern "C" int sf_abi_version(void) { return 1; }
+extern "C" int sf_abi_version(void) { return 2; }
 
 // ---------------------------------------------------------------------------
 // frame workspace layout
@@ -96,7 +96,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->cub_bytes = depth_sort_cub_bytes(Gp);
     ws->cub_tmp = c.take<char>(ws->cub_bytes);
     ws->stats = c.take<int64_t>(16);
-    ws->stats_f = c.take<double>(8 + kMaxLevels);
+    ws->stats_f = c.take<double>(8 + 2 * kMaxLevels);
     ws->geom = c.take<GeomRec>(Gp);
     ws->chan = c.take<unsigned char>((size_t)Gp * chan_rec_bytes(C));
     ws->tile_counts = c.take<uint32_t>(2 * n_tiles);
@@ -162,6 +162,19 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     }
     bool need_cmap = (f->features != nullptr) || (q && n_ch > 192);
     if (need_cmap && !f->coeff_map) return fail(SF_ERR_VALIDATION, "coefficient map buffer required");
+    // band mode: owned rows [y0, y1), rendered rows = tile rows covering the
+    // owned rows +- the mean-filter halo
+    const bool band = f->band_y1 > f->band_y0;
+    if (band && (f->band_y0 < 0 || f->band_y1 > H))
+        return fail(SF_ERR_VALIDATION, "band rows [%d, %d) outside the %d-row image", f->band_y0, f->band_y1, H);
+    if (!band && (f->band_y0 != 0 || f->band_y1 != 0))
+        return fail(SF_ERR_VALIDATION, "empty band [%d, %d)", f->band_y0, f->band_y1);
+    const int oy0 = band ? f->band_y0 : 0, oy1 = band ? f->band_y1 : H;
+    const int halo = (q && band) ? q->window / 2 : 0;
+    const int tiles_x = (W + SF_TILE - 1) / SF_TILE, tiles_y = (H + SF_TILE - 1) / SF_TILE;
+    const int tr0 = band ? max(0, oy0 - halo) / SF_TILE : 0;
+    const int tr1 = band ? (min(H, oy1 + halo) + SF_TILE - 1) / SF_TILE : tiles_y;
+    const int ry0 = tr0 * SF_TILE, ry1 = min(H, tr1 * SF_TILE);  // rendered pixel rows
 
     FrameWs ws;
     size_t need = carve_frame(workspace, workspace_bytes, s->num_gaussians, W, H, f->n_levels, L, K, D,
@@ -171,7 +184,7 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     const int64_t G = s->num_gaussians;
     if (f->events[0]) cudaEventRecord((cudaEvent_t)f->events[0], st);
     cudaMemsetAsync(ws.stats, 0, 16 * sizeof(int64_t), st);
-    cudaMemsetAsync(ws.stats_f, 0, (8 + kMaxLevels) * sizeof(double), st);
+    cudaMemsetAsync(ws.stats_f, 0, (8 + 2 * kMaxLevels) * sizeof(double), st);
     cudaMemsetAsync(ws.fixup, 0, sizeof(uint32_t), st);
     // K1
     launch_preprocess(*s, *cam, ws.geom, ws.keys_in, ws.vals_in, ws.stats, st);
@@ -188,7 +201,7 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     launch_rank_of_row(G, ws.vals_out, ws.stats, ws.rank_of_row, st);
     // K3/K4: (tile, depth rank) lists, stored as scene rows
     launch_binning(G, ws.stats, ws.geom, ws.rank_of_row, ws.vals_out, W, H, f->pair_capacity, ws.tile_counts,
-                   ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, ws.cta_base, st);
+                   ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, ws.cta_base, tr0, tr1, st);
     if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
                                    ws.proj_cb, st);
     // K5/K6 (+ fused relevancy)
@@ -196,8 +209,10 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     memset(&a, 0, sizeof(a));
     a.W = W;
     a.H = H;
-    a.tiles_x = (W + SF_TILE - 1) / SF_TILE;
-    a.tiles_y = (H + SF_TILE - 1) / SF_TILE;
+    a.tiles_x = tiles_x;
+    a.tiles_y = tiles_y;
+    a.tile0 = tr0 * tiles_x;
+    a.n_band_tiles = (tr1 - tr0) * tiles_x;
     a.n_ch = n_ch;
     a.C = C;
     a.early_exit = f->early_exit;
@@ -222,16 +237,18 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     a.relevancy_raw = q ? f->relevancy_raw : nullptr;
     if (launch_blend(a, st)) return fail(SF_ERR_VALIDATION, "blend configuration unsupported");
     if (rel_from_map)
-        launch_relevancy_from_cmap((int64_t)W * H, n_ch, f->coeff_map, ws.proj_cb, f->n_levels, L,
-                                   q->n_canonicals, f->relevancy_raw, st);
+        launch_relevancy_from_cmap((int64_t)W * (ry1 - ry0), n_ch, f->coeff_map + (size_t)ry0 * W * n_ch,
+                                   ws.proj_cb, f->n_levels, L, q->n_canonicals, f->relevancy_raw + (size_t)ry0 * W,
+                                   (int64_t)W * H, st);
     if (f->events[1]) cudaEventRecord((cudaEvent_t)f->events[1], st);
     // K7
     if (f->features) {
-        const int64_t P = (int64_t)W * H;
+        const int64_t HW = (int64_t)W * H;
+        const int64_t P = (int64_t)W * (ry1 - ry0);  // rendered rows only
         for (int b = 0; b < f->n_levels; ++b) {
-            if (launch_decode(P, L, D, f->coeff_map + (size_t)b * L, n_ch,
-                              s->codebooks + (size_t)lv.lv[b] * L * D, f->features + (size_t)b * P * D,
-                              ws.dec_ws, st))
+            if (launch_decode(P, L, D, f->coeff_map + (size_t)ry0 * W * n_ch + (size_t)b * L, n_ch,
+                              s->codebooks + (size_t)lv.lv[b] * L * D,
+                              f->features + (size_t)b * HW * D + (size_t)ry0 * W * D, ws.dec_ws, st))
                 return fail(SF_ERR_VALIDATION, "decode configuration unsupported (L=%d, D=%d)", L, D);
         }
     }
@@ -239,14 +256,14 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     // K8-K10
     if (q) {
         launch_mean_filter(f->n_levels, H, W, f->relevancy_raw, q->window, ws.filter_tmp,
-                           f->relevancy_filtered, st);
+                           f->relevancy_filtered, st, oy0, oy1);
         launch_select_segment(f->n_levels, H, W, f->relevancy_filtered, q->fixed_level, q->threshold,
-                              f->mask, ws.stats, ws.stats_f, ws.sel_ws, st);
+                              f->mask, ws.stats, ws.stats_f, ws.sel_ws, st, oy0, oy1);
     }
     if (f->events[3]) cudaEventRecord((cudaEvent_t)f->events[3], st);
     if (f->stats_i64) cudaMemcpyAsync(f->stats_i64, ws.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
     if (f->stats_f64)
-        cudaMemcpyAsync(f->stats_f64, ws.stats_f, (8 + f->n_levels) * sizeof(double),
+        cudaMemcpyAsync(f->stats_f64, ws.stats_f, (8 + 2 * f->n_levels) * sizeof(double),
                         cudaMemcpyDeviceToDevice, st);
     return check_cuda("sf_render_frame");
 }
@@ -432,7 +449,7 @@ extern "C" int sf_bin(int64_t n, const double* means2d, const double* inv_covs, 
     }
     k_bin_finish<<<blocks, 256, 0, st>>>(n, w.v0, w.proj, w.geom, order, w.stats);
     launch_binning(n, w.stats, w.geom, nullptr, nullptr, W, H, pair_cap, w.counts, w.offsets, w.cursor,
-                   (uint32_t*)tile_entries, w.scratch, w.aux, w.cta_base, st);
+                   (uint32_t*)tile_entries, w.scratch, w.aux, w.cta_base, 0, 0, st);
     k_offsets_to_i64<<<ceil_div(n_tiles + 1, 256), 256, 0, st>>>(n_tiles, w.offsets, tile_offsets);
     if (stats_i64) cudaMemcpyAsync(stats_i64, w.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
     return check_cuda("sf_bin");
@@ -516,4 +533,13 @@ extern "C" int sf_select_segment(int32_t n_maps, int32_t H, int32_t W, const dou
 
 extern "C" size_t sf_select_segment_workspace_bytes(int32_t n_maps, int32_t H, int32_t W) {
     return select_segment_ws_bytes(n_maps, H, W);
+}
+
+extern "C" int sf_mask_rows(const double* maps, int32_t H, int32_t W, int32_t level, double lo, double hi,
+                            double threshold, int32_t y0, int32_t y1, uint8_t* mask, void* stream) {
+    if (H < 1 || W < 1) return fail(SF_ERR_VALIDATION, "image size must be >= 1 pixel");
+    if (level < 0) return fail(SF_ERR_VALIDATION, "level must be >= 0");
+    if (y0 < 0 || y1 > H || y1 < y0) return fail(SF_ERR_VALIDATION, "rows [%d, %d) outside [0, %d)", y0, y1, H);
+    launch_mask_rows(H, W, maps, level, lo, hi, threshold, y0, y1, mask, (cudaStream_t)stream);
+    return check_cuda("sf_mask_rows");
 }

@@ -228,13 +228,14 @@ struct __align__(16) BinAux {
 void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint32_t* rank_of,
                     const uint32_t* rank_to_row, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
                     uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
-                    BinAux* aux, uint32_t* cta_base, cudaStream_t st);
+                    BinAux* aux, uint32_t* cta_base, int tile_row0, int tile_row1, cudaStream_t st);
 // per-(count CTA, tile) range bases of the aggregated count pass
 size_t bin_cta_base_elems(int W, int H);
 
 // sf_blend.cu
 struct BlendArgs {
     int W, H, tiles_x, tiles_y;
+    int tile0, n_band_tiles;  // tiles [tile0, tile0 + n_band_tiles) are blended (whole tile rows)
     int n_ch;          // n_levels * L
     int C;             // channels per Gaussian = n_levels * K
     int early_exit;
@@ -257,7 +258,8 @@ struct BlendArgs {
 int launch_blend(const BlendArgs& a, cudaStream_t st);
 // relevancy of every pixel/level from a coefficient map already in HBM
 void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const double* proj_cb,
-                                int n_levels, int L, int n_canon, double* out, cudaStream_t st);
+                                int n_levels, int L, int n_canon, double* out, int64_t out_level_stride,
+                                cudaStream_t st);
 
 // sf_post.cu
 void launch_project_codebook(const float* codebooks, const LevelSelDev& levels, int L, int D,
@@ -267,12 +269,15 @@ void launch_relevancy_f32(int64_t P, int D, const float* f, const double* q, con
                           int nc, double* out, cudaStream_t st);
 void launch_relevancy_f64(int64_t P, int D, const double* f, const double* q, const double* c,
                           int nc, double* out, cudaStream_t st);
+// [y0, y1): output / reduced rows (band mode); y1 <= y0 = all rows
 void launch_mean_filter(int n_maps, int H, int W, const double* in, int window, double* tmp,
-                        double* out, cudaStream_t st);
+                        double* out, cudaStream_t st, int y0 = 0, int y1 = 0);
 size_t select_segment_ws_bytes(int n_maps, int H, int W);
 void launch_select_segment(int n_maps, int H, int W, const double* maps, int fixed_level,
                            double threshold, uint8_t* mask, int64_t* stats_i64,
-                           double* stats_f64, void* ws, cudaStream_t st);
+                           double* stats_f64, void* ws, cudaStream_t st, int y0 = 0, int y1 = 0);
+void launch_mask_rows(int H, int W, const double* maps, int level, double lo, double hi, double threshold,
+                      int y0, int y1, uint8_t* mask, cudaStream_t st);
 
 // sf_decode.cu (SIMT cross-check) / sf_decode_tc.cu (tcgen05 3xTF32)
 int launch_decode_simt(int64_t P, int L, int D, const float* w, int64_t w_stride, const float* cb,

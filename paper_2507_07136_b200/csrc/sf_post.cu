@@ -76,11 +76,15 @@ void launch_relevancy_f64(int64_t P, int D, const double* f, const double* q, co
 }
 
 // Separable edge-clamped box filter.  Pass 1 sums rows, pass 2 columns.
+// Output rows [y0, y1) (band mode); pass 1 covers the rows pass 2 reads.
 __global__ void k_box_rows(int n_maps, int H, int W, const double* __restrict__ in, int r,
-                           double* __restrict__ out) {
+                           double* __restrict__ out, int ry0, int nrows) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t total = (int64_t)n_maps * H * W;
+    int64_t total = (int64_t)n_maps * nrows * W;
     if (i >= total) return;
+    const int64_t per = (int64_t)nrows * W;
+    const int64_t m = i / per;
+    i = m * (int64_t)H * W + (int64_t)ry0 * W + (i - m * per);  // index in the (n_maps, H, W) arrays
     int x = (int)(i % W);
     const double* row = in + (i - x);
     double s = 0.0;
@@ -91,10 +95,13 @@ __global__ void k_box_rows(int n_maps, int H, int W, const double* __restrict__ 
     out[i] = s;
 }
 __global__ void k_box_cols(int n_maps, int H, int W, const double* __restrict__ in, int r,
-                           double inv_area, double* __restrict__ out) {
+                           double inv_area, double* __restrict__ out, int y0, int nrows) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t total = (int64_t)n_maps * H * W;
+    int64_t total = (int64_t)n_maps * nrows * W;
     if (i >= total) return;
+    const int64_t per = (int64_t)nrows * W;
+    const int64_t mm = i / per;
+    i = mm * (int64_t)H * W + (int64_t)y0 * W + (i - mm * per);
     int64_t hw = (int64_t)H * W;
     int64_t m = i / hw;
     int64_t rem = i - m * hw;
@@ -109,17 +116,22 @@ __global__ void k_box_cols(int n_maps, int H, int W, const double* __restrict__ 
 }
 
 void launch_mean_filter(int n_maps, int H, int W, const double* in, int window, double* tmp,
-                        double* out, cudaStream_t st) {
-    int64_t total = (int64_t)n_maps * H * W;
+                        double* out, cudaStream_t st, int y0, int y1) {
+    if (y1 <= y0) y0 = 0, y1 = H;
+    int64_t total = (int64_t)n_maps * (y1 - y0) * W;
     if (total == 0) return;
     if (window == 1) {
-        cudaMemcpyAsync(out, in, total * sizeof(double), cudaMemcpyDeviceToDevice, st);
+        for (int m = 0; m < n_maps; ++m)
+            cudaMemcpyAsync(out + ((size_t)m * H + y0) * W, in + ((size_t)m * H + y0) * W,
+                            (size_t)(y1 - y0) * W * sizeof(double), cudaMemcpyDeviceToDevice, st);
         return;
     }
     int r = window / 2;
-    k_box_rows<<<ceil_div(total, 256), 256, 0, st>>>(n_maps, H, W, in, r, tmp);
-    k_box_cols<<<ceil_div(total, 256), 256, 0, st>>>(n_maps, H, W, tmp, r,
-                                                     (double)window * (double)window, out);
+    const int ry0 = max(0, y0 - r), ry1 = min(H, y1 + r);
+    const int64_t total_rows = (int64_t)n_maps * (ry1 - ry0) * W;
+    k_box_rows<<<ceil_div(total_rows, 256), 256, 0, st>>>(n_maps, H, W, in, r, tmp, ry0, ry1 - ry0);
+    k_box_cols<<<ceil_div(total, 256), 256, 0, st>>>(n_maps, H, W, tmp, r, (double)window * (double)window, out,
+                                                     y0, y1 - y0);
 }
 
 // ---- select_level / localize / segment ----
@@ -146,11 +158,11 @@ __device__ __forceinline__ MaxMin mm_combine(MaxMin a, MaxMin b) {
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs
 
 __global__ void __launch_bounds__(256) k_reduce_maps(int64_t hw, const double* __restrict__ maps,
-                                                     MaxMin* __restrict__ partial) {
+                                                     MaxMin* __restrict__ partial, int64_t i0, int64_t i1) {
     int m = blockIdx.y;
     const double* p = maps + (size_t)m * hw;
     MaxMin acc{-INFINITY, INT64_MAX, INFINITY};
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hw;
+    for (int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < i1;
          i += (int64_t)gridDim.x * blockDim.x) {
         double v = p[i];
         MaxMin x{v, i, v};
@@ -197,19 +209,39 @@ __global__ void k_finalize_select(int n_maps, int nblk, int W, const MaxMin* __r
         stats_i64[SF_STAT_DEGENERATE] = (c.mx <= c.mn) ? 1 : 0;
         stats_f64[SF_STATF_MIN] = c.mn;
         stats_f64[SF_STATF_MAX] = c.mx;
-        for (int m = 0; m < n_maps; ++m) stats_f64[SF_STATF_LEVEL_MAX + m] = per_map[m].mx;
+        for (int m = 0; m < n_maps; ++m) {
+            stats_f64[SF_STATF_LEVEL_MAX + m] = per_map[m].mx;
+            stats_f64[SF_STATF_LEVEL_MAX + n_maps + m] = per_map[m].mn;
+            stats_i64[SF_STAT_LEVEL_ARGMAX + m] = per_map[m].idx;
+        }
     }
 }
 
 __global__ void k_mask(int64_t hw, const double* __restrict__ maps, const int64_t* __restrict__ stats_i64,
-                       const double* __restrict__ stats_f64, double threshold, uint8_t* __restrict__ mask) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= hw) return;
+                       const double* __restrict__ stats_f64, double threshold, uint8_t* __restrict__ mask,
+                       int64_t i0, int64_t i1) {
+    int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= i1) return;
     int lvl = (int)stats_i64[SF_STAT_LEVEL];
     double lo = stats_f64[SF_STATF_MIN], hi = stats_f64[SF_STATF_MAX];
     uint8_t v = 0;
     if (!(hi <= lo)) v = ((maps[(size_t)lvl * hw + i] - lo) / (hi - lo)) > threshold;
     mask[i] = v;
+}
+
+__global__ void k_mask_rows(int64_t hw, const double* __restrict__ maps, int level, double lo, double hi,
+                            double threshold, uint8_t* __restrict__ mask, int64_t i0, int64_t i1) {
+    int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= i1) return;
+    uint8_t v = 0;
+    if (!(hi <= lo)) v = ((maps[(size_t)level * hw + i] - lo) / (hi - lo)) > threshold;
+    mask[i] = v;
+}
+
+void launch_mask_rows(int H, int W, const double* maps, int level, double lo, double hi, double threshold,
+                      int y0, int y1, uint8_t* mask, cudaStream_t st) {
+    const int64_t hw = (int64_t)H * W, i0 = (int64_t)y0 * W, i1 = (int64_t)y1 * W;
+    if (i1 > i0) k_mask_rows<<<ceil_div(i1 - i0, 256), 256, 0, st>>>(hw, maps, level, lo, hi, threshold, mask, i0, i1);
 }
 
 size_t select_segment_ws_bytes(int n_maps, int H, int W) {
@@ -218,13 +250,16 @@ size_t select_segment_ws_bytes(int n_maps, int H, int W) {
 
 void launch_select_segment(int n_maps, int H, int W, const double* maps, int fixed_level,
                            double threshold, uint8_t* mask, int64_t* stats_i64, double* stats_f64,
-                           void* ws, cudaStream_t st) {
+                           void* ws, cudaStream_t st, int y0, int y1) {
     int64_t hw = (int64_t)H * W;
+    if (y1 <= y0) y0 = 0, y1 = H;
+    const int64_t i0 = (int64_t)y0 * W, i1 = (int64_t)y1 * W;
     MaxMin* partial = (MaxMin*)ws;
-    k_reduce_maps<<<dim3(kRedBlocks, n_maps), 256, 0, st>>>(hw, maps, partial);
+    k_reduce_maps<<<dim3(kRedBlocks, n_maps), 256, 0, st>>>(hw, maps, partial, i0, i1);
     k_finalize_select<<<1, 32 * n_maps, 0, st>>>(n_maps, kRedBlocks, W, partial, fixed_level, stats_i64,
                                                   stats_f64);
-    if (mask) k_mask<<<ceil_div(hw, 256), 256, 0, st>>>(hw, maps, stats_i64, stats_f64, threshold, mask);
+    if (mask && i1 > i0)
+        k_mask<<<ceil_div(i1 - i0, 256), 256, 0, st>>>(hw, maps, stats_i64, stats_f64, threshold, mask, i0, i1);
 }
 
 }  // namespace sf

@@ -225,12 +225,15 @@ class FrameEngine:
             torch.empty((nl, H, W), dtype=f64, device=dev) if query else None,
             torch.empty((H, W), dtype=torch.uint8, device=dev) if (query and mask) else None,
             torch.zeros(16, dtype=torch.int64, device=dev),
-            torch.zeros(8 + 8, dtype=torch.float64, device=dev),
+            torch.zeros(8 + 2 * 8, dtype=torch.float64, device=dev),
         )
 
     def enqueue(self, cam, levels, out: FrameOutputs, *, query: QuerySpec | None = None,
-                early_exit: bool = True, qdev=None, timing: bool = False):
-        """Launch one frame on the current stream (no host synchronisation)."""
+                early_exit: bool = True, qdev=None, timing: bool = False, band=None):
+        """Launch one frame on the current stream (no host synchronisation).
+
+        ``band=(y0, y1)``: tile-band mode -- only pixel rows [y0, y1) are owned
+        (SfFrame.band_y0/1); ``None`` renders the whole image."""
         cfg = self.ds.config
         camc = camera_struct(cam)
         W, H = camc.width, camc.height
@@ -249,6 +252,8 @@ class FrameEngine:
         fr.mask = N.ptr(out.mask)
         fr.stats_i64 = N.ptr(out.stats_i64)
         fr.stats_f64 = N.ptr(out.stats_f64)
+        if band is not None:
+            fr.band_y0, fr.band_y1 = int(band[0]), int(band[1])
         if len(levels) * cfg.K <= 16:
             fr.chan_by_row = N.ptr(self.channel_plan(levels))
         if timing:

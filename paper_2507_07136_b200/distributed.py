@@ -56,6 +56,18 @@ def band_rows(height: int, world_size: int, rank: int, *, tile: int = 16, halo: 
     return Band(y0, y1, max(0, y0 - halo), min(height, y1 + halo))
 
 
+def combine_selection(level_max, level_argmax, level_min):
+    """Host-side combination of per-band statistics, the single-process twin of
+    ``global_selection``: lists (one entry per band) of per-level max / first
+    argmax (flat, whole image) / min -> (level, flat index, min, max) of the
+    reference's select_level / localize / segment (query.py:111-145)."""
+    mx = np.max(np.asarray(level_max, dtype=np.float64), axis=0)
+    mn = np.min(np.asarray(level_min, dtype=np.float64), axis=0)
+    level = int(np.argmax(mx))  # ties -> lowest level
+    cands = [int(a[level]) for m, a in zip(level_max, level_argmax) if m[level] == mx[level]]
+    return level, min(cands), float(mn[level]), float(mx[level])
+
+
 def global_selection(level_max, level_argmax, level_min, group=None):
     """All-reduce per-level (max, argmax, min) over ranks -> (level, flat index, min, max).
 
@@ -98,3 +110,82 @@ def gather_results(local: "torch.Tensor", group=None) -> "torch.Tensor":
     dist.all_gather_into_tensor(out, local.contiguous(), group=group) if local.is_cuda else \
         dist.all_gather(list(out.unbind(0)), local.contiguous(), group=group)
     return out
+
+
+@dataclass
+class BandQuery:
+    """One rank's share of a tile-band sharded query frame (config E)."""
+
+    band: Band
+    level: int
+    point: tuple
+    lo: float
+    hi: float
+    degenerate: bool
+    out: object  # FrameOutputs: filtered maps (owned rows) and mask rows [band.y0, band.y1)
+
+
+def band_statistics(out, n_levels: int):
+    """(max, first argmax, min) per level over the owned rows of a band frame."""
+    from . import _native as N
+
+    st_i, st_f = out.host_stats()
+    mx = [float(st_f[N.STATF_LEVEL_MAX + b]) for b in range(n_levels)]
+    mn = [float(st_f[N.STATF_LEVEL_MAX + n_levels + b]) for b in range(n_levels)]
+    am = [int(st_i[N.STAT_LEVEL_ARGMAX + b]) for b in range(n_levels)]
+    return mx, am, mn
+
+
+def mask_rows(out, level: int, lo: float, hi: float, threshold: float, y0: int, y1: int) -> None:
+    """segment().mask of rows [y0, y1) with the global normalisation (sf_mask_rows)."""
+    import ctypes
+
+    from . import _native as N
+    from .device import stream_ptr
+
+    H, W = out.height, out.width
+    N.check(N.load().sf_mask_rows(N.ptr(out.relevancy_filtered), H, W, int(level), ctypes.c_double(lo),
+                                  ctypes.c_double(hi), ctypes.c_double(threshold), int(y0), int(y1),
+                                  N.ptr(out.mask), stream_ptr()))
+
+
+def band_query(engine, cam, levels, spec, world_size: int, rank: int, group=None, out=None) -> BandQuery:
+    """Render and query the tile band of ``rank``.
+
+    The rank renders the tile rows covering its band plus the 5-pixel halo of
+    the 11x11 mean filter (the per-tile results are identical to the full
+    frame's), reduces per-level statistics over its own rows, max-all-reduces
+    them across ranks (``global_selection``; exact int64 keys) and writes its
+    mask rows with the global level / min / max.  With ``group=None`` and no
+    initialised process group the selection is the rank's own (world of 1)."""
+    import torch.distributed as dist
+
+    H = int(cam.height)
+    band = band_rows(H, world_size, rank, halo=int(spec.window) // 2)
+    if out is None:
+        # the coefficient map is only materialised when the channels span several
+        # blend CTAs (relevancy is then computed from the map, sf_capi.cu)
+        wide = len(levels) * int(engine.ds.config.L) > 192
+        out = engine.allocate(int(cam.width), H, levels, coeff_map=wide, features=False, query=True)
+    engine.run(cam, levels, out, query=spec, band=(band.y0, band.y1))
+    mx, am, mn = band_statistics(out, len(levels))
+    if dist.is_available() and dist.is_initialized():
+        level, idx, lo, hi = global_selection(mx, am, mn, group=group)
+    else:
+        level, idx, lo, hi = combine_selection([mx], [am], [mn])
+    if spec.fixed_level is not None and int(spec.fixed_level) >= 0:
+        level = int(spec.fixed_level)
+        if dist.is_available() and dist.is_initialized():
+            _, idx, lo, hi = _fixed_level_selection(mx, am, mn, level, group)
+        else:
+            idx, lo, hi = am[level], mn[level], mx[level]
+    mask_rows(out, level, lo, hi, float(spec.threshold), band.y0, band.y1)
+    W = int(cam.width)
+    return BandQuery(band, level, (idx // W, idx % W), lo, hi, not (hi > lo), out)
+
+
+def _fixed_level_selection(mx, am, mn, level, group):
+    """global_selection restricted to one level (query_pipeline(level=...))."""
+    one = [mx[level]], [am[level]], [mn[level]]
+    _, idx, lo, hi = global_selection(*one, group=group)
+    return level, idx, lo, hi

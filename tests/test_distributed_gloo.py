@@ -80,3 +80,18 @@ def test_band_sharded_selection_matches_single_process():
         assert ix == idx == 17 * 10 + 3
         assert mn == pytest.approx(maps[level].min()) and mx == pytest.approx(maps[level].max())
         assert n == world
+
+
+def test_combine_selection_rules():
+    """Host twin of global_selection: lowest level on ties, first row-major argmax."""
+    from paper_2507_07136_b200.distributed import combine_selection
+    # band 0 / band 1 of a 3-level, 4x5 image (rows 0-1 / 2-3)
+    mx = [[0.5, 0.9, 0.9], [0.7, 0.9, 0.2]]
+    am = [[3, 7, 1], [12, 11, 15]]
+    mn = [[0.1, 0.2, 0.3], [0.05, 0.25, 0.1]]
+    level, idx, lo, hi = combine_selection(mx, am, mn)
+    assert level == 1 and idx == 7 and lo == 0.2 and hi == 0.9
+    mx = [[0.5, 0.4], [0.5, 0.3]]
+    am = [[9, 0], [4, 0]]
+    level, idx, _, _ = combine_selection(mx, am, [[0.0, 0.0], [0.0, 0.0]])
+    assert level == 0 and idx == 4

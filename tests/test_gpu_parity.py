@@ -238,3 +238,56 @@ def test_tensor_core_decode_matches_simt_crosscheck(rng):
     ref = w[:, L:2 * L].double() @ cb.double()
     assert (a.double() - ref).abs().max().item() <= F_REL * ref.abs().max().item()
     assert (s.double() - ref).abs().max().item() <= F_REL * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("world,L", [(2, 64), (3, 64), (2, 128)])
+def test_tile_bands_stitch_to_the_full_frame(rng, world, L):
+    """tile-band sharding of one view.  Every rendered
+    tile is the full frame's tile, so stitched bands equal the full frame
+    exactly: coefficient map / features / final T on owned rows, filtered
+    relevancy maps, and level / point / mask after the cross-band reduction."""
+    from paper_2507_07136_b200.device import QuerySpec, device_scene
+    from paper_2507_07136_b200.distributed import band_query, band_rows, combine_selection, mask_rows
+    import torch
+
+    scene = random_scene(rng, 3000, num_levels=3, L=L, K=4, D=128)  # L=128: relevancy from the map in HBM
+    cam = make_camera(112, 90)
+    qv = rng.standard_normal(scene.codebooks[0].atoms.shape[1])
+    canon = rng.standard_normal((4, qv.shape[0]))
+    spec = QuerySpec(qv, canon, 11, -1, 0.5)
+    eng = device_scene(scene).engine
+    levels = (0, 1, 2)
+    full = eng.allocate(cam.width, cam.height, levels, coeff_map=True, final_t=True, features=True, query=True)
+    eng.run(cam, levels, full, query=spec)
+    st_i, st_f = full.host_stats()
+    stats, outs = [], []
+    for r in range(world):
+        b = band_rows(cam.height, world, r)
+        o = eng.allocate(cam.width, cam.height, levels, coeff_map=True, final_t=True, features=True, query=True)
+        eng.run(cam, levels, o, query=spec, band=(b.y0, b.y1))
+        torch.cuda.synchronize()
+        y0, y1 = b.y0, b.y1
+        assert torch.equal(o.coeff_map[y0:y1], full.coeff_map[y0:y1])
+        assert torch.equal(o.final_t[y0:y1], full.final_t[y0:y1])
+        assert torch.equal(o.features[:, y0:y1], full.features[:, y0:y1])
+        assert torch.equal(o.relevancy_filtered[:, y0:y1], full.relevancy_filtered[:, y0:y1])
+        from paper_2507_07136_b200.distributed import band_statistics
+        stats.append(band_statistics(o, len(levels)))
+        outs.append((b, o))
+    level, idx, lo, hi = combine_selection(*zip(*stats))
+    assert level == int(st_i[N_STAT_LEVEL()])
+    assert divmod(idx, cam.width) == (int(st_i[4]), int(st_i[5]))
+    assert lo == float(st_f[0]) and hi == float(st_f[1])
+    for b, o in outs:
+        mask_rows(o, level, lo, hi, 0.5, b.y0, b.y1)
+        torch.cuda.synchronize()
+        assert torch.equal(o.mask[b.y0:b.y1], full.mask[b.y0:b.y1])
+    # the one-call helper (no process group: a world of one band = whole image)
+    bq = band_query(eng, cam, levels, spec, 1, 0)
+    assert bq.level == level and bq.point == divmod(idx, cam.width)
+    assert torch.equal(bq.out.mask, full.mask)
+
+
+def N_STAT_LEVEL():
+    from paper_2507_07136_b200 import _native as N
+    return N.STAT_LEVEL

@@ -43,7 +43,7 @@ def test_ctypes_binding_covers_header(lib_path):
     for name in declared_functions():
         assert name in N.EXPORTS, name
         assert getattr(lib, name) is not None
-    assert lib.sf_abi_version() == 1
+    assert lib.sf_abi_version() == 2
 
 
 def test_workspace_queries_need_no_gpu(lib_path):
