@@ -42,15 +42,16 @@ CONFIGS = {
 # profiles/r01_launches_latest.csv: preprocess, CUB onesweep depth sort (10),
 # rank_of_row, count, tile scan, emit, 3 tile-sort kernels, project codebook,
 # blend, blend fixup, 3 x (codebook split + tcgen05 decode), 2 x box filter,
-# reduce, finalize, mask.
+# reduce, finalize, mask.  With the decode fused into the blend the 3 x
+# (split + decode) launches become one codebook-image launch (27 per frame).
 KERNELS_PER_FRAME = 32
 
 
-def ncu_traffic(kernel: str = "decode"):
-    """dram read+write bytes per launch of `kernel` from the committed ncu summary."""
+def ncu_traffic(kernel: str = "decode", summary: str = "r01_ncu_summary.txt"):
+    """dram read+write bytes per launch of `kernel` from a committed ncu summary."""
     try:
         cur, rd, wr = None, None, None
-        for ln in open(os.path.join(ROOT, "profiles", "r01_ncu_summary.txt")):
+        for ln in open(os.path.join(ROOT, "profiles", summary)):
             ln = ln.strip()
             if ln.startswith("kernel:"):
                 cur = ln.split(":", 1)[1].strip()
@@ -241,7 +242,9 @@ def main():
     eng = ds.engine
     levels = (0, 1, 2)
     spec = QuerySpec(qv, canon, 11, -1, 0.5)
-    out = eng.allocate(W, H, levels, coeff_map=True, features=True, query=True)
+    # decode fused into the blend kernel: the coefficient map never reaches HBM
+    fused = bool(N.load().sf_decode_fused(3, 64, 4, 512))
+    out = eng.allocate(W, H, levels, coeff_map=not fused, features=True, query=True)
     qdev = (torch.from_numpy(qv).cuda(), torch.from_numpy(canon).cuda())
     eng.run(cam, levels, out, query=spec, qdev=qdev)  # sizes the pair buffer
     stream = torch.cuda.current_stream()
@@ -260,7 +263,7 @@ def main():
     stage = []
     for _ in range(3):
         step(timing=True)
-        stage.append(out.stage_ms())
+        stage.append(out.stage_ms() + (out.blend_ms(),))
     torch.cuda.synchronize()
     st = out.stats_i64.cpu().numpy()
     assert st[N.STAT_OVERFLOW] == 0
@@ -290,10 +293,26 @@ def main():
     r_ms = statistics.median(s[0] for s in stage)
     d_ms = statistics.median(s[1] for s in stage)
     p_ms = statistics.median(s[2] for s in stage)
+    b_ms = statistics.median(s[3] for s in stage)
     P = W * H
-    dec_bytes = 3 * P * 512 * 4 + P * 192 * 4 + 3 * 64 * 512 * 4  # F written + W read + codebooks
+    pairs = int(st[N.STAT_PAIRS])
+    if fused:
+        # fused blend + decode: F written + every tile-list record gathered once
+        # (u32 entry + 80 B GeomRec + 80 B channel record per pair) + codebook image
+        dom_kernel = "k_blend<DEC> (blend + fused 3xTF32 decode, one frame)"
+        dec_bytes = 3 * P * 512 * 4 + pairs * (4 + 80 + 80) + 3 * 64 * 512 * 8
+        dom_ms = b_ms
+        traffic = ncu_traffic("blend_dec", "r01_ncu_fused.txt")
+        traffic_src = "profiles/r01_ncu_fused.txt (ncu --set full, one launch)"
+    else:
+        dom_kernel = "k_decode_tc (3 levels, one frame)"
+        dec_bytes = 3 * P * 512 * 4 + P * 192 * 4 + 3 * 64 * 512 * 4  # F written + W read + codebooks
+        dom_ms = d_ms
+        t1 = ncu_traffic("decode")
+        traffic = 3 * t1 if t1 else None
+        traffic_src = "profiles/r01_ncu_summary.txt (ncu --set full, per launch x 3 levels)"
     hbm_peak, peak_kind = peaks()
-    achieved = dec_bytes / (d_ms / 1e3) / 1e9
+    achieved = dec_bytes / (dom_ms / 1e3) / 1e9
 
     # ---- e2e through the public API: query_pipeline with host query inputs ----
     e2e = None
@@ -327,7 +346,7 @@ def main():
                "api": "paper_2507_07136_b200.query_pipeline(..., features='eager')"}
 
     # feature-splat FPS (render + decode, no query post) and lazy-feature query FPS
-    out_f = eng.allocate(W, H, levels, coeff_map=True, features=True, query=False)
+    out_f = eng.allocate(W, H, levels, coeff_map=not fused, features=True, query=False)
     out_q = eng.allocate(W, H, levels, coeff_map=False, features=False, query=True)
     extra = {}
     for name, o, q in (("feature_splat", out_f, None), ("text_query_lazy_features", out_q, spec)):
@@ -372,16 +391,16 @@ def main():
             "fps": {"text_query_full": fps_total / world,
                     "feature_splat": extra["feature_splat"],
                     "text_query_lazy_features": extra["text_query_lazy_features"]},
-            "stage_ms": {"render": r_ms, "decode": d_ms, "post": p_ms},
-            "roofline": {"bound": "hbm", "kernel": "k_decode_tc (3 levels, one frame)",
+            "stage_ms": {"render": r_ms, "decode": d_ms, "post": p_ms, "blend_kernel": b_ms,
+                         "decode_fused_into_blend": fused},
+            "roofline": {"bound": "hbm", "kernel": dom_kernel,
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                         "algorithmic_bytes": dec_bytes,
-                         "traffic": (3 * ncu_traffic("decode")) if ncu_traffic("decode") else None,
-                         "traffic_source": "profiles/r01_ncu_summary.txt (ncu --set full, per launch x 3 levels)"},
+                         "algorithmic_bytes": dec_bytes, "time_ms": dom_ms,
+                         "traffic": traffic, "traffic_source": traffic_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": KERNELS_PER_FRAME * args.steps,
+            "gpu_launches": (KERNELS_PER_FRAME - 5 if fused else KERNELS_PER_FRAME) * args.steps,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -80,7 +80,8 @@ typedef struct SfFrame {
     int32_t early_exit;         /* rasterizer.py:174-177 */
     int64_t pair_capacity;      /* size of the (tile, rank) pair buffer in the workspace */
     /* outputs */
-    float* coeff_map;           /* (H,W,n_levels*L) fp32      CoefficientMap.data */
+    float* coeff_map;           /* (H,W,n_levels*L) fp32      CoefficientMap.data (may be NULL;
+                                   required with features unless sf_decode_fused) */
     float* final_t;             /* (H,W) fp32                 RenderStats.final_transmittance */
     float* features;            /* (n_levels,H,W,D) fp32      FeatureMapSet.maps */
     double* relevancy_raw;      /* (n_levels,H,W) fp64        relevancy_map() per level */
@@ -89,8 +90,10 @@ typedef struct SfFrame {
     int64_t* stats_i64;         /* (16,) see SF_STAT_* */
     double* stats_f64;          /* (8 + 2*n_levels,) see SF_STATF_* */
     /* optional cudaEvent_t recorded at: frame start, after blend (render),
-     * after decode, after post -- the StageTimings of sparse_splat.py:202-215 */
-    void* events[4];
+     * after decode, after post -- the StageTimings of sparse_splat.py:202-215 --
+     * and [4] right before the blend launch (so [4] -> [1] times the blend
+     * kernel, which includes the decode when sf_decode_fused) */
+    void* events[5];
     /* optional cached per-row scatter plan of host_levels (sf_pack_channels);
      * NULL = built inside the frame */
     const unsigned char* chan_by_row;
@@ -220,7 +223,12 @@ float sf_event_elapsed_ms(void* start, void* end);
 /* Human-readable text of the last error on this thread. */
 const char* sf_last_error(void);
 /* ABI version (bumped on any signature change). */
-int sf_abi_version(void); /* 2: SfFrame band fields */
+int sf_abi_version(void); /* 2: SfFrame band fields; 3: fused decode (coeff_map optional with features) */
+
+/* 1 if sf_render_frame decodes features inside the blend kernel for this
+ * shape (then SfFrame.coeff_map may be NULL when features are requested);
+ * 0 if the decode runs as a separate tcgen05 GEMM over the coefficient map. */
+int sf_decode_fused(int32_t n_levels, int32_t L, int32_t K, int32_t D);
 
 #ifdef __cplusplus
 }

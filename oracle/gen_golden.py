@@ -103,9 +103,24 @@ def dump(name, scene, cam, *, query_seed=None, window=5, with_query=True):
     return path, os.path.getsize(path)
 
 
+def fused_fixtures():
+    """Shapes on which the blend kernel decodes features itself (sf_decode_fused:
+    L = 64, levels * K = 12, D % 32 == 0): ragged image, opaque enough that
+    early exit and the fp64 fixup replay occur."""
+    made = []
+    rng = np.random.default_rng(1005)
+    sc = random_scene(rng, num_gaussians=1500, num_levels=3, L=64, K=4, D=64, opacity_range=(0.5, 0.98))
+    made.append(dump("fused_s5", sc, camera(37, 29)))
+    return made
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
-    made = []
+    if "--only-fused" in sys.argv:
+        for p, sz in fused_fixtures():
+            print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
+        return
+    made = fused_fixtures()
     # 1. reference-test-like scenes (tests/conftest.py distribution)
     for seed, (g, nl, L, K, D, w, h) in enumerate([
         (50, 1, 16, 4, 8, 32, 32),

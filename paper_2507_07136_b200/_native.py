@@ -48,7 +48,7 @@ class SfFrame(ctypes.Structure):
     _fields_ = [("host_levels", P), ("n_levels", i32), ("early_exit", i32), ("pair_capacity", i64),
                 ("coeff_map", P), ("final_t", P), ("features", P), ("relevancy_raw", P),
                 ("relevancy_filtered", P), ("mask", P), ("stats_i64", P), ("stats_f64", P),
-                ("events", P * 4), ("chan_by_row", P), ("band_y0", i32), ("band_y1", i32)]
+                ("events", P * 5), ("chan_by_row", P), ("band_y0", i32), ("band_y1", i32)]
 
 
 EXPORTS = {
@@ -79,6 +79,7 @@ EXPORTS = {
     "sf_event_elapsed_ms": (ctypes.c_float, [P, P]),
     "sf_last_error": (ctypes.c_char_p, []),
     "sf_abi_version": (ctypes.c_int, []),
+    "sf_decode_fused": (ctypes.c_int, [i32, i32, i32, i32]),
 }
 
 _lib = None

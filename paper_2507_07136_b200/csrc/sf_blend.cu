@@ -1,39 +1,40 @@
-// sf_blend.cu -- K5/K6: per-tile front-to-back blending with top-K sparse scatter.
+// sf_blend.cu -- K5/K6 (+ fused K7): per-tile front-to-back blending with
+// top-K sparse scatter, optionally followed in the same CTA by the codebook
+// decode of the finished tile on the tcgen05 tensor cores.
 //
 // Reference: tile_blend_weights (rasterizer.py:133-181) and the scatter loop
 // of _splat_levels (sparse_splat.py:138-150):
 //     alpha_i = min(o_i * exp(-q_i / 2), 0.99), alpha_i = 0 if q_i > 9
 //     e_i = alpha_i * T_i  counted iff T_i >= 1e-4,  T_{i+1} = T_i (1 - alpha_i)
 //     W[p, cat_idx[i]] += e_i[p] * cat_vals[i]
+// and decode (sparse_splat.py:183-199): F_b = W_b @ atoms_b per level.
 //
-// B200 mapping.  One CTA per 16x16 tile (x channel block), one pixel per
-// thread; each warp owns an 8x4 pixel patch so the set of Gaussians live in
-// a warp stays small.  The tile's depth-ordered list streams through shared
-// memory in batches of 32 Gaussian records (80 B geometry + scatter plan),
-// double-buffered with cp.async so the next batch's L2/HBM gathers overlap
-// the current batch's math.  Per batch:
-//   phase A  every thread runs the q > 9 rejection in fp32 for all 32
-//            Gaussians (independent work, high ILP) with a conservative
-//            guard band (|q32 - q64| <= 1.5e-6 S, guard 1e-4 (1 + S),
-//            S = a dx^2 + c dy^2) -> a 32-bit candidate mask;
-//   phase B  the warp walks the union of its candidate masks in depth order;
-//            candidates are re-evaluated in fp64 with the reference's exact
-//            op order (bit-exact q <= 9 membership), alpha = o exp(-q/2) via
-//            a 1/128-step table times a degree-5 polynomial (~1e-16 rel.),
-//            and T / e carried in fp64, so the T >= 1e-4 early-exit decision
-//            matches the fp64 reference.
-// The coefficient accumulator is fp32 in shared memory, acc[channel][slot]
-// with a 257-float pitch: the K channel ids of a Gaussian are warp-uniform,
-// so every scatter is one conflict-free wavefront, and the transposed read
-// for the channel-contiguous HBM write is conflict-free too.  A warp skips
-// a Gaussian's scatter unless some lane has e > 0 (__any_sync), skips whole
-// batches once all its pixels saturated, and the CTA stops streaming when
-// every pixel is saturated (__syncthreads_and).
+// B200 mapping (K5).  One CTA per half tile (16x8 pixels): four
+// consumer warps own an 8x4 pixel patch each, one producer warp streams the
+// tile's depth-ordered list through a 2-stage cp.async/mbarrier ring.  fp32
+// alpha / transmittance with a guard band in which the reference's fp64 q
+// decides membership; early-exit decisions fp32 cannot certify are replayed
+// in fp64 by k_blend_fixup.  The coefficient accumulator is fp32 in shared
+// memory, acc[channel][slot] with a 129-float pitch (conflict-free scatter).
 //
-// Optional fused epilogue: per pixel and level, logits against the query and
-// the canonical phrases via the projected codebook P = atoms @ [q; c]^T
-// (fp64), then relevancy = min_j sigmoid(l_q - l_j) (query.py:65-84) -- the
-// coefficient tile never has to be re-read from HBM for the query.
+// Fused decode (DEC).  Decode is HBM-store bound (9.56 GB of fp32 features
+// per 1440x1080 frame) while blending is issue bound, so the decode of a
+// finished tile runs inside the blend CTA: with two CTAs per SM one CTA's
+// feature stores drain while the other blends, and the coefficient map never
+// round-trips HBM.  Per level b: consumer thread = pixel = TMEM lane splits
+// its 64 coefficients into tf32 hi/lo and stores them to TMEM (A operand);
+// the producer warp streams pre-swizzled codebook chunks (32 output columns,
+// hi + lo, 16 KB) by bulk copy into the freed level-0 accumulator space and
+// issues 3xTF32 tcgen05.mma (A from TMEM, B from SMEM) into four 32-column
+// TMEM accumulators; consumer warps drain them (tcgen05.ld) straight to HBM,
+// one 128-byte line per pixel per chunk.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_fp16.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
 #include <algorithm>
 
 #include "sf_common.cuh"
@@ -60,12 +61,34 @@ struct __align__(16) BlendStage {
     uint32_t off[kBatch][kMaxC];
 };
 
+// fused decode (DEC).  TMEM columns per CTA (two CTAs per SM share 512):
+// two A slots of 64 columns (fp16 hi [0, 32) + lo [32, 64), pairs per
+// column) -- level b uses slot b & 1 -- then two 64-column fp32 accumulators.
+// A-from-TMEM MMAs read 4 KB of A per K step at ~64 B/clk, so N = 64 keeps the
+// tensor core at its A-read floor; the A slots free the accumulator space
+// level by level for the codebook ring and the output staging.
+constexpr int kDecTmemCols = 256;
+constexpr int kDecN = 64;                     // output columns per chunk (MMA N)
+constexpr int kDecAcc = 2;                    // TMEM accumulators of kDecN columns
+constexpr int kDecAccCol = 128;
+constexpr int kDecChunkBytes = 2 * 64 * 128;  // B chunk: {hi, lo} x 64 rows (n) x 64 fp16 (128 B, SW128)
+constexpr int kDecStages = 2;                 // B chunk ring at the start of the accumulator space
+constexpr int kDecOutBytes = 8 * 4 * 32 * 4;  // per-warp output box: 8 x 4 pixels x 32 fp32 (SW128)
+constexpr int kDecMaxLevels = 3;
+
 struct __align__(16) BlendSmem {
     BlendStage st[kStages];
     uint64_t full[kStages];   // producer -> consumers: batch staged (count 1)
     uint64_t empty[kStages];  // consumers -> producer: batch consumed (one arrival per consumer warp)
     int nb[kStages];          // batch size; 0 = end of the tile's stream
     int n_done_warps;         // consumer warps whose pixels all saturated
+    // fused decode
+    uint64_t a_ready;              // consumers -> issuer: A of levels 0-1 (phase 0), level 2 (phase 1) in TMEM
+    uint64_t a_free;               // MMAs of level 0 done: its TMEM slot takes level 2 (tcgen05.commit)
+    uint64_t b_full[kDecStages];   // codebook chunk landed (tx count)
+    uint64_t acc_full[kDecAcc];    // accumulator complete (tcgen05.commit)
+    uint64_t acc_empty[kDecAcc];   // accumulator drained (4 warp arrivals)
+    uint32_t tmem_base;
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -85,6 +108,116 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
         "}\n" ::"r"(smem_addr(b)),
         "r"(parity)
         : "memory");
+}
+
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+                 : "memory");
+}
+// 1-D bulk copy global -> shared, completion on an mbarrier (tx bytes)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(b))
+        : "memory");
+}
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// K-major, 128B-swizzled operand: rows of 128 B, 8-row atoms 1024 B apart
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+// D (TMEM) [+]= A (TMEM, tf32, row = lane, K = column) x B (SMEM descriptor)
+__device__ __forceinline__ void mma_tf32_tmem_a(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d),
+        "r"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(b))
+                 : "memory");
+}
+#define SF_X32_REGS(v)                                                                                     \
+    "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),     \
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),    \
+        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),   \
+        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+#define SF_X32_OUTS(v)                                                                                     \
+    "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),        \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),           \
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),         \
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),         \
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+#define SF_X32_LIST                                                                                        \
+    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27," \
+    "%28,%29,%30,%31}"
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%32], " SF_X32_LIST ";" ::SF_X32_REGS(v), "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 " SF_X32_LIST ", [%32];" : SF_X32_OUTS(v) : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%16], "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15};" ::"r"(v[0]),
+        "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(taddr)
+        : "memory");
+}
+// D (TMEM, f32) [+]= A (TMEM, f16 pairs per column, row = lane) x B (SMEM descriptor, f16)
+__device__ __forceinline__ void mma_f16_tmem_a(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d),
+        "r"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"((uint64_t)map),
+        "r"(smem_addr(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -184,13 +317,19 @@ __device__ __forceinline__ bool patch_may_hit(const GeomRec& g, float x0, float 
     return best <= 9.f + fmaf(1e-4f, bs, 1e-4f);
 }
 
+__host__ __device__ constexpr int acc_bytes(int nch) { return (nch * kAccPitch * 4 + 15) / 16 * 16; }
+
 // CT: channels per Gaussian (0 = runtime), SINGLE: one channel block,
-// NC: canonical phrases of the fused relevancy (0 = none, -1 = runtime count).
-template <int CT, bool SINGLE, int NC>
-__global__ void __launch_bounds__(kCTAThreads, 2) k_blend(BlendArgs A, int ch_block) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
-    float* acc = reinterpret_cast<float*>(smem_raw + sizeof(BlendSmem));
+// NC: canonical phrases of the fused relevancy (0 = none, -1 = runtime count),
+// DEC: fused 3xTF32 decode of the finished tile into A.features.
+// Shared memory: [accumulator (1024-aligned when DEC)][BlendSmem].
+template <int CT, bool SINGLE, int NC, bool DEC>
+__global__ void __launch_bounds__(kCTAThreads, 2)
+k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t mis = DEC ? ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u) : 0u;
+    float* acc = reinterpret_cast<float*>(smem_raw + mis);
+    BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw + mis + acc_bytes(ch_block));
 
     if (A.stats[SF_STAT_OVERFLOW]) return;
     const int tile = A.tile0 + (blockIdx.x >> 1), half = blockIdx.x & 1;
@@ -218,10 +357,29 @@ __global__ void __launch_bounds__(kCTAThreads, 2) k_blend(BlendArgs A, int ch_bl
             bar_init(&S.empty[st], kConsumerWarps);
         }
         S.n_done_warps = 0;
+        if (DEC) {
+            bar_init(&S.a_ready, kConsumerWarps);
+            bar_init(&S.a_free, 1);
+            for (int i = 0; i < kDecStages; ++i) {
+                bar_init(&S.b_full[i], 1);
+            }
+            for (int i = 0; i < kDecAcc; ++i) {
+                bar_init(&S.acc_full[i], 1);
+                bar_init(&S.acc_empty[i], kConsumerWarps);
+            }
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (DEC && threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&S.tmem_base)),
+                     "n"(kDecTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
     for (int i = threadIdx.x; i < nchb * kAccPitch; i += kCTAThreads) acc[i] = 0.f;
+    if (DEC) tc_before();
     __syncthreads();
+    if (DEC) tc_after();
+    if (A.timeline && threadIdx.x == 0) A.timeline[4 * (blockIdx.x + gridDim.x * blockIdx.y)] = gtimer();
 
     const float pxf = (float)px, pyf = (float)py;
     const float pdx0 = (float)(x0 + (warp & 1) * 8), pdy0 = (float)(y0 + (warp >> 1) * 4);  // patch corner
@@ -355,6 +513,7 @@ __global__ void __launch_bounds__(kCTAThreads, 2) k_blend(BlendArgs A, int ch_bl
         }
     }
     // ---- outputs ----
+    if (A.timeline && threadIdx.x == 0) A.timeline[4 * (blockIdx.x + gridDim.x * blockIdx.y) + 1] = gtimer();
     if (blockIdx.y == 0 && A.final_t && inside) A.final_t[(size_t)py * A.W + px] = T;
     if (A.coeff_map) {
         // Each warp instruction writes 4 pixels x 32 channels as float4:
@@ -433,6 +592,223 @@ __global__ void __launch_bounds__(kCTAThreads, 2) k_blend(BlendArgs A, int ch_bl
                 A.relevancy_raw[(size_t)b * A.W * A.H + (size_t)py * A.W + px] = best;
             }
         }
+    }
+    if (DEC) {
+        // ---------------- fused decode: F_b = W_b @ atoms_b on tcgen05 ----------------
+        // 3-term fp16 split: W = Wh + Wl, atoms = Bh + Bl (each rounded to
+        // fp16), F ~= Wh Bh + Wh Bl + Wl Bh accumulated in fp32 (error ~2^-22
+        // |W||B|, plus 2^-25 absolute for subnormal low parts, which the
+        // per-level power-of-two codebook scale keeps below 2^-19 max|B|).
+        // Levels 0 and 1 go to TMEM first, freeing accumulator bytes
+        // [0, 64 KB) for the codebook ring (32 KB) and the per-warp output boxes
+        // (32 KB); level 2 replaces level 0 once level 0's MMAs are done.
+        const int nchunk = A.D / kDecN;
+        const int total = A.n_levels * nchunk;
+        const uint32_t tm = S.tmem_base;
+        unsigned char* bring = reinterpret_cast<unsigned char*>(acc);
+        unsigned char* obuf = bring + kDecStages * kDecChunkBytes;  // 2 output boxes per consumer warp
+        if (consumer) {
+            const uint32_t lane_off = (uint32_t)(cw * 32) << 16;  // this warp's TMEM lane quarter
+            // level b's coefficients (this thread's pixel) -> fp16 hi/lo pairs in A slot b & 1
+            auto convert = [&](int b) {
+#pragma unroll 1
+                for (int kb = 0; kb < 2; ++kb) {
+                    uint32_t hi[16], lo[16];
+                    const float* src = acc + (b * 64 + kb * 32) * kAccPitch + slot;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float x0 = src[(2 * k) * kAccPitch], x1 = src[(2 * k + 1) * kAccPitch];
+                        const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+                        const __half l0 = __float2half_rn(x0 - __half2float(h0));
+                        const __half l1 = __float2half_rn(x1 - __half2float(h1));
+                        hi[k] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+                        lo[k] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+                    }
+                    const uint32_t col = (uint32_t)(64 * (b & 1) + 16 * kb);
+                    tmem_st16(tm + lane_off + col, hi);
+                    tmem_st16(tm + lane_off + col + 32, lo);
+                }
+            };
+            for (int b = 0; b < A.n_levels && b < 2; ++b) convert(b);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            proxy_fence();  // accumulator reads precede the bulk copies / boxes written over them
+            tc_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&S.a_ready);
+            if (A.timeline && threadIdx.x == 0) A.timeline[4 * (blockIdx.x + gridDim.x * blockIdx.y) + 2] = gtimer();
+            // drain, each warp on its own: TMEM -> swizzled box (its 8 x 4 pixel
+            // patch x 32 fp32, row = lane) -> TMA store by lane 0; no CTA barriers
+            unsigned char* wbox = obuf + cw * 2 * kDecOutBytes;
+            const int bx = x0 + (warp & 1) * 8, by = y0 + (warp >> 1) * 4;
+            float scl[kDecMaxLevels];
+#pragma unroll
+            for (int b = 0; b < kDecMaxLevels; ++b) scl[b] = b < A.n_levels ? A.dec_scale[b] : 1.f;
+            int nbox = 0;
+            for (int g = 0; g < total; ++g) {
+                const int t = g & (kDecAcc - 1), b = g / nchunk, c = g - b * nchunk;
+                if (c == 0 && b == 1 && A.n_levels > 2) {
+                    // level 0's MMAs are done (its chunks were drained): level 2 -> slot 0
+                    bar_wait(&S.a_free, 0);
+                    tc_after();
+                    convert(2);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    tc_before();
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(&S.a_ready);
+                }
+                uint64_t* cdbg = (A.timeline && blockIdx.x == 2001 && lane == 0)
+                                     ? A.timeline + 4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * (1 + cw) + 8 * g
+                                     : nullptr;
+                if (cdbg) cdbg[0] = clock64();
+                bar_wait(&S.acc_full[t], (g / kDecAcc) & 1);
+                if (cdbg) cdbg[1] = clock64();
+                if (cw == 0 && lane == 0 && g + kDecStages < total) {
+                    // chunk g's MMAs are complete: its codebook stage takes chunk g + kDecStages
+                    const int sg = g % kDecStages;
+                    bar_expect_tx(&S.b_full[sg], kDecChunkBytes);
+                    bulk_g2s(bring + sg * kDecChunkBytes,
+                             reinterpret_cast<const unsigned char*>(A.dec_b) + (size_t)(g + kDecStages) * kDecChunkBytes,
+                             kDecChunkBytes, &S.b_full[sg]);
+                }
+                tc_after();
+                uint32_t v[64];
+                {
+                    uint32_t (&v0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[0]);
+                    uint32_t (&v1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[32]);
+                    tmem_ld32(tm + lane_off + (uint32_t)(kDecAccCol + t * kDecN), v0);
+                    tmem_ld32(tm + lane_off + (uint32_t)(kDecAccCol + t * kDecN + 32), v1);
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                tc_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(&S.acc_empty[t]);
+                if (cdbg) cdbg[2] = clock64();
+                const float sc = b == 0 ? scl[0] : (b == 1 ? scl[1] : scl[2]);
+                if (sc != 1.f) {
+#pragma unroll
+                    for (int i = 0; i < 64; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
+                }
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf, ++nbox) {
+                    if (lane == 0) bulk_wait_read<1>();  // the store issued two boxes ago has left this box
+                    __syncwarp();
+                    unsigned char* box = wbox + (nbox & 1) * kDecOutBytes;
+                    const uint32_t row = smem_addr(box) + lane * 128;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((u ^ (lane & 7)) << 4)),
+                                     "r"(v[32 * hf + 4 * u]), "r"(v[32 * hf + 4 * u + 1]),
+                                     "r"(v[32 * hf + 4 * u + 2]), "r"(v[32 * hf + 4 * u + 3])
+                                     : "memory");
+                    }
+                    proxy_fence();
+                    __syncwarp();
+                    if (lane == 0 && !(A.dev_mode & 1)) {
+                        tma_store_4d(&fmap, box, c * kDecN + 32 * hf, bx, by, b);
+                        bulk_commit();
+                    }
+                }
+                if (cdbg) cdbg[3] = clock64();
+            }
+            if (lane == 0) bulk_wait<0>();
+        } else {
+            // issuer: the whole producer warp walks the chunk ring; lane 0 issues.
+            // Per chunk 3 x 4 MMAs (128 x 64 x 16, fp16 -> fp32, A from TMEM).
+            const uint32_t idesc = (1u << 4) | ((uint32_t)(kDecN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            const unsigned char* img = reinterpret_cast<const unsigned char*>(A.dec_b);
+            const bool leader = lane == 0;
+            const uint64_t desc0 = sw128_desc(smem_addr(bring));
+            bar_wait(&S.a_ready, 0);
+            tc_after();
+            if (leader)
+                for (int g = 0; g < kDecStages && g < total; ++g) {
+                    bar_expect_tx(&S.b_full[g], kDecChunkBytes);
+                    bulk_g2s(bring + g * kDecChunkBytes, img + (size_t)g * kDecChunkBytes, kDecChunkBytes,
+                             &S.b_full[g]);
+                }
+            __syncwarp();
+            for (int g = 0; g < total; ++g) {
+                const int s = g % kDecStages, t = g & (kDecAcc - 1), b = g / nchunk, c = g - b * nchunk;
+                if (c == 0 && b >= 2) {  // level b's A replaced level b - 2's in its slot
+                    bar_wait(&S.a_ready, (b - 1) & 1);
+                    tc_after();
+                }
+                uint64_t* dbg = (A.timeline && blockIdx.x == 2001 && leader)
+                                    ? A.timeline + 4 * (size_t)gridDim.x * gridDim.y + 8 * g
+                                    : nullptr;
+                if (dbg) dbg[0] = clock64();
+                bar_wait(&S.b_full[s], (g / kDecStages) & 1);
+                if (dbg) dbg[1] = clock64();
+                if (g >= kDecAcc) bar_wait(&S.acc_empty[t], ((g / kDecAcc) - 1) & 1);
+                if (dbg) dbg[2] = clock64();
+                tc_after();
+                if (dbg) dbg[3] = clock64();
+                if (leader) {
+                    const uint32_t d = tm + (uint32_t)(kDecAccCol + t * kDecN);
+                    const uint64_t bd = desc0 + (uint64_t)((s * kDecChunkBytes) >> 4);
+                    const uint32_t ah0 = tm + (uint32_t)(64 * (b & 1));
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {  // K steps of 16: Wl Bh + Wh Bl + Wh Bh
+                        const uint64_t bh = bd + 2 * k, bl = bh + (8192 >> 4);
+                        const uint32_t ah = ah0 + (uint32_t)(8 * k), al = ah + 32;
+                        mma_f16_tmem_a(d, al, bh, idesc, k > 0 ? 1u : 0u);
+                        mma_f16_tmem_a(d, ah, bl, idesc, 1u);
+                        mma_f16_tmem_a(d, ah, bh, idesc, 1u);
+                    }
+                    if (dbg) dbg[4] = clock64();
+                    mma_commit(&S.acc_full[t]);
+                    if (c == nchunk - 1 && b + 2 < A.n_levels) mma_commit(&S.a_free);
+                    if (dbg) dbg[5] = clock64();
+                }
+                __syncwarp();
+            }
+        }
+        tc_before();
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            tc_after();
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(kDecTmemCols));
+        }
+        if (A.timeline && threadIdx.x == 0) A.timeline[4 * (blockIdx.x + gridDim.x * blockIdx.y) + 3] = gtimer();
+    }
+}
+
+// Codebook chunks of the fused decode, pre-swizzled so one linear bulk copy
+// lands the SW128 K-major fp16 operand image: for level b and output columns
+// [64 c, 64 c + 64): {hi, lo} x 64 rows (n) x 64 fp16 (128 B), 16-byte unit j
+// of row n stored at unit j ^ (n & 7).  The level's atoms are first scaled by
+// a power of two 2^s (s = 0 unless max |atom| lies outside [2^-6, 2^8)), so
+// both fp16 parts stay normal; dec_scale[b] = 2^-s undoes it in the epilogue.
+// One CTA per (level, chunk).
+__global__ void __launch_bounds__(256) k_dec_codebook_image(const float* __restrict__ cb, LevelSelDev lv, int L,
+                                                            int D, unsigned char* __restrict__ out,
+                                                            float* __restrict__ scale_out) {
+    const int nchunk = D / kDecN;
+    const int b = blockIdx.x / nchunk, c = blockIdx.x % nchunk;
+    const float* atoms = cb + (size_t)lv.lv[b] * L * D;
+    __shared__ float red[8];
+    float m = 0.f;
+    for (int i = threadIdx.x; i < L * D; i += blockDim.x) m = fmaxf(m, fabsf(atoms[i]));
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    m = red[0];
+    for (int i = 1; i < 8; ++i) m = fmaxf(m, red[i]);
+    int e = 0;
+    if (m > 0.f && (m < 0x1p-6f || m >= 0x1p8f)) {
+        frexpf(m, &e);  // m = f 2^e, f in [0.5, 1): scale by 2^-e
+        e = -e;
+    }
+    if (c == 0 && threadIdx.x == 0) scale_out[b] = ldexpf(1.f, -e);
+    unsigned char* dst = out + (size_t)blockIdx.x * kDecChunkBytes;
+    for (int i = threadIdx.x; i < kDecN * 64; i += blockDim.x) {
+        const int n = i / 64, k = i % 64;
+        const float x = ldexpf(atoms[(size_t)k * D + c * kDecN + n], e);
+        const __half h = __float2half_rn(x);
+        const __half l = __float2half_rn(x - __half2float(h));
+        const int off = n * 128 + (((k >> 3) ^ (n & 7)) << 4) + (k & 7) * 2;
+        *reinterpret_cast<__half*>(dst + off) = h;
+        *reinterpret_cast<__half*>(dst + kDecChunkBytes / 2 + off) = l;
     }
 }
 
@@ -593,6 +969,18 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_blend_fixup(BlendArgs A) {
         __syncwarp();
         if (local && row)
             for (int c = lane; c < A.n_ch; c += 32) row[c] = (float)wl[c];
+        if (local && A.features) {
+            // the fused decode used the fp32 tile: redo this pixel's features in fp64
+            for (int b = 0; b < A.n_levels; ++b) {
+                const float* cb = A.codebooks + (size_t)A.lv.lv[b] * A.L * A.D;
+                float* fo = A.features + (size_t)b * A.feat_level_stride + pix * A.D;
+                for (int n = lane; n < A.D; n += 32) {
+                    double f = 0.0;
+                    for (int l = 0; l < A.L; ++l) f = fma(wl[b * A.L + l], (double)cb[(size_t)l * A.D + n], f);
+                    fo[n] = (float)f;
+                }
+            }
+        }
         if (lane == 0 && A.final_t) A.final_t[pix] = (float)T;
         if (A.proj_cb && A.relevancy_raw && lane == 0) {
             const int nv = 1 + A.n_canon;
@@ -614,27 +1002,99 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_blend_fixup(BlendArgs A) {
     }
 }
 
+bool blend_dec_supported(int n_levels, int L, int K, int D) {
+    return L == 64 && n_levels * K == 12 && n_levels <= kDecMaxLevels && n_levels * L <= kChBlock && D >= kDecN &&
+           D % kDecN == 0;
+}
+size_t blend_dec_image_bytes(int n_levels, int D) {
+    return (size_t)n_levels * (D / kDecN) * kDecChunkBytes + 64;  // + per-level scales
+}
+void launch_dec_codebook_image(const float* codebooks, const LevelSelDev& lv, int L, int D, void* out,
+                               cudaStream_t st) {
+    unsigned char* img = (unsigned char*)out;
+    float* scale = (float*)(img + (size_t)lv.n * (D / kDecN) * kDecChunkBytes);
+    k_dec_codebook_image<<<lv.n * (D / kDecN), 256, 0, st>>>(codebooks, lv, L, D, img, scale);
+}
+
+// features (n_levels, H, W, D) fp32 as a 4-D TMA map: boxes of 32 columns x
+// 8 x 4 pixels of one level, 128-byte swizzle (a warp's fused-decode store box)
+static int make_feature_map(CUtensorMap* map, float* f, int D, int W, int H, int n_levels) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return -1;
+        enc = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n_levels};
+    cuuint64_t strides[3] = {(cuuint64_t)D * 4, (cuuint64_t)W * D * 4, (cuuint64_t)H * W * D * 4};
+    cuuint32_t box[4] = {32, 8, 4, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, f, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 int launch_blend(const BlendArgs& a, cudaStream_t st) {
     if (a.C > kMaxC) return -2;
     if (a.proj_cb && a.n_ch > kChBlock) return -3;  // fused relevancy needs every channel in one CTA
     int n_tiles = a.n_band_tiles;
     int ch_block = a.n_ch < kChBlock ? a.n_ch : kChBlock;
     int nblk = (a.n_ch + ch_block - 1) / ch_block;
-    size_t smem = sizeof(BlendSmem) + (size_t)ch_block * kAccPitch * sizeof(float);
+    const bool dec = a.features != nullptr;
+    CUtensorMap fmap;
+    memset(&fmap, 0, sizeof(fmap));
+    if (dec) {
+        if (!blend_dec_supported(a.n_levels, a.L, a.C / a.n_levels, a.D) || nblk != 1 || !a.dec_b) return -4;
+        if ((uintptr_t)a.features % 16) return -4;
+        if (make_feature_map(&fmap, a.features, a.D, a.W, a.H, a.n_levels)) return -5;
+    }
+    size_t smem = (dec ? 1024 : 0) + acc_bytes(ch_block) + sizeof(BlendSmem);
     const bool fast = (a.C == 12 && nblk == 1);
     const int nc = a.proj_cb ? a.n_canon : 0;
-    void (*kern)(BlendArgs, int);
+    void (*kern)(BlendArgs, int, const CUtensorMap);
     int ki;
-    if (fast && !a.proj_cb) { kern = k_blend<12, true, 0>; ki = 0; }
-    else if (fast && nc == 4) { kern = k_blend<12, true, 4>; ki = 1; }
-    else if (fast) { kern = k_blend<12, true, -1>; ki = 2; }
-    else { kern = k_blend<0, false, -1>; ki = 3; }
-    static size_t configured[4] = {0, 0, 0, 0};
+    if (dec && !a.proj_cb) { kern = k_blend<12, true, 0, true>; ki = 4; }
+    else if (dec && nc == 4) { kern = k_blend<12, true, 4, true>; ki = 5; }
+    else if (dec) { kern = k_blend<12, true, -1, true>; ki = 6; }
+    else if (fast && !a.proj_cb) { kern = k_blend<12, true, 0, false>; ki = 0; }
+    else if (fast && nc == 4) { kern = k_blend<12, true, 4, false>; ki = 1; }
+    else if (fast) { kern = k_blend<12, true, -1, false>; ki = 2; }
+    else { kern = k_blend<0, false, -1, false>; ki = 3; }
+    static size_t configured[7] = {0, 0, 0, 0, 0, 0, 0};
     if (smem > configured[ki]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured[ki] = smem;
     }
-    if (n_tiles > 0) kern<<<dim3(2 * n_tiles, nblk), kCTAThreads, smem, st>>>(a, ch_block);
+    // development aid: SF_BLEND_TIMELINE=<file> dumps per-CTA %globaltimer stamps
+    // (start, blend done, A in TMEM, end) of every launch
+    static const char* tl_path = getenv("SF_BLEND_TIMELINE");
+    BlendArgs a2 = a;
+    static const char* dm = getenv("SF_DEC_MODE");  // development ablations of the fused decode
+    a2.dev_mode = dm ? atoi(dm) : 0;
+    static uint64_t* tl = nullptr;
+    const size_t n_cta = (size_t)2 * n_tiles * nblk;
+    if (tl_path && n_tiles > 0) {
+        if (tl) cudaFree(tl);
+        cudaMalloc(&tl, (n_cta * 4 + 8 * 512) * sizeof(uint64_t));
+        cudaMemsetAsync(tl, 0, (n_cta * 4 + 8 * 512) * sizeof(uint64_t), st);
+        a2.timeline = tl;
+    }
+    if (n_tiles > 0) kern<<<dim3(2 * n_tiles, nblk), kCTAThreads, smem, st>>>(a2, ch_block, fmap);
+    if (tl_path && n_tiles > 0) {
+        uint64_t* h = (uint64_t*)malloc((n_cta * 4 + 8 * 512) * sizeof(uint64_t));
+        cudaMemcpyAsync(h, tl, (n_cta * 4 + 8 * 512) * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        FILE* fp = fopen(tl_path, "wb");
+        if (fp) {
+            fwrite(h, sizeof(uint64_t), n_cta * 4 + 8 * 512, fp);
+            fclose(fp);
+        }
+        free(h);
+    }
     if (n_tiles > 0 && a.fixup_list && a.early_exit) k_blend_fixup<<<296, 32 * kFixWarps, 0, st>>>(a);
     return 0;  // (relevancy for n_ch > one channel block: launch_relevancy_from_cmap by the caller)
 }

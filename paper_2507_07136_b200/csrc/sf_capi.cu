@@ -45,7 +45,11 @@ extern "C" float sf_event_elapsed_ms(void* a, void* b) {
     if (cudaEventElapsedTime(&ms, (cudaEvent_t)a, (cudaEvent_t)b) != cudaSuccess) return -1.f;
     return ms;
 }
-extern "C" int sf_abi_version(void) { return 2; }
+extern "C" int sf_abi_version(void) { return 3; }
+
+extern "C" int sf_decode_fused(int32_t n_levels, int32_t L, int32_t K, int32_t D) {
+    return blend_dec_supported(n_levels, L, K, D) ? 1 : 0;
+}
 
 // ---------------------------------------------------------------------------
 // frame workspace layout
@@ -73,6 +77,7 @@ struct FrameWs {
     double* filter_tmp;
     void* sel_ws;
     float* dec_ws;
+    float* dec_img;   // fused decode: pre-swizzled tf32 hi/lo codebook chunks
     uint32_t* fixup;  // [0] = count, then the list
 };
 
@@ -108,6 +113,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->filter_tmp = c.take<double>((size_t)n_levels * W * H);
     ws->sel_ws = c.take<char>(select_segment_ws_bytes(n_levels, H, W));
     ws->dec_ws = c.take<float>(decode_ws_bytes(L, D) / sizeof(float));
+    ws->dec_img = c.take<float>(blend_dec_image_bytes(n_levels, D) / sizeof(float));
     ws->fixup = c.take<uint32_t>(kFixupCapacity + 1);
     return c.off;
 }
@@ -160,7 +166,10 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
         if (!f->relevancy_raw || !f->relevancy_filtered)
             return fail(SF_ERR_VALIDATION, "query frames need relevancy buffers");
     }
-    bool need_cmap = (f->features != nullptr) || (q && n_ch > 192);
+    // decode fused into the blend CTAs whenever the shape allows (features
+    // then never need the coefficient map in HBM)
+    const bool fused_dec = f->features && blend_dec_supported(f->n_levels, L, K, D);
+    bool need_cmap = (f->features != nullptr && !fused_dec) || (q && n_ch > 192);
     if (need_cmap && !f->coeff_map) return fail(SF_ERR_VALIDATION, "coefficient map buffer required");
     // band mode: owned rows [y0, y1), rendered rows = tile rows covering the
     // owned rows +- the mean-filter halo
@@ -235,6 +244,17 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     a.L = L;
     a.n_canon = q ? q->n_canonicals : 0;
     a.relevancy_raw = q ? f->relevancy_raw : nullptr;
+    if (fused_dec) {
+        launch_dec_codebook_image(s->codebooks, lv, L, D, ws.dec_img, st);
+        a.features = f->features;
+        a.D = D;
+        a.feat_level_stride = (int64_t)W * H * D;
+        a.dec_b = ws.dec_img;
+        a.dec_scale = (const float*)((const char*)ws.dec_img + blend_dec_image_bytes(f->n_levels, D) - 64);
+        a.codebooks = s->codebooks;
+        a.lv = lv;
+    }
+    if (f->events[4]) cudaEventRecord((cudaEvent_t)f->events[4], st);
     if (launch_blend(a, st)) return fail(SF_ERR_VALIDATION, "blend configuration unsupported");
     if (rel_from_map)
         launch_relevancy_from_cmap((int64_t)W * (ry1 - ry0), n_ch, f->coeff_map + (size_t)ry0 * W * n_ch,
@@ -242,7 +262,7 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
                                    (int64_t)W * H, st);
     if (f->events[1]) cudaEventRecord((cudaEvent_t)f->events[1], st);
     // K7
-    if (f->features) {
+    if (f->features && !fused_dec) {
         const int64_t HW = (int64_t)W * H;
         const int64_t P = (int64_t)W * (ry1 - ry0);  // rendered rows only
         for (int b = 0; b < f->n_levels; ++b) {

@@ -254,8 +254,23 @@ struct BlendArgs {
     int n_levels, L, n_canon;
     double* relevancy_raw; // (n_levels, H, W)
     int64_t* fixups;
+    // fused decode (optional): features (n_levels, H, W, D) from the blended tile
+    float* features;
+    int D;
+    int64_t feat_level_stride;  // H * W * D
+    const void* dec_b;          // k_dec_codebook_image output (blend_dec_image_bytes)
+    const float* dec_scale;     // per-level output scale (inside that image)
+    const float* codebooks;     // scene codebooks (levels, L, D): exact fp64 decode of fixup pixels
+    LevelSelDev lv;
+    uint64_t* timeline;         // development aid (SF_BLEND_TIMELINE), normally null
+    int dev_mode;               // development ablations (SF_DEC_MODE), normally 0
 };
 int launch_blend(const BlendArgs& a, cudaStream_t st);
+// fused decode: supported shape, and the bytes of its codebook image
+bool blend_dec_supported(int n_levels, int L, int K, int D);
+size_t blend_dec_image_bytes(int n_levels, int D);
+void launch_dec_codebook_image(const float* codebooks, const LevelSelDev& lv, int L, int D, void* out,
+                               cudaStream_t st);
 // relevancy of every pixel/level from a coefficient map already in HBM
 void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const double* proj_cb,
                                 int n_levels, int L, int n_canon, double* out, int64_t out_level_stride,

@@ -167,6 +167,12 @@ class FrameOutputs:
         return (lib.sf_event_elapsed_ms(e[0], e[1]), lib.sf_event_elapsed_ms(e[1], e[2]),
                 lib.sf_event_elapsed_ms(e[2], e[3]))
 
+    def blend_ms(self):
+        """Time of the blend kernel alone (it includes the decode when it is fused)."""
+        if not self.events:
+            return None
+        return N.load().sf_event_elapsed_ms(self.events[4], self.events[1])
+
 
 class FrameEngine:
     """Launches frames of one DeviceScene; owns a growable workspace."""
@@ -259,8 +265,8 @@ class FrameEngine:
         if timing:
             if self._events is None:
                 lib = N.load()
-                self._events = tuple(lib.sf_event_create() for _ in range(4))
-            for i in range(4):
+                self._events = tuple(lib.sf_event_create() for _ in range(5))
+            for i in range(5):
                 fr.events[i] = self._events[i]
             out.events = self._events
         qs = None

@@ -290,7 +290,8 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
     if ds.bad_index:
         raise ValidationError("coefficient index >= L")
     eager = features == "eager"
-    need_cmap = eager or len(levels) * cfg.L > 192
+    fused = bool(N.load().sf_decode_fused(len(levels), cfg.L, cfg.K, cfg.D))
+    need_cmap = (eager and not fused) or len(levels) * cfg.L > 192
     eng = ds.engine
     out = eng.allocate(W, H, levels, coeff_map=need_cmap, features=eager, query=True)
     spec = QuerySpec(query.vector, canon, window, fixed, threshold)

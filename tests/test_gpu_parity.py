@@ -81,6 +81,52 @@ def test_query_pipeline_vs_reference(name):
 
 
 @pytest.mark.parametrize("name", golden_names(require_query=True))
+def test_eager_features_vs_reference(name):
+    """query_pipeline(..., features="eager"): the features are decoded inside
+    the frame -- by the blend kernel itself when sf_decode_fused (fused_s5:
+    L=64, 3 x K=4, D=64), else by the tcgen05 GEMM over the coefficient map."""
+    scene, cam, z = load_golden(name)
+    q = sf.QueryEmbedding("q", z["q_vector"])
+    res = sf.query_pipeline(scene, cam, q, z["q_canon"], window=int(z["q_window"]), features="eager")
+    for b in range(z["features"].shape[0]):
+        ref = z["features"][b]
+        scale = max(np.abs(ref).max(initial=0), 1e-30)
+        assert np.abs(res.feature_maps.maps[b] - ref).max(initial=0) <= F_REL * scale + 1e-7, b
+    for b, m in enumerate(res.level_maps):
+        assert np.abs(m.data - z["q_filtered"][b]).max(initial=0) <= R_TOL
+    assert_selection_matches(list(z["q_filtered"]), res.level, res.point, res.mask,
+                             int(z["q_level"]), tuple(z["q_point"]), z["q_mask"])
+    assert np.abs(res.coefficient_map.data - z["cmap"]).max(initial=0) <= W_TOL
+
+
+@pytest.mark.parametrize("opacity", [(0.2, 0.95), (0.8, 0.99)])
+def test_fused_decode_matches_fp64_decode_of_the_map(opacity):
+    """Fused blend+decode (D = 512, ragged 16x8 half tiles) against the fp64
+    product of the coefficient map the same frame wrote; the opaque case
+    routes pixels through the exact fp64 fixup, whose features are redone."""
+    import torch
+    from paper_2507_07136_b200 import _native as N
+    from paper_2507_07136_b200.device import device_scene
+    rng = np.random.default_rng(3)
+    scene = random_scene(rng, 6000, num_levels=3, L=64, K=4, D=512, opacity_range=opacity)
+    cam = make_camera(150, 101)
+    assert N.load().sf_decode_fused(3, 64, 4, 512) == 1
+    eng = device_scene(scene).engine
+    out = eng.allocate(cam.width, cam.height, (0, 1, 2), coeff_map=True, final_t=True, features=True)
+    eng.run(cam, (0, 1, 2), out)
+    torch.cuda.synchronize()
+    w = out.coeff_map.double()
+    for b in range(3):
+        atoms = torch.from_numpy(scene.codebooks[b].atoms).to(w.device).double()
+        ref = w[:, :, 64 * b:64 * (b + 1)] @ atoms
+        err = (out.features[b].double() - ref).abs().max().item()
+        assert err <= F_REL * ref.abs().max().item(), (b, err)
+    fix = int(out.host_stats()[0][N.STAT_FIXUPS]) if hasattr(N, "STAT_FIXUPS") else None
+    ocm = O.splat_multilevel(scene, cam)
+    assert np.abs(out.coeff_map.cpu().numpy() - ocm.data).max() <= W_TOL, fix
+
+
+@pytest.mark.parametrize("name", golden_names(require_query=True))
 def test_relevancy_ops_vs_reference(name):
     scene, cam, z = load_golden(name)
     q = sf.QueryEmbedding("q", z["q_vector"])

@@ -43,7 +43,9 @@ def test_ctypes_binding_covers_header(lib_path):
     for name in declared_functions():
         assert name in N.EXPORTS, name
         assert getattr(lib, name) is not None
-    assert lib.sf_abi_version() == 2
+    assert lib.sf_abi_version() == 3
+    assert lib.sf_decode_fused(3, 64, 4, 512) == 1
+    assert lib.sf_decode_fused(3, 32, 4, 512) == 0
 
 
 def test_workspace_queries_need_no_gpu(lib_path):
