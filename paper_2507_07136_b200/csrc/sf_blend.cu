@@ -72,8 +72,9 @@ constexpr int kDecN = 64;                     // output columns per chunk (MMA N
 constexpr int kDecAcc = 2;                    // TMEM accumulators of kDecN columns
 constexpr int kDecAccCol = 128;
 constexpr int kDecChunkBytes = 2 * 64 * 128;  // B chunk: {hi, lo} x 64 rows (n) x 64 fp16 (128 B, SW128)
-constexpr int kDecStages = 2;                 // B chunk ring at the start of the accumulator space
-constexpr int kDecOutBytes = 8 * 4 * 32 * 4;  // per-warp output box: 8 x 4 pixels x 32 fp32 (SW128)
+constexpr int kDecStages = 3;                 // B chunk ring at the start of the accumulator space
+constexpr int kDecBoxCols = 16;               // output box: 8 x 4 pixels (a warp's patch) x 16 fp32 (SW64)
+constexpr int kDecOutBytes = 8 * 4 * kDecBoxCols * 4;
 constexpr int kDecMaxLevels = 3;
 
 struct __align__(16) BlendSmem {
@@ -244,22 +245,36 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // Issue the cp.async copies of one batch (nb records) into stage buffer S
-// (called by the 32 lanes of the producer warp).
-__device__ __forceinline__ void stage_batch(BlendStage& S, const BlendArgs& A, uint32_t base, int nb, int cs) {
+// (called by the 32 lanes of the producer warp; lane j holds record j's row).
+__device__ __forceinline__ void stage_batch(BlendStage& S, const BlendArgs& A, uint32_t rows, int nb, int cs) {
     const int gchunks = (int)(sizeof(GeomRec) / 16);  // 5
     const int cchunks = cs / 16;
     const int per = gchunks + cchunks;
-    for (int idx = (int)(threadIdx.x & 31); idx < nb * per; idx += 32) {
-        int j = idx / per, c = idx - j * per;
-        uint32_t r = __ldg(A.entries + base + j);
-        if (c < gchunks) {
-            cp_async16(reinterpret_cast<char*>(&S.g[j]) + 16 * c,
-                       reinterpret_cast<const char*>(A.geom + r) + 16 * c);
-        } else {
-            c -= gchunks;
-            cp_async16(S.chan + j * kMaxChanRec + 16 * c, A.chan + (size_t)r * cs + 16 * c);
+    const int lane = (int)(threadIdx.x & 31);
+    const int n = nb * per;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        const int idx = i0 + lane;
+        const int j = min(idx / per, 31), c = idx - j * per;
+        const uint32_t r = __shfl_sync(0xffffffffu, rows, j);
+        if (idx < n) {
+            if (c < gchunks) {
+                cp_async16(reinterpret_cast<char*>(&S.g[j]) + 16 * c,
+                           reinterpret_cast<const char*>(A.geom + r) + 16 * c);
+            } else {
+                const int cc = c - gchunks;
+                cp_async16(S.chan + j * kMaxChanRec + 16 * cc, A.chan + (size_t)r * cs + 16 * cc);
+            }
         }
     }
+}
+// Warm L2 with the records of a later batch (lane j: record j)
+__device__ __forceinline__ void prefetch_records(const BlendArgs& A, uint32_t r, int cs) {
+    const char* g = reinterpret_cast<const char*>(A.geom + r);
+    const char* c = reinterpret_cast<const char*>(A.chan) + (size_t)r * cs;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(g));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(g + sizeof(GeomRec) - 1));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(c));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(c + cs - 1));
 }
 
 // alpha = min(o exp(-q/2), 0.99) with q <= 9 membership (0 if outside).
@@ -392,16 +407,23 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
 
     if (!consumer) {
         // ---------------- producer warp: stream the tile's list through the ring ----------------
+        // Entry rows are loaded two batches ahead and the next batch's records
+        // are prefetched into L2, so a batch's cp.async gathers hit L2.
         const int pl = threadIdx.x & 31;
+        auto entry = [&](uint32_t i) -> uint32_t { return i < end ? __ldg(A.entries + i) : 0u; };
+        uint32_t e_cur = entry(beg + pl), e_next = entry(beg + kBatch + pl);
+        if (beg + pl < end) prefetch_records(A, e_cur, cs);
         for (int bi = 0;; ++bi) {
             const int st = bi % kStages;
-            if (bi >= kStages) bar_wait(&S.empty[st], ((bi / kStages) - 1) & 1);
             const uint32_t base = beg + (uint32_t)bi * kBatch;
+            const uint32_t e_n2 = entry(base + 2 * kBatch + pl);
+            if (base + kBatch + pl < end) prefetch_records(A, e_next, cs);
+            if (bi >= kStages) bar_wait(&S.empty[st], ((bi / kStages) - 1) & 1);
             const bool all_done = *reinterpret_cast<volatile int*>(&S.n_done_warps) == kConsumerWarps;
             const int nb = (base < end && !all_done) ? (int)min((uint32_t)kBatch, end - base) : 0;
             BlendStage& B = S.st[st];
             if (nb) {
-                stage_batch(B, A, base, nb, cs);
+                stage_batch(B, A, e_cur, nb, cs);
                 cp_async_commit();
                 cp_async_wait<0>();
                 __syncwarp();
@@ -418,6 +440,8 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                 bar_arrive(&S.full[st]);
             }
             if (nb == 0) break;
+            e_cur = e_next;
+            e_next = e_n2;
         }
     } else {
         // ---------------- consumer warps: progress independently through the ring ----------------
@@ -542,6 +566,7 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             }
         }
     }
+    if (A.timeline && blockIdx.x == 2001 && threadIdx.x == 0) A.timeline[4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * 6 + 0] = clock64();
     if (NC != 0 && A.proj_cb && nchb == A.n_ch) {
         // fused relevancy (query.py:65-84): l_q - l_j = W . Pd_j with the
         // logit-difference vectors Pd_j = P_q - P_cj of the projected codebook
@@ -558,7 +583,33 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             }
             __syncthreads();
         }
-        if (inside) {
+        if (A.timeline && blockIdx.x == 2001 && threadIdx.x == 0) A.timeline[4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * 6 + 1] = clock64();
+        if (inside && NC == 4 && fits && A.n_levels == 3 && A.L == 64) {
+            // the three levels together: 12 independent fp64 accumulation chains
+            double d[3][4];
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) d[b][j] = 0.0;
+#pragma unroll 2
+            for (int l = 0; l < 64; ++l) {
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    const double w = (double)acc[(b * 64 + l) * kAccPitch + slot];
+                    const double* Pl = Pd + (size_t)(b * 64 + l) * 4;
+                    const double2 p01 = *reinterpret_cast<const double2*>(Pl);
+                    const double2 p23 = *reinterpret_cast<const double2*>(Pl + 2);
+                    d[b][0] = fma(w, p01.x, d[b][0]);
+                    d[b][1] = fma(w, p01.y, d[b][1]);
+                    d[b][2] = fma(w, p23.x, d[b][2]);
+                    d[b][3] = fma(w, p23.y, d[b][3]);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < 3; ++b)  // sigmoid is monotone: min_j sigmoid(d_j) = sigmoid(min_j d_j)
+                A.relevancy_raw[(size_t)b * A.W * A.H + (size_t)py * A.W + px] =
+                    sigmoid2(np_minimum(np_minimum(d[b][0], d[b][1]), np_minimum(d[b][2], d[b][3])));
+        } else if (inside) {
             for (int b = 0; b < A.n_levels; ++b) {
                 double best = INFINITY;
                 const float* wb = acc + (b * A.L) * kAccPitch + slot;
@@ -593,6 +644,7 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             }
         }
     }
+    if (A.timeline && blockIdx.x == 2001 && threadIdx.x == 0) A.timeline[4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * 6 + 2] = clock64();
     if (DEC) {
         // ---------------- fused decode: F_b = W_b @ atoms_b on tcgen05 ----------------
         // 3-term fp16 split: W = Wh + Wl, atoms = Bh + Bl (each rounded to
@@ -600,8 +652,8 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
         // |W||B|, plus 2^-25 absolute for subnormal low parts, which the
         // per-level power-of-two codebook scale keeps below 2^-19 max|B|).
         // Levels 0 and 1 go to TMEM first, freeing accumulator bytes
-        // [0, 64 KB) for the codebook ring (32 KB) and the per-warp output boxes
-        // (32 KB); level 2 replaces level 0 once level 0's MMAs are done.
+        // [0, 64 KB) for the codebook ring (3 x 16 KB) and the per-warp output
+        // boxes (16 KB); level 2 replaces level 0 once level 0's MMAs are done.
         const int nchunk = A.D / kDecN;
         const int total = A.n_levels * nchunk;
         const uint32_t tm = S.tmem_base;
@@ -631,6 +683,8 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             };
             for (int b = 0; b < A.n_levels && b < 2; ++b) convert(b);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (A.timeline && blockIdx.x == 2001 && threadIdx.x == 0) A.timeline[4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * 6 + 3] = clock64();
+
             proxy_fence();  // accumulator reads precede the bulk copies / boxes written over them
             tc_before();
             __syncwarp();
@@ -689,22 +743,23 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     for (int i = 0; i < 64; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
                 }
 #pragma unroll
-                for (int hf = 0; hf < 2; ++hf, ++nbox) {
-                    if (lane == 0) bulk_wait_read<1>();  // the store issued two boxes ago has left this box
+                for (int q = 0; q < kDecN / kDecBoxCols; ++q, ++nbox) {
+                    if (lane == 0 && !(A.dev_mode & 8)) bulk_wait_read<1>();  // the store issued two boxes ago has left this box
                     __syncwarp();
                     unsigned char* box = wbox + (nbox & 1) * kDecOutBytes;
-                    const uint32_t row = smem_addr(box) + lane * 128;
+                    const uint32_t row = smem_addr(box) + lane * (kDecBoxCols * 4);
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((u ^ (lane & 7)) << 4)),
-                                     "r"(v[32 * hf + 4 * u]), "r"(v[32 * hf + 4 * u + 1]),
-                                     "r"(v[32 * hf + 4 * u + 2]), "r"(v[32 * hf + 4 * u + 3])
+                    for (int u = 0; u < 4; ++u) {  // 64-byte swizzle: unit u of row r at u ^ ((r >> 1) & 3)
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                         row + ((u ^ ((lane >> 1) & 3)) << 4)),
+                                     "r"(v[16 * q + 4 * u]), "r"(v[16 * q + 4 * u + 1]),
+                                     "r"(v[16 * q + 4 * u + 2]), "r"(v[16 * q + 4 * u + 3])
                                      : "memory");
                     }
                     proxy_fence();
                     __syncwarp();
                     if (lane == 0 && !(A.dev_mode & 1)) {
-                        tma_store_4d(&fmap, box, c * kDecN + 32 * hf, bx, by, b);
+                        tma_store_4d(&fmap, box, c * kDecN + kDecBoxCols * q, bx, by, b);
                         bulk_commit();
                     }
                 }
@@ -1016,8 +1071,8 @@ void launch_dec_codebook_image(const float* codebooks, const LevelSelDev& lv, in
     k_dec_codebook_image<<<lv.n * (D / kDecN), 256, 0, st>>>(codebooks, lv, L, D, img, scale);
 }
 
-// features (n_levels, H, W, D) fp32 as a 4-D TMA map: boxes of 32 columns x
-// 8 x 4 pixels of one level, 128-byte swizzle (a warp's fused-decode store box)
+// features (n_levels, H, W, D) fp32 as a 4-D TMA map: boxes of 16 columns x
+// 8 x 4 pixels of one level, 64-byte swizzle (a warp's fused-decode store box)
 static int make_feature_map(CUtensorMap* map, float* f, int D, int W, int H, int n_levels) {
     static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
     if (!enc) {
@@ -1030,10 +1085,10 @@ static int make_feature_map(CUtensorMap* map, float* f, int D, int W, int H, int
     }
     cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n_levels};
     cuuint64_t strides[3] = {(cuuint64_t)D * 4, (cuuint64_t)W * D * 4, (cuuint64_t)H * W * D * 4};
-    cuuint32_t box[4] = {32, 8, 4, 1};
+    cuuint32_t box[4] = {(cuuint32_t)kDecBoxCols, 8, 4, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, f, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : -2;
 }

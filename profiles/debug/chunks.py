@@ -15,3 +15,5 @@ for w in range(1, 5):
     print(f"consumer warp {w-1}: g  start  accfull  ldtm  stored  (rel)")
     for g in range(0, 24, 4):
         print("  ", g, *(c[g] - t0))
+e = raw[-8 * 512:].reshape(8, 64, 8)[6, 0, :4]
+print("epilogue stamps (cycles): pre-rel->Pd staged", e[1] - e[0], " rel", e[2] - e[1], " convert", e[3] - e[2])
