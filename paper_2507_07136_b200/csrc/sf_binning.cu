@@ -70,17 +70,17 @@ __global__ void __launch_bounds__(256) k_pack_channels(int64_t G, const uint16_t
     const int cs = chan_rec_bytes(C);
     if (C <= 16) {
         // build the record in registers, write it with 16-byte stores
-        uint32_t rec[24];  // <= 96 bytes
+        uint32_t rec[32];  // <= 128 bytes
 #pragma unroll
-        for (int i = 0; i < 24; ++i) rec[i] = 0;
-        uint16_t* ch = reinterpret_cast<uint16_t*>(rec);
+        for (int i = 0; i < 32; ++i) rec[i] = 0;
+        uint32_t* ch = rec;
         float* val = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(rec) + chan_val_offset(C));
         for (int b = 0; b < levels.n; ++b) {
             const int lv = levels.lv[b];
             const uint16_t* ip = cidx + ((int64_t)lv * G + row) * K;
             const float* vp = cval + ((int64_t)lv * G + row) * K;
             for (int k = 0; k < K; ++k) {
-                ch[b * K + k] = (uint16_t)(__ldg(ip + k) + b * L);
+                ch[b * K + k] = (uint32_t)(__ldg(ip + k) + b * L) * kChanWord;
                 val[b * K + k] = __ldg(vp + k);
             }
         }
@@ -89,12 +89,12 @@ __global__ void __launch_bounds__(256) k_pack_channels(int64_t G, const uint16_t
         return;
     }
     unsigned char* rp = chan + (size_t)row * cs;
-    uint16_t* ch = reinterpret_cast<uint16_t*>(rp);
+    uint32_t* ch = reinterpret_cast<uint32_t*>(rp);
     float* val = reinterpret_cast<float*>(rp + chan_val_offset(C));
     for (int b = 0; b < levels.n; ++b) {
         const int lv = levels.lv[b];
         for (int k = 0; k < K; ++k) {
-            ch[b * K + k] = (uint16_t)(cidx[((int64_t)lv * G + row) * K + k] + b * L);
+            ch[b * K + k] = (uint32_t)(cidx[((int64_t)lv * G + row) * K + k] + b * L) * kChanWord;
             val[b * K + k] = cval[((int64_t)lv * G + row) * K + k];
         }
     }

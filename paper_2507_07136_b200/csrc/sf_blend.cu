@@ -48,18 +48,27 @@ constexpr int kBlendThreads = 128;  // consumer threads: one per pixel
 constexpr int kConsumerWarps = kBlendThreads / 32;
 constexpr int kCTAThreads = kBlendThreads + 32;  // + one producer warp
 constexpr int kTilePixels = 128;    // pixels per CTA (half a 16x16 tile)
-constexpr int kStages = 2;          // batch ring between the producer and the consumer warps
+constexpr int kStages = 3;          // batch ring between the producer and the consumer warps
 constexpr int kBatch = 32;
 constexpr int kAccPitch = 129;
 constexpr int kMaxC = 16;            // channels per Gaussian (levels*K) supported
-constexpr int kMaxChanRec = 96;      // chan_rec_bytes(16)
+constexpr int kStageChan = 3072;     // scatter-plan bytes per stage: 32 records of C <= 12, 24 of C <= 16
 constexpr int kChBlock = 192;        // accumulator channels per CTA (smem bound)
+static_assert(kChanWord == kAccPitch * 4, "channel words are accumulator byte offsets");
+
+// fp32 part of a GeomRec (its first 32 bytes): all the blend needs outside
+// the guard band, where the fp64 fields are read from global memory
+struct __align__(16) GeomF32 {
+    float mx_hi, mx_lo, my_hi, my_lo;
+    float a, k, d, opacity;
+};
 
 struct __align__(16) BlendStage {
-    GeomRec g[kBatch];
-    unsigned char chan[kBatch * kMaxChanRec];
-    uint32_t off[kBatch][kMaxC];
+    GeomF32 g[kBatch];
+    uint32_t row[kBatch];
+    unsigned char chan[kStageChan];
 };
+__host__ __device__ constexpr int batch_cap(int cs) { return kStageChan / cs < kBatch ? kStageChan / cs : kBatch; }
 
 // fused decode (DEC).  TMEM columns per CTA (two CTAs per SM share 512):
 // two A slots of 64 columns (fp16 hi [0, 32) + lo [32, 64), pairs per
@@ -72,8 +81,8 @@ constexpr int kDecN = 64;                     // output columns per chunk (MMA N
 constexpr int kDecAcc = 2;                    // TMEM accumulators of kDecN columns
 constexpr int kDecAccCol = 128;
 constexpr int kDecChunkBytes = 2 * 64 * 128;  // B chunk: {hi, lo} x 64 rows (n) x 64 fp16 (128 B, SW128)
-constexpr int kDecStages = 3;                 // B chunk ring at the start of the accumulator space
-constexpr int kDecBoxCols = 16;               // output box: 8 x 4 pixels (a warp's patch) x 16 fp32 (SW64)
+constexpr int kDecStages = 2;                 // B chunk ring at the start of the accumulator space
+constexpr int kDecBoxCols = 32;               // output box: 8 x 4 pixels (a warp's patch) x 32 fp32 (SW128)
 constexpr int kDecOutBytes = 8 * 4 * kDecBoxCols * 4;
 constexpr int kDecMaxLevels = 3;
 
@@ -247,7 +256,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // Issue the cp.async copies of one batch (nb records) into stage buffer S
 // (called by the 32 lanes of the producer warp; lane j holds record j's row).
 __device__ __forceinline__ void stage_batch(BlendStage& S, const BlendArgs& A, uint32_t rows, int nb, int cs) {
-    const int gchunks = (int)(sizeof(GeomRec) / 16);  // 5
+    constexpr int gchunks = (int)(sizeof(GeomF32) / 16);  // 2
     const int cchunks = cs / 16;
     const int per = gchunks + cchunks;
     const int lane = (int)(threadIdx.x & 31);
@@ -262,44 +271,49 @@ __device__ __forceinline__ void stage_batch(BlendStage& S, const BlendArgs& A, u
                            reinterpret_cast<const char*>(A.geom + r) + 16 * c);
             } else {
                 const int cc = c - gchunks;
-                cp_async16(S.chan + j * kMaxChanRec + 16 * cc, A.chan + (size_t)r * cs + 16 * cc);
+                cp_async16(S.chan + j * cs + 16 * cc, A.chan + (size_t)r * cs + 16 * cc);
             }
         }
     }
+    if (lane < nb) S.row[lane] = rows;
 }
 // Warm L2 with the records of a later batch (lane j: record j)
 __device__ __forceinline__ void prefetch_records(const BlendArgs& A, uint32_t r, int cs) {
     const char* g = reinterpret_cast<const char*>(A.geom + r);
     const char* c = reinterpret_cast<const char*>(A.chan) + (size_t)r * cs;
     asm volatile("prefetch.global.L2 [%0];" ::"l"(g));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(g + sizeof(GeomRec) - 1));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(c));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(c + cs - 1));
 }
 
 // alpha = min(o exp(-q/2), 0.99) with q <= 9 membership (0 if outside).
-// q is evaluated in fp32 as a (dx + k dy)^2 + d dy^2 (no cancellation); inside
-// the guard band around 9 the reference's fp64 q decides (rasterizer.py:161-168).
-__device__ __forceinline__ float blend_alpha(const GeomRec& g, float pxf, float pyf, double pxd, double pyd) {
+// q is evaluated in fp32 as a (dx + k dy)^2 + d dy^2 (no cancellation),
+// branch-free; inside the guard band around 9 (`amb`) the reference's fp64 q
+// decides instead (blend_alpha_exact, rasterizer.py:161-168).
+__device__ __forceinline__ float blend_alpha_fast(const GeomF32& g, float pxf, float pyf, bool& amb) {
     constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 / ln 2
     const float dx = (pxf - g.mx_hi) - g.mx_lo;
     const float dy = (pyf - g.my_hi) - g.my_lo;
     const float u = fmaf(g.k, dy, dx);
     const float ddy = g.d * dy * dy;
-    float q32 = fmaf(g.a * u, u, ddy);
+    const float q32 = fmaf(g.a * u, u, ddy);
     const float su = fabsf(dx) + fabsf(g.k * dy);
     const float guard = fmaf(1e-5f, fmaf(g.a * su, su, ddy), 1e-5f);
-    if (q32 > 9.f + guard) return 0.f;
-    if (q32 > 9.f - guard) {
-        double ddx = __dadd_rn(pxd, -g.mx), ddyd = __dadd_rn(pyd, -g.my);
-        double t1 = __dmul_rn(__dmul_rn(g.a64, ddx), ddx);
-        double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, g.b64), ddx), ddyd);
-        double t3 = __dmul_rn(__dmul_rn(g.c64, ddyd), ddyd);
-        double q = __dadd_rn(__dadd_rn(t1, t2), t3);
-        if (!(q <= SF_CUTOFF)) return 0.f;
-        q32 = (float)q;
-    }
-    return fminf(g.opacity * exp2f(kNegHalfLog2e * q32), 0.99f);
+    amb = fabsf(q32 - 9.f) <= guard;
+    const float al = fminf(g.opacity * exp2f(kNegHalfLog2e * fminf(q32, 9.5f)), 0.99f);
+    return q32 > 9.f ? 0.f : al;
+}
+__device__ __noinline__ float blend_alpha_exact(const GeomF32& g, const GeomRec* __restrict__ g64, double pxd,
+                                                double pyd) {
+    constexpr float kNegHalfLog2e = -0.72134752044448170368f;
+    const GeomRec& G = *g64;  // rare: the reference's fp64 values from global memory
+    double ddx = __dadd_rn(pxd, -G.mx), ddyd = __dadd_rn(pyd, -G.my);
+    double t1 = __dmul_rn(__dmul_rn(G.a64, ddx), ddx);
+    double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, G.b64), ddx), ddyd);
+    double t3 = __dmul_rn(__dmul_rn(G.c64, ddyd), ddyd);
+    double q = __dadd_rn(__dadd_rn(t1, t2), t3);
+    if (!(q <= SF_CUTOFF)) return 0.f;
+    return fminf(g.opacity * exp2f(kNegHalfLog2e * (float)q), 0.99f);
 }
 
 // Conservative patch culling: may any pixel of the 8x4 patch with corner
@@ -308,7 +322,7 @@ __device__ __forceinline__ float blend_alpha(const GeomRec& g, float pxf, float 
 // else on one of the four edges (1-D minimisation with clamping).  fp32 with
 // the same relative guard as blend_alpha; false positives only cost work,
 // blend_alpha still decides every pixel (exactly, inside the guard band).
-__device__ __forceinline__ bool patch_may_hit(const GeomRec& g, float x0, float y0) {
+__device__ __forceinline__ bool patch_may_hit(const GeomF32& g, float x0, float y0) {
     const float dx0 = (x0 - g.mx_hi) - g.mx_lo, dx1 = dx0 + 7.f;
     const float dy0 = (y0 - g.my_hi) - g.my_lo, dy1 = dy0 + 3.f;
     if (dx0 <= 0.f && dx1 >= 0.f && dy0 <= 0.f && dy1 >= 0.f) return true;
@@ -368,7 +382,7 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
     const bool consumer = threadIdx.x < kBlendThreads;
     if (threadIdx.x == 0) {
         for (int st = 0; st < kStages; ++st) {
-            bar_init(&S.full[st], 1);
+            bar_init(&S.full[st], 33);  // 32 cp.async arrivals + the producer's release of rows / nb
             bar_init(&S.empty[st], kConsumerWarps);
         }
         S.n_done_warps = 0;
@@ -408,37 +422,30 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
     if (!consumer) {
         // ---------------- producer warp: stream the tile's list through the ring ----------------
         // Entry rows are loaded two batches ahead and the next batch's records
-        // are prefetched into L2, so a batch's cp.async gathers hit L2.
+        // are prefetched into L2, so a batch's cp.async gathers hit L2.  The
+        // producer never waits for its gathers: each lane's
+        // cp.async.mbarrier.arrive fires the stage's `full` barrier when its
+        // copies land (32 arrivals + lane 0's arrive after rows and nb).
         const int pl = threadIdx.x & 31;
-        auto entry = [&](uint32_t i) -> uint32_t { return i < end ? __ldg(A.entries + i) : 0u; };
-        uint32_t e_cur = entry(beg + pl), e_next = entry(beg + kBatch + pl);
-        if (beg + pl < end) prefetch_records(A, e_cur, cs);
+        const int bcap = batch_cap(cs);
+        auto entry = [&](uint32_t i) -> uint32_t { return (i < end && pl < bcap) ? __ldg(A.entries + i) : 0u; };
+        uint32_t e_cur = entry(beg + pl), e_next = entry(beg + bcap + pl);
+        if (beg + pl < end && pl < bcap) prefetch_records(A, e_cur, cs);
         for (int bi = 0;; ++bi) {
             const int st = bi % kStages;
-            const uint32_t base = beg + (uint32_t)bi * kBatch;
-            const uint32_t e_n2 = entry(base + 2 * kBatch + pl);
-            if (base + kBatch + pl < end) prefetch_records(A, e_next, cs);
+            const uint32_t base = beg + (uint32_t)bi * bcap;
+            const uint32_t e_n2 = entry(base + 2 * bcap + pl);
+            if (base + bcap + pl < end && pl < bcap) prefetch_records(A, e_next, cs);
             if (bi >= kStages) bar_wait(&S.empty[st], ((bi / kStages) - 1) & 1);
             const bool all_done = *reinterpret_cast<volatile int*>(&S.n_done_warps) == kConsumerWarps;
-            const int nb = (base < end && !all_done) ? (int)min((uint32_t)kBatch, end - base) : 0;
+            const int nb = (base < end && !all_done) ? (int)min((uint32_t)bcap, end - base) : 0;
             BlendStage& B = S.st[st];
-            if (nb) {
-                stage_batch(B, A, e_cur, nb, cs);
-                cp_async_commit();
-                cp_async_wait<0>();
-                __syncwarp();
-                // channel ids -> accumulator byte offsets for this CTA's channel block
-                for (int idx = pl; idx < nb * C; idx += 32) {
-                    int j = idx / C, k = idx - j * C;
-                    int ch = (int)reinterpret_cast<const uint16_t*>(B.chan + j * kMaxChanRec)[k] - ch0;
-                    B.off[j][k] = ((unsigned)ch < (unsigned)nchb) ? (uint32_t)(ch * kAccPitch * 4) : 0xffffffffu;
-                }
-                __syncwarp();
-            }
-            if (pl == 0) {
-                S.nb[st] = nb;
-                bar_arrive(&S.full[st]);
-            }
+            if (nb) stage_batch(B, A, e_cur, nb, cs);
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&S.full[st]))
+                         : "memory");
+            if (pl == 0) S.nb[st] = nb;
+            __syncwarp();
+            if (pl == 0) bar_arrive(&S.full[st]);
             if (nb == 0) break;
             e_cur = e_next;
             e_next = e_n2;
@@ -458,61 +465,132 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             // (conservative fp32 minimum of q over the patch rectangle, see patch_may_hit)
             const uint32_t wcand = __ballot_sync(0xffffffffu, lane < nb && patch_may_hit(B.g[lane], pdx0, pdy0));
             // ---- phase B: alpha, transmittance, scatter -- depth order ----
-            // alpha of the next candidate is computed before the current scatter
-            // (it depends only on geometry), so its latency hides under the
-            // scatter's shared-memory traffic.
+            // Candidates go in groups of kGroup: the group's alphas are computed
+            // first, branch-free (independent work, high ILP); the rare pixels
+            // inside a guard band take the exact fp64 test afterwards; then the
+            // sequential part -- transmittance and scatter -- walks the group.
             uint32_t wmask = wcand;
-            int j = wmask ? __ffs(wmask) - 1 : -1;
-            if (j >= 0) wmask &= wmask - 1;
-            float al = (j >= 0 && !done) ? blend_alpha(B.g[j], pxf, pyf, pxd, pyd) : 0.f;
-            while (j >= 0) {
-                float ef = 0.f;
-                if (al > 0.f && !done) {
-                    ef = al * T;
-                    Tprev = T;
-                    T = fmaf(-al, T, T);
-                    eb = fmaf(al, rcp_approx(1.f - al), eb);  // 1 - al in [0.01, 1]: no denormals
-                    ++ncontrib;
-                    if (A.early_exit && T < (float)SF_EARLY_EXIT_T) done = true;
+            while (wmask) {
+                constexpr int kGroup = 8;
+                int jj[kGroup];
+                float alv[kGroup];
+                uint32_t amb = 0;
+#pragma unroll
+                for (int u = 0; u < kGroup; ++u) {
+                    jj[u] = wmask ? __ffs(wmask) - 1 : -1;
+                    wmask &= wmask - 1;
                 }
-                const int jn = wmask ? __ffs(wmask) - 1 : -1;
-                if (jn >= 0) wmask &= wmask - 1;
-                const float aln = (jn >= 0 && !done) ? blend_alpha(B.g[jn], pxf, pyf, pxd, pyd) : 0.f;
-                if (__any_sync(0xffffffffu, ef > 0.f)) {
-                    const float* val = reinterpret_cast<const float*>(B.chan + j * kMaxChanRec + voff);
+#pragma unroll
+                for (int u = 0; u < kGroup; ++u) {
+                    bool g = false;
+                    alv[u] = jj[u] >= 0 ? blend_alpha_fast(B.g[jj[u] & 31], pxf, pyf, g) : 0.f;
+                    amb |= (g ? 1u : 0u) << u;
+                }
+                if (__any_sync(0xffffffffu, amb != 0)) {
+                    for (int u = 0; u < kGroup; ++u)
+                        if (amb & (1u << u))
+                            alv[u] = blend_alpha_exact(B.g[jj[u]], A.geom + B.row[jj[u]], pxd, pyd);
+                }
+                if (CT > 0 && CT % 4 == 0 && SINGLE) {
+                    // Branch-free walk: every member scatters (ef = 0 leaves the
+                    // accumulator unchanged), and the next member's channel words
+                    // and values are loaded before this member's stores, so the
+                    // only chain is acc load -> FMA -> store through shared memory.
+                    constexpr int NH = CT > 0 ? CT : 4;
                     char* accs = reinterpret_cast<char*>(acc + slot);
-                    if (CT > 0 && CT % 4 == 0 && SINGLE) {
-                        // a Gaussian's channel ids are distinct: all loads, then FMAs, then stores
-                        constexpr int NH = CT > 0 ? CT : 4;
-                        const uint4* oh = reinterpret_cast<const uint4*>(B.off[j]);
-                        const float4* vh = reinterpret_cast<const float4*>(val);
-                        uint32_t oo[NH];
-                        float vv[NH], av[NH];
+                    uint32_t oo[NH], on[NH];
+                    float vv[NH], vn[NH];
+                    auto load_rec = [&](int j, uint32_t (&o)[NH], float (&v)[NH]) {
+                        const unsigned char* rec = B.chan + j * cs;
+                        const uint4* oh = reinterpret_cast<const uint4*>(rec);
+                        const float4* vh = reinterpret_cast<const float4*>(rec + voff);
 #pragma unroll
                         for (int e = 0; e < NH / 4; ++e) {
                             const uint4 o4 = oh[e];
                             const float4 v4 = vh[e];
-                            oo[4 * e] = o4.x, oo[4 * e + 1] = o4.y, oo[4 * e + 2] = o4.z, oo[4 * e + 3] = o4.w;
-                            vv[4 * e] = v4.x, vv[4 * e + 1] = v4.y, vv[4 * e + 2] = v4.z, vv[4 * e + 3] = v4.w;
+                            o[4 * e] = o4.x, o[4 * e + 1] = o4.y, o[4 * e + 2] = o4.z, o[4 * e + 3] = o4.w;
+                            v[4 * e] = v4.x, v[4 * e + 1] = v4.y, v[4 * e + 2] = v4.z, v[4 * e + 3] = v4.w;
                         }
+                    };
+                    load_rec(jj[0], oo, vv);
+#pragma unroll
+                    for (int u = 0; u < kGroup; ++u) {
+                        if (jj[u] < 0) break;
+                        if (u + 1 < kGroup && jj[u + 1 < kGroup ? u + 1 : u] >= 0)
+                            load_rec(jj[u + 1 < kGroup ? u + 1 : u], on, vn);
+                        const float al = alv[u];
+                        const bool live = al > 0.f && !done;
+                        const float ef = live ? al * T : 0.f;
+                        if (live) {
+                            Tprev = T;
+                            T = fmaf(-al, T, T);
+                            eb = fmaf(al, rcp_approx(1.f - al), eb);  // 1 - al in [0.01, 1]: no denormals
+                            ++ncontrib;
+                            if (A.early_exit && T < (float)SF_EARLY_EXIT_T) done = true;
+                        }
+                        float av[NH];
 #pragma unroll
                         for (int e = 0; e < NH; ++e) av[e] = *reinterpret_cast<const float*>(accs + oo[e]);
 #pragma unroll
                         for (int e = 0; e < NH; ++e) av[e] = fmaf(ef, vv[e], av[e]);
 #pragma unroll
                         for (int e = 0; e < NH; ++e) *reinterpret_cast<float*>(accs + oo[e]) = av[e];
-                    } else {
-                        for (int k = 0; k < C; ++k) {
-                            const uint32_t off = B.off[j][k];
-                            if (off != 0xffffffffu) {
-                                float* a = reinterpret_cast<float*>(accs + off);
-                                *a = fmaf(ef, val[k], *a);
+#pragma unroll
+                        for (int e = 0; e < NH; ++e) oo[e] = on[e], vv[e] = vn[e];
+                    }
+                    continue;
+                }
+#pragma unroll
+                for (int u = 0; u < kGroup; ++u) {
+                    if (jj[u] < 0) break;
+                    const int j = jj[u];
+                    const float al = alv[u];
+                    float ef = 0.f;
+                    if (al > 0.f && !done) {
+                        ef = al * T;
+                        Tprev = T;
+                        T = fmaf(-al, T, T);
+                        eb = fmaf(al, rcp_approx(1.f - al), eb);  // 1 - al in [0.01, 1]: no denormals
+                        ++ncontrib;
+                        if (A.early_exit && T < (float)SF_EARLY_EXIT_T) done = true;
+                    }
+                    if (__any_sync(0xffffffffu, ef > 0.f)) {
+                        const unsigned char* rec = B.chan + j * cs;
+                        const float* val = reinterpret_cast<const float*>(rec + voff);
+                        char* accs = reinterpret_cast<char*>(acc + slot);
+                        if (CT > 0 && CT % 4 == 0 && SINGLE) {
+                            // channel words are accumulator byte offsets; a Gaussian's
+                            // channels are distinct: all loads, then FMAs, then stores
+                            constexpr int NH = CT > 0 ? CT : 4;
+                            const uint4* oh = reinterpret_cast<const uint4*>(rec);
+                            const float4* vh = reinterpret_cast<const float4*>(val);
+                            uint32_t oo[NH];
+                            float vv[NH], av[NH];
+#pragma unroll
+                            for (int e = 0; e < NH / 4; ++e) {
+                                const uint4 o4 = oh[e];
+                                const float4 v4 = vh[e];
+                                oo[4 * e] = o4.x, oo[4 * e + 1] = o4.y, oo[4 * e + 2] = o4.z, oo[4 * e + 3] = o4.w;
+                                vv[4 * e] = v4.x, vv[4 * e + 1] = v4.y, vv[4 * e + 2] = v4.z, vv[4 * e + 3] = v4.w;
+                            }
+#pragma unroll
+                            for (int e = 0; e < NH; ++e) av[e] = *reinterpret_cast<const float*>(accs + oo[e]);
+#pragma unroll
+                            for (int e = 0; e < NH; ++e) av[e] = fmaf(ef, vv[e], av[e]);
+#pragma unroll
+                            for (int e = 0; e < NH; ++e) *reinterpret_cast<float*>(accs + oo[e]) = av[e];
+                        } else {
+                            const uint32_t* words = reinterpret_cast<const uint32_t*>(rec);
+                            for (int k = 0; k < C; ++k) {
+                                const int ch = chan_id(words[k]) - ch0;
+                                if ((unsigned)ch < (unsigned)nchb) {
+                                    float* a = reinterpret_cast<float*>(accs + (size_t)ch * kChanWord);
+                                    *a = fmaf(ef, val[k], *a);
+                                }
                             }
                         }
                     }
                 }
-                j = jn;
-                al = aln;
             }
             }
             __syncwarp();
@@ -652,8 +730,9 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
         // |W||B|, plus 2^-25 absolute for subnormal low parts, which the
         // per-level power-of-two codebook scale keeps below 2^-19 max|B|).
         // Levels 0 and 1 go to TMEM first, freeing accumulator bytes
-        // [0, 64 KB) for the codebook ring (3 x 16 KB) and the per-warp output
-        // boxes (16 KB); level 2 replaces level 0 once level 0's MMAs are done.
+        // [0, 64 KB) for the codebook ring (2 x 16 KB) and the per-warp output
+        // boxes (2 x 4 KB each); level 2 replaces level 0 once level 0's MMAs
+        // are done.
         const int nchunk = A.D / kDecN;
         const int total = A.n_levels * nchunk;
         const uint32_t tm = S.tmem_base;
@@ -749,11 +828,12 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     unsigned char* box = wbox + (nbox & 1) * kDecOutBytes;
                     const uint32_t row = smem_addr(box) + lane * (kDecBoxCols * 4);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {  // 64-byte swizzle: unit u of row r at u ^ ((r >> 1) & 3)
-                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
-                                         row + ((u ^ ((lane >> 1) & 3)) << 4)),
-                                     "r"(v[16 * q + 4 * u]), "r"(v[16 * q + 4 * u + 1]),
-                                     "r"(v[16 * q + 4 * u + 2]), "r"(v[16 * q + 4 * u + 3])
+                    for (int u = 0; u < kDecBoxCols / 4; ++u) {
+                        // 128-byte swizzle: unit u of row r at u ^ (r & 7); 64-byte: u ^ ((r >> 1) & 3)
+                        const int pu = kDecBoxCols == 32 ? (u ^ (lane & 7)) : (u ^ ((lane >> 1) & 3));
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + (pu << 4)),
+                                     "r"(v[kDecBoxCols * q + 4 * u]), "r"(v[kDecBoxCols * q + 4 * u + 1]),
+                                     "r"(v[kDecBoxCols * q + 4 * u + 2]), "r"(v[kDecBoxCols * q + 4 * u + 3])
                                      : "memory");
                     }
                     proxy_fence();
@@ -1002,11 +1082,12 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_blend_fixup(BlendArgs A) {
             if (counted) {
                 const double e = __dmul_rn(al, Tb);
                 const unsigned char* rec = A.chan + (size_t)r * cs;
-                const uint16_t* ch = reinterpret_cast<const uint16_t*>(rec);
+                const uint32_t* words = reinterpret_cast<const uint32_t*>(rec);
                 const float* val = reinterpret_cast<const float*>(rec + voff);
                 for (int k = 0; k < C; ++k) {
-                    if (local) atomicAdd(&wl[ch[k]], e * (double)val[k]);
-                    else atomicAdd(&row[ch[k]], (float)(e * (double)val[k]));
+                    const int ch = chan_id(words[k]);
+                    if (local) atomicAdd(&wl[ch], e * (double)val[k]);
+                    else atomicAdd(&row[ch], (float)(e * (double)val[k]));
                 }
             }
             T = __dmul_rn(T, __shfl_sync(0xffffffffu, incl, 31));
@@ -1071,8 +1152,8 @@ void launch_dec_codebook_image(const float* codebooks, const LevelSelDev& lv, in
     k_dec_codebook_image<<<lv.n * (D / kDecN), 256, 0, st>>>(codebooks, lv, L, D, img, scale);
 }
 
-// features (n_levels, H, W, D) fp32 as a 4-D TMA map: boxes of 16 columns x
-// 8 x 4 pixels of one level, 64-byte swizzle (a warp's fused-decode store box)
+// features (n_levels, H, W, D) fp32 as a 4-D TMA map: boxes of kDecBoxCols
+// columns x 8 x 4 pixels of one level (a warp's fused-decode store box)
 static int make_feature_map(CUtensorMap* map, float* f, int D, int W, int H, int n_levels) {
     static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
     if (!enc) {
@@ -1088,7 +1169,9 @@ static int make_feature_map(CUtensorMap* map, float* f, int D, int W, int H, int
     cuuint32_t box[4] = {(cuuint32_t)kDecBoxCols, 8, 4, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, f, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     kDecBoxCols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : -2;
 }

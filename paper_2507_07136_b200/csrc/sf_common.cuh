@@ -163,11 +163,14 @@ __host__ __device__ __forceinline__ Proj64 geom_proj(const GeomRec& g) {
     p.c = g.c64;
     return p;
 }
-// Scatter plan of one Gaussian (sparse_splat.py:126-132): C u16 channel ids
-// (level block * L + index), then at a 16-byte boundary C f32 values, padded
-// to 16 bytes (C = 12 -> 80 B).
-__host__ __device__ __forceinline__ int chan_val_offset(int C) { return (2 * C + 15) / 16 * 16; }
-__host__ __device__ __forceinline__ int chan_rec_bytes(int C) { return chan_val_offset(C) + (4 * C + 15) / 16 * 16; }
+// Scatter plan of one Gaussian (sparse_splat.py:126-132): C u32 channel
+// words = channel id (level block * L + index) x kChanWord -- the byte offset
+// of the channel's row in the blend accumulator -- then, at a 16-byte
+// boundary, C f32 values; both parts padded to 16 bytes (C = 12 -> 96 B).
+constexpr uint32_t kChanWord = 129 * 4;  // blend accumulator pitch (floats) x 4 bytes
+__host__ __device__ __forceinline__ int chan_val_offset(int C) { return (4 * C + 15) / 16 * 16; }
+__host__ __device__ __forceinline__ int chan_rec_bytes(int C) { return 2 * chan_val_offset(C); }
+__host__ __device__ __forceinline__ int chan_id(uint32_t word) { return (int)(word / kChanWord); }
 
 // Workspace carving helper.
 struct Carver {

@@ -17,3 +17,7 @@ for w in range(1, 5):
         print("  ", g, *(c[g] - t0))
 e = raw[-8 * 512:].reshape(8, 64, 8)[6, 0, :4]
 print("epilogue stamps (cycles): pre-rel->Pd staged", e[1] - e[0], " rel", e[2] - e[1], " convert", e[3] - e[2])
+b = raw[-8 * 512:].reshape(8, 64, 8)[7, :4, :7]
+for w in range(4):
+    t_wait, t_a, t_b, nc, ns, nbat, nlist = b[w]
+    print(f"warp {w}: list {nlist} batches {nbat} cand {nc} scatters {ns} | cycles wait {t_wait} phaseA {t_a} phaseB {t_b} -> {t_b / max(nc, 1):.0f}/cand")
