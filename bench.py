@@ -2,8 +2,9 @@
 
 One step = one full query frame of config C (BASELINE.json
 configs[2]): preprocess -> depth-rank sort -> binning -> blend (+ fused
-projected-codebook relevancy) -> 3 x 512-d feature decode written to HBM
-(3xTF32 tcgen05) -> mean filter -> select_level / localize / segment.  That
+projected-codebook relevancy, + the 3 x 512-d feature decode on tcgen05
+inside the same CTA, written to HBM) -> mean filter -> select_level /
+localize / segment.  That
 is the reference's query_pipeline (sparse_splat.py:243-297) plus segment,
 with every feature map materialised, so the same step also bounds
 feature-splat FPS (render + decode).
@@ -297,10 +298,12 @@ def main():
     P = W * H
     pairs = int(st[N.STAT_PAIRS])
     if fused:
-        # fused blend + decode: F written + every tile-list record gathered once
-        # (u32 entry + 80 B GeomRec + 80 B channel record per pair) + codebook image
-        dom_kernel = "k_blend<DEC> (blend + fused 3xTF32 decode, one frame)"
-        dec_bytes = 3 * P * 512 * 4 + pairs * (4 + 80 + 80) + 3 * 64 * 512 * 8
+        # fused blend + decode: compulsory HBM bytes = features written + the
+        # per-Gaussian records read once (80 B GeomRec + 96 B scatter plan;
+        # a record's re-reads by the other tiles it touches hit L2) + one u32
+        # tile-list entry per pair + the codebook image
+        dom_kernel = "k_blend<DEC> (blend + fused relevancy + fused 3-term fp16 tcgen05 decode, one frame)"
+        dec_bytes = 3 * P * 512 * 4 + int(st[N.STAT_VISIBLE]) * (80 + 96) + pairs * 4 + 3 * 8 * 16384
         dom_ms = b_ms
         traffic = ncu_traffic("blend_dec", "r01_ncu_fused.txt")
         traffic_src = "profiles/r01_ncu_fused.txt (ncu --set full, one launch)"
@@ -381,7 +384,7 @@ def main():
             "data": "synthetic (SURVEY 8(d) generator, seed 1; random codebooks/query)",
             "config": {
                 "workload": (f"config {args.config}: {n_g} Gaussians, {W}x{H}, 3 levels, L=64, K=4, "
-                             "D=512 features decoded (3xTF32) + 1 text query vs 4 canonicals, "
+                             "D=512 features decoded (3-term fp16 tcgen05, fused into the blend) + 1 text query vs 4 canonicals, "
                              "window 11, level select + localize + segment"),
                 "parallelism": f"views x{world}" if world > 1 else "single",
                 "l2": "inputs/outputs larger than L2 (9.56 GB of features per frame)",

@@ -1052,21 +1052,37 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_blend_fixup(BlendArgs A) {
         double T = 1.0;  // transmittance before the current chunk
         const double pxd = (double)px, pyd = (double)py;
         const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
+        // list rows are loaded two chunks ahead, their geometry one chunk ahead
+        struct G64 {
+            double mx, my, a, b, c;
+            float o;
+        };
+        auto ld_geo = [&](uint32_t r) {
+            const GeomRec* g = A.geom + r;
+            return G64{g->mx, g->my, g->a64, g->b64, g->c64, g->opacity};
+        };
+        uint32_t r_cur = (beg + lane < end) ? A.entries[beg + lane] : 0u;
+        uint32_t r_nxt = (beg + 32 + lane < end) ? A.entries[beg + 32 + lane] : 0u;
+        G64 g_cur = (beg + lane < end) ? ld_geo(r_cur) : G64{};
         for (uint32_t i0 = beg; i0 < end && T >= SF_EARLY_EXIT_T; i0 += 32) {
             const uint32_t i = i0 + lane;
+            const uint32_t r_n2 = (i + 64 < end) ? A.entries[i + 64] : 0u;
+            const G64 g_nxt = (i + 32 < end) ? ld_geo(r_nxt) : G64{};
             double al = 0.0;
-            uint32_t r = 0;
+            const uint32_t r = r_cur;
             if (i < end) {
-                r = A.entries[i];
-                const GeomRec g = A.geom[r];
+                const G64& g = g_cur;
                 double ddx = __dadd_rn(pxd, -g.mx), ddy = __dadd_rn(pyd, -g.my);
-                double t1 = __dmul_rn(__dmul_rn(g.a64, ddx), ddx);
-                double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, g.b64), ddx), ddy);
-                double t3 = __dmul_rn(__dmul_rn(g.c64, ddy), ddy);
+                double t1 = __dmul_rn(__dmul_rn(g.a, ddx), ddx);
+                double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, g.b), ddx), ddy);
+                double t3 = __dmul_rn(__dmul_rn(g.c, ddy), ddy);
                 double q = __dadd_rn(__dadd_rn(t1, t2), t3);
                 if (q <= SF_CUTOFF)
-                    al = np_minimum(__dmul_rn((double)g.opacity, exp(__dmul_rn(-0.5, q))), SF_ALPHA_CLAMP);
+                    al = np_minimum(__dmul_rn((double)g.o, exp(__dmul_rn(-0.5, q))), SF_ALPHA_CLAMP);
             }
+            r_cur = r_nxt;
+            r_nxt = r_n2;
+            g_cur = g_nxt;
             // inclusive prefix product of (1 - alpha) -> T before each lane's entry
             double f = __dadd_rn(1.0, -al);
             double incl = f;
@@ -1106,14 +1122,27 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_blend_fixup(BlendArgs A) {
         if (local && row)
             for (int c = lane; c < A.n_ch; c += 32) row[c] = (float)wl[c];
         if (local && A.features) {
-            // the fused decode used the fp32 tile: redo this pixel's features in fp64
+            // the fused decode used the fp32 tile: redo this pixel's features
+            // from the exact coefficients (fp32 FMA over L = 64 terms: ~4e-6
+            // relative, inside the 3-term tensor-core tolerance); lanes own
+            // columns n = lane + 32 i, so codebook rows are read coalesced
             for (int b = 0; b < A.n_levels; ++b) {
                 const float* cb = A.codebooks + (size_t)A.lv.lv[b] * A.L * A.D;
                 float* fo = A.features + (size_t)b * A.feat_level_stride + pix * A.D;
-                for (int n = lane; n < A.D; n += 32) {
-                    double f = 0.0;
-                    for (int l = 0; l < A.L; ++l) f = fma(wl[b * A.L + l], (double)cb[(size_t)l * A.D + n], f);
-                    fo[n] = (float)f;
+                for (int n0 = 0; n0 < A.D; n0 += 32 * 8) {
+                    float f[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) f[i] = 0.f;
+                    for (int l = 0; l < A.L; ++l) {
+                        const float w = (float)wl[b * A.L + l];
+                        const float* row = cb + (size_t)l * A.D + n0 + lane;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            if (n0 + lane + 32 * i < A.D) f[i] = fmaf(w, __ldg(row + 32 * i), f[i]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (n0 + lane + 32 * i < A.D) fo[n0 + lane + 32 * i] = f[i];
                 }
             }
         }
