@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(512) k_count_pairs_agg(int64_t N, int64_t per,
         for (int k = 0; k < kBinSlots; ++k) a.pos[k] = 0;
         int bit = 0, nh = 0;
         for (int ty = ty0; ty <= ty1; ++ty)
-            for (int tx = tx0; tx <= tx1; ++tx, ++bit)
+            for (int tx = tx0; tx <= tx1; ++tx, ++bit) {
                 if (tile_hit(mp, tx, ty, g)) {
                     const int t = ty * g.tiles_x + tx;
                     if (nh < kBinSlots) {
@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(512) k_count_pairs_agg(int64_t N, int64_t per,
                     ++nh;
                     if (bit < 64) a.mask |= 1ull << bit;
                 }
+            }
         const uint4* src = reinterpret_cast<const uint4*>(&a);
         uint4* dst = reinterpret_cast<uint4*>(aux + i);
 #pragma unroll

@@ -392,6 +392,7 @@ __global__ void k_bin_finish(int64_t n, const uint32_t* order32, const Proj64* p
     g.a64 = p.a;
     g.b64 = p.b;
     g.c64 = p.c;
+    geom_fill_f32(g);
     geom[i] = g;
     order[i] = r;
 }

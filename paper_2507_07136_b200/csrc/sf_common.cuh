@@ -154,6 +154,17 @@ struct __align__(16) GeomRec {
     double c64;                        // inv_cov2d[1][1]
     uint32_t row, pad;
 };
+// fp32 fields of a GeomRec from its fp64 ones (mean split hi + lo; the conic
+// as a, k = b / a, d = det / a)
+__host__ __device__ __forceinline__ void geom_fill_f32(GeomRec& q) {
+    q.mx_hi = (float)q.mx;
+    q.mx_lo = (float)(q.mx - (double)q.mx_hi);
+    q.my_hi = (float)q.my;
+    q.my_lo = (float)(q.my - (double)q.my_hi);
+    q.a = (float)q.a64;
+    q.k = (float)(q.b64 / q.a64);
+    q.d = (float)((q.a64 * q.c64 - q.b64 * q.b64) / q.a64);
+}
 __host__ __device__ __forceinline__ Proj64 geom_proj(const GeomRec& g) {
     Proj64 p;
     p.mx = g.mx;

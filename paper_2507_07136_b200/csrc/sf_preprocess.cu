@@ -99,19 +99,13 @@ __global__ void __launch_bounds__(256) k_preprocess(SfScene s, SfCamera cam, Geo
                     vis = true;
                     // blend record of this row: fp32 rejection inputs + the fp64 values
                     GeomRec q;
-                    q.mx_hi = (float)m0;
-                    q.mx_lo = (float)(m0 - (double)q.mx_hi);
-                    q.my_hi = (float)m1;
-                    q.my_lo = (float)(m1 - (double)q.my_hi);
-                    q.a = (float)i00;
-                    q.k = (float)(off / i00);
-                    q.d = (float)((i00 * i11 - off * off) / i00);
-                    q.opacity = s.opacities[g];
                     q.mx = m0;
                     q.my = m1;
                     q.a64 = i00;
                     q.b64 = off;
                     q.c64 = i11;
+                    geom_fill_f32(q);
+                    q.opacity = s.opacities[g];
                     q.row = (uint32_t)g;
                     q.pad = 0;
                     geom[g] = q;
