@@ -258,8 +258,24 @@ def main():
         if dist is not None:
             dist.all_gather_into_tensor(gathered, out.mask)
 
+    # the timed loop pipelines frames (device.FramePipeline): every frame does
+    # the complete work into its own buffers, but frame i+1's projection /
+    # sort / binning and blend overlap frame i's blend tail, fixup and post
+    from paper_2507_07136_b200.device import FramePipeline
+    pipe = FramePipeline(ds, W, H, levels, coeff_map=not fused, features=True, query=True)
+
+    def pstep():
+        o = pipe.enqueue(cam, levels, query=spec, qdev=qdev)
+        if dist is not None:
+            with torch.cuda.stream(pipe.render[(pipe.k - 1) % 2]):
+                dist.all_gather_into_tensor(gathered, o.mask)
+
     for _ in range(args.warmup):
         step()
+    pipe.begin()
+    for _ in range(args.warmup):
+        pstep()
+    pipe.end()
     # per-stage kernel times (render / decode / post) over a few frames
     stage = []
     for _ in range(3):
@@ -276,13 +292,25 @@ def main():
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev0.record(stream)
+        pipe.begin()
         for _ in range(args.steps):
-            step()
+            pstep()
+        pipe.end()
         ev1.record(stream)
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
+    for o in pipe.outs:
+        assert int(o.stats_i64[N.STAT_OVERFLOW].item()) == 0
+    # the same K frames one after the other on one stream (no overlap)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    fps_serial = args.steps / (ev0.elapsed_time(ev1) / 1e3)
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -349,21 +377,36 @@ def main():
                "api": "paper_2507_07136_b200.query_pipeline(..., features='eager')"}
 
     # feature-splat FPS (render + decode, no query post) and lazy-feature query FPS
-    out_f = eng.allocate(W, H, levels, coeff_map=not fused, features=True, query=False)
-    out_q = eng.allocate(W, H, levels, coeff_map=False, features=False, query=True)
+    del pipe
+    torch.cuda.empty_cache()
     extra = {}
-    for name, o, q in (("feature_splat", out_f, None), ("text_query_lazy_features", out_q, spec)):
+    for name, alloc, q in (("feature_splat", dict(coeff_map=not fused, features=True, query=False), None),
+                           ("text_query_lazy_features", dict(coeff_map=False, features=False, query=True), spec)):
+        o = eng.allocate(W, H, levels, **alloc)
+        p2 = FramePipeline(ds, W, H, levels, **alloc)
+        p2.begin()
         for _ in range(3):
             eng.enqueue(cam, levels, o, query=q, qdev=qdev)
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            eng.enqueue(cam, levels, o, query=q, qdev=qdev)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        extra[name] = args.steps / (ev0.elapsed_time(ev1) / 1e3)
-    del out_f, out_q
-    torch.cuda.empty_cache()
+            p2.enqueue(cam, levels, query=q, qdev=qdev)
+        p2.end()
+        for mode in ("serial", "pipelined"):
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            if mode == "pipelined":
+                p2.begin()
+            for _ in range(args.steps):
+                if mode == "serial":
+                    eng.enqueue(cam, levels, o, query=q, qdev=qdev)
+                else:
+                    p2.enqueue(cam, levels, query=q, qdev=qdev)
+            if mode == "pipelined":
+                p2.end()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            fps = args.steps / (ev0.elapsed_time(ev1) / 1e3)
+            extra[name if mode == "pipelined" else name + "_serial"] = fps
+        del o, p2
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -392,8 +435,16 @@ def main():
                 "exact_fp64_fixup_pixels": int(st[7]),
             },
             "fps": {"text_query_full": fps_total / world,
+                    "text_query_full_serial": fps_serial,
                     "feature_splat": extra["feature_splat"],
-                    "text_query_lazy_features": extra["text_query_lazy_features"]},
+                    "feature_splat_serial": extra["feature_splat_serial"],
+                    "text_query_lazy_features": extra["text_query_lazy_features"],
+                    "text_query_lazy_features_serial": extra["text_query_lazy_features_serial"],
+                    "note": ("pipelined (value): every frame does the complete work into its own buffers; "
+                             "frame i's projection/sort/binning run on a shared prepare stream and its "
+                             "blend/decode/post on render stream i%2 (sf_render_frame_split, two "
+                             "workspaces), so consecutive frames overlap; serial: one frame after another "
+                             "on one stream")},
             "stage_ms": {"render": r_ms, "decode": d_ms, "post": p_ms, "blend_kernel": b_ms,
                          "decode_fused_into_blend": fused},
             "roofline": {"bound": "hbm", "kernel": dom_kernel,

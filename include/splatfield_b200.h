@@ -150,6 +150,19 @@ int sf_render_frame(const SfScene* scene, const SfCamera* cam, const SfQuery* qu
                     const SfFrame* frame, void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * sf_render_frame with its first half -- projection, depth sort, tile
+ * binning and the per-frame codebook products -- on stream_prepare, and the
+ * rest -- blend (+ fused decode), filter, selection -- on stream_render,
+ * ordered by handoff_event (a cudaEvent_t from sf_event_create).  With two
+ * workspaces and output sets a caller can prepare frame i+1 (e.g. on a
+ * higher-priority stream) while frame i blends; it must not reuse a
+ * workspace before the frame that used it has finished on stream_render.
+ */
+int sf_render_frame_split(const SfScene* scene, const SfCamera* cam, const SfQuery* query,
+                          const SfFrame* frame, void* workspace, size_t workspace_bytes,
+                          void* stream_prepare, void* stream_render, void* handoff_event);
+
+/*
  * project_scene, projection.py:240-315: the same surviving set, in scene-row
  * order, with bitwise-identical fp64 values.  Outputs sized for G rows;
  * *count_out (device int64) receives N.  inv_covs is (N,2,2).

@@ -55,6 +55,8 @@ EXPORTS = {
     "sf_frame_workspace_bytes": (ctypes.c_int, [i64, i32, i32, i32, i32, i32, i32, i64, ctypes.POINTER(sz)]),
     "sf_render_frame": (ctypes.c_int, [ctypes.POINTER(SfScene), ctypes.POINTER(SfCamera),
                                        ctypes.POINTER(SfQuery), ctypes.POINTER(SfFrame), P, sz, P]),
+    "sf_render_frame_split": (ctypes.c_int, [ctypes.POINTER(SfScene), ctypes.POINTER(SfCamera),
+                                       ctypes.POINTER(SfQuery), ctypes.POINTER(SfFrame), P, sz, P, P, P]),
     "sf_project_workspace_bytes": (ctypes.c_int, [i64, ctypes.POINTER(sz)]),
     "sf_project": (ctypes.c_int, [ctypes.POINTER(SfScene), ctypes.POINTER(SfCamera), P, P, P, P, P,
                                   P, P, P, sz, P]),

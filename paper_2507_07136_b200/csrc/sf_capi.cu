@@ -135,10 +135,12 @@ static int validate_scene_cam(const SfScene* s, const SfCamera* cam) {
     return SF_OK;
 }
 
-extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
-                               const SfFrame* f, void* workspace, size_t workspace_bytes,
-                               void* stream_) {
-    cudaStream_t st = (cudaStream_t)stream_;
+// One frame.  Projection, sort, binning and the per-frame codebook products
+// go to st_prep; blend (+ decode), filter and selection to st.  When the two
+// differ, `handoff` (a cudaEvent_t) orders them.
+static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q, const SfFrame* f,
+                        void* workspace, size_t workspace_bytes, cudaStream_t st_prep, cudaStream_t st,
+                        cudaEvent_t handoff) {
     int rc = validate_scene_cam(s, cam);
     if (rc) return rc;
     if (!f || f->n_levels < 1 || f->n_levels > kMaxLevels)
@@ -191,28 +193,28 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     if (need > workspace_bytes) return fail(SF_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, need);
 
     const int64_t G = s->num_gaussians;
-    if (f->events[0]) cudaEventRecord((cudaEvent_t)f->events[0], st);
-    cudaMemsetAsync(ws.stats, 0, 16 * sizeof(int64_t), st);
-    cudaMemsetAsync(ws.stats_f, 0, (8 + 2 * kMaxLevels) * sizeof(double), st);
-    cudaMemsetAsync(ws.fixup, 0, sizeof(uint32_t), st);
+    if (f->events[0]) cudaEventRecord((cudaEvent_t)f->events[0], st_prep);
+    cudaMemsetAsync(ws.stats, 0, 16 * sizeof(int64_t), st_prep);
+    cudaMemsetAsync(ws.stats_f, 0, (8 + 2 * kMaxLevels) * sizeof(double), st_prep);
+    cudaMemsetAsync(ws.fixup, 0, sizeof(uint32_t), st_prep);
     // K1
-    launch_preprocess(*s, *cam, ws.geom, ws.keys_in, ws.vals_in, ws.stats, st);
+    launch_preprocess(*s, *cam, ws.geom, ws.keys_in, ws.vals_in, ws.stats, st_prep);
     // per-row scatter plan: a scene constant for a level selection, so callers
     // may pass a cached copy (sf_pack_channels)
     const unsigned char* chan = f->chan_by_row;
     if (!chan) {
-        launch_pack_channels(*s, lv, ws.chan, st);
+        launch_pack_channels(*s, lv, ws.chan, st_prep);
         chan = ws.chan;
     }
     // K2
-    if (depth_sort(ws.keys_in, ws.keys_out, ws.vals_in, ws.vals_out, G, ws.cub_tmp, ws.cub_bytes, st))
+    if (depth_sort(ws.keys_in, ws.keys_out, ws.vals_in, ws.vals_out, G, ws.cub_tmp, ws.cub_bytes, st_prep))
         return check_cuda("depth sort");
-    launch_rank_of_row(G, ws.vals_out, ws.stats, ws.rank_of_row, st);
+    launch_rank_of_row(G, ws.vals_out, ws.stats, ws.rank_of_row, st_prep);
     // K3/K4: (tile, depth rank) lists, stored as scene rows
     launch_binning(G, ws.stats, ws.geom, ws.rank_of_row, ws.vals_out, W, H, f->pair_capacity, ws.tile_counts,
-                   ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, ws.cta_base, tr0, tr1, st);
+                   ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, ws.cta_base, tr0, tr1, st_prep);
     if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
-                                   ws.proj_cb, st);
+                                   ws.proj_cb, st_prep);
     // K5/K6 (+ fused relevancy)
     BlendArgs a;
     memset(&a, 0, sizeof(a));
@@ -244,8 +246,12 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
     a.L = L;
     a.n_canon = q ? q->n_canonicals : 0;
     a.relevancy_raw = q ? f->relevancy_raw : nullptr;
+    if (fused_dec) launch_dec_codebook_image(s->codebooks, lv, L, D, ws.dec_img, st_prep);
+    if (st_prep != st) {
+        cudaEventRecord(handoff, st_prep);
+        cudaStreamWaitEvent(st, handoff, 0);
+    }
     if (fused_dec) {
-        launch_dec_codebook_image(s->codebooks, lv, L, D, ws.dec_img, st);
         a.features = f->features;
         a.D = D;
         a.feat_level_stride = (int64_t)W * H * D;
@@ -286,6 +292,21 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
         cudaMemcpyAsync(f->stats_f64, ws.stats_f, (8 + 2 * f->n_levels) * sizeof(double),
                         cudaMemcpyDeviceToDevice, st);
     return check_cuda("sf_render_frame");
+}
+
+extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q, const SfFrame* f,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+    return render_frame(s, cam, q, f, workspace, workspace_bytes, (cudaStream_t)stream, (cudaStream_t)stream,
+                        nullptr);
+}
+
+extern "C" int sf_render_frame_split(const SfScene* s, const SfCamera* cam, const SfQuery* q, const SfFrame* f,
+                                     void* workspace, size_t workspace_bytes, void* stream_prepare,
+                                     void* stream_render, void* handoff_event) {
+    if (stream_prepare != stream_render && !handoff_event)
+        return fail(SF_ERR_VALIDATION, "two streams need a handoff event");
+    return render_frame(s, cam, q, f, workspace, workspace_bytes, (cudaStream_t)stream_prepare,
+                        (cudaStream_t)stream_render, (cudaEvent_t)handoff_event);
 }
 
 // ---------------------------------------------------------------------------

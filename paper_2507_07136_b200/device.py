@@ -185,6 +185,7 @@ class FrameEngine:
         self._ws_key = None
         self._lock = threading.Lock()
         self._events = None
+        self._handoff = None
         self._plans = {}
 
     def channel_plan(self, levels) -> "torch.Tensor":
@@ -235,11 +236,13 @@ class FrameEngine:
         )
 
     def enqueue(self, cam, levels, out: FrameOutputs, *, query: QuerySpec | None = None,
-                early_exit: bool = True, qdev=None, timing: bool = False, band=None):
+                early_exit: bool = True, qdev=None, timing: bool = False, band=None, prep_stream=None):
         """Launch one frame on the current stream (no host synchronisation).
 
         ``band=(y0, y1)``: tile-band mode -- only pixel rows [y0, y1) are owned
-        (SfFrame.band_y0/1); ``None`` renders the whole image."""
+        (SfFrame.band_y0/1); ``None`` renders the whole image.
+        ``prep_stream``: run projection / sort / binning there instead
+        (sf_render_frame_split); the rest stays on the current stream."""
         cfg = self.ds.config
         camc = camera_struct(cam)
         W, H = camc.width, camc.height
@@ -278,9 +281,18 @@ class FrameEngine:
             keep = qdev
             qs = N.SfQuery(N.ptr(qdev[0]), N.ptr(qdev[1]), int(query.canonicals.shape[0]),
                            int(query.window), int(query.fixed_level), float(query.threshold))
-        rc = N.load().sf_render_frame(ctypes.byref(self.ds.struct), ctypes.byref(camc),
-                                      ctypes.byref(qs) if qs is not None else None, ctypes.byref(fr),
-                                      N.ptr(ws), ws.numel(), stream_ptr())
+        lib = N.load()
+        if prep_stream is None:
+            rc = lib.sf_render_frame(ctypes.byref(self.ds.struct), ctypes.byref(camc),
+                                     ctypes.byref(qs) if qs is not None else None, ctypes.byref(fr),
+                                     N.ptr(ws), ws.numel(), stream_ptr())
+        else:
+            if self._handoff is None:
+                self._handoff = lib.sf_event_create()
+            rc = lib.sf_render_frame_split(ctypes.byref(self.ds.struct), ctypes.byref(camc),
+                                           ctypes.byref(qs) if qs is not None else None, ctypes.byref(fr),
+                                           N.ptr(ws), ws.numel(), ctypes.c_void_p(prep_stream.cuda_stream),
+                                           stream_ptr(), self._handoff)
         N.check(rc)
         return keep
 
@@ -296,3 +308,45 @@ class FrameEngine:
                     return out
                 self.pair_capacity = int(int(st[N.STAT_PAIRS]) * 1.25) + 1024
             raise SplatfieldError("pair buffer overflow persisted after growing")
+
+
+class FramePipeline:
+    """Frames of one scene overlapped on the GPU: frame i's projection / sort /
+    binning run on a shared prepare stream and its blend (+ decode) / post on
+    render stream i % 2 (sf_render_frame_split), with two engines
+    (workspaces) and two output sets used alternately.  So frame i+1's
+    first half overlaps frame i's blend, and frame i+1's blend overlaps frame
+    i's fixup / post tail.  Every frame does the complete work.
+
+    begin() / end() join the pipeline's streams with the caller's stream."""
+
+    def __init__(self, dscene: DeviceScene, W: int, H: int, levels, **alloc):
+        # engines of their own: the scene's default engine may be in use on another stream
+        self.engines = [FrameEngine(dscene), FrameEngine(dscene)]
+        for e in self.engines:
+            e.pair_capacity = dscene.engine.pair_capacity
+            e._plans = dscene.engine._plans  # the cached scatter plans are read-only
+        self.outs = [e.allocate(W, H, levels, **alloc) for e in self.engines]
+        self.prep = torch.cuda.Stream()
+        self.render = [torch.cuda.Stream(), torch.cuda.Stream()]
+        self.k = 0
+
+    def begin(self):
+        cur = torch.cuda.current_stream()
+        for st in (self.prep, *self.render):
+            st.wait_stream(cur)
+
+    def enqueue(self, cam, levels, **kw) -> FrameOutputs:
+        i = self.k % 2
+        self.k += 1
+        rs = self.render[i]
+        self.prep.wait_stream(rs)  # buffer i: the frame two back has finished with it
+        out = self.outs[i]
+        with torch.cuda.stream(rs):
+            self.engines[i].enqueue(cam, levels, out, prep_stream=self.prep, **kw)
+        return out
+
+    def end(self):
+        cur = torch.cuda.current_stream()
+        for st in self.render:
+            cur.wait_stream(st)
