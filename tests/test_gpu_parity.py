@@ -337,3 +337,39 @@ def test_tile_bands_stitch_to_the_full_frame(rng, world, L):
 def N_STAT_LEVEL():
     from paper_2507_07136_b200 import _native as N
     return N.STAT_LEVEL
+
+
+def test_frame_pipeline_matches_serial_frames(rng):
+    """device.FramePipeline (sf_render_frame_split: prepare stream + two render
+    streams, two workspaces) gives every frame the same results as a serial frame."""
+    import torch
+    from paper_2507_07136_b200.device import FramePipeline, QuerySpec, device_scene
+    scene = random_scene(rng, 4000, num_levels=3, L=64, K=4, D=64)
+    cams = [make_camera(96, 70), make_camera(96, 70, fov=40.0), make_camera(96, 70, fov=50.0)]
+    qv = rng.standard_normal(64)
+    canon = rng.standard_normal((4, 64))
+    spec = QuerySpec(qv, canon, 11, -1, 0.5)
+    ds = device_scene(scene)
+    eng = ds.engine
+    levels = (0, 1, 2)
+    ref = []
+    for cam in cams:
+        o = eng.allocate(96, 70, levels, coeff_map=False, features=True, query=True)
+        eng.run(cam, levels, o, query=spec)
+        ref.append(o)
+    pipe = FramePipeline(ds, 96, 70, levels, coeff_map=False, features=True, query=True)
+    order = cams * 2
+    got = []
+    for k0 in range(0, len(order), 2):  # two frames in flight (both buffers), then read them
+        pipe.begin()
+        outs = [pipe.enqueue(cam, levels, query=spec) for cam in order[k0:k0 + 2]]
+        pipe.end()
+        for o in outs:
+            got.append((o.features.clone(), o.relevancy_filtered.clone(), o.mask.clone(), o.stats_i64.clone()))
+    torch.cuda.synchronize()
+    for k, (f, r, m, st) in enumerate(got):
+        o = ref[k % 3]
+        assert (f - o.features).abs().max().item() <= 1e-6 * o.features.abs().max().item()
+        assert (r - o.relevancy_filtered).abs().max().item() <= 1e-12
+        assert torch.equal(m, o.mask)
+        assert torch.equal(st[:8], o.stats_i64[:8])
