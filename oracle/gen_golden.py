@@ -114,13 +114,42 @@ def fused_fixtures():
     return made
 
 
+def dense_fixtures():
+    """render_dense (rasterizer.py:206-272): colours, a 20-channel feature array
+    (two 16-channel GPU passes) and a background composite, ragged image."""
+    from splatfield import rasterizer as RR
+    rng = np.random.default_rng(1006)
+    sc = random_scene(rng, num_gaussians=400, num_levels=1, L=16, K=4, D=8, opacity_range=(0.3, 0.97))
+    cam = camera(45, 37)
+    feats = rng.standard_normal((400, 20))
+    col, st = RR.render_dense(sc, cam, "color", with_stats=True)
+    fe = RR.render_dense(sc, cam, feats)
+    bg = RR.render_dense(sc, cam, "color", background=[0.2, 0.4, 0.6])
+    d = dict(positions=sc.positions, rotations=sc.rotations, scales=sc.scales, opacities=sc.opacities,
+             colors=sc.colors, coeff_indices=sc.coeff_indices, coeff_values=sc.coeff_values, ids=sc.ids,
+             codebooks=np.stack([cb.atoms for cb in sc.codebooks]),
+             config=np.array([1, 16, 4, 8], dtype=np.int64),
+             cam_R=cam.rotation, cam_t=cam.translation,
+             cam_intr=np.array([cam.fx, cam.fy, cam.cx, cam.cy, cam.near]),
+             cam_size=np.array([cam.width, cam.height], dtype=np.int64),
+             dense_feats=feats, dense_color=col.data, dense_color_t=st.final_transmittance,
+             dense_color_pairs=np.int64(st.pairs_blended), dense_feat=fe.data, dense_bg=bg.data)
+    path = os.path.join(OUT, "dense_s6.npz")
+    np.savez_compressed(path, **d)
+    return [(path, os.path.getsize(path))]
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--only-dense" in sys.argv:
+        for p, sz in dense_fixtures():
+            print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
+        return
     if "--only-fused" in sys.argv:
         for p, sz in fused_fixtures():
             print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
         return
-    made = fused_fixtures()
+    made = fused_fixtures() + dense_fixtures()
     # 1. reference-test-like scenes (tests/conftest.py distribution)
     for seed, (g, nl, L, K, D, w, h) in enumerate([
         (50, 1, 16, 4, 8, 32, 32),

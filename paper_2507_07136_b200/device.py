@@ -203,13 +203,15 @@ class FrameEngine:
             self._plans[key] = plan
         return plan
 
-    def workspace(self, W: int, H: int, n_levels: int) -> "torch.Tensor":
+    def workspace(self, W: int, H: int, n_levels: int, L: int | None = None, K: int | None = None) -> "torch.Tensor":
         cfg = self.ds.config
-        key = (W, H, n_levels, self.pair_capacity)
+        L = cfg.L if L is None else L
+        K = cfg.K if K is None else K
+        key = (W, H, n_levels, L, K, self.pair_capacity)
         if self._ws is None or self._ws_key != key:
             nbytes = ctypes.c_size_t(0)
-            N.check(N.load().sf_frame_workspace_bytes(self.ds.num_gaussians, W, H, n_levels, cfg.L,
-                                                      cfg.K, cfg.D, self.pair_capacity,
+            N.check(N.load().sf_frame_workspace_bytes(self.ds.num_gaussians, W, H, n_levels, L,
+                                                      K, cfg.D, self.pair_capacity,
                                                       ctypes.byref(nbytes)))
             if self._ws is None or self._ws.numel() < nbytes.value:
                 self._ws = None
@@ -236,18 +238,29 @@ class FrameEngine:
         )
 
     def enqueue(self, cam, levels, out: FrameOutputs, *, query: QuerySpec | None = None,
-                early_exit: bool = True, qdev=None, timing: bool = False, band=None, prep_stream=None):
+                early_exit: bool = True, qdev=None, timing: bool = False, band=None, prep_stream=None,
+                dense=None):
         """Launch one frame on the current stream (no host synchronisation).
 
         ``band=(y0, y1)``: tile-band mode -- only pixel rows [y0, y1) are owned
         (SfFrame.band_y0/1); ``None`` renders the whole image.
         ``prep_stream``: run projection / sort / binning there instead
-        (sf_render_frame_split); the rest stays on the current stream."""
+        (sf_render_frame_split); the rest stays on the current stream.
+        ``dense=(plan, C)``: blend C <= 16 dense channels per Gaussian from a
+        ready scatter plan (render_dense) instead of the scene's coefficients."""
         cfg = self.ds.config
         camc = camera_struct(cam)
         W, H = camc.width, camc.height
         lv = (ctypes.c_int32 * len(levels))(*[int(x) for x in levels])
-        ws = self.workspace(W, H, len(levels))
+        sst = self.ds.struct
+        if dense is not None:
+            plan, cc = dense
+            s0 = self.ds.struct
+            sst = N.SfScene(s0.num_gaussians, 1, cc, cc, s0.D, s0.positions, s0.rotations, s0.scales,
+                            s0.opacities, s0.coeff_indices, s0.coeff_values, s0.ids, s0.codebooks)
+            ws = self.workspace(W, H, 1, cc, cc)
+        else:
+            ws = self.workspace(W, H, len(levels))
         fr = N.SfFrame()
         fr.host_levels = ctypes.cast(lv, ctypes.c_void_p)
         fr.n_levels = len(levels)
@@ -263,7 +276,9 @@ class FrameEngine:
         fr.stats_f64 = N.ptr(out.stats_f64)
         if band is not None:
             fr.band_y0, fr.band_y1 = int(band[0]), int(band[1])
-        if len(levels) * cfg.K <= 16:
+        if dense is not None:
+            fr.chan_by_row = N.ptr(dense[0])
+        elif len(levels) * cfg.K <= 16:
             fr.chan_by_row = N.ptr(self.channel_plan(levels))
         if timing:
             if self._events is None:
@@ -283,13 +298,13 @@ class FrameEngine:
                            int(query.window), int(query.fixed_level), float(query.threshold))
         lib = N.load()
         if prep_stream is None:
-            rc = lib.sf_render_frame(ctypes.byref(self.ds.struct), ctypes.byref(camc),
+            rc = lib.sf_render_frame(ctypes.byref(sst), ctypes.byref(camc),
                                      ctypes.byref(qs) if qs is not None else None, ctypes.byref(fr),
                                      N.ptr(ws), ws.numel(), stream_ptr())
         else:
             if self._handoff is None:
                 self._handoff = lib.sf_event_create()
-            rc = lib.sf_render_frame_split(ctypes.byref(self.ds.struct), ctypes.byref(camc),
+            rc = lib.sf_render_frame_split(ctypes.byref(sst), ctypes.byref(camc),
                                            ctypes.byref(qs) if qs is not None else None, ctypes.byref(fr),
                                            N.ptr(ws), ws.numel(), ctypes.c_void_p(prep_stream.cuda_stream),
                                            stream_ptr(), self._handoff)

@@ -1,8 +1,10 @@
-"""Compositing contract shared by the splat path (splatfield/rasterizer.py:45-203).
+"""Compositing contract shared by the splat path (splatfield/rasterizer.py:45-272).
 
 The blend itself is the sm_100a kernel behind ``sparse_splat``; this module
-keeps the reference's constants, ``RenderStats`` and the up-front render
-budget check.
+keeps the reference's constants, ``RenderStats``, ``Framebuffer``, the
+up-front render budget check, and ``render_dense`` -- the dense comparator
+(rasterizer.py:206-272), run by the same blend kernel with a dense scatter
+plan (channel c of every Gaussian -> accumulator row c), 16 channels per pass.
 """
 
 from __future__ import annotations
@@ -11,7 +13,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import ResourceLimitError
+from .errors import ResourceLimitError, ValidationError
 
 EARLY_EXIT_T = 1e-4                      # rasterizer.py:45
 DEFAULT_MAX_RENDER_ELEMENTS = 1 << 27    # rasterizer.py:46
@@ -19,6 +21,9 @@ DEFAULT_MAX_RENDER_ELEMENTS = 1 << 27    # rasterizer.py:46
 TAG_COLOR = "color"
 TAG_FEATURE = "dense-feature"
 TAG_COEFFICIENT = "coefficient"
+_TAGS = (TAG_COLOR, TAG_FEATURE, TAG_COEFFICIENT)
+DEFAULT_TILE_SIZE = 16
+DENSE_CHANNELS_PER_PASS = 16  # channels a Gaussian's scatter plan can hold (kMaxC)
 
 
 @dataclass
@@ -38,3 +43,107 @@ def check_render_budget(width: int, height: int, channels: int, max_elements: in
         raise ResourceLimitError(
             f"render of {height}x{width}x{channels} = {total} elements exceeds "
             f"the budget of {max_elements}")
+
+
+@dataclass
+class Framebuffer:
+    """H x W x C scalar grid with a channel-semantics tag (rasterizer.py:55-86)."""
+
+    data: np.ndarray
+    tag: str
+
+    def __post_init__(self):
+        self.data = np.asarray(self.data)
+        if self.data.ndim != 3:
+            raise ValidationError(f"framebuffer data must be H x W x C, got {self.data.shape}")
+        if self.tag not in _TAGS:
+            raise ValidationError(f"unknown framebuffer tag {self.tag!r}")
+
+    @property
+    def height(self) -> int:
+        return int(self.data.shape[0])
+
+    @property
+    def width(self) -> int:
+        return int(self.data.shape[1])
+
+    @property
+    def channels(self) -> int:
+        return int(self.data.shape[2])
+
+    def validate(self) -> None:
+        if not np.all(np.isfinite(self.data)):
+            raise ValidationError("framebuffer entries must be finite")
+        if self.tag == TAG_COEFFICIENT:
+            if np.any(self.data < 0) or np.any(self.data > 1):
+                raise ValidationError("coefficient channels must lie in [0, 1]")
+
+
+def _resolve_channels(scene, channels):
+    """'color' or a (num_gaussians, C) array (rasterizer.py:184-195)."""
+    if isinstance(channels, str):
+        if channels != "color":
+            raise ValidationError(f"unknown channel source {channels!r}")
+        return np.asarray(scene.colors, dtype=np.float64), TAG_COLOR
+    values = np.asarray(channels, dtype=np.float64)
+    if values.ndim != 2 or values.shape[0] != scene.num_gaussians:
+        raise ValidationError(f"channel array must be (num_gaussians, C), got {values.shape}")
+    return values, TAG_FEATURE
+
+
+def render_dense(scene, cam, channels="color", *, tag: str | None = None,
+                 tile_size: int = DEFAULT_TILE_SIZE, early_exit: bool = True, background=None,
+                 max_elements: int = DEFAULT_MAX_RENDER_ELEMENTS, workers: int = 1,
+                 with_stats: bool = False):
+    """Dense render of per-Gaussian channel vectors (rasterizer.py:206-272) on the GPU.
+
+    The sm_100a blend kernel runs with a dense scatter plan -- Gaussian g adds
+    e * values[g, c] to accumulator channel c -- in passes of 16 channels
+    (values are blended in fp32, like the coefficient path).  ``workers`` is
+    accepted and echoed; tiles are independent CTAs.  Errors are raised before
+    any work, as in the reference."""
+    import torch
+
+    from .device import device_scene
+    values, inferred = _resolve_channels(scene, channels)
+    tag = tag or inferred
+    c = values.shape[1]
+    W, H = int(cam.width), int(cam.height)
+    check_render_budget(W, H, c, max_elements)
+    bg = None
+    if background is not None:
+        bg = np.asarray(background, dtype=np.float64)
+        if bg.shape != (c,):
+            raise ValidationError(f"background must have {c} channels")
+    if tile_size != DEFAULT_TILE_SIZE:
+        raise ValidationError("the sm_100a kernels are specialised for 16x16 tiles")
+    ds = device_scene(scene)
+    eng = ds.engine
+    dev = ds.device
+    g = ds.num_gaussians
+    vals = values if ds.orig_rows is None else values[ds.orig_rows.cpu().numpy()]
+    vals = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float32)).to(dev)
+    out = torch.zeros((H, W, c), dtype=torch.float32, device=dev)
+    final_t = torch.ones((H, W), dtype=torch.float32, device=dev)
+    pairs = 0
+    for c0 in range(0, c, DENSE_CHANNELS_PER_PASS):
+        cc = min(DENSE_CHANNELS_PER_PASS, c - c0)
+        half = (4 * cc + 15) // 16 * 4  # words per record half (chan_val_offset / 4)
+        plan = torch.zeros((max(g, 1), 2 * half), dtype=torch.int32, device=dev)
+        plan[:, :cc] = torch.arange(cc, dtype=torch.int32, device=dev) * 516  # accumulator byte offsets
+        if g:
+            plan[:g, half:half + cc] = vals[:, c0:c0 + cc].contiguous().view(torch.int32)
+        fo = eng.allocate(W, H, (0,), coeff_map=False, final_t=True, mask=False)
+        fo.coeff_map = torch.empty((H, W, cc), dtype=torch.float32, device=dev)
+        eng.run(cam, (0,), fo, early_exit=early_exit, dense=(plan, cc))
+        out[:, :, c0:c0 + cc] = fo.coeff_map
+        final_t = fo.final_t
+        pairs = int(fo.host_stats()[0][1])
+    data = out.double()
+    if bg is not None:
+        data = data + final_t.double()[:, :, None] * torch.from_numpy(bg).to(dev)[None, None, :]
+    fb = Framebuffer(data=data.cpu().numpy(), tag=tag)
+    if not with_stats:
+        return fb
+    return fb, RenderStats(final_transmittance=final_t.double().cpu().numpy(), pairs_blended=pairs,
+                           channels_per_gaussian=c, workers=workers)

@@ -373,3 +373,48 @@ def test_frame_pipeline_matches_serial_frames(rng):
         assert (r - o.relevancy_filtered).abs().max().item() <= 1e-12
         assert torch.equal(m, o.mask)
         assert torch.equal(st[:8], o.stats_i64[:8])
+
+
+def test_render_dense_vs_reference():
+    """render_dense (rasterizer.py:206-272) against the reference's own outputs
+    (tests/golden/dense_s6.npz): colours with stats, a 20-channel feature array
+    (two 16-channel passes), and a background composite.  Values are blended in
+    fp32: |d| <= 2e-6 for colours in [0, 1], 1e-5 x max|value| for features."""
+    scene, cam, z = load_golden("dense_s6")
+    fb, st = sf.render_dense(scene, cam, "color", with_stats=True)
+    assert fb.tag == "color" and fb.data.shape == z["dense_color"].shape
+    assert np.abs(fb.data - z["dense_color"]).max() <= W_TOL
+    assert np.abs(st.final_transmittance - z["dense_color_t"]).max() <= T_TOL
+    assert st.pairs_blended == int(z["dense_color_pairs"]) and st.channels_per_gaussian == 3
+    fe = sf.render_dense(scene, cam, z["dense_feats"])
+    assert fe.tag == "dense-feature"
+    assert np.abs(fe.data - z["dense_feat"]).max() <= 1e-5 * np.abs(z["dense_feats"]).max()
+    bg = sf.render_dense(scene, cam, "color", background=[0.2, 0.4, 0.6])
+    assert np.abs(bg.data - z["dense_bg"]).max() <= W_TOL
+
+
+def test_render_dense_contract(rng):
+    """The reference's render_dense tests (test_rasterizer.py:67-163): linearity,
+    one-hot coefficients == the sparse splat, permutation invariance, errors."""
+    scene = random_scene(rng, num_gaussians=300, num_levels=1, L=16, K=4)
+    cam = make_camera(40, 36)
+    x = rng.standard_normal((300, 5))
+    y = rng.standard_normal((300, 5))
+    combo = sf.render_dense(scene, cam, 0.7 * x - 1.3 * y).data
+    ref = 0.7 * sf.render_dense(scene, cam, x).data - 1.3 * sf.render_dense(scene, cam, y).data
+    assert np.abs(combo - ref).max() <= 1e-5
+    dense = np.zeros((300, 16))
+    np.put_along_axis(dense, scene.coeff_indices[0].astype(np.int64), scene.coeff_values[0], axis=1)
+    fb = sf.render_dense(scene, cam, dense)
+    assert np.abs(fb.data - sf.splat_sparse(scene, cam, 0).level_view(0)).max() <= W_TOL
+    base = sf.render_dense(scene, cam, "color").data
+    assert base.tobytes() == sf.render_dense(scene.permuted(rng.permutation(300)), cam, "color").data.tobytes()
+    with pytest.raises(sf.ResourceLimitError):
+        sf.render_dense(scene, cam, rng.standard_normal((300, 64)), max_elements=1000)
+    with pytest.raises(sf.ValidationError):
+        sf.render_dense(scene, cam, "depth")
+    with pytest.raises(sf.ValidationError):
+        sf.render_dense(scene, cam, "color", background=[0.1, 0.2])
+    empty = random_scene(rng, num_gaussians=0)
+    e = sf.render_dense(empty, make_camera(8, 8), "color", background=[0.2, 0.4, 0.6])
+    np.testing.assert_allclose(e.data[0, 0], [0.2, 0.4, 0.6])
