@@ -236,6 +236,25 @@ float sf_event_elapsed_ms(void* start, void* end);
 /* Human-readable text of the last error on this thread. */
 const char* sf_last_error(void);
 /* ABI version (bumped on any signature change). */
+/*
+ * LSV2 scene records (io.py:7-11, 42-124) -> SoA on the device, with the
+ * checks of Scene.validate (core.py:285-331) OR-ed into *flags (device u32,
+ * zero it first): the file is read once into pinned host memory and copied
+ * raw to the device; one thread per record de-interleaves it.  coeff_indices /
+ * coeff_values are [levels][G][K].  The codebook tail is already SoA (copy it).
+ */
+#define SF_LSV2_NONFINITE 1u
+#define SF_LSV2_QUATERNION 2u
+#define SF_LSV2_SCALE 4u
+#define SF_LSV2_OPACITY 8u
+#define SF_LSV2_INDEX_RANGE 16u
+#define SF_LSV2_INDEX_ORDER 32u
+#define SF_LSV2_VALUE_SIGN 64u
+#define SF_LSV2_VALUE_SUM 128u
+int sf_lsv2_unpack(const void* records, int64_t num_gaussians, int32_t num_levels, int32_t K, int32_t L,
+                   float* positions, float* rotations, float* scales, float* opacities, float* colors,
+                   uint16_t* coeff_indices, float* coeff_values, uint32_t* flags, void* stream);
+
 int sf_abi_version(void); /* 2: SfFrame band fields; 3: fused decode (coeff_map optional with features) */
 
 /* 1 if sf_render_frame decodes features inside the blend kernel for this

@@ -139,8 +139,40 @@ def dense_fixtures():
     return [(path, os.path.getsize(path))]
 
 
+def io_fixtures():
+    """Reference-written files (io.py): an LSV2 scene (3 levels, K = 4, odd K = 3
+    variant), a framebuffer and a query set, for byte-exact format tests."""
+    from splatfield import io as RIO
+    from splatfield import rasterizer as RR
+    from splatfield.query import QueryEmbedding as RQE
+    made = []
+    for name, (g, nl, L, K, D) in (("io_scene_k4", (300, 3, 16, 4, 8)), ("io_scene_k3", (120, 2, 8, 3, 5))):
+        rng = np.random.default_rng(1007 + K)
+        sc = random_scene(rng, num_gaussians=g, num_levels=nl, L=L, K=K, D=D)
+        path = os.path.join(OUT, name + ".lsv2")
+        RIO.save_scene(path, sc)
+        made.append((path, os.path.getsize(path)))
+    fb = RR.Framebuffer(data=np.random.default_rng(3).random((7, 5, 3)), tag="color")
+    path = os.path.join(OUT, "io_frame.fbuf")
+    RIO.dump_framebuffer(path, fb)
+    made.append((path, os.path.getsize(path)))
+    r = np.random.default_rng(4)
+    qs = RIO.QuerySet(dim=6, canonicals=r.standard_normal((4, 6)),
+                      queries=[RQE(name="chair", vector=r.standard_normal(6)),
+                               RQE(name="lamp", vector=r.standard_normal(6))],
+                      gt_mask_paths={"lamp": "masks/lamp.fbuf"})
+    path = os.path.join(OUT, "io_queries.json")
+    RIO.save_query_set(path, qs)
+    made.append((path, os.path.getsize(path)))
+    return made
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--only-io" in sys.argv:
+        for p, sz in io_fixtures():
+            print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
+        return
     if "--only-dense" in sys.argv:
         for p, sz in dense_fixtures():
             print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
@@ -149,7 +181,7 @@ def main():
         for p, sz in fused_fixtures():
             print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
         return
-    made = fused_fixtures() + dense_fixtures()
+    made = fused_fixtures() + dense_fixtures() + io_fixtures()
     # 1. reference-test-like scenes (tests/conftest.py distribution)
     for seed, (g, nl, L, K, D, w, h) in enumerate([
         (50, 1, 16, 4, 8, 32, 32),

@@ -82,6 +82,7 @@ EXPORTS = {
     "sf_last_error": (ctypes.c_char_p, []),
     "sf_abi_version": (ctypes.c_int, []),
     "sf_decode_fused": (ctypes.c_int, [i32, i32, i32, i32]),
+    "sf_lsv2_unpack": (ctypes.c_int, [P, i64, i32, i32, i32, P, P, P, P, P, P, P, P, P]),
 }
 
 _lib = None

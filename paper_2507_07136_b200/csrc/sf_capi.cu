@@ -585,3 +585,18 @@ extern "C" int sf_mask_rows(const double* maps, int32_t H, int32_t W, int32_t le
     launch_mask_rows(H, W, maps, level, lo, hi, threshold, y0, y1, mask, (cudaStream_t)stream);
     return check_cuda("sf_mask_rows");
 }
+
+// ---------------------------------------------------------------------------
+// LSV2 records -> device SoA
+
+extern "C" int sf_lsv2_unpack(const void* records, int64_t G, int32_t num_levels, int32_t K, int32_t L,
+                              float* positions, float* rotations, float* scales, float* opacities, float* colors,
+                              uint16_t* coeff_indices, float* coeff_values, uint32_t* flags, void* stream) {
+    if (G < 0 || num_levels < 0 || K < 1 || L < 1) return fail(SF_ERR_VALIDATION, "bad LSV2 header values");
+    if (G > 0 && (!records || !positions || !rotations || !scales || !opacities || !colors || !flags ||
+                  (num_levels > 0 && (!coeff_indices || !coeff_values))))
+        return fail(SF_ERR_VALIDATION, "null buffer");
+    launch_lsv2_unpack((const uint8_t*)records, G, num_levels, K, L, positions, rotations, scales, opacities,
+                       colors, coeff_indices, coeff_values, flags, (cudaStream_t)stream);
+    return check_cuda("sf_lsv2_unpack");
+}

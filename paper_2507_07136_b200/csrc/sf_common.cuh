@@ -308,6 +308,11 @@ void launch_select_segment(int n_maps, int H, int W, const double* maps, int fix
 void launch_mask_rows(int H, int W, const double* maps, int level, double lo, double hi, double threshold,
                       int y0, int y1, uint8_t* mask, cudaStream_t st);
 
+// sf_io.cu
+void launch_lsv2_unpack(const uint8_t* rec, int64_t G, int levels, int K, int L, float* pos, float* rot,
+                        float* scl, float* opa, float* col, uint16_t* cidx, float* cval, uint32_t* flags,
+                        cudaStream_t st);
+
 // sf_decode.cu (SIMT cross-check) / sf_decode_tc.cu (tcgen05 3xTF32)
 int launch_decode_simt(int64_t P, int L, int D, const float* w, int64_t w_stride, const float* cb,
                        float* out, cudaStream_t st);

@@ -26,6 +26,14 @@ __global__ void __launch_bounds__(256) k_decode_simt(int64_t P, int L, int D, co
     int64_t p = row0 + warp;
     if (p >= P) return;
     const float* wr = sw + warp * L;
+    if (D % 4) {  // any D: one column per lane
+        for (int d = lane; d < D; d += 32) {
+            float acc = 0.f;
+            for (int l = 0; l < L; ++l) acc = fmaf(wr[l], __ldg(cb + (size_t)l * D + d), acc);
+            out[p * D + d] = acc;
+        }
+        return;
+    }
     for (int d0 = lane * 4; d0 < D; d0 += 128) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int l = 0; l < L; ++l) {
@@ -42,7 +50,6 @@ __global__ void __launch_bounds__(256) k_decode_simt(int64_t P, int L, int D, co
 
 int launch_decode_simt(int64_t P, int L, int D, const float* w, int64_t w_stride, const float* cb,
                        float* out, cudaStream_t st) {
-    if (D % 4) return -1;
     if (P == 0) return 0;
     size_t smem = sizeof(float) * 8 * L;
     k_decode_simt<<<ceil_div(P, 8), 256, smem, st>>>(P, L, D, w, w_stride, cb, out);

@@ -91,12 +91,39 @@ class DeviceScene:
         atoms = np.stack([np.asarray(cb.atoms, dtype=np.float32) for cb in scene.codebooks]) \
             if len(scene.codebooks) else np.zeros((0, cfg.L, cfg.D), np.float32)
         self.codebooks = _dev(atoms, device)
+        self.host_codebooks = tuple(scene.codebooks)
+        self.colors = _dev(sel(np.asarray(scene.colors)).reshape(g, 3), device, np.float32)
         self.struct = N.SfScene(
             g, cfg.num_levels, cfg.L, cfg.K, cfg.D,
             N.ptr(self.positions), N.ptr(self.rotations), N.ptr(self.scales), N.ptr(self.opacities),
             N.ptr(self.coeff_indices), N.ptr(self.coeff_values), N.ptr(self.ids), N.ptr(self.codebooks))
         self._engine = None
         self._lock = threading.Lock()
+
+    @classmethod
+    def from_device(cls, config, tensors: dict, host_codebooks, device) -> "DeviceScene":
+        """A resident scene from SoA tensors already in HBM (io.load_scene_device):
+        positions, rotations, scales, opacities, colors, coeff_indices (int16 view of
+        u16), coeff_values, codebooks; rows are in id order (ids = arange)."""
+        self = cls.__new__(cls)
+        g = int(tensors["positions"].shape[0])
+        self.device = device
+        self.num_gaussians = g
+        self.config = config
+        self.bad_index = False  # checked by the unpack kernel (SF_LSV2_INDEX_RANGE)
+        for k in ("positions", "rotations", "scales", "opacities", "colors", "coeff_indices", "coeff_values",
+                  "codebooks"):
+            setattr(self, k, tensors[k])
+        self.ids = torch.arange(g, dtype=torch.int64, device=device)
+        self.orig_rows = None
+        self.host_codebooks = tuple(host_codebooks)
+        self.struct = N.SfScene(
+            g, config.num_levels, config.L, config.K, config.D,
+            N.ptr(self.positions), N.ptr(self.rotations), N.ptr(self.scales), N.ptr(self.opacities),
+            N.ptr(self.coeff_indices), N.ptr(self.coeff_values), N.ptr(self.ids), N.ptr(self.codebooks))
+        self._engine = None
+        self._lock = threading.Lock()
+        return self
 
     @property
     def engine(self) -> "FrameEngine":

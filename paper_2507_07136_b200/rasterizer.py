@@ -105,7 +105,12 @@ def render_dense(scene, cam, channels="color", *, tag: str | None = None,
     import torch
 
     from .device import device_scene
-    values, inferred = _resolve_channels(scene, channels)
+    from .device import DeviceScene
+    device_rows = isinstance(scene, DeviceScene) and isinstance(channels, str) and channels == "color"
+    if device_rows:  # a resident scene's colours, already in device row order
+        values, inferred = scene.colors.double().cpu().numpy(), TAG_COLOR
+    else:
+        values, inferred = _resolve_channels(scene, channels)
     tag = tag or inferred
     c = values.shape[1]
     W, H = int(cam.width), int(cam.height)
@@ -121,7 +126,7 @@ def render_dense(scene, cam, channels="color", *, tag: str | None = None,
     eng = ds.engine
     dev = ds.device
     g = ds.num_gaussians
-    vals = values if ds.orig_rows is None else values[ds.orig_rows.cpu().numpy()]
+    vals = values if (ds.orig_rows is None or device_rows) else values[ds.orig_rows.cpu().numpy()]
     vals = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float32)).to(dev)
     out = torch.zeros((H, W, c), dtype=torch.float32, device=dev)
     final_t = torch.ones((H, W), dtype=torch.float32, device=dev)

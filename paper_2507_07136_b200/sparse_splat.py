@@ -320,7 +320,7 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
         def _decode_lazy():
             if "cm" not in holder:
                 holder["cm"] = res.coefficient_map
-            return decode(holder["cm"], scene.codebooks).dev
+            return decode(holder["cm"], getattr(scene, "host_codebooks", None) or scene.codebooks).dev
 
         fms = FeatureMapSet(levels=levels, thunk=_decode_lazy)
     res = QueryResult(query=query.name, level_maps=maps, level=levels[chosen_b], chosen=maps[chosen_b],
