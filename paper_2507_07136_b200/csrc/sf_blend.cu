@@ -1205,6 +1205,127 @@ static int make_feature_map(CUtensorMap* map, float* f, int D, int W, int H, int
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+// CTA-per-pixel variant of k_blend_fixup (accumulators in one CTA's shared
+// memory, n_ch <= kChBlock): 8 warps take 8 consecutive 32-entry chunks of
+// the list per round, so a long replay takes 1/8 of the sequential chunk
+// steps.  T before an entry = T before the round x the product of the earlier
+// warps' (1 - alpha) x the warp's exclusive prefix product.
+constexpr int kFxWarps = 8;
+__global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) {
+    __shared__ double wl[kChBlock];
+    __shared__ double wtot[kFxWarps];
+    __shared__ double Tround, Tfinal;
+    __shared__ unsigned int last_counted;
+    const uint32_t count = min(*A.fixup_count, A.fixup_capacity);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        const_cast<int64_t*>(A.stats)[SF_STAT_FIXUPS] = (int64_t)*A.fixup_count;
+    const int C = A.C;
+    const int cs = chan_rec_bytes(C);
+    const int voff = chan_val_offset(C);
+    const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    constexpr double thr = SF_EARLY_EXIT_T;
+    for (uint32_t idx = blockIdx.x; idx < count; idx += gridDim.x) {
+        const uint32_t code = A.fixup_list[idx];
+        const int tile = (int)(code >> 8), slot = (int)(code & 255u);
+        const int w8 = slot >> 5, l8 = slot & 31;
+        const int px = (tile % A.tiles_x) * SF_TILE + (w8 & 1) * 8 + (l8 & 7);
+        const int py = (tile / A.tiles_x) * SF_TILE + (w8 >> 1) * 4 + (l8 >> 3);
+        const size_t pix = (size_t)py * A.W + px;
+        for (int c = tid; c < A.n_ch; c += blockDim.x) wl[c] = 0.0;
+        if (tid == 0) {
+            Tround = 1.0;
+            Tfinal = -1.0;
+        }
+        __syncthreads();
+        const double pxd = (double)px, pyd = (double)py;
+        const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
+        for (uint32_t r0 = beg; r0 < end; r0 += 32 * kFxWarps) {
+            const double T = Tround;
+            const uint32_t i = r0 + (uint32_t)(wid * 32 + lane);
+            double al = 0.0;
+            uint32_t r = 0;
+            if (i < end) {
+                r = A.entries[i];
+                const GeomRec* g = A.geom + r;
+                double ddx = __dadd_rn(pxd, -g->mx), ddy = __dadd_rn(pyd, -g->my);
+                double t1 = __dmul_rn(__dmul_rn(g->a64, ddx), ddx);
+                double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, g->b64), ddx), ddy);
+                double t3 = __dmul_rn(__dmul_rn(g->c64, ddy), ddy);
+                double q = __dadd_rn(__dadd_rn(t1, t2), t3);
+                if (q <= SF_CUTOFF)
+                    al = np_minimum(__dmul_rn((double)g->opacity, exp(__dmul_rn(-0.5, q))), SF_ALPHA_CLAMP);
+            }
+            const double f = __dadd_rn(1.0, -al);
+            double incl = f;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl = __dmul_rn(v, incl);
+            }
+            if (lane == 31) wtot[wid] = incl;
+            if (tid == 0) last_counted = 0u;
+            __syncthreads();
+            double pre = 1.0;
+            for (int v = 0; v < wid; ++v) pre = __dmul_rn(pre, wtot[v]);
+            double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) excl = 1.0;
+            const double Tb = __dmul_rn(__dmul_rn(T, pre), excl);
+            const bool live = (i < end) && (Tb >= thr);
+            if (live && al > 0.0) {
+                const double e = __dmul_rn(al, Tb);
+                const unsigned char* rec = A.chan + (size_t)r * cs;
+                const uint32_t* words = reinterpret_cast<const uint32_t*>(rec);
+                const float* val = reinterpret_cast<const float*>(rec + voff);
+                for (int k = 0; k < C; ++k) atomicAdd(&wl[chan_id(words[k])], e * (double)val[k]);
+            }
+            const bool stop = __syncthreads_or((i < end) && !(Tb >= thr));
+            if (stop) {
+                // final T = T after the last entry still counted (T is non-increasing);
+                // none counted in this round: the T the round started with
+                if (live) atomicMax(&last_counted, i + 1u);
+                __syncthreads();
+                if (live && last_counted == i + 1u) Tfinal = __dmul_rn(Tb, f);
+                if (tid == 0 && last_counted == 0u) Tfinal = T;
+                __syncthreads();
+                break;
+            }
+            if (tid == 0) {
+                double p = T;
+                for (int v = 0; v < kFxWarps; ++v) p = __dmul_rn(p, wtot[v]);
+                Tround = p;
+            }
+            __syncthreads();
+        }
+        const double Tend = Tfinal >= 0.0 ? Tfinal : Tround;
+        if (A.coeff_map)
+            for (int c = tid; c < A.n_ch; c += blockDim.x) A.coeff_map[pix * A.n_ch + c] = (float)wl[c];
+        if (tid == 0 && A.final_t) A.final_t[pix] = (float)Tend;
+        if (A.features) {
+            // the fused decode used the fp32 tile: redo this pixel's features from
+            // the exact coefficients (fp32 FMA over L terms, ~4e-6 relative)
+            for (int bn = tid; bn < A.n_levels * A.D; bn += blockDim.x) {
+                const int b = bn / A.D, n = bn - b * A.D;
+                const float* cb = A.codebooks + (size_t)A.lv.lv[b] * A.L * A.D + n;
+                float fv = 0.f;
+                for (int l = 0; l < A.L; ++l) fv = fmaf((float)wl[b * A.L + l], __ldg(cb + (size_t)l * A.D), fv);
+                A.features[(size_t)b * A.feat_level_stride + pix * A.D + n] = fv;
+            }
+        }
+        if (A.proj_cb && A.relevancy_raw && tid < A.n_levels) {
+            const int b = tid, nv = 1 + A.n_canon;
+            const double* P = A.proj_cb + (size_t)b * A.L * nv;
+            double best = INFINITY;
+            for (int j = 1; j < nv; ++j) {
+                double dj = 0.0;
+                for (int l = 0; l < A.L; ++l) dj = fma((double)(float)wl[b * A.L + l], P[l * nv] - P[l * nv + j], dj);
+                best = np_minimum(best, sigmoid2(dj));
+            }
+            A.relevancy_raw[(size_t)b * A.W * A.H + pix] = best;
+        }
+        __syncthreads();
+    }
+}
+
 int launch_blend(const BlendArgs& a, cudaStream_t st) {
     if (a.C > kMaxC) return -2;
     if (a.proj_cb && a.n_ch > kChBlock) return -3;  // fused relevancy needs every channel in one CTA
@@ -1262,7 +1383,10 @@ int launch_blend(const BlendArgs& a, cudaStream_t st) {
         }
         free(h);
     }
-    if (n_tiles > 0 && a.fixup_list && a.early_exit) k_blend_fixup<<<296, 32 * kFixWarps, 0, st>>>(a);
+    if (n_tiles > 0 && a.fixup_list && a.early_exit) {
+        if (a.n_ch <= kChBlock) k_blend_fixup_cta<<<1184, 32 * kFxWarps, 0, st>>>(a);
+        else k_blend_fixup<<<296, 32 * kFixWarps, 0, st>>>(a);
+    }
     return 0;  // (relevancy for n_ch > one channel block: launch_relevancy_from_cmap by the caller)
 }
 
