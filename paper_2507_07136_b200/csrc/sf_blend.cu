@@ -380,6 +380,20 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
 
     const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
     const bool consumer = threadIdx.x < kBlendThreads;
+    // fused relevancy: this thread's share of the logit-difference vectors
+    // Pd = P_q - P_cj, loaded now so the global latency hides under the blend
+    constexpr int kPdRegs = 6;
+    double pd_pre[kPdRegs];
+    if (NC != 0 && A.proj_cb) {
+        const int nc = NC > 0 ? NC : A.n_canon, nv = 1 + A.n_canon;
+        const int np = A.n_levels * A.L * nc;
+#pragma unroll
+        for (int u = 0; u < kPdRegs; ++u) {
+            const int i = threadIdx.x + u * kCTAThreads;
+            const int j = i % nc, bl = i / nc;
+            pd_pre[u] = i < np ? A.proj_cb[(size_t)bl * nv] - A.proj_cb[(size_t)bl * nv + 1 + j] : 0.0;
+        }
+    }
     if (threadIdx.x == 0) {
         for (int st = 0; st < kStages; ++st) {
             bar_init(&S.full[st], 33);  // 32 cp.async arrivals + the producer's release of rows / nb
@@ -655,14 +669,24 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
         double* Pd = reinterpret_cast<double*>(&S.st[0]);
         const bool fits = np * (int)sizeof(double) <= (int)sizeof(S.st);
         if (fits) {
-            for (int i = threadIdx.x; i < np; i += kCTAThreads) {
-                const int j = i % nc, bl = i / nc;
-                Pd[i] = A.proj_cb[(size_t)bl * nv] - A.proj_cb[(size_t)bl * nv + 1 + j];
+            if (np <= kPdRegs * kCTAThreads) {
+#pragma unroll
+                for (int u = 0; u < kPdRegs; ++u) {
+                    const int i = threadIdx.x + u * kCTAThreads;
+                    if (i < np) Pd[i] = pd_pre[u];
+                }
+            } else {
+                for (int i = threadIdx.x; i < np; i += kCTAThreads) {
+                    const int j = i % nc, bl = i / nc;
+                    Pd[i] = A.proj_cb[(size_t)bl * nv] - A.proj_cb[(size_t)bl * nv + 1 + j];
+                }
             }
             __syncthreads();
         }
         if (A.timeline && blockIdx.x == 2001 && threadIdx.x == 0) A.timeline[4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * 6 + 1] = clock64();
-        if (inside && NC == 4 && fits && A.n_levels == 3 && A.L == 64) {
+        if (DEC && NC == 4 && fits && A.n_levels == 3 && A.L == 64) {
+            // computed level by level inside the decode's A conversion (same reads)
+        } else if (inside && NC == 4 && fits && A.n_levels == 3 && A.L == 64) {
             // the three levels together: 12 independent fp64 accumulation chains
             double d[3][4];
 #pragma unroll
@@ -741,7 +765,13 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
         if (consumer) {
             const uint32_t lane_off = (uint32_t)(cw * 32) << 16;  // this warp's TMEM lane quarter
             // level b's coefficients (this thread's pixel) -> fp16 hi/lo pairs in A slot b & 1
-            auto convert = [&](int b) {
+            // fused relevancy rides on the conversion's reads (Pd staged in S.st)
+            const bool rel = NC == 4 && A.proj_cb && A.n_levels == 3 && A.L == 64 &&
+                             A.n_levels * A.L * 4 * (int)sizeof(double) <= (int)sizeof(S.st);
+            const double* Pd = reinterpret_cast<const double*>(&S.st[0]);
+            auto convert = [&](int b, bool with_rel) {
+                const bool rel_b = rel && with_rel;
+                double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll 1
                 for (int kb = 0; kb < 2; ++kb) {
                     uint32_t hi[16], lo[16];
@@ -749,6 +779,18 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
 #pragma unroll
                     for (int k = 0; k < 16; ++k) {
                         const float x0 = src[(2 * k) * kAccPitch], x1 = src[(2 * k + 1) * kAccPitch];
+                        if (rel_b) {
+                            const double* P0 = Pd + (size_t)(b * 64 + kb * 32 + 2 * k) * 4;
+                            const double2 a01 = *reinterpret_cast<const double2*>(P0);
+                            const double2 a23 = *reinterpret_cast<const double2*>(P0 + 2);
+                            const double2 b01 = *reinterpret_cast<const double2*>(P0 + 4);
+                            const double2 b23 = *reinterpret_cast<const double2*>(P0 + 6);
+                            const double w0 = (double)x0, w1 = (double)x1;
+                            d0 = fma(w0, a01.x, d0), d1 = fma(w0, a01.y, d1);
+                            d2 = fma(w0, a23.x, d2), d3 = fma(w0, a23.y, d3);
+                            d0 = fma(w1, b01.x, d0), d1 = fma(w1, b01.y, d1);
+                            d2 = fma(w1, b23.x, d2), d3 = fma(w1, b23.y, d3);
+                        }
                         const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
                         const __half l0 = __float2half_rn(x0 - __half2float(h0));
                         const __half l1 = __float2half_rn(x1 - __half2float(h1));
@@ -759,8 +801,29 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     tmem_st16(tm + lane_off + col, hi);
                     tmem_st16(tm + lane_off + col + 32, lo);
                 }
+                // sigmoid is monotone: min_j sigmoid(d_j) = sigmoid(min_j d_j)
+                if (rel_b && inside)
+                    A.relevancy_raw[(size_t)b * A.W * A.H + (size_t)py * A.W + px] =
+                        sigmoid2(np_minimum(np_minimum(d0, d1), np_minimum(d2, d3)));
             };
-            for (int b = 0; b < A.n_levels && b < 2; ++b) convert(b);
+            for (int b = 0; b < A.n_levels && b < 2; ++b) convert(b, true);
+            if (rel && inside) {
+                // level 2's relevancy now: its accumulator rows are converted
+                // later, while the tensor cores run levels 0 and 1
+                double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+                const float* src = acc + 128 * kAccPitch + slot;
+#pragma unroll 4
+                for (int l = 0; l < 64; ++l) {
+                    const double w = (double)src[l * kAccPitch];
+                    const double* P0 = Pd + (size_t)(128 + l) * 4;
+                    const double2 a01 = *reinterpret_cast<const double2*>(P0);
+                    const double2 a23 = *reinterpret_cast<const double2*>(P0 + 2);
+                    d0 = fma(w, a01.x, d0), d1 = fma(w, a01.y, d1);
+                    d2 = fma(w, a23.x, d2), d3 = fma(w, a23.y, d3);
+                }
+                A.relevancy_raw[(size_t)2 * A.W * A.H + (size_t)py * A.W + px] =
+                    sigmoid2(np_minimum(np_minimum(d0, d1), np_minimum(d2, d3)));
+            }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             if (A.timeline && blockIdx.x == 2001 && threadIdx.x == 0) A.timeline[4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * 6 + 3] = clock64();
 
@@ -783,7 +846,7 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     // level 0's MMAs are done (its chunks were drained): level 2 -> slot 0
                     bar_wait(&S.a_free, 0);
                     tc_after();
-                    convert(2);
+                    convert(2, false);
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     tc_before();
                     __syncwarp();
