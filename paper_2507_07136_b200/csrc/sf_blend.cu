@@ -658,7 +658,6 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             }
         }
     }
-    if (A.timeline && blockIdx.x == 2001 && threadIdx.x == 0) A.timeline[4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * 6 + 0] = clock64();
     if (NC != 0 && A.proj_cb && nchb == A.n_ch) {
         // fused relevancy (query.py:65-84): l_q - l_j = W . Pd_j with the
         // logit-difference vectors Pd_j = P_q - P_cj of the projected codebook
@@ -683,7 +682,6 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             }
             __syncthreads();
         }
-        if (A.timeline && blockIdx.x == 2001 && threadIdx.x == 0) A.timeline[4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * 6 + 1] = clock64();
         if (DEC && NC == 4 && fits && A.n_levels == 3 && A.L == 64) {
             // computed level by level inside the decode's A conversion (same reads)
         } else if (inside && NC == 4 && fits && A.n_levels == 3 && A.L == 64) {
@@ -746,7 +744,6 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             }
         }
     }
-    if (A.timeline && blockIdx.x == 2001 && threadIdx.x == 0) A.timeline[4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * 6 + 2] = clock64();
     if (DEC) {
         // ---------------- fused decode: F_b = W_b @ atoms_b on tcgen05 ----------------
         // 3-term fp16 split: W = Wh + Wl, atoms = Bh + Bl (each rounded to
@@ -825,7 +822,6 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     sigmoid2(np_minimum(np_minimum(d0, d1), np_minimum(d2, d3)));
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            if (A.timeline && blockIdx.x == 2001 && threadIdx.x == 0) A.timeline[4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * 6 + 3] = clock64();
 
             proxy_fence();  // accumulator reads precede the bulk copies / boxes written over them
             tc_before();
@@ -852,12 +848,7 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     __syncwarp();
                     if (lane == 0) bar_arrive(&S.a_ready);
                 }
-                uint64_t* cdbg = (A.timeline && blockIdx.x == 2001 && lane == 0)
-                                     ? A.timeline + 4 * (size_t)gridDim.x * gridDim.y + 64 * 8 * (1 + cw) + 8 * g
-                                     : nullptr;
-                if (cdbg) cdbg[0] = clock64();
                 bar_wait(&S.acc_full[t], (g / kDecAcc) & 1);
-                if (cdbg) cdbg[1] = clock64();
                 if (cw == 0 && lane == 0 && g + kDecStages < total) {
                     // chunk g's MMAs are complete: its codebook stage takes chunk g + kDecStages
                     const int sg = g % kDecStages;
@@ -878,7 +869,6 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                 tc_before();
                 __syncwarp();
                 if (lane == 0) bar_arrive(&S.acc_empty[t]);
-                if (cdbg) cdbg[2] = clock64();
                 const float sc = b == 0 ? scl[0] : (b == 1 ? scl[1] : scl[2]);
                 if (sc != 1.f) {
 #pragma unroll
@@ -886,7 +876,7 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                 }
 #pragma unroll
                 for (int q = 0; q < kDecN / kDecBoxCols; ++q, ++nbox) {
-                    if (lane == 0 && !(A.dev_mode & 8)) bulk_wait_read<1>();  // the store issued two boxes ago has left this box
+                    if (lane == 0) bulk_wait_read<1>();  // the store issued two boxes ago has left this box
                     __syncwarp();
                     unsigned char* box = wbox + (nbox & 1) * kDecOutBytes;
                     const uint32_t row = smem_addr(box) + lane * (kDecBoxCols * 4);
@@ -901,12 +891,11 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     }
                     proxy_fence();
                     __syncwarp();
-                    if (lane == 0 && !(A.dev_mode & 1)) {
+                    if (lane == 0) {
                         tma_store_4d(&fmap, box, c * kDecN + kDecBoxCols * q, bx, by, b);
                         bulk_commit();
                     }
                 }
-                if (cdbg) cdbg[3] = clock64();
             }
             if (lane == 0) bulk_wait<0>();
         } else {
@@ -931,16 +920,9 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     bar_wait(&S.a_ready, (b - 1) & 1);
                     tc_after();
                 }
-                uint64_t* dbg = (A.timeline && blockIdx.x == 2001 && leader)
-                                    ? A.timeline + 4 * (size_t)gridDim.x * gridDim.y + 8 * g
-                                    : nullptr;
-                if (dbg) dbg[0] = clock64();
                 bar_wait(&S.b_full[s], (g / kDecStages) & 1);
-                if (dbg) dbg[1] = clock64();
                 if (g >= kDecAcc) bar_wait(&S.acc_empty[t], ((g / kDecAcc) - 1) & 1);
-                if (dbg) dbg[2] = clock64();
                 tc_after();
-                if (dbg) dbg[3] = clock64();
                 if (leader) {
                     const uint32_t d = tm + (uint32_t)(kDecAccCol + t * kDecN);
                     const uint64_t bd = desc0 + (uint64_t)((s * kDecChunkBytes) >> 4);
@@ -953,10 +935,8 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                         mma_f16_tmem_a(d, ah, bl, idesc, 1u);
                         mma_f16_tmem_a(d, ah, bh, idesc, 1u);
                     }
-                    if (dbg) dbg[4] = clock64();
                     mma_commit(&S.acc_full[t]);
                     if (c == nchunk - 1 && b + 2 < A.n_levels) mma_commit(&S.a_free);
-                    if (dbg) dbg[5] = clock64();
                 }
                 __syncwarp();
             }
@@ -1424,24 +1404,22 @@ int launch_blend(const BlendArgs& a, cudaStream_t st) {
     // (start, blend done, A in TMEM, end) of every launch
     static const char* tl_path = getenv("SF_BLEND_TIMELINE");
     BlendArgs a2 = a;
-    static const char* dm = getenv("SF_DEC_MODE");  // development ablations of the fused decode
-    a2.dev_mode = dm ? atoi(dm) : 0;
     static uint64_t* tl = nullptr;
     const size_t n_cta = (size_t)2 * n_tiles * nblk;
     if (tl_path && n_tiles > 0) {
         if (tl) cudaFree(tl);
-        cudaMalloc(&tl, (n_cta * 4 + 8 * 512) * sizeof(uint64_t));
-        cudaMemsetAsync(tl, 0, (n_cta * 4 + 8 * 512) * sizeof(uint64_t), st);
+        cudaMalloc(&tl, n_cta * 4 * sizeof(uint64_t));
+        cudaMemsetAsync(tl, 0, n_cta * 4 * sizeof(uint64_t), st);
         a2.timeline = tl;
     }
     if (n_tiles > 0) kern<<<dim3(2 * n_tiles, nblk), kCTAThreads, smem, st>>>(a2, ch_block, fmap);
     if (tl_path && n_tiles > 0) {
-        uint64_t* h = (uint64_t*)malloc((n_cta * 4 + 8 * 512) * sizeof(uint64_t));
-        cudaMemcpyAsync(h, tl, (n_cta * 4 + 8 * 512) * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+        uint64_t* h = (uint64_t*)malloc(n_cta * 4 * sizeof(uint64_t));
+        cudaMemcpyAsync(h, tl, n_cta * 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         FILE* fp = fopen(tl_path, "wb");
         if (fp) {
-            fwrite(h, sizeof(uint64_t), n_cta * 4 + 8 * 512, fp);
+            fwrite(h, sizeof(uint64_t), n_cta * 4, fp);
             fclose(fp);
         }
         free(h);

@@ -277,7 +277,6 @@ struct BlendArgs {
     const float* codebooks;     // scene codebooks (levels, L, D): exact fp64 decode of fixup pixels
     LevelSelDev lv;
     uint64_t* timeline;         // development aid (SF_BLEND_TIMELINE), normally null
-    int dev_mode;               // development ablations (SF_DEC_MODE), normally 0
 };
 int launch_blend(const BlendArgs& a, cudaStream_t st);
 // fused decode: supported shape, and the bytes of its codebook image

@@ -5,7 +5,7 @@ usage: SF_BLEND_TIMELINE=/tmp/tl.bin python bench.py --steps 1 --warmup 1 ...; p
 import sys
 import numpy as np
 
-t = np.fromfile(sys.argv[1], dtype=np.uint64)[:-8 * 512].reshape(-1, 4).astype(np.int64)
+t = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 4).astype(np.int64)
 ok = (t > 0).all(axis=1)
 t = t[ok]
 t0 = t[:, 0].min()
