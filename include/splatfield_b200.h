@@ -109,6 +109,9 @@ typedef struct SfFrame {
      * rendered / owned range are not written. */
     int32_t band_y0;
     int32_t band_y1;
+    /* optional cached codebook image of host_levels for the fused decode
+     * (sf_pack_decode_image); NULL = built inside the frame */
+    const void* dec_image;
 } SfFrame;
 
 /* stats_i64 slots */
@@ -132,6 +135,13 @@ typedef struct SfFrame {
 size_t sf_channel_plan_bytes(int64_t num_gaussians, int32_t n_levels, int32_t K);
 int sf_pack_channels(const SfScene* scene, const int32_t* host_levels, int32_t n_levels, void* out,
                      size_t out_bytes, void* stream);
+
+/* The fused decode's codebook image of host_levels (pre-swizzled fp16 hi/lo
+ * tiles + per-level scales) -- a scene constant worth caching; 0 bytes when
+ * sf_decode_fused is false for the shape. */
+size_t sf_decode_image_bytes(int32_t n_levels, int32_t L, int32_t K, int32_t D);
+int sf_pack_decode_image(const SfScene* scene, const int32_t* host_levels, int32_t n_levels, void* out,
+                         size_t out_bytes, void* stream);
 
 /* Scratch needed by sf_render_frame for this scene/frame shape. */
 int sf_frame_workspace_bytes(int64_t num_gaussians, int32_t width, int32_t height,

@@ -48,7 +48,8 @@ class SfFrame(ctypes.Structure):
     _fields_ = [("host_levels", P), ("n_levels", i32), ("early_exit", i32), ("pair_capacity", i64),
                 ("coeff_map", P), ("final_t", P), ("features", P), ("relevancy_raw", P),
                 ("relevancy_filtered", P), ("mask", P), ("stats_i64", P), ("stats_f64", P),
-                ("events", P * 5), ("chan_by_row", P), ("band_y0", i32), ("band_y1", i32)]
+                ("events", P * 5), ("chan_by_row", P), ("band_y0", i32), ("band_y1", i32),
+                ("dec_image", P)]
 
 
 EXPORTS = {
@@ -82,6 +83,8 @@ EXPORTS = {
     "sf_last_error": (ctypes.c_char_p, []),
     "sf_abi_version": (ctypes.c_int, []),
     "sf_decode_fused": (ctypes.c_int, [i32, i32, i32, i32]),
+    "sf_decode_image_bytes": (sz, [i32, i32, i32, i32]),
+    "sf_pack_decode_image": (ctypes.c_int, [ctypes.POINTER(SfScene), P, i32, P, sz, P]),
     "sf_lsv2_unpack": (ctypes.c_int, [P, i64, i32, i32, i32, P, P, P, P, P, P, P, P, P]),
 }
 

@@ -246,7 +246,8 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
     a.L = L;
     a.n_canon = q ? q->n_canonicals : 0;
     a.relevancy_raw = q ? f->relevancy_raw : nullptr;
-    if (fused_dec) launch_dec_codebook_image(s->codebooks, lv, L, D, ws.dec_img, st_prep);
+    const void* dec_img = f->dec_image ? f->dec_image : ws.dec_img;
+    if (fused_dec && !f->dec_image) launch_dec_codebook_image(s->codebooks, lv, L, D, ws.dec_img, st_prep);
     if (st_prep != st) {
         cudaEventRecord(handoff, st_prep);
         cudaStreamWaitEvent(st, handoff, 0);
@@ -255,8 +256,8 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
         a.features = f->features;
         a.D = D;
         a.feat_level_stride = (int64_t)W * H * D;
-        a.dec_b = ws.dec_img;
-        a.dec_scale = (const float*)((const char*)ws.dec_img + blend_dec_image_bytes(f->n_levels, D) - 64);
+        a.dec_b = dec_img;
+        a.dec_scale = (const float*)((const char*)dec_img + blend_dec_image_bytes(f->n_levels, D) - 64);
         a.codebooks = s->codebooks;
         a.lv = lv;
     }
@@ -529,6 +530,27 @@ extern "C" int sf_pack_channels(const SfScene* s, const int32_t* host_levels, in
     }
     launch_pack_channels(*s, lv, (unsigned char*)out, (cudaStream_t)stream);
     return check_cuda("sf_pack_channels");
+}
+
+extern "C" size_t sf_decode_image_bytes(int32_t n_levels, int32_t L, int32_t K, int32_t D) {
+    return blend_dec_supported(n_levels, L, K, D) ? blend_dec_image_bytes(n_levels, D) : 0;
+}
+
+extern "C" int sf_pack_decode_image(const SfScene* s, const int32_t* host_levels, int32_t n_levels, void* out,
+                                    size_t out_bytes, void* stream) {
+    if (!s || n_levels < 1 || n_levels > kMaxLevels) return fail(SF_ERR_VALIDATION, "bad level selection");
+    if (!blend_dec_supported(n_levels, s->L, s->K, s->D))
+        return fail(SF_ERR_VALIDATION, "the decode is not fused for this shape");
+    if (out_bytes < blend_dec_image_bytes(n_levels, s->D)) return fail(SF_ERR_WORKSPACE, "image buffer too small");
+    LevelSelDev lv;
+    lv.n = n_levels;
+    for (int b = 0; b < n_levels; ++b) {
+        if (host_levels[b] < 0 || host_levels[b] >= s->num_levels)
+            return fail(SF_ERR_VALIDATION, "level %d out of range", host_levels[b]);
+        lv.lv[b] = host_levels[b];
+    }
+    launch_dec_codebook_image(s->codebooks, lv, s->L, s->D, out, (cudaStream_t)stream);
+    return check_cuda("sf_pack_decode_image");
 }
 
 extern "C" int sf_decode_simt(int64_t P, int32_t L, int32_t D, const float* w, int64_t w_stride,

@@ -230,6 +230,22 @@ class FrameEngine:
             self._plans[key] = plan
         return plan
 
+    def decode_image(self, levels):
+        """Cached codebook image of the fused decode for a level selection (or None)."""
+        key = ("dec",) + tuple(int(x) for x in levels)
+        if key not in self._plans:
+            lib = N.load()
+            cfg = self.ds.config
+            nbytes = int(lib.sf_decode_image_bytes(len(levels), cfg.L, cfg.K, cfg.D))
+            img = None
+            if nbytes:
+                img = torch.empty(nbytes, dtype=torch.uint8, device=self.ds.device)
+                lv = (ctypes.c_int32 * len(levels))(*key[1:])
+                N.check(lib.sf_pack_decode_image(ctypes.byref(self.ds.struct), ctypes.cast(lv, ctypes.c_void_p),
+                                                 len(levels), N.ptr(img), nbytes, stream_ptr()))
+            self._plans[key] = img
+        return self._plans[key]
+
     def workspace(self, W: int, H: int, n_levels: int, L: int | None = None, K: int | None = None) -> "torch.Tensor":
         cfg = self.ds.config
         L = cfg.L if L is None else L
@@ -307,6 +323,8 @@ class FrameEngine:
             fr.chan_by_row = N.ptr(dense[0])
         elif len(levels) * cfg.K <= 16:
             fr.chan_by_row = N.ptr(self.channel_plan(levels))
+        if dense is None and out.features is not None:
+            fr.dec_image = N.ptr(self.decode_image(levels))
         if timing:
             if self._events is None:
                 lib = N.load()
