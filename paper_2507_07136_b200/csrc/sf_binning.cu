@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(256, 4) k_count_pairs(int64_t N, const int64_t
 // atomic per (CTA, tile) then reserves the CTA's range inside the tile and
 // its base is kept in cta_base[c][tile].  4x fewer global atomics than one
 // per pair, with the same emit-time arithmetic.
-__global__ void __launch_bounds__(512) k_count_pairs_agg(int64_t N, int64_t per, const int64_t* __restrict__ stats,
+__global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t per, const int64_t* __restrict__ stats,
                                                          const GeomRec* __restrict__ geom,
                                                          const uint32_t* __restrict__ rank_of, TileGrid g,
                                                          uint32_t* __restrict__ tile_counts, BinAux* __restrict__ aux,
