@@ -336,8 +336,10 @@ class FrameEngine:
         keep = None
         if query is not None:
             if qdev is None:
-                qdev = (torch.from_numpy(np.ascontiguousarray(query.vector, dtype=np.float64)).to(self.ds.device),
-                        torch.from_numpy(np.ascontiguousarray(query.canonicals, dtype=np.float64)).to(self.ds.device))
+                # pinned staging + async copies: the launches need not wait for them
+                hq = torch.from_numpy(np.ascontiguousarray(query.vector, dtype=np.float64)).pin_memory()
+                hc = torch.from_numpy(np.ascontiguousarray(query.canonicals, dtype=np.float64)).pin_memory()
+                qdev = (hq.to(self.ds.device, non_blocking=True), hc.to(self.ds.device, non_blocking=True), hq, hc)
             keep = qdev
             qs = N.SfQuery(N.ptr(qdev[0]), N.ptr(qdev[1]), int(query.canonicals.shape[0]),
                            int(query.window), int(query.fixed_level), float(query.threshold))
@@ -356,13 +358,25 @@ class FrameEngine:
         N.check(rc)
         return keep
 
-    def run(self, cam, levels, out: FrameOutputs, **kw) -> FrameOutputs:
-        """Launch and synchronise; grows the pair buffer and re-runs on overflow."""
+    def run(self, cam, levels, out: FrameOutputs, *, fetch_mask: bool = False, **kw) -> FrameOutputs:
+        """Launch and synchronise once; grows the pair buffer and re-runs on overflow.
+
+        The statistics (and with ``fetch_mask`` the mask) come back through
+        pinned host buffers with asynchronous copies behind the frame."""
         with self._lock:
             for _ in range(4):
                 keep = self.enqueue(cam, levels, out, **kw)
-                out._host = None
-                st = out.host_stats()[0]
+                hi = torch.empty(out.stats_i64.shape, dtype=out.stats_i64.dtype, pin_memory=True)
+                hf = torch.empty(out.stats_f64.shape, dtype=out.stats_f64.dtype, pin_memory=True)
+                hi.copy_(out.stats_i64, non_blocking=True)
+                hf.copy_(out.stats_f64, non_blocking=True)
+                if fetch_mask and out.mask is not None:
+                    hm = torch.empty(out.mask.shape, dtype=out.mask.dtype, pin_memory=True)
+                    hm.copy_(out.mask, non_blocking=True)
+                    out.mask_host = hm
+                torch.cuda.current_stream().synchronize()
+                out._host = (hi.numpy(), hf.numpy())
+                st = out._host[0]
                 del keep
                 if int(st[N.STAT_OVERFLOW]) == 0:
                     return out

@@ -295,7 +295,7 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
     eng = ds.engine
     out = eng.allocate(W, H, levels, coeff_map=need_cmap, features=eager, query=True)
     spec = QuerySpec(query.vector, canon, window, fixed, threshold)
-    eng.run(cam, levels, out, query=spec, timing=instrument)
+    eng.run(cam, levels, out, query=spec, timing=instrument, fetch_mask=True)
     st_i, st_f = out.host_stats()
     timings = None
     if instrument:
@@ -305,7 +305,7 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
                               dev=out.relevancy_filtered[b]) for b, lv in enumerate(levels))
     chosen_b = int(st_i[N.STAT_LEVEL])
     point = (int(st_i[N.STAT_ROW]), int(st_i[N.STAT_COL]))
-    mask = out.mask.cpu().numpy().astype(bool)
+    mask = out.mask_host.numpy().view(np.bool_)  # 0/1 bytes; the pinned buffer is this call's own
 
     if need_cmap:
         cm = CoefficientMap(L=cfg.L, K=cfg.K, levels=levels, dev=out.coeff_map)

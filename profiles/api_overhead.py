@@ -30,7 +30,7 @@ print(f'per call {1e3*tot/n:.2f} ms')
 for k, v in T.items(): print(f'  {k}: {1e3*v/n:.2f} ms')
 # device-only frame for comparison
 eng = device.device_scene(scene).engine
-out = eng.allocate(1440, 1080, (0,1,2), coeff_map=True, features=True, query=True)
+out = eng.allocate(1440, 1080, (0,1,2), coeff_map=False, features=True, query=True)
 spec = device.QuerySpec(qv, canon, 11, -1, 0.5)
 qdev = (torch.from_numpy(qv).cuda(), torch.from_numpy(canon).cuda())
 torch.cuda.synchronize(); t0 = time.perf_counter()
