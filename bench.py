@@ -43,9 +43,13 @@ CONFIGS = {
 # profiles/r01_launches_latest.csv: preprocess, CUB onesweep depth sort (10),
 # rank_of_row, count, tile scan, emit, 3 tile-sort kernels, project codebook,
 # blend, blend fixup, 3 x (codebook split + tcgen05 decode), 2 x box filter,
-# reduce, finalize, mask.  With the decode fused into the blend the 3 x
-# (split + decode) launches become one codebook-image launch (27 per frame).
+# reduce, finalize, mask.
 KERNELS_PER_FRAME = 32
+# With the decode fused into the blend (profiles/r01_launches_fused.csv): preprocess,
+# CUB onesweep depth sort (10), rank_of_row, count, tile scan, emit, 3 tile-sort
+# kernels, project codebook, blend (+ decode), fixup, 2 x box filter, reduce,
+# finalize, mask (the codebook image is cached per level selection).
+KERNELS_PER_FRAME_FUSED = 26
 
 
 def ncu_traffic(kernel: str = "decode", summary: str = "r01_ncu_summary.txt"):
@@ -454,7 +458,7 @@ def main():
                          "traffic": traffic, "traffic_source": traffic_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": (KERNELS_PER_FRAME - 5 if fused else KERNELS_PER_FRAME) * args.steps,
+            "gpu_launches": (KERNELS_PER_FRAME_FUSED if fused else KERNELS_PER_FRAME) * args.steps,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
