@@ -86,6 +86,23 @@ class CameraPose:
         return Camera.look_at(self.position, self.look_at, self.up, fov_y_deg=self.fov_y_deg,
                               width=self.width, height=self.height, near=self.near)
 
+    def to_dict(self) -> dict:
+        """JSON form (projection.py:124-133)."""
+        return {"position": list(self.position), "look_at": list(self.look_at), "up": list(self.up),
+                "fov_y_deg": self.fov_y_deg, "width": self.width, "height": self.height, "near": self.near}
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "CameraPose":
+        """projection.py:135-148; missing / malformed fields raise ValidationError."""
+        try:
+            vec = lambda v: tuple(float(x) for x in v)  # noqa: E731
+            return cls(position=vec(d["position"]), look_at=vec(d["look_at"]),
+                       up=vec(d.get("up", (0.0, 1.0, 0.0))), fov_y_deg=float(d.get("fov_y_deg", 50.0)),
+                       width=int(d.get("width", 64)), height=int(d.get("height", 64)),
+                       near=float(d.get("near", 0.01)))
+        except (KeyError, TypeError, ValueError) as exc:
+            raise ValidationError(f"bad camera pose: {exc}") from exc
+
 
 @dataclass(frozen=True)
 class ProjectedGaussian:

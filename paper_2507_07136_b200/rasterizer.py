@@ -94,7 +94,7 @@ def _resolve_channels(scene, channels):
 def render_dense(scene, cam, channels="color", *, tag: str | None = None,
                  tile_size: int = DEFAULT_TILE_SIZE, early_exit: bool = True, background=None,
                  max_elements: int = DEFAULT_MAX_RENDER_ELEMENTS, workers: int = 1,
-                 with_stats: bool = False):
+                 with_stats: bool = False, engine=None):
     """Dense render of per-Gaussian channel vectors (rasterizer.py:206-272) on the GPU.
 
     The sm_100a blend kernel runs with a dense scatter plan -- Gaussian g adds
@@ -123,7 +123,7 @@ def render_dense(scene, cam, channels="color", *, tag: str | None = None,
     if tile_size != DEFAULT_TILE_SIZE:
         raise ValidationError("the sm_100a kernels are specialised for 16x16 tiles")
     ds = device_scene(scene)
-    eng = ds.engine
+    eng = ds.engine if engine is None else engine
     dev = ds.device
     g = ds.num_gaussians
     vals = values if (ds.orig_rows is None or device_rows) else values[ds.orig_rows.cpu().numpy()]

@@ -252,7 +252,7 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
                    level: int | None = None, tile_size: int = DEFAULT_TILE_SIZE, workers: int = 1,
                    instrument: bool = True, threshold: float = 0.5,
                    features: str = "lazy",
-                   max_elements: int = DEFAULT_MAX_RENDER_ELEMENTS) -> QueryResult:
+                   max_elements: int = DEFAULT_MAX_RENDER_ELEMENTS, engine=None) -> QueryResult:
     """Fused multilevel splat -> decode -> post-process (sparse_splat.py:243-297).
 
     One ``sf_render_frame``: the blend kernel also computes the per-level
@@ -261,7 +261,9 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
     so the 512-d features are decoded only when asked for
     (``features="eager"`` decodes them inside the timed frame).
     ``max_elements`` (extension, default = the reference's fixed budget) lets
-    configurations above 2^27 coefficient elements run.
+    configurations above 2^27 coefficient elements run; ``engine`` (extension)
+    runs the frame on a given FrameEngine (its own workspace) on the current
+    stream, so concurrent requests need not serialise on the scene's engine.
     """
     from .device import QuerySpec, device_scene
     cfg = scene.config
@@ -292,7 +294,7 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
     eager = features == "eager"
     fused = bool(N.load().sf_decode_fused(len(levels), cfg.L, cfg.K, cfg.D))
     need_cmap = (eager and not fused) or len(levels) * cfg.L > 192
-    eng = ds.engine
+    eng = ds.engine if engine is None else engine  # serve.py: one engine + stream per concurrent request
     out = eng.allocate(W, H, levels, coeff_map=need_cmap, features=eager, query=True)
     spec = QuerySpec(query.vector, canon, window, fixed, threshold)
     eng.run(cam, levels, out, query=spec, timing=instrument, fetch_mask=True)
