@@ -47,9 +47,9 @@ CONFIGS = {
 KERNELS_PER_FRAME = 32
 # With the decode fused into the blend (profiles/r01_launches_fused.csv): preprocess,
 # CUB onesweep depth sort (10), rank_of_row, count, tile scan, emit, 3 tile-sort
-# kernels, project codebook, blend (+ decode), fixup, 2 x box filter, reduce,
+# kernels, project codebook, blend (+ decode), fixup, fused box filter + statistics,
 # finalize, mask (the codebook image is cached per level selection).
-KERNELS_PER_FRAME_FUSED = 26
+KERNELS_PER_FRAME_FUSED = 24
 
 
 def ncu_traffic(kernel: str = "decode", summary: str = "r01_ncu_summary.txt"):

@@ -281,7 +281,10 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
     }
     if (f->events[2]) cudaEventRecord((cudaEvent_t)f->events[2], st);
     // K8-K10
-    if (q) {
+    if (q && filter_select_fusable(q->window)) {
+        launch_filter_select(f->n_levels, H, W, f->relevancy_raw, q->window, f->relevancy_filtered,
+                             q->fixed_level, q->threshold, f->mask, ws.stats, ws.stats_f, ws.sel_ws, st, oy0, oy1);
+    } else if (q) {
         launch_mean_filter(f->n_levels, H, W, f->relevancy_raw, q->window, ws.filter_tmp,
                            f->relevancy_filtered, st, oy0, oy1);
         launch_select_segment(f->n_levels, H, W, f->relevancy_filtered, q->fixed_level, q->threshold,

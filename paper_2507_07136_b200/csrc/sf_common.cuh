@@ -304,6 +304,11 @@ size_t select_segment_ws_bytes(int n_maps, int H, int W);
 void launch_select_segment(int n_maps, int H, int W, const double* maps, int fixed_level,
                            double threshold, uint8_t* mask, int64_t* stats_i64,
                            double* stats_f64, void* ws, cudaStream_t st, int y0 = 0, int y1 = 0);
+// fused mean filter + selection statistics + mask (window / 2 <= 8)
+bool filter_select_fusable(int window);
+void launch_filter_select(int n_maps, int H, int W, const double* raw, int window, double* filtered,
+                          int fixed_level, double threshold, uint8_t* mask, int64_t* stats_i64,
+                          double* stats_f64, void* ws, cudaStream_t st, int y0 = 0, int y1 = 0);
 void launch_mask_rows(int H, int W, const double* maps, int level, double lo, double hi, double threshold,
                       int y0, int y1, uint8_t* mask, cudaStream_t st);
 

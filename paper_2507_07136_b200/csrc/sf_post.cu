@@ -244,8 +244,122 @@ void launch_mask_rows(int H, int W, const double* maps, int level, double lo, do
     if (i1 > i0) k_mask_rows<<<ceil_div(i1 - i0, 256), 256, 0, st>>>(hw, maps, level, lo, hi, threshold, mask, i0, i1);
 }
 
+// Fused mean filter + selection statistics: one CTA per 64 x 16 output tile
+// of one map.  The edge-clamped input tile (+ r halo) is staged in shared
+// memory; row sums then column sums are taken in exactly k_box_rows /
+// k_box_cols's order (bitwise the same filtered values), and the CTA's
+// max / first argmax / min over its owned pixels go to the partials that
+// k_finalize_select reduces -- the filtered maps are written once, never
+// re-read for the statistics.
+// k_finalize_select for many partials: the whole CTA reduces one map at a time
+__global__ void __launch_bounds__(1024) k_finalize_select_wide(int n_maps, int nblk, int W,
+                                                               const MaxMin* __restrict__ partial, int fixed_level,
+                                                               int64_t* stats_i64, double* stats_f64) {
+    typedef cub::BlockReduce<MaxMin, 1024> Red;
+    __shared__ typename Red::TempStorage tmp;
+    __shared__ MaxMin per_map[kMaxLevels];
+    struct Op {
+        __device__ MaxMin operator()(const MaxMin& a, const MaxMin& b) const { return mm_combine(a, b); }
+    };
+    for (int m = 0; m < n_maps; ++m) {
+        MaxMin acc{-INFINITY, INT64_MAX, INFINITY};
+        for (int b = threadIdx.x; b < nblk; b += blockDim.x) acc = mm_combine(acc, partial[(size_t)m * nblk + b]);
+        const MaxMin r = Red(tmp).Reduce(acc, Op());
+        if (threadIdx.x == 0) per_map[m] = r;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        int lvl = fixed_level;
+        if (lvl < 0) {
+            lvl = 0;
+            for (int m = 1; m < n_maps; ++m)
+                if (per_map[m].mx > per_map[lvl].mx) lvl = m;  // ties -> lowest level
+        }
+        const MaxMin c = per_map[lvl];
+        stats_i64[SF_STAT_LEVEL] = lvl;
+        stats_i64[SF_STAT_ROW] = c.idx / W;
+        stats_i64[SF_STAT_COL] = c.idx % W;
+        stats_i64[SF_STAT_DEGENERATE] = (c.mx <= c.mn) ? 1 : 0;
+        stats_f64[SF_STATF_MIN] = c.mn;
+        stats_f64[SF_STATF_MAX] = c.mx;
+        for (int m = 0; m < n_maps; ++m) {
+            stats_f64[SF_STATF_LEVEL_MAX + m] = per_map[m].mx;
+            stats_f64[SF_STATF_LEVEL_MAX + n_maps + m] = per_map[m].mn;
+            stats_i64[SF_STAT_LEVEL_ARGMAX + m] = per_map[m].idx;
+        }
+    }
+}
+
+constexpr int kBoxTX = 64, kBoxTY = 16, kBoxRMax = 8;
+__global__ void __launch_bounds__(256) k_box2d_stats(int H, int W, const double* __restrict__ in, int r,
+                                                     double area, double* __restrict__ out,
+                                                     MaxMin* __restrict__ partial, int y0, int y1) {
+    __shared__ double tin[kBoxTY + 2 * kBoxRMax][kBoxTX + 2 * kBoxRMax];
+    __shared__ double trs[kBoxTY + 2 * kBoxRMax][kBoxTX];
+    const int m = blockIdx.z;
+    const int x0 = blockIdx.x * kBoxTX, ty0 = y0 + blockIdx.y * kBoxTY;
+    const int64_t hw = (int64_t)H * W;
+    const double* src = in + (size_t)m * hw;
+    const int nr = kBoxTY + 2 * r, nc = kBoxTX + 2 * r;
+    for (int i = threadIdx.x; i < nr * nc; i += blockDim.x) {
+        const int rr = i / nc, cc = i - rr * nc;
+        const int yy = min(max(ty0 - r + rr, 0), H - 1), xx = min(max(x0 - r + cc, 0), W - 1);
+        tin[rr][cc] = src[(int64_t)yy * W + xx];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr * kBoxTX; i += blockDim.x) {
+        const int rr = i / kBoxTX, x = i - rr * kBoxTX;
+        double acc = 0.0;
+        for (int d = -r; d <= r; ++d) acc += tin[rr][x + r + d];
+        trs[rr][x] = acc;
+    }
+    __syncthreads();
+    MaxMin best{-INFINITY, INT64_MAX, INFINITY};
+    for (int i = threadIdx.x; i < kBoxTY * kBoxTX; i += blockDim.x) {
+        const int yl = i / kBoxTX, x = i - yl * kBoxTX;
+        const int y = ty0 + yl, gx = x0 + x;
+        if (y >= y1 || gx >= W) continue;
+        double acc = 0.0;
+        for (int d = -r; d <= r; ++d) acc += trs[yl + r + d][x];
+        const double v = acc / area;
+        const int64_t idx = (int64_t)y * W + gx;
+        out[(size_t)m * hw + idx] = v;
+        best = mm_combine(best, MaxMin{v, idx, v});
+    }
+    typedef cub::BlockReduce<MaxMin, 256> Red;
+    __shared__ typename Red::TempStorage tmp;
+    struct Op {
+        __device__ MaxMin operator()(const MaxMin& a, const MaxMin& b) const { return mm_combine(a, b); }
+    };
+    const MaxMin rsum = Red(tmp).Reduce(best, Op());
+    if (threadIdx.x == 0)
+        partial[(size_t)m * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = rsum;
+}
+
+static int box_tiles(int H, int W) { return ceil_div(W, kBoxTX) * ceil_div(H, kBoxTY); }
+
 size_t select_segment_ws_bytes(int n_maps, int H, int W) {
-    return sizeof(MaxMin) * (size_t)kRedBlocks * (size_t)n_maps + 256;
+    const size_t nblk = (size_t)(box_tiles(H, W) > kRedBlocks ? box_tiles(H, W) : kRedBlocks);
+    return sizeof(MaxMin) * nblk * (size_t)n_maps + 256;
+}
+
+bool filter_select_fusable(int window) { return window > 1 && window / 2 <= kBoxRMax; }
+
+void launch_filter_select(int n_maps, int H, int W, const double* raw, int window, double* filtered,
+                          int fixed_level, double threshold, uint8_t* mask, int64_t* stats_i64,
+                          double* stats_f64, void* ws, cudaStream_t st, int y0, int y1) {
+    if (y1 <= y0) y0 = 0, y1 = H;
+    if (y1 <= y0 || W == 0) return;
+    const int r = window / 2;
+    MaxMin* partial = (MaxMin*)ws;
+    dim3 grid(ceil_div(W, kBoxTX), ceil_div(y1 - y0, kBoxTY), n_maps);
+    k_box2d_stats<<<grid, 256, 0, st>>>(H, W, raw, r, (double)window * (double)window, filtered, partial, y0, y1);
+    k_finalize_select_wide<<<1, 1024, 0, st>>>(n_maps, (int)(grid.x * grid.y), W, partial, fixed_level, stats_i64,
+                                                stats_f64);
+    const int64_t hw = (int64_t)H * W, i0 = (int64_t)y0 * W, i1 = (int64_t)y1 * W;
+    if (mask && i1 > i0)
+        k_mask<<<ceil_div(i1 - i0, 256), 256, 0, st>>>(hw, filtered, stats_i64, stats_f64, threshold, mask, i0,
+                                                       i1);
 }
 
 void launch_select_segment(int n_maps, int H, int W, const double* maps, int fixed_level,
