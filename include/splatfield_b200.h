@@ -112,6 +112,13 @@ typedef struct SfFrame {
     /* optional cached codebook image of host_levels for the fused decode
      * (sf_pack_decode_image); NULL = built inside the frame */
     const void* dec_image;
+    /* Training backward (train.py:324-330): when grad_coeff_map (dL/dW,
+     * (H,W,n_levels*L) fp32) is set, the frame runs the transpose of the splat
+     * instead of the blend -- grad_values (n_levels, G, K) fp32 (zero it first)
+     * receives sum_p e(p) dL/dW[p][channel] for every Gaussian's K entries per
+     * level -- and nothing after it. */
+    const float* grad_coeff_map;
+    float* grad_values;
 } SfFrame;
 
 /* stats_i64 slots */

@@ -167,8 +167,46 @@ def io_fixtures():
     return made
 
 
+def train_fixtures():
+    """forward_loss + backward (train.py:201-344) on a small scene: loss, dL/dlogits,
+    dL/datoms, with a validity mask and the cosine term, and without either."""
+    from splatfield import train as RT
+    made = []
+    for name, (cosw, use_mask) in (("train_s8", (0.5, True)), ("train_s9", (0.0, False))):
+        rng = np.random.default_rng(1008 if use_mask else 1009)
+        sc = random_scene(rng, num_gaussians=300, num_levels=2, L=8, K=2, D=8)
+        cam = camera(40, 32)
+        fld = RT.TrainableField(logits=rng.standard_normal((2, 300, 8)),
+                                codebooks=rng.standard_normal((2, 8, 8)))
+        targets = rng.standard_normal((2, 32, 40, 8))
+        mask = rng.random((32, 40)) > 0.2 if use_mask else None
+        batch = RT.TrainingBatch(camera=cam, targets=targets, mask=mask)
+        cfg = RT.TrainConfig(cosine_weight=cosw)
+        loss, cache = RT.forward_loss(fld, sc, batch, cfg)
+        grads = RT.backward(cache)
+        d = dict(positions=sc.positions, rotations=sc.rotations, scales=sc.scales, opacities=sc.opacities,
+                 colors=sc.colors, coeff_indices=sc.coeff_indices, coeff_values=sc.coeff_values, ids=sc.ids,
+                 codebooks=np.stack([cb.atoms for cb in sc.codebooks]),
+                 config=np.array([2, 8, 2, 8], dtype=np.int64),
+                 cam_R=cam.rotation, cam_t=cam.translation,
+                 cam_intr=np.array([cam.fx, cam.fy, cam.cx, cam.cy, cam.near]),
+                 cam_size=np.array([cam.width, cam.height], dtype=np.int64),
+                 t_logits=fld.logits, t_codebooks=fld.codebooks, t_targets=targets,
+                 t_mask=mask if mask is not None else np.zeros(0, bool), t_cosine=np.float64(cosw),
+                 t_loss=np.float64(loss), t_grad_logits=grads.logits, t_grad_codebooks=grads.codebooks,
+                 t_coeff_maps=cache.coeff_maps)
+        path = os.path.join(OUT, name + ".npz")
+        np.savez_compressed(path, **d)
+        made.append((path, os.path.getsize(path)))
+    return made
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--only-train" in sys.argv:
+        for p, sz in train_fixtures():
+            print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
+        return
     if "--only-io" in sys.argv:
         for p, sz in io_fixtures():
             print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
@@ -181,7 +219,7 @@ def main():
         for p, sz in fused_fixtures():
             print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
         return
-    made = fused_fixtures() + dense_fixtures() + io_fixtures()
+    made = fused_fixtures() + dense_fixtures() + io_fixtures() + train_fixtures()
     # 1. reference-test-like scenes (tests/conftest.py distribution)
     for seed, (g, nl, L, K, D, w, h) in enumerate([
         (50, 1, 16, 4, 8, 32, 32),

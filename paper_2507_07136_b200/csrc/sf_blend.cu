@@ -1248,6 +1248,107 @@ static int make_feature_map(CUtensorMap* map, float* f, int D, int W, int H, int
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+// Transpose of the splat (train.py:324-330, the blend weights being constants
+// of the coefficient optimisation):
+//     ghat[b][row][k] = sum over pixels p of e_row(p) * dL/dW[p][b L + idx_bk]
+// One 128-thread CTA per half tile, thread = pixel.  The tile's dL/dW rows sit
+// in shared memory as dw[channel][pixel]; the list streams through in
+// batches of 32 records; each warp walks its candidates (patch culling as in
+// k_blend), recomputes alpha / T / e with the blend's rule, and reduces
+// e * dW over its 32 pixels with shuffles into per-batch shared sums, which
+// are added to ghat once per CTA and record.
+constexpr int kTrBatch = 32;
+__global__ void __launch_bounds__(128) k_splat_transpose(BlendArgs A, const float* __restrict__ dW,
+                                                         float* __restrict__ ghat, int K, int64_t G) {
+    extern __shared__ __align__(16) unsigned char smem_tr[];
+    const int n_ch = A.n_ch, C = A.C;
+    const int cs = chan_rec_bytes(C), voff = chan_val_offset(C);
+    float* dw = reinterpret_cast<float*>(smem_tr);                                   // [n_ch][kAccPitch]
+    GeomF32* g = reinterpret_cast<GeomF32*>(smem_tr + acc_bytes(n_ch));              // [32]
+    uint32_t* rows = reinterpret_cast<uint32_t*>(g + kTrBatch);                      // [32]
+    unsigned char* rec = reinterpret_cast<unsigned char*>(rows + kTrBatch);          // [32][cs]
+    float* gsum = reinterpret_cast<float*>(rec + kTrBatch * cs);                     // [32][C]
+    const int tile = A.tile0 + (blockIdx.x >> 1), half = blockIdx.x & 1;
+    const int tx = tile % A.tiles_x, ty = tile / A.tiles_x;
+    const int x0 = tx * SF_TILE, y0 = ty * SF_TILE;
+    const int slot = threadIdx.x, lane = slot & 31, cw = slot >> 5;
+    const int warp = half * kConsumerWarps + cw;
+    const int px = x0 + (warp & 1) * 8 + (lane & 7), py = y0 + (warp >> 1) * 4 + (lane >> 3);
+    const bool inside = px < A.W && py < A.H;
+    if (A.stats[SF_STAT_OVERFLOW]) return;
+    for (int i = threadIdx.x; i < kTilePixels * n_ch; i += blockDim.x) {
+        const int sl = i / n_ch, c = i - sl * n_ch;
+        const int w8 = half * kConsumerWarps + (sl >> 5), l8 = sl & 31;
+        const int gx = x0 + (w8 & 1) * 8 + (l8 & 7), gy = y0 + (w8 >> 1) * 4 + (l8 >> 3);
+        dw[c * kAccPitch + sl] = (gx < A.W && gy < A.H) ? dW[((size_t)gy * A.W + gx) * n_ch + c] : 0.f;
+    }
+    const float pxf = (float)px, pyf = (float)py;
+    const double pxd = (double)px, pyd = (double)py;
+    const float pdx0 = (float)(x0 + (warp & 1) * 8), pdy0 = (float)(y0 + (warp >> 1) * 4);
+    float T = 1.f;
+    bool done = !inside;
+    const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
+    for (uint32_t base = beg; base < end; base += kTrBatch) {
+        const int nb = (int)min((uint32_t)kTrBatch, end - base);
+        __syncthreads();  // previous batch flushed
+        for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+            const uint32_t r = A.entries[base + i];
+            rows[i] = r;
+            g[i] = *reinterpret_cast<const GeomF32*>(A.geom + r);
+        }
+        for (int i = threadIdx.x; i < nb * cs / 16; i += blockDim.x) {
+            const int j = i / (cs / 16), q = i - j * (cs / 16);
+            reinterpret_cast<uint4*>(rec + j * cs)[q] =
+                reinterpret_cast<const uint4*>(A.chan + (size_t)A.entries[base + j] * cs)[q];
+        }
+        for (int i = threadIdx.x; i < kTrBatch * C; i += blockDim.x) gsum[i] = 0.f;
+        __syncthreads();
+        uint32_t wmask = __ballot_sync(0xffffffffu, lane < nb && patch_may_hit(g[lane & 31], pdx0, pdy0));
+        if (__all_sync(0xffffffffu, done)) wmask = 0;
+        while (wmask) {
+            const int j = __ffs(wmask) - 1;
+            wmask &= wmask - 1;
+            bool amb = false;
+            float al = blend_alpha_fast(g[j], pxf, pyf, amb);
+            if (amb) al = blend_alpha_exact(g[j], A.geom + rows[j], pxd, pyd);
+            float e = 0.f;
+            if (al > 0.f && !done) {
+                e = al * T;
+                T = fmaf(-al, T, T);
+                if (A.early_exit && T < (float)SF_EARLY_EXIT_T) done = true;
+            }
+            if (!__any_sync(0xffffffffu, e > 0.f)) continue;
+            const uint32_t* words = reinterpret_cast<const uint32_t*>(rec + j * cs);
+            for (int k = 0; k < C; ++k) {
+                float v = e * dw[chan_id(words[k]) * kAccPitch + slot];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) atomicAdd(&gsum[j * C + k], v);
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nb * C; i += blockDim.x) {
+            const int j = i / C, k = i - j * C;
+            const float v = gsum[i];
+            if (v != 0.f) atomicAdd(&ghat[((size_t)(k / K) * G + rows[j]) * K + (k % K)], v);
+        }
+        if (__syncthreads_and(done)) break;
+    }
+}
+
+int launch_splat_transpose(const BlendArgs& a, const float* dW, float* ghat, int K, int64_t G, cudaStream_t st) {
+    if (a.n_ch > kChBlock || a.C > kMaxC || a.C % K) return -1;
+    const int cs = chan_rec_bytes(a.C);
+    const size_t smem = acc_bytes(a.n_ch) + kTrBatch * (sizeof(GeomF32) + 4 + cs + 4 * a.C);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaFuncSetAttribute(k_splat_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    if (a.n_band_tiles > 0) k_splat_transpose<<<2 * a.n_band_tiles, 128, smem, st>>>(a, dW, ghat, K, G);
+    return 0;
+}
+
 // CTA-per-pixel variant of k_blend_fixup (accumulators in one CTA's shared
 // memory, n_ch <= kChBlock): 8 warps take 8 consecutive 32-entry chunks of
 // the list per round, so a long replay takes 1/8 of the sequential chunk

@@ -215,6 +215,25 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
                    ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, ws.cta_base, tr0, tr1, st_prep);
     if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
                                    ws.proj_cb, st_prep);
+    if (f->grad_coeff_map) {
+        // training backward: transpose of the splat over the same tile lists
+        if (!f->grad_values) return fail(SF_ERR_VALIDATION, "grad_values buffer required");
+        if (st_prep != st) {
+            cudaEventRecord(handoff, st_prep);
+            cudaStreamWaitEvent(st, handoff, 0);
+        }
+        BlendArgs t;
+        memset(&t, 0, sizeof(t));
+        t.W = W, t.H = H, t.tiles_x = tiles_x, t.tiles_y = tiles_y;
+        t.tile0 = tr0 * tiles_x, t.n_band_tiles = (tr1 - tr0) * tiles_x;
+        t.n_ch = n_ch, t.C = C, t.early_exit = f->early_exit;
+        t.tile_offsets = ws.tile_offsets, t.entries = ws.entries, t.geom = ws.geom, t.chan = chan;
+        t.stats = ws.stats;
+        if (launch_splat_transpose(t, f->grad_coeff_map, f->grad_values, K, G, st))
+            return fail(SF_ERR_VALIDATION, "transpose splat needs levels*L <= 192 channels");
+        if (f->stats_i64) cudaMemcpyAsync(f->stats_i64, ws.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+        return check_cuda("sf_render_frame (transpose)");
+    }
     // K5/K6 (+ fused relevancy)
     BlendArgs a;
     memset(&a, 0, sizeof(a));

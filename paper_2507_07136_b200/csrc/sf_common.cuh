@@ -279,6 +279,8 @@ struct BlendArgs {
     uint64_t* timeline;         // development aid (SF_BLEND_TIMELINE), normally null
 };
 int launch_blend(const BlendArgs& a, cudaStream_t st);
+// transpose of the splat (training backward): ghat (levels, G, K) += e * dW gathers
+int launch_splat_transpose(const BlendArgs& a, const float* dW, float* ghat, int K, int64_t G, cudaStream_t st);
 // fused decode: supported shape, and the bytes of its codebook image
 bool blend_dec_supported(int n_levels, int L, int K, int D);
 size_t blend_dec_image_bytes(int n_levels, int D);

@@ -25,7 +25,7 @@ def golden_names(require_query=False, require_features=False):
     out = []
     for p in sorted(glob.glob(os.path.join(GOLDEN, "*.npz"))):
         name = os.path.basename(p)[:-4]
-        if name.startswith("config") or name.startswith("dense"):
+        if name.startswith(("config", "dense", "train")):
             continue
         with np.load(p) as z:
             if require_query and "q_filtered" not in z:
