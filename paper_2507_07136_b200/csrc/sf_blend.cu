@@ -897,7 +897,7 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     }
                 }
             }
-            if (lane == 0) bulk_wait<0>();
+            if (lane == 0) bulk_wait_read<0>();  // the boxes may be released once read; the writes complete with the grid
         } else {
             // issuer: the whole producer warp walks the chunk ring; lane 0 issues.
             // Per chunk 3 x 4 MMAs (128 x 64 x 16, fp16 -> fp32, A from TMEM).
