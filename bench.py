@@ -377,7 +377,7 @@ def main():
             dt = float(t.item())
         e2e = {"value": world * n_e2e / dt, "unit": "frames/s",
                "h2d_bytes_per_step": int(qv.nbytes + canon.nbytes),
-               "d2h_bytes_per_step": int(H * W + 16 * 8 + 16 * 8), "steps": n_e2e,
+               "d2h_bytes_per_step": int(H * W + 16 * 8 + (8 + 2 * 8) * 8), "steps": n_e2e,
                "api": "paper_2507_07136_b200.query_pipeline(..., features='eager')"}
 
     # feature-splat FPS (render + decode, no query post) and lazy-feature query FPS
