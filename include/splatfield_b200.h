@@ -180,6 +180,21 @@ int sf_render_frame_split(const SfScene* scene, const SfCamera* cam, const SfQue
                           void* stream_prepare, void* stream_render, void* handoff_event);
 
 /*
+ * A sweep of text prompts over one frame (BASELINE config E): the
+ * coefficient map is rendered once (frame->coeff_map required; frame must
+ * carry no features), then every prompt gets the query_pipeline post --
+ * relevancy from the map through the projected codebook (fp64), mean filter,
+ * select_level / localize / segment with an automatic level.
+ *   prompts (n_prompts, D) fp64; relevancy_filtered (n_prompts, n_levels, H, W)
+ *   fp64; masks (n_prompts, H, W) u8; stats_i64 (n_prompts, 16) and stats_f64
+ *   (n_prompts, 8 + 2 n_levels) laid out like SfFrame's.
+ */
+int sf_query_sweep(const SfScene* scene, const SfCamera* cam, const SfFrame* frame, const double* prompts,
+                   int32_t n_prompts, const double* canonicals, int32_t n_canonicals, int32_t window,
+                   double threshold, double* relevancy_filtered, uint8_t* masks, int64_t* stats_i64,
+                   double* stats_f64, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * project_scene, projection.py:240-315: the same surviving set, in scene-row
  * order, with bitwise-identical fp64 values.  Outputs sized for G rows;
  * *count_out (device int64) receives N.  inv_covs is (N,2,2).

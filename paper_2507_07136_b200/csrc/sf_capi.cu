@@ -323,6 +323,52 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
                         nullptr);
 }
 
+extern "C" int sf_query_sweep(const SfScene* s, const SfCamera* cam, const SfFrame* f, const double* prompts,
+                              int32_t n_prompts, const double* canon, int32_t n_canon, int32_t window,
+                              double threshold, double* filtered, uint8_t* masks, int64_t* stats_i64,
+                              double* stats_f64, void* workspace, size_t workspace_bytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!f || !f->coeff_map || f->features || f->grad_coeff_map)
+        return fail(SF_ERR_VALIDATION, "a sweep renders a coefficient map (and no features)");
+    if (n_prompts < 0 || (n_prompts > 0 && (!prompts || !filtered || !stats_i64 || !stats_f64)))
+        return fail(SF_ERR_VALIDATION, "bad prompt buffers");
+    if (n_canon < 1 || n_canon > kMaxCanon) return fail(SF_ERR_VALIDATION, "1..%d canonicals required", kMaxCanon);
+    if (window < 1 || window % 2 == 0) return fail(SF_ERR_VALIDATION, "filter window must be odd and >= 1");
+    if (f->band_y0 != 0 || f->band_y1 != 0) return fail(SF_ERR_VALIDATION, "sweeps render the whole image");
+    int rc = render_frame(s, cam, nullptr, f, workspace, workspace_bytes, st, st, nullptr);
+    if (rc) return rc;
+    const int W = cam->width, H = cam->height, L = s->L, D = s->D, nl = f->n_levels;
+    FrameWs ws;
+    carve_frame(workspace, workspace_bytes, s->num_gaussians, W, H, nl, L, s->K, D, f->pair_capacity, &ws);
+    LevelSelDev lv;
+    lv.n = nl;
+    for (int b = 0; b < nl; ++b) lv.lv[b] = f->host_levels[b];
+    const int64_t hw = (int64_t)W * H;
+    // raw relevancy: the frame's buffer when given, else the row-sum buffer
+    // (free when the filter is fused with selection)
+    if (!filter_select_fusable(window) && !f->relevancy_raw)
+        return fail(SF_ERR_VALIDATION, "windows above 17 need frame->relevancy_raw");
+    double* raw = f->relevancy_raw ? f->relevancy_raw : ws.filter_tmp;
+    for (int i = 0; i < n_prompts; ++i) {
+        launch_project_codebook(s->codebooks, lv, L, D, prompts + (size_t)i * D, canon, n_canon, ws.proj_cb, st);
+        launch_relevancy_from_cmap(hw, nl * L, f->coeff_map, ws.proj_cb, nl, L, n_canon, raw, hw, st);
+        double* fi = filtered + (size_t)i * nl * hw;
+        uint8_t* mi = masks ? masks + (size_t)i * hw : nullptr;
+        int64_t* si = stats_i64 + (size_t)i * 16;
+        double* sf = stats_f64 + (size_t)i * (8 + 2 * nl);
+        // each prompt starts from the frame's counters, as a single query would
+        cudaMemcpyAsync(si, ws.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(sf, ws.stats_f, (8 + 2 * nl) * sizeof(double), cudaMemcpyDeviceToDevice, st);
+        if (filter_select_fusable(window)) {
+            launch_filter_select(nl, H, W, raw, window, fi, -1, threshold, mi, si, sf, ws.sel_ws, st);
+        } else {
+            launch_mean_filter(nl, H, W, raw, window, ws.filter_tmp, fi, st);
+            launch_select_segment(nl, H, W, fi, -1, threshold, mi, si, sf, ws.sel_ws, st);
+        }
+    }
+    return check_cuda("sf_query_sweep");
+}
+
 extern "C" int sf_render_frame_split(const SfScene* s, const SfCamera* cam, const SfQuery* q, const SfFrame* f,
                                      void* workspace, size_t workspace_bytes, void* stream_prepare,
                                      void* stream_render, void* handoff_event) {

@@ -384,6 +384,57 @@ class FrameEngine:
             raise SplatfieldError("pair buffer overflow persisted after growing")
 
 
+    def sweep(self, cam, levels, out: FrameOutputs, prompts: np.ndarray, canonicals: np.ndarray, *,
+              window: int = 11, threshold: float = 0.5):
+        """Render ``out.coeff_map`` once, then run the query post of every
+        prompt over it (sf_query_sweep); returns device tensors
+        (filtered (n, levels, H, W) fp64, masks (n, H, W) u8, stats_i64 (n, 16),
+        stats_f64 (n, 8 + 2 levels)) and the host statistics, after one sync."""
+        cfg = self.ds.config
+        dev = self.ds.device
+        n, nl = int(prompts.shape[0]), len(levels)
+        W, H = int(cam.width), int(cam.height)
+        hp = torch.from_numpy(np.ascontiguousarray(prompts, dtype=np.float64)).pin_memory()
+        hc = torch.from_numpy(np.ascontiguousarray(canonicals, dtype=np.float64)).pin_memory()
+        filt = torch.empty((n, nl, H, W), dtype=torch.float64, device=dev)
+        masks = torch.empty((n, H, W), dtype=torch.uint8, device=dev)
+        si = torch.empty((max(n, 1), 16), dtype=torch.int64, device=dev)
+        sf = torch.empty((max(n, 1), 8 + 2 * nl), dtype=torch.float64, device=dev)
+        camc = camera_struct(cam)
+        lv = (ctypes.c_int32 * nl)(*[int(x) for x in levels])
+        lib = N.load()
+        with self._lock:
+            for _ in range(4):
+                qd, cd = hp.to(dev, non_blocking=True), hc.to(dev, non_blocking=True)
+                ws = self.workspace(W, H, nl)
+                fr = N.SfFrame()
+                fr.host_levels = ctypes.cast(lv, ctypes.c_void_p)
+                fr.n_levels = nl
+                fr.early_exit = 1
+                fr.pair_capacity = self.pair_capacity
+                fr.coeff_map = N.ptr(out.coeff_map)
+                fr.final_t = N.ptr(out.final_t)
+                fr.relevancy_raw = N.ptr(out.relevancy_raw)
+                fr.stats_i64 = N.ptr(out.stats_i64)
+                fr.stats_f64 = N.ptr(out.stats_f64)
+                if nl * cfg.K <= 16:
+                    fr.chan_by_row = N.ptr(self.channel_plan(levels))
+                N.check(lib.sf_query_sweep(ctypes.byref(self.ds.struct), ctypes.byref(camc), ctypes.byref(fr),
+                                           N.ptr(qd), n, N.ptr(cd), int(canonicals.shape[0]), int(window),
+                                           float(threshold), N.ptr(filt), N.ptr(masks), N.ptr(si), N.ptr(sf),
+                                           N.ptr(ws), ws.numel(), stream_ptr()))
+                hsi = torch.empty(si.shape, dtype=si.dtype, pin_memory=True)
+                hsf = torch.empty(sf.shape, dtype=sf.dtype, pin_memory=True)
+                hsi.copy_(si, non_blocking=True)
+                hsf.copy_(sf, non_blocking=True)
+                fst = out.stats_i64.cpu().numpy()  # synchronises the stream
+                if int(fst[N.STAT_OVERFLOW]) == 0:
+                    out._host = (fst, out.stats_f64.cpu().numpy())
+                    return filt, masks, hsi.numpy()[:n], hsf.numpy()[:n]
+                self.pair_capacity = int(int(fst[N.STAT_PAIRS]) * 1.25) + 1024
+            raise SplatfieldError("pair buffer overflow persisted after growing")
+
+
 class FramePipeline:
     """Frames of one scene overlapped on the GPU: frame i's projection / sort /
     binning run on a shared prepare stream and its blend (+ decode) / post on

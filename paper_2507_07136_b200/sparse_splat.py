@@ -329,3 +329,63 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
                       point=point, timings=timings, cmap_thunk=cmap_thunk, features=fms, mask=mask,
                       degenerate=bool(st_i[N.STAT_DEGENERATE]))
     return res
+
+
+def query_sweep(scene, cam, queries, canonicals, *, window: int = 11, threshold: float = 0.5,
+                tile_size: int = DEFAULT_TILE_SIZE,
+                max_elements: int = DEFAULT_MAX_RENDER_ELEMENTS, engine=None) -> list:
+    """Many text prompts over one view (BASELINE config E; extension).
+
+    The reference answers each prompt with its own query_pipeline call
+    (sparse_splat.py:243-297), re-rendering the frame every time.  Here the
+    multilevel coefficient map is rendered once and every prompt runs only
+    its post: relevancy from the map through its projected codebook (fp64),
+    mean filter, select_level / localize / segment (sf_query_sweep).  Each
+    returned QueryResult equals query_pipeline(scene, cam, q, canonicals,
+    window=window, threshold=threshold) for its prompt (automatic level;
+    timings None)."""
+    from .device import device_scene
+    cfg = scene.config
+    W, H = int(cam.width), int(cam.height)
+    levels = tuple(range(cfg.num_levels))
+    if tile_size != DEFAULT_TILE_SIZE:
+        raise ValidationError("the sm_100a kernels are specialised for 16x16 tiles")
+    queries = list(queries)
+    canon = np.asarray(canonicals, dtype=np.float64)
+    if canon.ndim != 2 or canon.shape[0] < 1:
+        raise ValidationError("at least one canonical D-vector is required")
+    for q in queries:
+        if canon.shape[1] != cfg.D or q.vector.shape[0] != cfg.D:
+            raise ValidationError(
+                f"dimension mismatch: features D={cfg.D}, query D={q.vector.shape[0]}, "
+                f"canonicals D={canon.shape[1]}")
+    if window < 1 or window % 2 == 0:
+        raise ValidationError(f"filter window must be odd and >= 1, got {window}")
+    check_render_budget(W, H, len(levels) * cfg.L, max_elements)
+    ds = device_scene(scene)
+    if ds.bad_index:
+        raise ValidationError("coefficient index >= L")
+    eng = ds.engine if engine is None else engine
+    out = eng.allocate(W, H, levels, coeff_map=True, query=window > 17, mask=False)
+    prompts = np.stack([q.vector for q in queries]) if queries else np.zeros((0, cfg.D))
+    filt, masks, st_i, _ = eng.sweep(cam, levels, out, prompts, canon, window=window, threshold=threshold)
+    host_masks = masks.cpu().numpy().view(np.bool_)
+    cm = CoefficientMap(L=cfg.L, K=cfg.K, levels=levels, dev=out.coeff_map)
+    holder = {}
+
+    def _decode_lazy():
+        if "f" not in holder:
+            holder["f"] = decode(cm, getattr(scene, "host_codebooks", None) or scene.codebooks).dev
+        return holder["f"]
+
+    results = []
+    for i, q in enumerate(queries):
+        maps = tuple(RelevancyMap(query=q.name, level=lv, filtered=True, window=window, dev=filt[i, b])
+                     for b, lv in enumerate(levels))
+        b = int(st_i[i][N.STAT_LEVEL])
+        results.append(QueryResult(
+            query=q.name, level_maps=maps, level=levels[b], chosen=maps[b],
+            point=(int(st_i[i][N.STAT_ROW]), int(st_i[i][N.STAT_COL])), timings=None,
+            cmap_thunk=(lambda cm=cm: cm), features=FeatureMapSet(levels=levels, thunk=_decode_lazy),
+            mask=host_masks[i], degenerate=bool(st_i[i][N.STAT_DEGENERATE])))
+    return results

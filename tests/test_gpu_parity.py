@@ -418,3 +418,28 @@ def test_render_dense_contract(rng):
     empty = random_scene(rng, num_gaussians=0)
     e = sf.render_dense(empty, make_camera(8, 8), "color", background=[0.2, 0.4, 0.6])
     np.testing.assert_allclose(e.data[0, 0], [0.2, 0.4, 0.6])
+
+
+@pytest.mark.parametrize("L,window", [(64, 11), (128, 11), (32, 21)])
+def test_query_sweep_matches_per_prompt_pipelines(rng, L, window):
+    """query_sweep (one render, n prompt posts: sf_query_sweep) gives every
+    prompt the result of its own query_pipeline call and of the oracle."""
+    scene = random_scene(rng, 3000, num_levels=3, L=L, K=4, D=64)
+    cam = make_camera(96, 72)
+    canon = rng.standard_normal((4, 64))
+    queries = [sf.QueryEmbedding(f"q{i}", rng.standard_normal(64)) for i in range(5)]
+    sweep = sf.query_sweep(scene, cam, queries, canon, window=window)
+    assert len(sweep) == 5
+    for q, r in zip(queries, sweep):
+        one = sf.query_pipeline(scene, cam, q, canon, window=window)
+        ores = O.query_pipeline(scene, cam, q.vector, canon, window=window, keep_features=False)
+        for b in range(3):
+            a, e = r.level_maps[b].data, one.level_maps[b].data
+            # fused epilogue vs map pass: fp64 sums of the same fp32 coefficients
+            assert np.abs(a - e).max() <= 1e-12 * max(1.0, np.abs(e).max())
+            assert np.abs(a - ores.level_maps[b]).max() <= R_TOL
+        assert (r.level, r.point) == (one.level, one.point) == (ores.level, ores.point)
+        assert np.count_nonzero(r.mask != one.mask) == 0
+    # the shared coefficient map is the multilevel splat
+    assert np.array_equal(sweep[0].coefficient_map.data, sf.splat_multilevel(scene, cam).data)
+    assert sf.query_sweep(scene, cam, [], canon) == []
