@@ -184,7 +184,9 @@ int sf_render_frame_split(const SfScene* scene, const SfCamera* cam, const SfQue
  * coefficient map is rendered once (frame->coeff_map required; frame must
  * carry no features), then every prompt gets the query_pipeline post --
  * relevancy from the map through the projected codebook (fp64), mean filter,
- * select_level / localize / segment with an automatic level.
+ * select_level / localize / segment with an automatic level.  The map is
+ * read once per 65 - n_canonicals prompts; frame->relevancy_raw is the
+ * (n_prompts, n_levels, H, W) fp64 raw-relevancy buffer.
  *   prompts (n_prompts, D) fp64; relevancy_filtered (n_prompts, n_levels, H, W)
  *   fp64; masks (n_prompts, H, W) u8; stats_i64 (n_prompts, 16) and stats_f64
  *   (n_prompts, 8 + 2 n_levels) laid out like SfFrame's.

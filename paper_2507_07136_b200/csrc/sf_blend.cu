@@ -1062,6 +1062,109 @@ void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const do
                                                             out_stride);
 }
 
+// Relevancy of many prompts over one coefficient map (query sweep).  The map
+// is read once: a CTA (one level: blockIdx.y) stages 256 pixels x L coefficients in
+// shared memory (level-major, pixel-contiguous: conflict-free reads), each
+// thread owns two pixels and forms the fp64 logits l = W . P of 8 columns at a
+// time (8 x 2 independent DFMA chains per coefficient; the P column block is
+// a 64-byte shared broadcast).  Canonical logits first (<= 8, kept in
+// registers), then the prompts; rel = sigmoid(min_j (l_q - l_j)), the
+// two-branch sigmoid of query.py:65-84.  Same value as the single-query
+// Pd = P_q - P_cj form up to rounding (~1e-16 of the logits).
+constexpr int kSwPx = 256, kSwThreads = 128, kSwCols = 8;
+
+__global__ void __launch_bounds__(kSwThreads) k_relevancy_sweep(int64_t P, int n_ch, const float* __restrict__ cmap,
+                                                                const double* __restrict__ proj, int n_levels, int L,
+                                                                int nq, int nc, double* __restrict__ out,
+                                                                int64_t pstride) {
+    extern __shared__ __align__(16) unsigned char sw_smem[];
+    const int nqp = (nq + kSwCols - 1) / kSwCols * kSwCols, nvp = nqp + kSwCols, nv = nq + nc;
+    double* pj = reinterpret_cast<double*>(sw_smem);       // [L][nvp]: prompts, pad, canonicals, pad
+    float* ws = reinterpret_cast<float*>(pj + (size_t)L * nvp);  // [L][kSwPx]
+    const int t = threadIdx.x;
+    const int b = blockIdx.y;  // one level per CTA: its projected codebook is loaded once
+    for (int i = t; i < L * nvp; i += kSwThreads) {
+        const int l = i / nvp, v = i % nvp;
+        const double* src = proj + ((size_t)b * L + l) * nv;
+        pj[i] = v < nq ? src[v] : ((v >= nqp && v - nqp < nc) ? src[nq + v - nqp] : 0.0);
+    }
+    for (int64_t base = (int64_t)blockIdx.x * kSwPx; base < P; base += (int64_t)gridDim.x * kSwPx) {
+        const int np = (int)(P - base < kSwPx ? P - base : kSwPx);
+        {
+            __syncthreads();
+            for (int h = 0; h < kSwPx / kSwThreads; ++h) {
+                const int px = t + h * kSwThreads;
+                if (px >= np) continue;
+                const float4* src = reinterpret_cast<const float4*>(cmap + (size_t)(base + px) * n_ch + b * L);
+#pragma unroll 8
+                for (int k = 0; k < L / 4; ++k) {
+                    const float4 v = __ldg(src + k);
+                    ws[(4 * k + 0) * kSwPx + px] = v.x;
+                    ws[(4 * k + 1) * kSwPx + px] = v.y;
+                    ws[(4 * k + 2) * kSwPx + px] = v.z;
+                    ws[(4 * k + 3) * kSwPx + px] = v.w;
+                }
+            }
+            __syncthreads();
+            auto dots = [&](int c0, double (&acc)[2][kSwCols]) {
+#pragma unroll
+                for (int j = 0; j < kSwCols; ++j) acc[0][j] = acc[1][j] = 0.0;
+#pragma unroll 2
+                for (int l = 0; l < L; ++l) {
+                    const double w0 = ws[l * kSwPx + t], w1 = ws[l * kSwPx + t + kSwThreads];
+                    const double2* pr = reinterpret_cast<const double2*>(pj + (size_t)l * nvp + c0);
+#pragma unroll
+                    for (int j2 = 0; j2 < kSwCols / 2; ++j2) {
+                        const double2 pv = pr[j2];
+                        acc[0][2 * j2] = fma(w0, pv.x, acc[0][2 * j2]);
+                        acc[0][2 * j2 + 1] = fma(w0, pv.y, acc[0][2 * j2 + 1]);
+                        acc[1][2 * j2] = fma(w1, pv.x, acc[1][2 * j2]);
+                        acc[1][2 * j2 + 1] = fma(w1, pv.y, acc[1][2 * j2 + 1]);
+                    }
+                }
+            };
+            double lc[2][kSwCols];
+            dots(nqp, lc);
+            for (int c0 = 0; c0 < nq; c0 += kSwCols) {
+                double lq[2][kSwCols];
+                dots(c0, lq);
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int px = t + r * kSwThreads;
+                    if (px >= np) continue;
+#pragma unroll
+                    for (int j = 0; j < kSwCols; ++j) {
+                        if (c0 + j >= nq) break;
+                        double d = INFINITY;
+#pragma unroll
+                        for (int c = 0; c < kSwCols; ++c)
+                            if (c < nc) d = np_minimum(d, lq[r][j] - lc[r][c]);
+                        out[(size_t)(c0 + j) * pstride + (size_t)b * P + base + px] = sigmoid2(d);
+                    }
+                }
+            }
+        }
+    }
+}
+
+int launch_relevancy_sweep(int64_t P, int n_ch, const float* cmap, const double* proj, int n_levels, int L, int nq,
+                           int n_canon, double* out, int64_t out_prompt_stride, cudaStream_t st) {
+    const int nvp = (nq + kSwCols - 1) / kSwCols * kSwCols + kSwCols;
+    const size_t smem = sizeof(double) * (size_t)L * nvp + sizeof(float) * (size_t)L * kSwPx;
+    if (n_canon < 1 || n_canon > kSwCols || L % 4 || n_ch % 4 || (uintptr_t)cmap % 16 || smem > 200 * 1024)
+        return 1;
+    if (P == 0 || nq == 0) return 0;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_relevancy_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    const int blocks = (int)std::min<int64_t>(ceil_div(P, kSwPx), std::max(1, 148 * 2 / n_levels));  // one wave
+    k_relevancy_sweep<<<dim3(blocks, n_levels), kSwThreads, smem, st>>>(P, n_ch, cmap, proj, n_levels, L, nq, n_canon, out,
+                                                        out_prompt_stride);
+    return 0;
+}
+
 // Exact fp64 replay (rasterizer.py:161-177) of the pixels whose early-exit
 // decision the fp32 transmittance could not certify.  One warp per pixel:
 // lanes evaluate 32 list entries at once in fp64 (reference op order), a

@@ -330,7 +330,7 @@ extern "C" int sf_query_sweep(const SfScene* s, const SfCamera* cam, const SfFra
     cudaStream_t st = (cudaStream_t)stream;
     if (!f || !f->coeff_map || f->features || f->grad_coeff_map)
         return fail(SF_ERR_VALIDATION, "a sweep renders a coefficient map (and no features)");
-    if (n_prompts < 0 || (n_prompts > 0 && (!prompts || !filtered || !stats_i64 || !stats_f64)))
+    if (n_prompts < 0 || (n_prompts > 0 && (!prompts || !filtered || !stats_i64 || !stats_f64 || !f->relevancy_raw)))
         return fail(SF_ERR_VALIDATION, "bad prompt buffers");
     if (n_canon < 1 || n_canon > kMaxCanon) return fail(SF_ERR_VALIDATION, "1..%d canonicals required", kMaxCanon);
     if (window < 1 || window % 2 == 0) return fail(SF_ERR_VALIDATION, "filter window must be odd and >= 1");
@@ -343,26 +343,52 @@ extern "C" int sf_query_sweep(const SfScene* s, const SfCamera* cam, const SfFra
     LevelSelDev lv;
     lv.n = nl;
     for (int b = 0; b < nl; ++b) lv.lv[b] = f->host_levels[b];
-    const int64_t hw = (int64_t)W * H;
-    // raw relevancy: the frame's buffer when given, else the row-sum buffer
-    // (free when the filter is fused with selection)
-    if (!filter_select_fusable(window) && !f->relevancy_raw)
-        return fail(SF_ERR_VALIDATION, "windows above 17 need frame->relevancy_raw");
-    double* raw = f->relevancy_raw ? f->relevancy_raw : ws.filter_tmp;
+    const int64_t hw = (int64_t)W * H, qstride = nl * hw;
+    double* raw = f->relevancy_raw;  // (n_prompts, nl, H, W)
+    // every prompt starts from the frame's counters, as a single query would
     for (int i = 0; i < n_prompts; ++i) {
+        cudaMemcpyAsync(stats_i64 + (size_t)i * 16, ws.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(stats_f64 + (size_t)i * (8 + 2 * nl), ws.stats_f, (8 + 2 * nl) * sizeof(double),
+                        cudaMemcpyDeviceToDevice, st);
+    }
+    // relevancy: the map read once per chunk of prompts (projected-codebook
+    // columns: chunk prompts + canonicals, within proj_cb's 1 + kMaxCanon)
+    const int chunk = kMaxCanon + 1 - n_canon;
+    bool batched = filter_select_fusable(window);
+    for (int i0 = 0; i0 < n_prompts && batched; i0 += chunk) {
+        const int nq = std::min(chunk, n_prompts - i0);
+        launch_project_vectors(s->codebooks, lv, L, D, prompts + (size_t)i0 * D, nq, canon, n_canon, ws.proj_cb, st);
+        if (launch_relevancy_sweep(hw, nl * L, f->coeff_map, ws.proj_cb, nl, L, nq, n_canon, raw + i0 * qstride,
+                                   qstride, st)) {
+            batched = false;  // shape outside the sweep kernel: per-prompt passes below
+        }
+    }
+    if (batched) {
+        // filter + statistics + mask of many prompts per launch; partials in
+        // the row-sum buffer (unused by the fused filter)
+        const size_t per_q = filter_select_batch_ws_bytes(1, nl, H, W) - 256;
+        const size_t cap = sizeof(double) * (size_t)qstride - 256;
+        const int qb = (int)std::max<size_t>(1, std::min<size_t>(n_prompts, cap / per_q));
+        for (int i0 = 0; i0 < n_prompts; i0 += qb) {
+            const int nq = std::min(qb, n_prompts - i0);
+            launch_filter_select_batch(nq, nl, H, W, raw + i0 * qstride, window, filtered + i0 * qstride, threshold,
+                                       masks ? masks + i0 * hw : nullptr, stats_i64 + (size_t)i0 * 16,
+                                       stats_f64 + (size_t)i0 * (8 + 2 * nl), ws.filter_tmp, st);
+        }
+        return check_cuda("sf_query_sweep");
+    }
+    for (int i = 0; i < n_prompts; ++i) {
+        double* ri = raw + i * qstride;
         launch_project_codebook(s->codebooks, lv, L, D, prompts + (size_t)i * D, canon, n_canon, ws.proj_cb, st);
-        launch_relevancy_from_cmap(hw, nl * L, f->coeff_map, ws.proj_cb, nl, L, n_canon, raw, hw, st);
-        double* fi = filtered + (size_t)i * nl * hw;
-        uint8_t* mi = masks ? masks + (size_t)i * hw : nullptr;
+        launch_relevancy_from_cmap(hw, nl * L, f->coeff_map, ws.proj_cb, nl, L, n_canon, ri, hw, st);
+        double* fi = filtered + i * qstride;
+        uint8_t* mi = masks ? masks + i * hw : nullptr;
         int64_t* si = stats_i64 + (size_t)i * 16;
         double* sf = stats_f64 + (size_t)i * (8 + 2 * nl);
-        // each prompt starts from the frame's counters, as a single query would
-        cudaMemcpyAsync(si, ws.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
-        cudaMemcpyAsync(sf, ws.stats_f, (8 + 2 * nl) * sizeof(double), cudaMemcpyDeviceToDevice, st);
         if (filter_select_fusable(window)) {
-            launch_filter_select(nl, H, W, raw, window, fi, -1, threshold, mi, si, sf, ws.sel_ws, st);
+            launch_filter_select(nl, H, W, ri, window, fi, -1, threshold, mi, si, sf, ws.sel_ws, st);
         } else {
-            launch_mean_filter(nl, H, W, raw, window, ws.filter_tmp, fi, st);
+            launch_mean_filter(nl, H, W, ri, window, ws.filter_tmp, fi, st);
             launch_select_segment(nl, H, W, fi, -1, threshold, mi, si, sf, ws.sel_ws, st);
         }
     }

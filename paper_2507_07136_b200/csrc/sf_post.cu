@@ -17,13 +17,13 @@ __device__ __forceinline__ double sigmoid2p(double x) {
     return ex / (1.0 + ex);
 }
 
-// P[b][l][j] = atoms_{lv_b}[l] . v_j, v_0 = query, v_j = canonical j-1 (fp64).
-// One warp per (b, l, j) dot product of length D, shuffle-reduced.
+// P[b][l][j] = atoms_{lv_b}[l] . v_j, v_j = q[j] for j < nq, else canonical
+// j - nq (fp64).  One warp per (b, l, j) dot product of length D, shuffle-reduced.
 __global__ void __launch_bounds__(256) k_project_codebook(const float* __restrict__ cb, LevelSelDev lv, int L, int D,
-                                                          const double* __restrict__ q,
+                                                          const double* __restrict__ q, int nq,
                                                           const double* __restrict__ canon, int n_canon,
                                                           double* __restrict__ out) {
-    const int nv = 1 + n_canon;
+    const int nv = nq + n_canon;
     const int lane = threadIdx.x & 31;
     const int idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int total = lv.n * L * nv;
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) k_project_codebook(const float* __restric
     const int l = (idx / nv) % L;
     const int b = idx / (nv * L);
     const float* a = cb + ((size_t)lv.lv[b] * L + l) * D;
-    const double* v = (j == 0) ? q : canon + (size_t)(j - 1) * D;
+    const double* v = (j < nq) ? q + (size_t)j * D : canon + (size_t)(j - nq) * D;
     double s = 0.0;
     for (int d = lane; d < D; d += 32) s = fma((double)a[d], v[d], s);
 #pragma unroll
@@ -43,8 +43,13 @@ __global__ void __launch_bounds__(256) k_project_codebook(const float* __restric
 void launch_project_codebook(const float* codebooks, const LevelSelDev& lv, int L, int D,
                              const double* q, const double* canon, int n_canon, double* out,
                              cudaStream_t st) {
-    int total = lv.n * L * (1 + n_canon);
-    k_project_codebook<<<ceil_div((int64_t)total * 32, 256), 256, 0, st>>>(codebooks, lv, L, D, q, canon,
+    launch_project_vectors(codebooks, lv, L, D, q, 1, canon, n_canon, out, st);
+}
+
+void launch_project_vectors(const float* codebooks, const LevelSelDev& lv, int L, int D, const double* q, int nq,
+                            const double* canon, int n_canon, double* out, cudaStream_t st) {
+    int total = lv.n * L * (nq + n_canon);
+    k_project_codebook<<<ceil_div((int64_t)total * 32, 256), 256, 0, st>>>(codebooks, lv, L, D, q, nq, canon,
                                                                           n_canon, out);
 }
 
@@ -217,11 +222,17 @@ __global__ void k_finalize_select(int n_maps, int nblk, int W, const MaxMin* __r
     }
 }
 
+// blockIdx.y: query of a batch (maps / statistics / mask of query y at
+// y * (n_maps hw, 16, 8 + 2 n_maps, hw)).
 __global__ void k_mask(int64_t hw, const double* __restrict__ maps, const int64_t* __restrict__ stats_i64,
                        const double* __restrict__ stats_f64, double threshold, uint8_t* __restrict__ mask,
-                       int64_t i0, int64_t i1) {
+                       int64_t i0, int64_t i1, int n_maps = 0) {
     int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= i1) return;
+    maps += (size_t)blockIdx.y * n_maps * hw;
+    stats_i64 += (size_t)blockIdx.y * 16;
+    stats_f64 += (size_t)blockIdx.y * (8 + 2 * n_maps);
+    mask += (size_t)blockIdx.y * hw;
     int lvl = (int)stats_i64[SF_STAT_LEVEL];
     double lo = stats_f64[SF_STATF_MIN], hi = stats_f64[SF_STATF_MAX];
     uint8_t v = 0;
@@ -258,6 +269,10 @@ __global__ void __launch_bounds__(1024) k_finalize_select_wide(int n_maps, int n
     typedef cub::BlockReduce<MaxMin, 1024> Red;
     __shared__ typename Red::TempStorage tmp;
     __shared__ MaxMin per_map[kMaxLevels];
+    // blockIdx.x: query of a batch
+    partial += (size_t)blockIdx.x * n_maps * nblk;
+    stats_i64 += (size_t)blockIdx.x * 16;
+    stats_f64 += (size_t)blockIdx.x * (8 + 2 * n_maps);
     struct Op {
         __device__ MaxMin operator()(const MaxMin& a, const MaxMin& b) const { return mm_combine(a, b); }
     };
@@ -360,6 +375,30 @@ void launch_filter_select(int n_maps, int H, int W, const double* raw, int windo
     if (mask && i1 > i0)
         k_mask<<<ceil_div(i1 - i0, 256), 256, 0, st>>>(hw, filtered, stats_i64, stats_f64, threshold, mask, i0,
                                                        i1);
+}
+
+// n_queries filter + select + mask passes in three launches: raw / filtered
+// (n_queries, n_maps, H, W), masks (n_queries, H, W), statistics
+// (n_queries, 16) / (n_queries, 8 + 2 n_maps); ws holds
+// filter_select_batch_ws_bytes.  Whole images, automatic level.
+size_t filter_select_batch_ws_bytes(int n_queries, int n_maps, int H, int W) {
+    return sizeof(MaxMin) * (size_t)box_tiles(H, W) * n_maps * n_queries + 256;
+}
+
+void launch_filter_select_batch(int n_queries, int n_maps, int H, int W, const double* raw, int window,
+                                double* filtered, double threshold, uint8_t* masks, int64_t* stats_i64,
+                                double* stats_f64, void* ws, cudaStream_t st) {
+    if (n_queries == 0 || W == 0 || H == 0) return;
+    const int r = window / 2;
+    MaxMin* partial = (MaxMin*)ws;
+    dim3 grid(ceil_div(W, kBoxTX), ceil_div(H, kBoxTY), n_maps * n_queries);
+    k_box2d_stats<<<grid, 256, 0, st>>>(H, W, raw, r, (double)window * (double)window, filtered, partial, 0, H);
+    k_finalize_select_wide<<<n_queries, 1024, 0, st>>>(n_maps, (int)(grid.x * grid.y), W, partial, -1, stats_i64,
+                                                       stats_f64);
+    const int64_t hw = (int64_t)H * W;
+    if (masks)
+        k_mask<<<dim3(ceil_div(hw, 256), n_queries), 256, 0, st>>>(hw, filtered, stats_i64, stats_f64, threshold,
+                                                                   masks, 0, hw, n_maps);
 }
 
 void launch_select_segment(int n_maps, int H, int W, const double* maps, int fixed_level,

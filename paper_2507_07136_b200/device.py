@@ -397,6 +397,7 @@ class FrameEngine:
         hp = torch.from_numpy(np.ascontiguousarray(prompts, dtype=np.float64)).pin_memory()
         hc = torch.from_numpy(np.ascontiguousarray(canonicals, dtype=np.float64)).pin_memory()
         filt = torch.empty((n, nl, H, W), dtype=torch.float64, device=dev)
+        raw = torch.empty((n, nl, H, W), dtype=torch.float64, device=dev)
         masks = torch.empty((n, H, W), dtype=torch.uint8, device=dev)
         si = torch.empty((max(n, 1), 16), dtype=torch.int64, device=dev)
         sf = torch.empty((max(n, 1), 8 + 2 * nl), dtype=torch.float64, device=dev)
@@ -414,7 +415,7 @@ class FrameEngine:
                 fr.pair_capacity = self.pair_capacity
                 fr.coeff_map = N.ptr(out.coeff_map)
                 fr.final_t = N.ptr(out.final_t)
-                fr.relevancy_raw = N.ptr(out.relevancy_raw)
+                fr.relevancy_raw = N.ptr(raw)
                 fr.stats_i64 = N.ptr(out.stats_i64)
                 fr.stats_f64 = N.ptr(out.stats_f64)
                 if nl * cfg.K <= 16:

@@ -366,7 +366,7 @@ def query_sweep(scene, cam, queries, canonicals, *, window: int = 11, threshold:
     if ds.bad_index:
         raise ValidationError("coefficient index >= L")
     eng = ds.engine if engine is None else engine
-    out = eng.allocate(W, H, levels, coeff_map=True, query=window > 17, mask=False)
+    out = eng.allocate(W, H, levels, coeff_map=True, mask=False)
     prompts = np.stack([q.vector for q in queries]) if queries else np.zeros((0, cfg.D))
     filt, masks, st_i, _ = eng.sweep(cam, levels, out, prompts, canon, window=window, threshold=threshold)
     host_masks = masks.cpu().numpy().view(np.bool_)

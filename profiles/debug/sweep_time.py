@@ -1,7 +1,7 @@
 """Time query_sweep (one render + n prompt posts, sf_query_sweep) against n
 separate lazy query frames, at a BASELINE config.  Dev aid.
 
-    python profiles/debug/sweep_time.py [E|C] [n_prompts]
+    python profiles/debug/sweep_time.py [E|C] [n_prompts] [once]
 """
 import os
 import sys
@@ -26,6 +26,9 @@ ds = device_scene(scene)
 eng = ds.engine
 levels = (0, 1, 2)
 out = eng.allocate(W, H, levels, coeff_map=True, mask=False)
+if len(sys.argv) > 3 and sys.argv[3] == "once":  # one sweep, for an ncu launch list
+    eng.sweep(cam, levels, out, prompts, canon)
+    sys.exit(0)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for _ in range(2):
     eng.sweep(cam, levels, out, prompts, canon)

@@ -420,26 +420,33 @@ def test_render_dense_contract(rng):
     np.testing.assert_allclose(e.data[0, 0], [0.2, 0.4, 0.6])
 
 
-@pytest.mark.parametrize("L,window", [(64, 11), (128, 11), (32, 21)])
-def test_query_sweep_matches_per_prompt_pipelines(rng, L, window):
-    """query_sweep (one render, n prompt posts: sf_query_sweep) gives every
-    prompt the result of its own query_pipeline call and of the oracle."""
+@pytest.mark.parametrize("L,window,n_prompts,n_canon", [(64, 11, 5, 4), (128, 11, 5, 4), (32, 21, 5, 4),
+                                                       (64, 11, 70, 4), (64, 11, 4, 9)])
+def test_query_sweep_matches_per_prompt_pipelines(rng, L, window, n_prompts, n_canon):
+    """query_sweep (one render, then the prompts' relevancy -- the map read once
+    per 65 - n_canon prompts -- and batched filter / select / mask:
+    sf_query_sweep) gives every prompt its own query_pipeline result.  Covers
+    prompt chunking (70), the per-prompt passes (window 21 > the fused
+    filter's, 9 canonicals > the sweep kernel's 8) and the oracle."""
     scene = random_scene(rng, 3000, num_levels=3, L=L, K=4, D=64)
     cam = make_camera(96, 72)
-    canon = rng.standard_normal((4, 64))
-    queries = [sf.QueryEmbedding(f"q{i}", rng.standard_normal(64)) for i in range(5)]
+    canon = rng.standard_normal((n_canon, 64))
+    queries = [sf.QueryEmbedding(f"q{i}", rng.standard_normal(64)) for i in range(n_prompts)]
     sweep = sf.query_sweep(scene, cam, queries, canon, window=window)
-    assert len(sweep) == 5
-    for q, r in zip(queries, sweep):
+    assert len(sweep) == n_prompts
+    check = range(n_prompts) if n_prompts <= 5 else [0, 7, 60, 61, 69]
+    for i in check:
+        q, r = queries[i], sweep[i]
         one = sf.query_pipeline(scene, cam, q, canon, window=window)
-        ores = O.query_pipeline(scene, cam, q.vector, canon, window=window, keep_features=False)
+        ref = [m.data for m in one.level_maps]
         for b in range(3):
-            a, e = r.level_maps[b].data, one.level_maps[b].data
-            # fused epilogue vs map pass: fp64 sums of the same fp32 coefficients
-            assert np.abs(a - e).max() <= 1e-12 * max(1.0, np.abs(e).max())
-            assert np.abs(a - ores.level_maps[b]).max() <= R_TOL
-        assert (r.level, r.point) == (one.level, one.point) == (ores.level, ores.point)
-        assert np.count_nonzero(r.mask != one.mask) == 0
+            # logit differences vs differences of logits: fp64 rounding only
+            assert np.abs(r.level_maps[b].data - ref[b]).max() <= 1e-12
+        assert_selection_matches(ref, r.level, r.point, r.mask, one.level, one.point)
+        if i < 2:
+            ores = O.query_pipeline(scene, cam, q.vector, canon, window=window, keep_features=False)
+            for b in range(3):
+                assert np.abs(r.level_maps[b].data - ores.level_maps[b]).max() <= R_TOL
     # the shared coefficient map is the multilevel splat
     assert np.array_equal(sweep[0].coefficient_map.data, sf.splat_multilevel(scene, cam).data)
     assert sf.query_sweep(scene, cam, [], canon) == []
