@@ -214,6 +214,7 @@ def main():
     ap.add_argument("--band-rows", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -412,6 +413,32 @@ def main():
         del o, p2
         torch.cuda.empty_cache()
 
+    # config E's prompt sweep: 32 prompts over one view -- one
+    # render of the coefficient map, then every prompt's relevancy / filter /
+    # select / mask from it (sf_query_sweep); reported beside the main line
+    sweep = None
+    if not args.no_sweep:
+        n_prompts = 32
+        prng = np.random.default_rng(7)
+        prompts = np.concatenate([qv[None], prng.standard_normal((n_prompts - 1, qv.shape[0]))])
+        so = eng.allocate(W, H, levels, coeff_map=True, mask=False)
+        for _ in range(2):
+            eng.sweep(cam, levels, so, prompts, canon)
+        n_sw = max(3, args.steps // 4)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(n_sw):
+            eng.sweep(cam, levels, so, prompts, canon)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        sw_ms = ev0.elapsed_time(ev1) / n_sw
+        sweep = {"prompts": n_prompts, "ms_per_sweep": sw_ms, "prompt_frames_per_s": n_prompts / sw_ms * 1e3,
+                 "sweeps": n_sw,
+                 "note": ("paper_2507_07136_b200.query_sweep's device part (FrameEngine.sweep): each sweep "
+                          "renders the view and answers 32 prompts; one host sync per sweep (its statistics)")}
+        del so
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
@@ -458,6 +485,7 @@ def main():
                          "traffic": traffic, "traffic_source": traffic_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "query_sweep": sweep,
             "gpu_launches": (KERNELS_PER_FRAME_FUSED if fused else KERNELS_PER_FRAME) * args.steps,
             "clocks": clocks,
         }
