@@ -201,10 +201,44 @@ def train_fixtures():
     return made
 
 
+def train_field_fixtures():
+    """init_field (k-means seeding) + train_field (train.py:347-518): two batches,
+    a holdout, 6 Adam iterations; and the random-codebook init."""
+    from splatfield import train as RT
+    made = []
+    rng = np.random.default_rng(1010)
+    sc = random_scene(rng, num_gaussians=400, num_levels=2, L=8, K=2, D=8)
+    cams = [camera(40, 32), camera(40, 32, pos=(0.4, 0.1, -3.0)), camera(40, 32, pos=(-0.3, 0.2, -3.0))]
+    batches = [RT.TrainingBatch(camera=c, targets=rng.standard_normal((2, 32, 40, 8)),
+                                mask=(rng.random((32, 40)) > 0.1) if i == 1 else None)
+               for i, c in enumerate(cams)]
+    cfg = RT.TrainConfig(lr_logits=0.05, lr_codebook=0.02, cosine_weight=0.25)
+    init = RT.init_field(sc, batches[:2], seed=3)
+    init_r = RT.init_field(sc, batches[:2], seed=4, codebook_init="random")
+    res = RT.train_field(sc, batches[:2], 6, cfg, seed=3, holdout=batches[2])
+    d = dict(positions=sc.positions, rotations=sc.rotations, scales=sc.scales, opacities=sc.opacities,
+             colors=sc.colors, coeff_indices=sc.coeff_indices, coeff_values=sc.coeff_values, ids=sc.ids,
+             codebooks=np.stack([cb.atoms for cb in sc.codebooks]),
+             config=np.array([2, 8, 2, 8], dtype=np.int64),
+             cam_R=cams[0].rotation, cam_t=cams[0].translation,
+             cam_intr=np.array([cams[0].fx, cams[0].fy, cams[0].cx, cams[0].cy, cams[0].near]),
+             cam_size=np.array([40, 32], dtype=np.int64),
+             cams_pos=np.array([(0.0, 0.0, -3.0), (0.4, 0.1, -3.0), (-0.3, 0.2, -3.0)]),
+             t_targets=np.stack([b.targets for b in batches]), t_mask1=batches[1].mask,
+             i_logits=init.logits, i_codebooks=init.codebooks, r_codebooks=init_r.codebooks,
+             f_curve=np.array(res.loss_curve), f_logits=res.field.logits, f_codebooks=res.field.codebooks,
+             f_coeff_indices=res.scene.coeff_indices, f_coeff_values=res.scene.coeff_values,
+             f_holdout=np.array([res.holdout_initial, res.holdout_final]))
+    path = os.path.join(OUT, "train_field_s10.npz")
+    np.savez_compressed(path, **d)
+    made.append((path, os.path.getsize(path)))
+    return made
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     if "--only-train" in sys.argv:
-        for p, sz in train_fixtures():
+        for p, sz in train_fixtures() + train_field_fixtures():
             print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
         return
     if "--only-io" in sys.argv:
@@ -219,7 +253,7 @@ def main():
         for p, sz in fused_fixtures():
             print(f"{os.path.basename(p)}: {sz / 1024:.1f} KiB")
         return
-    made = fused_fixtures() + dense_fixtures() + io_fixtures() + train_fixtures()
+    made = fused_fixtures() + dense_fixtures() + io_fixtures() + train_fixtures() + train_field_fixtures()
     # 1. reference-test-like scenes (tests/conftest.py distribution)
     for seed, (g, nl, L, K, D, w, h) in enumerate([
         (50, 1, 16, 4, 8, 32, 32),
