@@ -1062,6 +1062,12 @@ void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const do
                                                             out_stride);
 }
 
+#ifndef SF_SW_THREADS
+#define SF_SW_THREADS 256
+#endif
+#ifndef SF_SW_QCOLS
+#define SF_SW_QCOLS 8
+#endif
 // Relevancy of many prompts over one coefficient map (query sweep).  The map
 // is read once: a CTA (one level: blockIdx.y) stages 256 pixels x L coefficients in
 // shared memory (level-major, pixel-contiguous: conflict-free reads), each
@@ -1071,14 +1077,15 @@ void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const do
 // registers), then the prompts; rel = sigmoid(min_j (l_q - l_j)), the
 // two-branch sigmoid of query.py:65-84.  Same value as the single-query
 // Pd = P_q - P_cj form up to rounding (~1e-16 of the logits).
-constexpr int kSwPx = 256, kSwThreads = 128, kSwCols = 8;
+constexpr int kSwPx = 256, kSwThreads = SF_SW_THREADS, kSwCols = 8, kSwPT = kSwPx / kSwThreads;
+constexpr int kSwQCols = SF_SW_QCOLS;  // prompt columns per pass
 
 __global__ void __launch_bounds__(kSwThreads) k_relevancy_sweep(int64_t P, int n_ch, const float* __restrict__ cmap,
                                                                 const double* __restrict__ proj, int n_levels, int L,
                                                                 int nq, int nc, double* __restrict__ out,
                                                                 int64_t pstride) {
     extern __shared__ __align__(16) unsigned char sw_smem[];
-    const int nqp = (nq + kSwCols - 1) / kSwCols * kSwCols, nvp = nqp + kSwCols, nv = nq + nc;
+    const int nqp = (nq + kSwQCols - 1) / kSwQCols * kSwQCols, nvp = nqp + kSwCols, nv = nq + nc;
     double* pj = reinterpret_cast<double*>(sw_smem);       // [L][nvp]: prompts, pad, canonicals, pad
     float* ws = reinterpret_cast<float*>(pj + (size_t)L * nvp);  // [L][kSwPx]
     const int t = threadIdx.x;
@@ -1106,34 +1113,40 @@ __global__ void __launch_bounds__(kSwThreads) k_relevancy_sweep(int64_t P, int n
                 }
             }
             __syncthreads();
-            auto dots = [&](int c0, double (&acc)[2][kSwCols]) {
+            auto dots = [&](int c0, auto& acc) {
+                constexpr int NCOL = sizeof(acc[0]) / sizeof(double);
 #pragma unroll
-                for (int j = 0; j < kSwCols; ++j) acc[0][j] = acc[1][j] = 0.0;
+                for (int r = 0; r < kSwPT; ++r)
+#pragma unroll
+                    for (int j = 0; j < NCOL; ++j) acc[r][j] = 0.0;
 #pragma unroll 2
                 for (int l = 0; l < L; ++l) {
-                    const double w0 = ws[l * kSwPx + t], w1 = ws[l * kSwPx + t + kSwThreads];
+                    double w[kSwPT];
+#pragma unroll
+                    for (int r = 0; r < kSwPT; ++r) w[r] = ws[l * kSwPx + t + r * kSwThreads];
                     const double2* pr = reinterpret_cast<const double2*>(pj + (size_t)l * nvp + c0);
 #pragma unroll
-                    for (int j2 = 0; j2 < kSwCols / 2; ++j2) {
+                    for (int j2 = 0; j2 < NCOL / 2; ++j2) {
                         const double2 pv = pr[j2];
-                        acc[0][2 * j2] = fma(w0, pv.x, acc[0][2 * j2]);
-                        acc[0][2 * j2 + 1] = fma(w0, pv.y, acc[0][2 * j2 + 1]);
-                        acc[1][2 * j2] = fma(w1, pv.x, acc[1][2 * j2]);
-                        acc[1][2 * j2 + 1] = fma(w1, pv.y, acc[1][2 * j2 + 1]);
+#pragma unroll
+                        for (int r = 0; r < kSwPT; ++r) {
+                            acc[r][2 * j2] = fma(w[r], pv.x, acc[r][2 * j2]);
+                            acc[r][2 * j2 + 1] = fma(w[r], pv.y, acc[r][2 * j2 + 1]);
+                        }
                     }
                 }
             };
-            double lc[2][kSwCols];
+            double lc[kSwPT][kSwCols];
             dots(nqp, lc);
-            for (int c0 = 0; c0 < nq; c0 += kSwCols) {
-                double lq[2][kSwCols];
+            for (int c0 = 0; c0 < nq; c0 += kSwQCols) {
+                double lq[kSwPT][kSwQCols];
                 dots(c0, lq);
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
+                for (int r = 0; r < kSwPT; ++r) {
                     const int px = t + r * kSwThreads;
                     if (px >= np) continue;
 #pragma unroll
-                    for (int j = 0; j < kSwCols; ++j) {
+                    for (int j = 0; j < kSwQCols; ++j) {
                         if (c0 + j >= nq) break;
                         double d = INFINITY;
 #pragma unroll
@@ -1149,7 +1162,7 @@ __global__ void __launch_bounds__(kSwThreads) k_relevancy_sweep(int64_t P, int n
 
 int launch_relevancy_sweep(int64_t P, int n_ch, const float* cmap, const double* proj, int n_levels, int L, int nq,
                            int n_canon, double* out, int64_t out_prompt_stride, cudaStream_t st) {
-    const int nvp = (nq + kSwCols - 1) / kSwCols * kSwCols + kSwCols;
+    const int nvp = (nq + kSwQCols - 1) / kSwQCols * kSwQCols + kSwCols;
     const size_t smem = sizeof(double) * (size_t)L * nvp + sizeof(float) * (size_t)L * kSwPx;
     if (n_canon < 1 || n_canon > kSwCols || L % 4 || n_ch % 4 || (uintptr_t)cmap % 16 || smem > 200 * 1024)
         return 1;
