@@ -77,11 +77,25 @@ __host__ __device__ constexpr int batch_cap(int cs) { return kStageChan / cs < k
 // tensor core at its A-read floor; the A slots free the accumulator space
 // level by level for the codebook ring and the output staging.
 constexpr int kDecTmemCols = 256;
-constexpr int kDecN = 64;                     // output columns per chunk (MMA N)
-constexpr int kDecAcc = 2;                    // TMEM accumulators of kDecN columns
+#ifndef SF_DEC_N
+#define SF_DEC_N 64
+#endif
+#ifndef SF_DEC_ACC
+#define SF_DEC_ACC 2
+#endif
+constexpr int kDecN = SF_DEC_N;               // output columns per chunk (MMA N)
+constexpr int kDecAcc = SF_DEC_ACC;           // TMEM accumulators of kDecN columns
 constexpr int kDecAccCol = 128;
-constexpr int kDecChunkBytes = 2 * 64 * 128;  // B chunk: {hi, lo} x 64 rows (n) x 64 fp16 (128 B, SW128)
-constexpr int kDecStages = 2;                 // B chunk ring at the start of the accumulator space
+constexpr int kDecChunkBytes = 2 * kDecN * 128;  // B chunk: {hi, lo} x kDecN rows (n) x 64 fp16 (128 B, SW128)
+static_assert(kDecAccCol + kDecAcc * kDecN <= 256, "accumulators exceed the CTA's TMEM columns");
+#ifndef SF_DEC_STAGES
+#define SF_DEC_STAGES 2
+#endif
+#ifndef SF_DEC_BOXES
+#define SF_DEC_BOXES 2
+#endif
+constexpr int kDecStages = SF_DEC_STAGES;     // B chunk ring at the start of the accumulator space
+constexpr int kDecBoxes = SF_DEC_BOXES;       // output boxes per consumer warp
 constexpr int kDecBoxCols = 32;               // output box: 8 x 4 pixels (a warp's patch) x 32 fp32 (SW128)
 constexpr int kDecOutBytes = 8 * 4 * kDecBoxCols * 4;
 constexpr int kDecMaxLevels = 3;
@@ -758,7 +772,9 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
         const int total = A.n_levels * nchunk;
         const uint32_t tm = S.tmem_base;
         unsigned char* bring = reinterpret_cast<unsigned char*>(acc);
-        unsigned char* obuf = bring + kDecStages * kDecChunkBytes;  // 2 output boxes per consumer warp
+        unsigned char* obuf = bring + kDecStages * kDecChunkBytes;  // kDecBoxes output boxes per consumer warp
+        static_assert(kDecStages * kDecChunkBytes + kConsumerWarps * kDecBoxes * kDecOutBytes <= 64 * 128 * kAccPitch * 4,
+                      "ring + boxes must fit in the accumulator rows of levels 0-1");
         if (consumer) {
             const uint32_t lane_off = (uint32_t)(cw * 32) << 16;  // this warp's TMEM lane quarter
             // level b's coefficients (this thread's pixel) -> fp16 hi/lo pairs in A slot b & 1
@@ -830,7 +846,7 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             if (A.timeline && threadIdx.x == 0) A.timeline[4 * (blockIdx.x + gridDim.x * blockIdx.y) + 2] = gtimer();
             // drain, each warp on its own: TMEM -> swizzled box (its 8 x 4 pixel
             // patch x 32 fp32, row = lane) -> TMA store by lane 0; no CTA barriers
-            unsigned char* wbox = obuf + cw * 2 * kDecOutBytes;
+            unsigned char* wbox = obuf + cw * kDecBoxes * kDecOutBytes;
             const int bx = x0 + (warp & 1) * 8, by = y0 + (warp >> 1) * 4;
             float scl[kDecMaxLevels];
 #pragma unroll
@@ -858,12 +874,11 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                              kDecChunkBytes, &S.b_full[sg]);
                 }
                 tc_after();
-                uint32_t v[64];
-                {
-                    uint32_t (&v0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[0]);
-                    uint32_t (&v1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[32]);
-                    tmem_ld32(tm + lane_off + (uint32_t)(kDecAccCol + t * kDecN), v0);
-                    tmem_ld32(tm + lane_off + (uint32_t)(kDecAccCol + t * kDecN + 32), v1);
+                uint32_t v[kDecN];
+#pragma unroll
+                for (int h = 0; h < kDecN / 32; ++h) {
+                    uint32_t (&vh)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[32 * h]);
+                    tmem_ld32(tm + lane_off + (uint32_t)(kDecAccCol + t * kDecN + 32 * h), vh);
                 }
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 tc_before();
@@ -872,13 +887,13 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                 const float sc = b == 0 ? scl[0] : (b == 1 ? scl[1] : scl[2]);
                 if (sc != 1.f) {
 #pragma unroll
-                    for (int i = 0; i < 64; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
+                    for (int i = 0; i < kDecN; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
                 }
 #pragma unroll
                 for (int q = 0; q < kDecN / kDecBoxCols; ++q, ++nbox) {
-                    if (lane == 0) bulk_wait_read<1>();  // the store issued two boxes ago has left this box
+                    if (lane == 0) bulk_wait_read<kDecBoxes - 1>();  // the store issued kDecBoxes ago has left this box
                     __syncwarp();
-                    unsigned char* box = wbox + (nbox & 1) * kDecOutBytes;
+                    unsigned char* box = wbox + (nbox % kDecBoxes) * kDecOutBytes;
                     const uint32_t row = smem_addr(box) + lane * (kDecBoxCols * 4);
 #pragma unroll
                     for (int u = 0; u < kDecBoxCols / 4; ++u) {
@@ -929,7 +944,7 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     const uint32_t ah0 = tm + (uint32_t)(64 * (b & 1));
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {  // K steps of 16: Wl Bh + Wh Bl + Wh Bh
-                        const uint64_t bh = bd + 2 * k, bl = bh + (8192 >> 4);
+                        const uint64_t bh = bd + 2 * k, bl = bh + ((kDecChunkBytes / 2) >> 4);
                         const uint32_t ah = ah0 + (uint32_t)(8 * k), al = ah + 32;
                         mma_f16_tmem_a(d, al, bh, idesc, k > 0 ? 1u : 0u);
                         mma_f16_tmem_a(d, ah, bl, idesc, 1u);
