@@ -890,10 +890,8 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     for (int i = 0; i < kDecN; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
                 }
 #pragma unroll
-                for (int q = 0; q < kDecN / kDecBoxCols; ++q, ++nbox) {
-                    if (lane == 0) bulk_wait_read<kDecBoxes - 1>();  // the store issued kDecBoxes ago has left this box
-                    __syncwarp();
-                    unsigned char* box = wbox + (nbox % kDecBoxes) * kDecOutBytes;
+                constexpr int kBoxesPerChunk = kDecN / kDecBoxCols;
+                auto fill_box = [&](unsigned char* box, int q) {
                     const uint32_t row = smem_addr(box) + lane * (kDecBoxCols * 4);
 #pragma unroll
                     for (int u = 0; u < kDecBoxCols / 4; ++u) {
@@ -904,11 +902,34 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                                      "r"(v[kDecBoxCols * q + 4 * u + 2]), "r"(v[kDecBoxCols * q + 4 * u + 3])
                                      : "memory");
                     }
+                };
+                if (kDecBoxes == kBoxesPerChunk) {
+                    // one box per chunk column block: the previous chunk's stores
+                    // must have left the boxes; one fence and one commit per chunk
+                    if (lane == 0) bulk_wait_read<0>();
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < kBoxesPerChunk; ++q) fill_box(wbox + q * kDecOutBytes, q);
                     proxy_fence();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_4d(&fmap, box, c * kDecN + kDecBoxCols * q, bx, by, b);
+#pragma unroll
+                        for (int q = 0; q < kBoxesPerChunk; ++q)
+                            tma_store_4d(&fmap, wbox + q * kDecOutBytes, c * kDecN + kDecBoxCols * q, bx, by, b);
                         bulk_commit();
+                    }
+                } else {
+                    for (int q = 0; q < kBoxesPerChunk; ++q, ++nbox) {
+                        if (lane == 0) bulk_wait_read<kDecBoxes - 1>();  // the store issued kDecBoxes ago has left this box
+                        __syncwarp();
+                        unsigned char* box = wbox + (nbox % kDecBoxes) * kDecOutBytes;
+                        fill_box(box, q);
+                        proxy_fence();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_4d(&fmap, box, c * kDecN + kDecBoxCols * q, bx, by, b);
+                            bulk_commit();
+                        }
                     }
                 }
             }
