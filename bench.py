@@ -96,19 +96,26 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            # nvidia-smi needs a moment to start: wait for its first sample so
+            # the timed region is covered, then keep only samples taken in it
+            t_end = time.time() + 3.0
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
+        self.t_start = time.time()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *exc):
+        self.t_stop = time.time()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -119,7 +126,8 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        inside = [ln for t, ln in self.lines if self.t_start <= t <= self.t_stop + 0.02]
+        for ln in inside or [ln for _, ln in self.lines[-1:]]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
