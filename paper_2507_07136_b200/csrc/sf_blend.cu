@@ -629,7 +629,8 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             }
         }
     }
-    __syncthreads();
+    // no contribution anywhere in the half tile: its decoded features are zero
+    const bool any_contrib = __syncthreads_or(ncontrib > 0);
 
     // Early-exit decisions (counted iff T >= 1e-4) that fp32 T cannot certify
     // are replayed exactly in fp64 by k_blend_fixup.
@@ -852,7 +853,25 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
 #pragma unroll
             for (int b = 0; b < kDecMaxLevels; ++b) scl[b] = b < A.n_levels ? A.dec_scale[b] : 1.f;
             int nbox = 0;
-            for (int g = 0; g < total; ++g) {
+            constexpr int kBoxesPerChunk = kDecN / kDecBoxCols;
+            if (!any_contrib) {
+                // empty half tile: zero boxes, stored for every chunk (no MMAs, no drains)
+                for (int i = lane; i < kDecBoxes * kDecOutBytes / 16; i += 32)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(smem_addr(wbox) + 16 * i), "r"(0u)
+                                 : "memory");
+                proxy_fence();
+                __syncwarp();
+                if (lane == 0) {
+                    for (int g = 0; g < total; ++g) {
+                        const int b = g / nchunk, c = g - b * nchunk;
+                        for (int q = 0; q < kBoxesPerChunk; ++q)
+                            tma_store_4d(&fmap, wbox + (q % kDecBoxes) * kDecOutBytes, c * kDecN + kDecBoxCols * q, bx,
+                                         by, b);
+                    }
+                    bulk_commit();
+                }
+            }
+            for (int g = 0; g < total && any_contrib; ++g) {
                 const int t = g & (kDecAcc - 1), b = g / nchunk, c = g - b * nchunk;
                 if (c == 0 && b == 1 && A.n_levels > 2) {
                     // level 0's MMAs are done (its chunks were drained): level 2 -> slot 0
@@ -890,7 +909,6 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     for (int i = 0; i < kDecN; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
                 }
 #pragma unroll
-                constexpr int kBoxesPerChunk = kDecN / kDecBoxCols;
                 auto fill_box = [&](unsigned char* box, int q) {
                     const uint32_t row = smem_addr(box) + lane * (kDecBoxCols * 4);
 #pragma unroll
@@ -941,16 +959,17 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             const unsigned char* img = reinterpret_cast<const unsigned char*>(A.dec_b);
             const bool leader = lane == 0;
             const uint64_t desc0 = sw128_desc(smem_addr(bring));
-            bar_wait(&S.a_ready, 0);
+            const int n_issue = any_contrib ? total : 0;  // empty half tile: nothing to multiply
+            if (n_issue) bar_wait(&S.a_ready, 0);
             tc_after();
-            if (leader)
+            if (leader && n_issue)
                 for (int g = 0; g < kDecStages && g < total; ++g) {
                     bar_expect_tx(&S.b_full[g], kDecChunkBytes);
                     bulk_g2s(bring + g * kDecChunkBytes, img + (size_t)g * kDecChunkBytes, kDecChunkBytes,
                              &S.b_full[g]);
                 }
             __syncwarp();
-            for (int g = 0; g < total; ++g) {
+            for (int g = 0; g < n_issue; ++g) {
                 const int s = g % kDecStages, t = g & (kDecAcc - 1), b = g / nchunk, c = g - b * nchunk;
                 if (c == 0 && b >= 2) {  // level b's A replaced level b - 2's in its slot
                     bar_wait(&S.a_ready, (b - 1) & 1);

@@ -450,3 +450,34 @@ def test_query_sweep_matches_per_prompt_pipelines(rng, L, window, n_prompts, n_c
     # the shared coefficient map is the multilevel splat
     assert np.array_equal(sweep[0].coefficient_map.data, sf.splat_multilevel(scene, cam).data)
     assert sf.query_sweep(scene, cam, [], canon) == []
+
+
+def test_fused_decode_empty_half_tiles_store_exact_zeros(rng):
+    """Half tiles no Gaussian contributes to skip the MMAs and store zero boxes:
+    their features are exactly 0 (buffers pre-filled with NaN), the rest of the
+    frame still matches the fp64 product of its coefficient map, and the fused
+    relevancy there is sigmoid(0) = 0.5."""
+    import torch
+    from paper_2507_07136_b200.device import QuerySpec, device_scene
+    scene = random_scene(rng, 2000, num_levels=3, L=64, K=4, D=512)
+    scene.positions[:, 0] = -np.abs(scene.positions[:, 0]) - 0.3  # left part of the view only
+    cam = make_camera(160, 96)
+    eng = device_scene(scene).engine
+    levels = (0, 1, 2)
+    qv = rng.standard_normal(512)
+    canon = rng.standard_normal((4, 512))
+    out = eng.allocate(cam.width, cam.height, levels, coeff_map=True, features=True, query=True)
+    out.features.fill_(float("nan"))
+    out.relevancy_raw.fill_(float("nan"))
+    eng.run(cam, levels, out, query=QuerySpec(qv, canon))
+    torch.cuda.synchronize()
+    w = out.coeff_map.double()
+    empty = (w == 0).all(dim=2)
+    assert empty.any() and not empty.all()
+    for b in range(3):
+        f = out.features[b]
+        assert torch.isfinite(f).all()
+        assert (f[empty] == 0).all()
+        ref = w[:, :, 64 * b:64 * (b + 1)] @ torch.from_numpy(scene.codebooks[b].atoms).to(w.device).double()
+        assert (f.double() - ref).abs().max().item() <= F_REL * ref.abs().max().item()
+        assert (out.relevancy_raw[b][empty] == 0.5).all()
