@@ -481,3 +481,16 @@ def test_fused_decode_empty_half_tiles_store_exact_zeros(rng):
         ref = w[:, :, 64 * b:64 * (b + 1)] @ torch.from_numpy(scene.codebooks[b].atoms).to(w.device).double()
         assert (f.double() - ref).abs().max().item() <= F_REL * ref.abs().max().item()
         assert (out.relevancy_raw[b][empty] == 0.5).all()
+
+
+@pytest.mark.parametrize("L", [16, 256])
+def test_sparse_equals_dense_coefficient_render(rng, L):
+    """SURVEY 8(f) f1's cost-decoupling comparator: the dense render of the
+    densified coefficient rows (render_dense, 16 channels per pass) is the
+    sparse multilevel map (splat_multilevel; L = 256 spans four channel blocks)."""
+    scene = random_scene(rng, 1500, num_levels=3, L=L, K=4, D=16)
+    cam = make_camera(64, 48)
+    rows = np.concatenate([scene.densified_coefficients(lv) for lv in range(3)], axis=1)
+    sparse = sf.splat_multilevel(scene, cam, max_elements=1 << 40).data
+    dense = sf.render_dense(scene, cam, rows, tag="coefficient", max_elements=1 << 40).data
+    assert np.abs(sparse - dense).max() <= W_TOL
