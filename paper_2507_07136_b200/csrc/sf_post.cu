@@ -306,11 +306,15 @@ __global__ void __launch_bounds__(1024) k_finalize_select_wide(int n_maps, int n
 }
 
 constexpr int kBoxTX = 64, kBoxTY = 16, kBoxRMax = 8;
-__global__ void __launch_bounds__(256) k_box2d_stats(int H, int W, const double* __restrict__ in, int r,
+// RC > 0: the radius as a compile-time constant (unrolled sums, constant
+// divisors); RC = 0 takes it from r.  Same summation order either way.
+template <int RC>
+__global__ void __launch_bounds__(256) k_box2d_stats(int H, int W, const double* __restrict__ in, int r_rt,
                                                      double area, double* __restrict__ out,
                                                      MaxMin* __restrict__ partial, int y0, int y1) {
     __shared__ double tin[kBoxTY + 2 * kBoxRMax][kBoxTX + 2 * kBoxRMax];
     __shared__ double trs[kBoxTY + 2 * kBoxRMax][kBoxTX];
+    const int r = RC > 0 ? RC : r_rt;
     const int m = blockIdx.z;
     const int x0 = blockIdx.x * kBoxTX, ty0 = y0 + blockIdx.y * kBoxTY;
     const int64_t hw = (int64_t)H * W;
@@ -325,7 +329,12 @@ __global__ void __launch_bounds__(256) k_box2d_stats(int H, int W, const double*
     for (int i = threadIdx.x; i < nr * kBoxTX; i += blockDim.x) {
         const int rr = i / kBoxTX, x = i - rr * kBoxTX;
         double acc = 0.0;
-        for (int d = -r; d <= r; ++d) acc += tin[rr][x + r + d];
+        if (RC > 0) {
+#pragma unroll
+            for (int d = -RC; d <= RC; ++d) acc += tin[rr][x + RC + d];
+        } else {
+            for (int d = -r; d <= r; ++d) acc += tin[rr][x + r + d];
+        }
         trs[rr][x] = acc;
     }
     __syncthreads();
@@ -335,7 +344,12 @@ __global__ void __launch_bounds__(256) k_box2d_stats(int H, int W, const double*
         const int y = ty0 + yl, gx = x0 + x;
         if (y >= y1 || gx >= W) continue;
         double acc = 0.0;
-        for (int d = -r; d <= r; ++d) acc += trs[yl + r + d][x];
+        if (RC > 0) {
+#pragma unroll
+            for (int d = -RC; d <= RC; ++d) acc += trs[yl + RC + d][x];
+        } else {
+            for (int d = -r; d <= r; ++d) acc += trs[yl + r + d][x];
+        }
         const double v = acc / area;
         const int64_t idx = (int64_t)y * W + gx;
         out[(size_t)m * hw + idx] = v;
@@ -349,6 +363,15 @@ __global__ void __launch_bounds__(256) k_box2d_stats(int H, int W, const double*
     const MaxMin rsum = Red(tmp).Reduce(best, Op());
     if (threadIdx.x == 0)
         partial[(size_t)m * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = rsum;
+}
+
+static void launch_box2d_stats(dim3 grid, int H, int W, const double* in, int r, double* out, MaxMin* partial,
+                               int y0, int y1, cudaStream_t st) {
+    const double area = (double)(2 * r + 1) * (double)(2 * r + 1);
+    if (r == 5)
+        k_box2d_stats<5><<<grid, 256, 0, st>>>(H, W, in, r, area, out, partial, y0, y1);
+    else
+        k_box2d_stats<0><<<grid, 256, 0, st>>>(H, W, in, r, area, out, partial, y0, y1);
 }
 
 static int box_tiles(int H, int W) { return ceil_div(W, kBoxTX) * ceil_div(H, kBoxTY); }
@@ -368,7 +391,7 @@ void launch_filter_select(int n_maps, int H, int W, const double* raw, int windo
     const int r = window / 2;
     MaxMin* partial = (MaxMin*)ws;
     dim3 grid(ceil_div(W, kBoxTX), ceil_div(y1 - y0, kBoxTY), n_maps);
-    k_box2d_stats<<<grid, 256, 0, st>>>(H, W, raw, r, (double)window * (double)window, filtered, partial, y0, y1);
+    launch_box2d_stats(grid, H, W, raw, r, filtered, partial, y0, y1, st);
     k_finalize_select_wide<<<1, 1024, 0, st>>>(n_maps, (int)(grid.x * grid.y), W, partial, fixed_level, stats_i64,
                                                 stats_f64);
     const int64_t hw = (int64_t)H * W, i0 = (int64_t)y0 * W, i1 = (int64_t)y1 * W;
@@ -392,7 +415,7 @@ void launch_filter_select_batch(int n_queries, int n_maps, int H, int W, const d
     const int r = window / 2;
     MaxMin* partial = (MaxMin*)ws;
     dim3 grid(ceil_div(W, kBoxTX), ceil_div(H, kBoxTY), n_maps * n_queries);
-    k_box2d_stats<<<grid, 256, 0, st>>>(H, W, raw, r, (double)window * (double)window, filtered, partial, 0, H);
+    launch_box2d_stats(grid, H, W, raw, r, filtered, partial, 0, H, st);
     k_finalize_select_wide<<<n_queries, 1024, 0, st>>>(n_maps, (int)(grid.x * grid.y), W, partial, -1, stats_i64,
                                                        stats_f64);
     const int64_t hw = (int64_t)H * W;
