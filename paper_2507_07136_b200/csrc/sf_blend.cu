@@ -785,7 +785,8 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             const double* Pd = reinterpret_cast<const double*>(&S.st[0]);
             auto convert = [&](int b, bool with_rel) {
                 const bool rel_b = rel && with_rel;
-                double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+                // even / odd K in separate chains (8 independent fp64 FMA chains)
+                double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll 1
                 for (int kb = 0; kb < 2; ++kb) {
                     uint32_t hi[16], lo[16];
@@ -802,8 +803,8 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                             const double w0 = (double)x0, w1 = (double)x1;
                             d0 = fma(w0, a01.x, d0), d1 = fma(w0, a01.y, d1);
                             d2 = fma(w0, a23.x, d2), d3 = fma(w0, a23.y, d3);
-                            d0 = fma(w1, b01.x, d0), d1 = fma(w1, b01.y, d1);
-                            d2 = fma(w1, b23.x, d2), d3 = fma(w1, b23.y, d3);
+                            e0 = fma(w1, b01.x, e0), e1 = fma(w1, b01.y, e1);
+                            e2 = fma(w1, b23.x, e2), e3 = fma(w1, b23.y, e3);
                         }
                         const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
                         const __half l0 = __float2half_rn(x0 - __half2float(h0));
@@ -816,28 +817,12 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                     tmem_st16(tm + lane_off + col + 32, lo);
                 }
                 // sigmoid is monotone: min_j sigmoid(d_j) = sigmoid(min_j d_j)
+                d0 += e0, d1 += e1, d2 += e2, d3 += e3;
                 if (rel_b && inside)
                     A.relevancy_raw[(size_t)b * A.W * A.H + (size_t)py * A.W + px] =
                         sigmoid2(np_minimum(np_minimum(d0, d1), np_minimum(d2, d3)));
             };
             for (int b = 0; b < A.n_levels && b < 2; ++b) convert(b, true);
-            if (rel && inside) {
-                // level 2's relevancy now: its accumulator rows are converted
-                // later, while the tensor cores run levels 0 and 1
-                double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-                const float* src = acc + 128 * kAccPitch + slot;
-#pragma unroll 4
-                for (int l = 0; l < 64; ++l) {
-                    const double w = (double)src[l * kAccPitch];
-                    const double* P0 = Pd + (size_t)(128 + l) * 4;
-                    const double2 a01 = *reinterpret_cast<const double2*>(P0);
-                    const double2 a23 = *reinterpret_cast<const double2*>(P0 + 2);
-                    d0 = fma(w, a01.x, d0), d1 = fma(w, a01.y, d1);
-                    d2 = fma(w, a23.x, d2), d3 = fma(w, a23.y, d3);
-                }
-                A.relevancy_raw[(size_t)2 * A.W * A.H + (size_t)py * A.W + px] =
-                    sigmoid2(np_minimum(np_minimum(d0, d1), np_minimum(d2, d3)));
-            }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 
             proxy_fence();  // accumulator reads precede the bulk copies / boxes written over them
@@ -845,6 +830,29 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
             __syncwarp();
             if (lane == 0) bar_arrive(&S.a_ready);
             if (A.timeline && threadIdx.x == 0) A.timeline[4 * (blockIdx.x + gridDim.x * blockIdx.y) + 2] = gtimer();
+            if (rel && inside) {
+                // level 2's relevancy while the tensor cores start on level 0: its
+                // accumulator rows stay intact until level 2 is converted
+                double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+                const float* src = acc + 128 * kAccPitch + slot;
+#pragma unroll 2
+                for (int l = 0; l < 64; l += 2) {
+                    const double w = (double)src[l * kAccPitch], v = (double)src[(l + 1) * kAccPitch];
+                    const double* P0 = Pd + (size_t)(128 + l) * 4;
+                    const double2 a01 = *reinterpret_cast<const double2*>(P0);
+                    const double2 a23 = *reinterpret_cast<const double2*>(P0 + 2);
+                    const double2 b01 = *reinterpret_cast<const double2*>(P0 + 4);
+                    const double2 b23 = *reinterpret_cast<const double2*>(P0 + 6);
+                    d0 = fma(w, a01.x, d0), d1 = fma(w, a01.y, d1);
+                    d2 = fma(w, a23.x, d2), d3 = fma(w, a23.y, d3);
+                    e0 = fma(v, b01.x, e0), e1 = fma(v, b01.y, e1);
+                    e2 = fma(v, b23.x, e2), e3 = fma(v, b23.y, e3);
+                }
+                d0 += e0, d1 += e1, d2 += e2, d3 += e3;
+                A.relevancy_raw[(size_t)2 * A.W * A.H + (size_t)py * A.W + px] =
+                    sigmoid2(np_minimum(np_minimum(d0, d1), np_minimum(d2, d3)));
+            }
+
             // drain, each warp on its own: TMEM -> swizzled box (its 8 x 4 pixel
             // patch x 32 fp32, row = lane) -> TMA store by lane 0; no CTA barriers
             unsigned char* wbox = obuf + cw * kDecBoxes * kDecOutBytes;
