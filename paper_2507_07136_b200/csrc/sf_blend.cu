@@ -250,10 +250,11 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
+// two-branch logistic (query.py:65-84), evaluated branch-free: both branches
+// take exp(-|x|), so a warp with mixed signs runs one exp instead of two
 __device__ __forceinline__ double sigmoid2(double x) {
-    if (x >= 0) return 1.0 / (1.0 + exp(-x));
-    double ex = exp(x);
-    return ex / (1.0 + ex);
+    const double e = exp(-fabs(x));
+    return (x >= 0 ? 1.0 : e) / (1.0 + e);
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {

@@ -11,10 +11,11 @@
 
 namespace sf {
 
+// two-branch logistic (query.py:65-84), evaluated branch-free: both branches
+// take exp(-|x|), so a warp with mixed signs runs one exp instead of two
 __device__ __forceinline__ double sigmoid2p(double x) {
-    if (x >= 0) return 1.0 / (1.0 + exp(-x));
-    double ex = exp(x);
-    return ex / (1.0 + ex);
+    const double e = exp(-fabs(x));
+    return (x >= 0 ? 1.0 : e) / (1.0 + e);
 }
 
 // P[b][l][j] = atoms_{lv_b}[l] . v_j, v_j = q[j] for j < nq, else canonical
