@@ -96,7 +96,13 @@ static_assert(kDecAccCol + kDecAcc * kDecN <= 256, "accumulators exceed the CTA'
 #endif
 constexpr int kDecStages = SF_DEC_STAGES;     // B chunk ring at the start of the accumulator space
 constexpr int kDecBoxes = SF_DEC_BOXES;       // output boxes per consumer warp
-constexpr int kDecBoxCols = 32;               // output box: 8 x 4 pixels (a warp's patch) x 32 fp32 (SW128)
+#ifndef SF_DEC_BOXCOLS
+#define SF_DEC_BOXCOLS 32
+#endif
+#ifndef SF_DEC_BATCHED
+#define SF_DEC_BATCHED 1
+#endif
+constexpr int kDecBoxCols = SF_DEC_BOXCOLS;   // output box: 8 x 4 pixels (a warp's patch) x 32 fp32 (SW128) or 16 (SW64)
 constexpr int kDecOutBytes = 8 * 4 * kDecBoxCols * 4;
 constexpr int kDecMaxLevels = 3;
 
@@ -930,7 +936,7 @@ k_blend(BlendArgs A, int ch_block, const __grid_constant__ CUtensorMap fmap) {
                                      : "memory");
                     }
                 };
-                if (kDecBoxes == kBoxesPerChunk) {
+                if (SF_DEC_BATCHED && kDecBoxes == kBoxesPerChunk) {
                     // one box per chunk column block: the previous chunk's stores
                     // must have left the boxes; one fence and one commit per chunk
                     if (lane == 0) bulk_wait_read<0>();
