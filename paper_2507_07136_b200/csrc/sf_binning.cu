@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const uint32_t* __restr
 
 // Per-tile sort of unique depth ranks, n <= CAP: MSD bucket sort in shared
 // memory.  Keys are distinct, so placement may use atomics (no stability is
-// needed): bucket = (key - min) * NB / (max - min + 1), histogram, scan,
+// needed): bucket ~ (key - min) * NB / (max - min + 1), histogram, scan,
 // scatter, then an insertion sort inside each bucket (a few keys on average).
 // A tile whose largest bucket exceeds kMaxBucket (strongly clustered ranks)
 // is bitonic-sorted instead.  The sorted ranks are written back as rows.
@@ -497,12 +497,13 @@ __global__ void __launch_bounds__(256) k_tile_sort_bucket(const uint32_t* __rest
     }
     __syncthreads();
     const uint32_t kmin = s_min;
-    const uint64_t span = (uint64_t)(s_max - kmin) + 1;
+    // bucket = floor((key - min) * NB / span) in fp32: rounding is monotone, so
+    // the buckets stay in key order (the sorted output does not depend on where
+    // exactly the boundaries fall) -- no 64-bit integer division per key
+    const float bscale = (float)NB / ((float)(s_max - kmin) + 1.0f);
+    auto bucket_of = [&](uint32_t k) { return min(NB - 1, (int)((float)(k - kmin) * bscale)); };
     // histogram
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int b = (int)(((uint64_t)(keys[i] - kmin) * NB) / span);
-        atomicAdd(&cursor[b], 1u);
-    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cursor[bucket_of(keys[i])], 1u);
     __syncthreads();
     // exclusive scan of the NB bucket counts (NB / 256 per thread)
     {
@@ -542,8 +543,7 @@ __global__ void __launch_bounds__(256) k_tile_sort_bucket(const uint32_t* __rest
     // scatter into buckets
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const uint32_t k = keys[i];
-        const int b = (int)(((uint64_t)(k - kmin) * NB) / span);
-        outk[atomicAdd(&cursor[b], 1u)] = k;
+        outk[atomicAdd(&cursor[bucket_of(k)], 1u)] = k;
     }
     __syncthreads();
     // insertion sort inside each bucket
