@@ -457,7 +457,16 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const uint32_t* __restr
 // scatter, then an insertion sort inside each bucket (a few keys on average).
 // A tile whose largest bucket exceeds kMaxBucket (strongly clustered ranks)
 // is bitonic-sorted instead.  The sorted ranks are written back as rows.
-constexpr int kMaxBucket = 48;
+#ifndef SF_TS_CAP
+#define SF_TS_CAP 4096
+#endif
+#ifndef SF_TS_NB
+#define SF_TS_NB 1024
+#endif
+#ifndef SF_TS_MAXB
+#define SF_TS_MAXB 48
+#endif
+constexpr int kMaxBucket = SF_TS_MAXB;
 template <int CAP, int NB>
 __global__ void __launch_bounds__(256) k_tile_sort_bucket(const uint32_t* __restrict__ offsets,
                                                           uint32_t* __restrict__ entries, int lo_exclusive,
@@ -620,7 +629,7 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
     if (blocks)
         k_emit_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, aux, tile_offsets, tile_cursor,
                                              entries, agg ? cta_base : nullptr, per);
-    // per-tile canonical order: most lists fit one CUB block sort (<= 2048),
+    // per-tile canonical order: most lists fit the shared-memory bucket sort (<= 4096),
     // the rest go to the larger-capacity kernels (each CTA skips other sizes)
     static bool configured = false;
     if (!configured) {
@@ -628,8 +637,9 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
                              2 * 8192 * 4);
         configured = true;
     }
-    k_tile_sort_bucket<2048, 512><<<n_tiles, 256, 2 * 2048 * 4, st>>>(tile_offsets, entries, 0, stats, rank_to_row);
-    k_tile_sort_bucket<8192, 1024><<<n_tiles, 256, 2 * 8192 * 4, st>>>(tile_offsets, entries, 2048, stats,
+    k_tile_sort_bucket<SF_TS_CAP, SF_TS_NB><<<n_tiles, 256, 2 * SF_TS_CAP * 4, st>>>(tile_offsets, entries, 0, stats,
+                                                                                   rank_to_row);
+    k_tile_sort_bucket<8192, 1024><<<n_tiles, 256, 2 * 8192 * 4, st>>>(tile_offsets, entries, SF_TS_CAP, stats,
                                                                        rank_to_row);
     k_tile_sort_large<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192, stats, rank_to_row);
 }
