@@ -1132,32 +1132,27 @@ void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const do
                                                             out_stride);
 }
 
-#ifndef SF_SW_THREADS
-#define SF_SW_THREADS 256
-#endif
-#ifndef SF_SW_QCOLS
-#define SF_SW_QCOLS 8
-#endif
 // Relevancy of many prompts over one coefficient map (query sweep).  The map
-// is read once: a CTA (one level: blockIdx.y) stages 256 pixels x L coefficients in
-// shared memory (level-major, pixel-contiguous: conflict-free reads), each
-// thread owns two pixels and forms the fp64 logits l = W . P of 8 columns at a
-// time (8 x 2 independent DFMA chains per coefficient; the P column block is
-// a 64-byte shared broadcast).  Canonical logits first (<= 8, kept in
-// registers), then the prompts; rel = sigmoid(min_j (l_q - l_j)), the
-// two-branch sigmoid of query.py:65-84.  Same value as the single-query
-// Pd = P_q - P_cj form up to rounding (~1e-16 of the logits).
-constexpr int kSwPx = 256, kSwThreads = SF_SW_THREADS, kSwCols = 8, kSwPT = kSwPx / kSwThreads;
-constexpr int kSwQCols = SF_SW_QCOLS;  // prompt columns per pass
+// is read once: a CTA (one level: blockIdx.y) stages 256 pixels x L
+// coefficients in shared memory (level-major, pixel-contiguous).  First each
+// thread forms its pixel's canonical logits (<= 8) and keeps their max; then
+// a thread takes 4 consecutive pixels x one block of 8 prompt columns (a 4 x 8
+// register tile of fp64 FMA chains over l, 5 shared loads per 32 FMAs).
+// rel = sigmoid(l_q - max_j l_j) = sigmoid(min_j (l_q - l_j)), the two-branch
+// sigmoid of query.py:65-84; same value as the single-query Pd = P_q - P_cj
+// form up to rounding (~1e-16 of the logits).
+constexpr int kSwPx = 256, kSwThreads = 256, kSwCols = 8;  // pixels per tile, threads, columns per block
+static_assert(kSwThreads == kSwPx, "the canonical pass maps one thread to one pixel");
 
-__global__ void __launch_bounds__(kSwThreads) k_relevancy_sweep(int64_t P, int n_ch, const float* __restrict__ cmap,
+__global__ void __launch_bounds__(kSwThreads, 2) k_relevancy_sweep(int64_t P, int n_ch, const float* __restrict__ cmap,
                                                                 const double* __restrict__ proj, int n_levels, int L,
                                                                 int nq, int nc, double* __restrict__ out,
                                                                 int64_t pstride) {
     extern __shared__ __align__(16) unsigned char sw_smem[];
-    const int nqp = (nq + kSwQCols - 1) / kSwQCols * kSwQCols, nvp = nqp + kSwCols, nv = nq + nc;
+    const int nqp = (nq + kSwCols - 1) / kSwCols * kSwCols, nvp = nqp + kSwCols, nv = nq + nc;
     double* pj = reinterpret_cast<double*>(sw_smem);       // [L][nvp]: prompts, pad, canonicals, pad
     float* ws = reinterpret_cast<float*>(pj + (size_t)L * nvp);  // [L][kSwPx]
+    double* lcs = reinterpret_cast<double*>(ws + (size_t)L * kSwPx);  // [kSwPx] max canonical logit
     const int t = threadIdx.x;
     const int b = blockIdx.y;  // one level per CTA: its projected codebook is loaded once
     for (int i = t; i < L * nvp; i += kSwThreads) {
@@ -1183,46 +1178,74 @@ __global__ void __launch_bounds__(kSwThreads) k_relevancy_sweep(int64_t P, int n
                 }
             }
             __syncthreads();
-            auto dots = [&](int c0, auto& acc) {
-                constexpr int NCOL = sizeof(acc[0]) / sizeof(double);
+            // canonical logits: thread = pixel, 8 columns (the canonical block)
+            {
+                double lc[kSwCols];
 #pragma unroll
-                for (int r = 0; r < kSwPT; ++r)
-#pragma unroll
-                    for (int j = 0; j < NCOL; ++j) acc[r][j] = 0.0;
+                for (int c = 0; c < kSwCols; ++c) lc[c] = 0.0;
 #pragma unroll 2
                 for (int l = 0; l < L; ++l) {
-                    double w[kSwPT];
+                    const double w = ws[l * kSwPx + t];
+                    const double2* pr = reinterpret_cast<const double2*>(pj + (size_t)l * nvp + nqp);
 #pragma unroll
-                    for (int r = 0; r < kSwPT; ++r) w[r] = ws[l * kSwPx + t + r * kSwThreads];
+                    for (int c2 = 0; c2 < kSwCols / 2; ++c2) {
+                        const double2 pv = pr[c2];
+                        lc[2 * c2] = fma(w, pv.x, lc[2 * c2]);
+                        lc[2 * c2 + 1] = fma(w, pv.y, lc[2 * c2 + 1]);
+                    }
+                }
+                // min_j (l_q - l_j) = l_q - max_j l_j exactly (rounded subtraction is
+                // monotone); NaN propagates as through np.minimum
+                double mx = lc[0];
+#pragma unroll
+                for (int c = 1; c < kSwCols; ++c)
+                    if (c < nc) mx = (mx != mx || lc[c] != lc[c]) ? NAN : fmax(mx, lc[c]);
+                lcs[t] = mx;
+            }
+            __syncthreads();
+            // prompt logits: thread = 4 consecutive pixels x one 8-column block
+            // (4 x 8 register tile: 5 shared loads per 32 FMAs)
+            const int pg = t % (kSwPx / 4), cg = t / (kSwPx / 4);
+            const int px0 = 4 * pg;
+            for (int cb = cg; cb * kSwCols < nq; cb += kSwThreads / (kSwPx / 4)) {
+                const int c0 = cb * kSwCols;
+                double acc[4][kSwCols];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int j = 0; j < kSwCols; ++j) acc[r][j] = 0.0;
+#pragma unroll 2
+                for (int l = 0; l < L; ++l) {
+                    const float4 w4 = *reinterpret_cast<const float4*>(ws + l * kSwPx + px0);
+                    const double w[4] = {w4.x, w4.y, w4.z, w4.w};
                     const double2* pr = reinterpret_cast<const double2*>(pj + (size_t)l * nvp + c0);
 #pragma unroll
-                    for (int j2 = 0; j2 < NCOL / 2; ++j2) {
+                    for (int j2 = 0; j2 < kSwCols / 2; ++j2) {
                         const double2 pv = pr[j2];
 #pragma unroll
-                        for (int r = 0; r < kSwPT; ++r) {
+                        for (int r = 0; r < 4; ++r) {
                             acc[r][2 * j2] = fma(w[r], pv.x, acc[r][2 * j2]);
                             acc[r][2 * j2 + 1] = fma(w[r], pv.y, acc[r][2 * j2 + 1]);
                         }
                     }
                 }
-            };
-            double lc[kSwPT][kSwCols];
-            dots(nqp, lc);
-            for (int c0 = 0; c0 < nq; c0 += kSwQCols) {
-                double lq[kSwPT][kSwQCols];
-                dots(c0, lq);
+                const double2 m01 = *reinterpret_cast<const double2*>(lcs + px0);
+                const double2 m23 = *reinterpret_cast<const double2*>(lcs + px0 + 2);
+                const double lmax[4] = {m01.x, m01.y, m23.x, m23.y};
 #pragma unroll
-                for (int r = 0; r < kSwPT; ++r) {
-                    const int px = t + r * kSwThreads;
-                    if (px >= np) continue;
+                for (int j = 0; j < kSwCols; ++j) {
+                    if (c0 + j >= nq) break;
+                    double v[4];
 #pragma unroll
-                    for (int j = 0; j < kSwQCols; ++j) {
-                        if (c0 + j >= nq) break;
-                        double d = INFINITY;
+                    for (int r = 0; r < 4; ++r) v[r] = sigmoid2(acc[r][j] - lmax[r]);
+                    double* o = out + (size_t)(c0 + j) * pstride + (size_t)b * P + base + px0;
+                    if (px0 + 3 < np && (((uintptr_t)o) & 15) == 0) {
+                        reinterpret_cast<double2*>(o)[0] = make_double2(v[0], v[1]);
+                        reinterpret_cast<double2*>(o)[1] = make_double2(v[2], v[3]);
+                    } else {
 #pragma unroll
-                        for (int c = 0; c < kSwCols; ++c)
-                            if (c < nc) d = np_minimum(d, lq[r][j] - lc[r][c]);
-                        out[(size_t)(c0 + j) * pstride + (size_t)b * P + base + px] = sigmoid2(d);
+                        for (int r = 0; r < 4; ++r)
+                            if (px0 + r < np) o[r] = v[r];
                     }
                 }
             }
@@ -1232,8 +1255,9 @@ __global__ void __launch_bounds__(kSwThreads) k_relevancy_sweep(int64_t P, int n
 
 int launch_relevancy_sweep(int64_t P, int n_ch, const float* cmap, const double* proj, int n_levels, int L, int nq,
                            int n_canon, double* out, int64_t out_prompt_stride, cudaStream_t st) {
-    const int nvp = (nq + kSwQCols - 1) / kSwQCols * kSwQCols + kSwCols;
-    const size_t smem = sizeof(double) * (size_t)L * nvp + sizeof(float) * (size_t)L * kSwPx;
+    const int nvp = (nq + kSwCols - 1) / kSwCols * kSwCols + kSwCols;
+    const size_t smem = sizeof(double) * (size_t)L * nvp + sizeof(float) * (size_t)L * kSwPx +
+                        sizeof(double) * kSwPx;
     if (n_canon < 1 || n_canon > kSwCols || L % 4 || n_ch % 4 || (uintptr_t)cmap % 16 || smem > 200 * 1024)
         return 1;
     if (P == 0 || nq == 0) return 0;
