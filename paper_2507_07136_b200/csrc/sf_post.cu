@@ -225,20 +225,48 @@ __global__ void k_finalize_select(int n_maps, int nblk, int W, const MaxMin* __r
 
 // blockIdx.y: query of a batch (maps / statistics / mask of query y at
 // y * (n_maps hw, 16, 8 + 2 n_maps, hw)).
+// V pixels per thread (V = 4: two 16-byte map loads, one 4-byte mask store;
+// the launcher uses it when hw, i0 and i1 are multiples of 4).
+template <int V>
 __global__ void k_mask(int64_t hw, const double* __restrict__ maps, const int64_t* __restrict__ stats_i64,
                        const double* __restrict__ stats_f64, double threshold, uint8_t* __restrict__ mask,
                        int64_t i0, int64_t i1, int n_maps = 0) {
-    int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = i0 + V * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (i >= i1) return;
     maps += (size_t)blockIdx.y * n_maps * hw;
     stats_i64 += (size_t)blockIdx.y * 16;
     stats_f64 += (size_t)blockIdx.y * (8 + 2 * n_maps);
     mask += (size_t)blockIdx.y * hw;
-    int lvl = (int)stats_i64[SF_STAT_LEVEL];
-    double lo = stats_f64[SF_STATF_MIN], hi = stats_f64[SF_STATF_MAX];
-    uint8_t v = 0;
-    if (!(hi <= lo)) v = ((maps[(size_t)lvl * hw + i] - lo) / (hi - lo)) > threshold;
-    mask[i] = v;
+    const int lvl = (int)stats_i64[SF_STAT_LEVEL];
+    const double lo = stats_f64[SF_STATF_MIN], hi = stats_f64[SF_STATF_MAX];
+    const double* m = maps + (size_t)lvl * hw + i;
+    if (V == 4) {
+        const double2 a = reinterpret_cast<const double2*>(m)[0], b = reinterpret_cast<const double2*>(m)[1];
+        const double x[4] = {a.x, a.y, b.x, b.y};
+        uint32_t packed = 0;
+        if (!(hi <= lo)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) packed |= (uint32_t)(((x[k] - lo) / (hi - lo)) > threshold) << (8 * k);
+        }
+        *reinterpret_cast<uint32_t*>(mask + i) = packed;
+    } else {
+        uint8_t v = 0;
+        if (!(hi <= lo)) v = ((m[0] - lo) / (hi - lo)) > threshold;
+        mask[i] = v;
+    }
+}
+
+static void launch_mask(int64_t hw, const double* maps, const int64_t* stats_i64, const double* stats_f64,
+                        double threshold, uint8_t* mask, int64_t i0, int64_t i1, int n_queries, int n_maps,
+                        cudaStream_t st) {
+    const bool vec = hw % 4 == 0 && i0 % 4 == 0 && i1 % 4 == 0 && ((uintptr_t)maps & 15) == 0 &&
+                     ((uintptr_t)mask & 3) == 0;
+    if (vec)
+        k_mask<4><<<dim3(ceil_div((i1 - i0) / 4, 256), n_queries), 256, 0, st>>>(hw, maps, stats_i64, stats_f64,
+                                                                                  threshold, mask, i0, i1, n_maps);
+    else
+        k_mask<1><<<dim3(ceil_div(i1 - i0, 256), n_queries), 256, 0, st>>>(hw, maps, stats_i64, stats_f64, threshold,
+                                                                           mask, i0, i1, n_maps);
 }
 
 __global__ void k_mask_rows(int64_t hw, const double* __restrict__ maps, int level, double lo, double hi,
@@ -397,8 +425,7 @@ void launch_filter_select(int n_maps, int H, int W, const double* raw, int windo
                                                 stats_f64);
     const int64_t hw = (int64_t)H * W, i0 = (int64_t)y0 * W, i1 = (int64_t)y1 * W;
     if (mask && i1 > i0)
-        k_mask<<<ceil_div(i1 - i0, 256), 256, 0, st>>>(hw, filtered, stats_i64, stats_f64, threshold, mask, i0,
-                                                       i1);
+        launch_mask(hw, filtered, stats_i64, stats_f64, threshold, mask, i0, i1, 1, 0, st);
 }
 
 // n_queries filter + select + mask passes in three launches: raw / filtered
@@ -421,8 +448,7 @@ void launch_filter_select_batch(int n_queries, int n_maps, int H, int W, const d
                                                        stats_f64);
     const int64_t hw = (int64_t)H * W;
     if (masks)
-        k_mask<<<dim3(ceil_div(hw, 256), n_queries), 256, 0, st>>>(hw, filtered, stats_i64, stats_f64, threshold,
-                                                                   masks, 0, hw, n_maps);
+        launch_mask(hw, filtered, stats_i64, stats_f64, threshold, masks, 0, hw, n_queries, n_maps, st);
 }
 
 void launch_select_segment(int n_maps, int H, int W, const double* maps, int fixed_level,
@@ -436,7 +462,7 @@ void launch_select_segment(int n_maps, int H, int W, const double* maps, int fix
     k_finalize_select<<<1, 32 * n_maps, 0, st>>>(n_maps, kRedBlocks, W, partial, fixed_level, stats_i64,
                                                   stats_f64);
     if (mask && i1 > i0)
-        k_mask<<<ceil_div(i1 - i0, 256), 256, 0, st>>>(hw, maps, stats_i64, stats_f64, threshold, mask, i0, i1);
+        launch_mask(hw, maps, stats_i64, stats_f64, threshold, mask, i0, i1, 1, 0, st);
 }
 
 }  // namespace sf
