@@ -341,14 +341,16 @@ template <int RC>
 __global__ void __launch_bounds__(256) k_box2d_stats(int H, int W, const double* __restrict__ in, int r_rt,
                                                      double area, double* __restrict__ out,
                                                      MaxMin* __restrict__ partial, int y0, int y1) {
-    __shared__ double tin[kBoxTY + 2 * kBoxRMax][kBoxTX + 2 * kBoxRMax];
-    __shared__ double trs[kBoxTY + 2 * kBoxRMax][kBoxTX];
+    // a fixed radius sizes the halo exactly, which leaves room for 32-row tiles
+    constexpr int TY = RC > 0 ? 2 * kBoxTY : kBoxTY, RR = RC > 0 ? RC : kBoxRMax;
+    __shared__ double tin[TY + 2 * RR][kBoxTX + 2 * RR];
+    __shared__ double trs[TY + 2 * RR][kBoxTX];
     const int r = RC > 0 ? RC : r_rt;
     const int m = blockIdx.z;
-    const int x0 = blockIdx.x * kBoxTX, ty0 = y0 + blockIdx.y * kBoxTY;
+    const int x0 = blockIdx.x * kBoxTX, ty0 = y0 + blockIdx.y * TY;
     const int64_t hw = (int64_t)H * W;
     const double* src = in + (size_t)m * hw;
-    const int nr = kBoxTY + 2 * r, nc = kBoxTX + 2 * r;
+    const int nr = TY + 2 * r, nc = kBoxTX + 2 * r;
     for (int i = threadIdx.x; i < nr * nc; i += blockDim.x) {
         const int rr = i / nc, cc = i - rr * nc;
         const int yy = min(max(ty0 - r + rr, 0), H - 1), xx = min(max(x0 - r + cc, 0), W - 1);
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(256) k_box2d_stats(int H, int W, const double*
     }
     __syncthreads();
     MaxMin best{-INFINITY, INT64_MAX, INFINITY};
-    for (int i = threadIdx.x; i < kBoxTY * kBoxTX; i += blockDim.x) {
+    for (int i = threadIdx.x; i < TY * kBoxTX; i += blockDim.x) {
         const int yl = i / kBoxTX, x = i - yl * kBoxTX;
         const int y = ty0 + yl, gx = x0 + x;
         if (y >= y1 || gx >= W) continue;
@@ -394,13 +396,17 @@ __global__ void __launch_bounds__(256) k_box2d_stats(int H, int W, const double*
         partial[(size_t)m * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = rsum;
 }
 
-static void launch_box2d_stats(dim3 grid, int H, int W, const double* in, int r, double* out, MaxMin* partial,
-                               int y0, int y1, cudaStream_t st) {
+// returns the number of partials per map (the grid's x * y)
+static int launch_box2d_stats(int n_maps, int H, int W, const double* in, int r, double* out, MaxMin* partial,
+                              int y0, int y1, cudaStream_t st) {
     const double area = (double)(2 * r + 1) * (double)(2 * r + 1);
+    const int ty = r == 5 ? 2 * kBoxTY : kBoxTY;
+    dim3 grid(ceil_div(W, kBoxTX), ceil_div(y1 - y0, ty), n_maps);
     if (r == 5)
         k_box2d_stats<5><<<grid, 256, 0, st>>>(H, W, in, r, area, out, partial, y0, y1);
     else
         k_box2d_stats<0><<<grid, 256, 0, st>>>(H, W, in, r, area, out, partial, y0, y1);
+    return (int)(grid.x * grid.y);
 }
 
 static int box_tiles(int H, int W) { return ceil_div(W, kBoxTX) * ceil_div(H, kBoxTY); }
@@ -419,10 +425,8 @@ void launch_filter_select(int n_maps, int H, int W, const double* raw, int windo
     if (y1 <= y0 || W == 0) return;
     const int r = window / 2;
     MaxMin* partial = (MaxMin*)ws;
-    dim3 grid(ceil_div(W, kBoxTX), ceil_div(y1 - y0, kBoxTY), n_maps);
-    launch_box2d_stats(grid, H, W, raw, r, filtered, partial, y0, y1, st);
-    k_finalize_select_wide<<<1, 1024, 0, st>>>(n_maps, (int)(grid.x * grid.y), W, partial, fixed_level, stats_i64,
-                                                stats_f64);
+    const int nblk = launch_box2d_stats(n_maps, H, W, raw, r, filtered, partial, y0, y1, st);
+    k_finalize_select_wide<<<1, 1024, 0, st>>>(n_maps, nblk, W, partial, fixed_level, stats_i64, stats_f64);
     const int64_t hw = (int64_t)H * W, i0 = (int64_t)y0 * W, i1 = (int64_t)y1 * W;
     if (mask && i1 > i0)
         launch_mask(hw, filtered, stats_i64, stats_f64, threshold, mask, i0, i1, 1, 0, st);
@@ -442,10 +446,8 @@ void launch_filter_select_batch(int n_queries, int n_maps, int H, int W, const d
     if (n_queries == 0 || W == 0 || H == 0) return;
     const int r = window / 2;
     MaxMin* partial = (MaxMin*)ws;
-    dim3 grid(ceil_div(W, kBoxTX), ceil_div(H, kBoxTY), n_maps * n_queries);
-    launch_box2d_stats(grid, H, W, raw, r, filtered, partial, 0, H, st);
-    k_finalize_select_wide<<<n_queries, 1024, 0, st>>>(n_maps, (int)(grid.x * grid.y), W, partial, -1, stats_i64,
-                                                       stats_f64);
+    const int nblk = launch_box2d_stats(n_maps * n_queries, H, W, raw, r, filtered, partial, 0, H, st);
+    k_finalize_select_wide<<<n_queries, 1024, 0, st>>>(n_maps, nblk, W, partial, -1, stats_i64, stats_f64);
     const int64_t hw = (int64_t)H * W;
     if (masks)
         launch_mask(hw, filtered, stats_i64, stats_f64, threshold, masks, 0, hw, n_queries, n_maps, st);
