@@ -274,14 +274,29 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
     __shared__ unsigned long long carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    for (int base = 0; base < n_tiles; base += 1024) {
-        int t = base + threadIdx.x;
-        unsigned long long c0 = (t < n_tiles) ? counts[t] : 0;
-        unsigned long long c = (t < n_tiles) ? c0 + counts[n_tiles + t] : 0, ex, tot;
-        Scan(tmp).ExclusiveSum(c, ex, tot);
-        if (t < n_tiles) {
-            offsets[t] = (uint32_t)(carry + ex);
-            cursor[t] = (uint32_t)(carry + ex + c0);
+    // 8 consecutive tiles per thread and pass: one block scan covers 8192 tiles
+    constexpr int kPer = 8;
+    for (int base = 0; base < n_tiles; base += 1024 * kPer) {
+        const int t0 = base + threadIdx.x * kPer;
+        unsigned long long c0[kPer], c[kPer], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int t = t0 + k;
+            c0[k] = (t < n_tiles) ? counts[t] : 0;
+            c[k] = (t < n_tiles) ? c0[k] + counts[n_tiles + t] : 0;
+            sum += c[k];
+        }
+        unsigned long long ex, tot;
+        Scan(tmp).ExclusiveSum(sum, ex, tot);
+        ex += carry;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int t = t0 + k;
+            if (t < n_tiles) {
+                offsets[t] = (uint32_t)ex;
+                cursor[t] = (uint32_t)(ex + c0[k]);
+            }
+            ex += c[k];
         }
         __syncthreads();
         if (threadIdx.x == 0) carry += tot;
