@@ -494,3 +494,20 @@ def test_sparse_equals_dense_coefficient_render(rng, L):
     sparse = sf.splat_multilevel(scene, cam, max_elements=1 << 40).data
     dense = sf.render_dense(scene, cam, rows, tag="coefficient", max_elements=1 << 40).data
     assert np.abs(sparse - dense).max() <= W_TOL
+
+
+def test_query_sweep_ragged_image(rng):
+    """A pixel count that is not a multiple of the sweep kernel's 256-pixel tile
+    (and odd, so the relevancy rows are not 16-byte aligned): every prompt still
+    equals its own query_pipeline."""
+    scene = random_scene(rng, 2000, num_levels=3, L=64, K=4, D=32)
+    cam = make_camera(97, 71)
+    canon = rng.standard_normal((3, 32))
+    queries = [sf.QueryEmbedding(f"q{i}", rng.standard_normal(32)) for i in range(11)]
+    sweep = sf.query_sweep(scene, cam, queries, canon)
+    for q, r in zip(queries, sweep):
+        one = sf.query_pipeline(scene, cam, q, canon)
+        ref = [m.data for m in one.level_maps]
+        for b in range(3):
+            assert np.abs(r.level_maps[b].data - ref[b]).max() <= 1e-12
+        assert_selection_matches(ref, r.level, r.point, r.mask, one.level, one.point)
