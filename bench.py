@@ -388,6 +388,36 @@ def main():
                "h2d_bytes_per_step": int(qv.nbytes + canon.nbytes),
                "d2h_bytes_per_step": int(H * W + 16 * 8 + (8 + 2 * 8) * 8), "steps": n_e2e,
                "api": "paper_2507_07136_b200.query_pipeline(..., features='eager')"}
+        # the same frames through the pipelined serving API: per frame the query
+        # vector goes up from pinned memory and the mask + statistics come back;
+        # results are read one frame behind the submits
+        qstream = sf.QueryStream(scene, W, H, canon, features="eager")
+        for _ in range(3):
+            qstream.result(qstream.submit(cam, qe))
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        n_st = max(3, args.steps)
+        pending = None
+        for _ in range(n_st):
+            h = qstream.submit(cam, qe)
+            if pending is not None:
+                _ = qstream.result(pending).mask
+            pending = h
+        _ = qstream.result(pending).mask
+        qstream.close()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e["pipelined"] = {"value": world * n_st / dt, "unit": "frames/s", "steps": n_st,
+                            "h2d_bytes_per_step": int(qv.nbytes), "d2h_bytes_per_step": int(H * W + 16 * 8),
+                            "api": "paper_2507_07136_b200.QueryStream(..., features='eager').submit / .result"}
+        del qstream
+        torch.cuda.empty_cache()
 
     # feature-splat FPS (render + decode, no query post) and lazy-feature query FPS
     del pipe

@@ -389,3 +389,102 @@ def query_sweep(scene, cam, queries, canonicals, *, window: int = 11, threshold:
             cmap_thunk=(lambda cm=cm: cm), features=FeatureMapSet(levels=levels, thunk=_decode_lazy),
             mask=host_masks[i], degenerate=bool(st_i[i][N.STAT_DEGENERATE])))
     return results
+
+
+@dataclass
+class StreamResult:
+    """What one streamed query returns (the serving fields of QueryResult)."""
+
+    query: str
+    level: int
+    point: tuple
+    mask: np.ndarray      # (H, W) bool, this frame's own pinned host copy
+    degenerate: bool
+
+
+class QueryStream:
+    """Pipelined text queries over one scene at one image size (extension).
+
+    The reference answers one query_pipeline call at a time
+    (sparse_splat.py:243-297).  submit() enqueues a frame and returns at once:
+    the query vector is copied from pinned host memory, the frame runs
+    query_pipeline's work on the GPU (features="eager" also decodes the 3 x D
+    feature maps), and the mask and statistics are copied back into pinned
+    host buffers of that frame.  result() waits for that frame only.  Frames
+    overlap on the GPU (device.FramePipeline): frame i+1's projection / sort /
+    binning run under frame i's blend.  The canonicals are the stream's
+    constant and are uploaded once.  A frame whose pairs overflowed the pair
+    buffer is re-run through query_pipeline (which grows it) inside result().
+    """
+
+    def __init__(self, scene, width: int, height: int, canonicals, *, window: int = 11, threshold: float = 0.5,
+                 features: str = "lazy"):
+        import torch
+
+        from .device import FramePipeline, device_scene
+        cfg = scene.config
+        canon = np.asarray(canonicals, dtype=np.float64)
+        if canon.ndim != 2 or canon.shape[0] < 1 or canon.shape[1] != cfg.D:
+            raise ValidationError("canonicals must be a non-empty (n, D) array")
+        if window < 1 or window % 2 == 0:
+            raise ValidationError(f"filter window must be odd and >= 1, got {window}")
+        self.scene, self.W, self.H = scene, int(width), int(height)
+        self.canonicals, self.window, self.threshold = canon, int(window), float(threshold)
+        self.levels = tuple(range(cfg.num_levels))
+        self.features = features
+        self.ds = device_scene(scene)
+        if self.ds.bad_index:
+            raise ValidationError("coefficient index >= L")
+        eager = features == "eager"
+        fused = bool(N.load().sf_decode_fused(len(self.levels), cfg.L, cfg.K, cfg.D))
+        need_cmap = (eager and not fused) or len(self.levels) * cfg.L > 192
+        self.pipe = FramePipeline(self.ds, self.W, self.H, self.levels, coeff_map=need_cmap, features=eager,
+                                  query=True)
+        self.canon_dev = torch.from_numpy(canon).to(self.ds.device)
+        self._began = False
+
+    def submit(self, cam, query: QueryEmbedding):
+        import torch
+
+        from .device import QuerySpec
+        if (int(cam.width), int(cam.height)) != (self.W, self.H):
+            raise ValidationError("camera size differs from the stream's image size")
+        if query.vector.shape[0] != self.scene.config.D:
+            raise ValidationError("query dimension mismatch")
+        if not self._began:
+            self.pipe.begin()
+            self._began = True
+        hq = torch.from_numpy(np.ascontiguousarray(query.vector, dtype=np.float64)).pin_memory()
+        rs = self.pipe.render[self.pipe.k % 2]
+        with torch.cuda.stream(rs):
+            qd = hq.to(self.ds.device, non_blocking=True)
+        spec = QuerySpec(query.vector, self.canonicals, self.window, -1, self.threshold)
+        out = self.pipe.enqueue(cam, self.levels, query=spec, qdev=(qd, self.canon_dev))
+        hm = torch.empty((self.H, self.W), dtype=torch.uint8, pin_memory=True)
+        hi = torch.empty(16, dtype=torch.int64, pin_memory=True)
+        with torch.cuda.stream(rs):
+            hm.copy_(out.mask, non_blocking=True)
+            hi.copy_(out.stats_i64, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(rs)
+        return (ev, hm, hi, hq, qd, cam, query)
+
+    def result(self, handle) -> StreamResult:
+        ev, hm, hi, _, _, cam, query = handle
+        ev.synchronize()
+        st = hi.numpy()
+        if int(st[N.STAT_OVERFLOW]):
+            r = query_pipeline(self.scene, cam, query, self.canonicals, window=self.window,
+                               threshold=self.threshold, instrument=False, features=self.features,
+                               max_elements=1 << 62)
+            for e in self.pipe.engines:
+                e.pair_capacity = max(e.pair_capacity, self.ds.engine.pair_capacity)
+            return StreamResult(query.name, r.level, r.point, r.mask, bool(r.degenerate))
+        return StreamResult(query.name, self.levels[int(st[N.STAT_LEVEL])],
+                            (int(st[N.STAT_ROW]), int(st[N.STAT_COL])), hm.numpy().view(np.bool_),
+                            bool(st[N.STAT_DEGENERATE]))
+
+    def close(self):
+        if self._began:
+            self.pipe.end()
+            self._began = False

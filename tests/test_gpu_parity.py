@@ -511,3 +511,22 @@ def test_query_sweep_ragged_image(rng):
         for b in range(3):
             assert np.abs(r.level_maps[b].data - ref[b]).max() <= 1e-12
         assert_selection_matches(ref, r.level, r.point, r.mask, one.level, one.point)
+
+
+@pytest.mark.parametrize("features", ["lazy", "eager"])
+def test_query_stream_matches_query_pipeline(rng, features):
+    """QueryStream (pipelined frames, per-frame pinned H2D / D2H) returns every
+    frame's query_pipeline result: level, point and mask, bit for bit."""
+    from paper_2507_07136_b200 import synthetic
+    scene = random_scene(rng, 3000, num_levels=3, L=64, K=4, D=512)
+    canon = rng.standard_normal((4, 512))
+    cams = [make_camera(96, 72)] + [synthetic.make_camera(96, 72) for _ in range(1)]
+    qs = [sf.QueryEmbedding(f"q{i}", rng.standard_normal(512)) for i in range(5)]
+    stream = sf.QueryStream(scene, 96, 72, canon, features=features)
+    handles = [stream.submit(cams[i % 2], q) for i, q in enumerate(qs)]
+    results = [stream.result(h) for h in handles]
+    stream.close()
+    for i, (q, r) in enumerate(zip(qs, results)):
+        one = sf.query_pipeline(scene, cams[i % 2], q, canon, features=features, max_elements=1 << 40)
+        assert (r.level, r.point, r.degenerate) == (one.level, one.point, one.degenerate)
+        assert np.array_equal(r.mask, one.mask)
