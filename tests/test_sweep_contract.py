@@ -25,3 +25,13 @@ def test_query_sweep_validates_before_work(rng):
         sf.query_sweep(scene, cam, q, canon, tile_size=8)        # kernels are 16x16-tile
     with pytest.raises(sf.ResourceLimitError):
         sf.query_sweep(scene, cam, q, canon, max_elements=10)    # render budget
+
+
+def test_query_stream_validates_before_work(rng):
+    scene = random_scene(rng, 50, num_levels=2, L=16, K=4, D=8)
+    with pytest.raises(sf.ValidationError):
+        sf.QueryStream(scene, 32, 24, np.zeros((0, 8)))
+    with pytest.raises(sf.ValidationError):
+        sf.QueryStream(scene, 32, 24, rng.standard_normal((2, 7)))
+    with pytest.raises(sf.ValidationError):
+        sf.QueryStream(scene, 32, 24, rng.standard_normal((2, 8)), window=6)
