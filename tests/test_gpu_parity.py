@@ -530,3 +530,21 @@ def test_query_stream_matches_query_pipeline(rng, features):
         one = sf.query_pipeline(scene, cams[i % 2], q, canon, features=features, max_elements=1 << 40)
         assert (r.level, r.point, r.degenerate) == (one.level, one.point, one.degenerate)
         assert np.array_equal(r.mask, one.mask)
+
+
+def test_query_stream_overflow_rerun(rng):
+    """A streamed frame whose pairs overflow the pipeline's pair buffer is
+    re-run through query_pipeline (which grows the buffer): same answer."""
+    scene = random_scene(rng, 3000, num_levels=3, L=64, K=4, D=64)
+    canon = rng.standard_normal((4, 64))
+    cam = make_camera(96, 72)
+    q = sf.QueryEmbedding("q", rng.standard_normal(64))
+    stream = sf.QueryStream(scene, 96, 72, canon)
+    for e in stream.pipe.engines:
+        e.pair_capacity = 64  # far below the frame's pairs
+    r = stream.result(stream.submit(cam, q))
+    stream.close()
+    one = sf.query_pipeline(scene, cam, q, canon)
+    assert (r.level, r.point) == (one.level, one.point)
+    assert np.array_equal(r.mask, one.mask)
+    assert all(e.pair_capacity > 64 for e in stream.pipe.engines)
