@@ -1147,7 +1147,7 @@ static_assert(kSwThreads == kSwPx, "the canonical pass maps one thread to one pi
 __global__ void __launch_bounds__(kSwThreads, 2) k_relevancy_sweep(int64_t P, int n_ch, const float* __restrict__ cmap,
                                                                 const double* __restrict__ proj, int n_levels, int L,
                                                                 int nq, int nc, double* __restrict__ out,
-                                                                int64_t pstride) {
+                                                                int64_t pstride, int64_t lstride) {
     extern __shared__ __align__(16) unsigned char sw_smem[];
     const int nqp = (nq + kSwCols - 1) / kSwCols * kSwCols, nvp = nqp + kSwCols, nv = nq + nc;
     double* pj = reinterpret_cast<double*>(sw_smem);       // [L][nvp]: prompts, pad, canonicals, pad
@@ -1238,7 +1238,7 @@ __global__ void __launch_bounds__(kSwThreads, 2) k_relevancy_sweep(int64_t P, in
                     double v[4];
 #pragma unroll
                     for (int r = 0; r < 4; ++r) v[r] = sigmoid2(acc[r][j] - lmax[r]);
-                    double* o = out + (size_t)(c0 + j) * pstride + (size_t)b * P + base + px0;
+                    double* o = out + (size_t)(c0 + j) * pstride + (size_t)b * lstride + base + px0;
                     if (px0 + 3 < np && (((uintptr_t)o) & 15) == 0) {
                         reinterpret_cast<double2*>(o)[0] = make_double2(v[0], v[1]);
                         reinterpret_cast<double2*>(o)[1] = make_double2(v[2], v[3]);
@@ -1254,7 +1254,8 @@ __global__ void __launch_bounds__(kSwThreads, 2) k_relevancy_sweep(int64_t P, in
 }
 
 int launch_relevancy_sweep(int64_t P, int n_ch, const float* cmap, const double* proj, int n_levels, int L, int nq,
-                           int n_canon, double* out, int64_t out_prompt_stride, cudaStream_t st) {
+                           int n_canon, double* out, int64_t out_prompt_stride, int64_t out_level_stride,
+                           cudaStream_t st) {
     const int nvp = (nq + kSwCols - 1) / kSwCols * kSwCols + kSwCols;
     const size_t smem = sizeof(double) * (size_t)L * nvp + sizeof(float) * (size_t)L * kSwPx +
                         sizeof(double) * kSwPx;
@@ -1268,7 +1269,7 @@ int launch_relevancy_sweep(int64_t P, int n_ch, const float* cmap, const double*
     }
     const int blocks = (int)std::min<int64_t>(ceil_div(P, kSwPx), std::max(1, 148 * 2 / n_levels));  // one wave
     k_relevancy_sweep<<<dim3(blocks, n_levels), kSwThreads, smem, st>>>(P, n_ch, cmap, proj, n_levels, L, nq, n_canon, out,
-                                                        out_prompt_stride);
+                                                        out_prompt_stride, out_level_stride);
     return 0;
 }
 

@@ -140,7 +140,7 @@ static int validate_scene_cam(const SfScene* s, const SfCamera* cam) {
 // differ, `handoff` (a cudaEvent_t) orders them.
 static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q, const SfFrame* f,
                         void* workspace, size_t workspace_bytes, cudaStream_t st_prep, cudaStream_t st,
-                        cudaEvent_t handoff) {
+                        cudaEvent_t handoff, int band_halo = -1) {
     int rc = validate_scene_cam(s, cam);
     if (rc) return rc;
     if (!f || f->n_levels < 1 || f->n_levels > kMaxLevels)
@@ -181,7 +181,9 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
     if (!band && (f->band_y0 != 0 || f->band_y1 != 0))
         return fail(SF_ERR_VALIDATION, "empty band [%d, %d)", f->band_y0, f->band_y1);
     const int oy0 = band ? f->band_y0 : 0, oy1 = band ? f->band_y1 : H;
-    const int halo = (q && band) ? q->window / 2 : 0;
+    // band mode renders the owned rows +- the mean-filter halo (a sweep passes
+    // its window's halo, having no SfQuery)
+    const int halo = band ? (q ? q->window / 2 : (band_halo > 0 ? band_halo : 0)) : 0;
     const int tiles_x = (W + SF_TILE - 1) / SF_TILE, tiles_y = (H + SF_TILE - 1) / SF_TILE;
     const int tr0 = band ? max(0, oy0 - halo) / SF_TILE : 0;
     const int tr1 = band ? (min(H, oy1 + halo) + SF_TILE - 1) / SF_TILE : tiles_y;
@@ -334,38 +336,44 @@ extern "C" int sf_query_sweep(const SfScene* s, const SfCamera* cam, const SfFra
         return fail(SF_ERR_VALIDATION, "bad prompt buffers");
     if (n_canon < 1 || n_canon > kMaxCanon) return fail(SF_ERR_VALIDATION, "1..%d canonicals required", kMaxCanon);
     if (window < 1 || window % 2 == 0) return fail(SF_ERR_VALIDATION, "filter window must be odd and >= 1");
-    if (f->band_y0 != 0 || f->band_y1 != 0) return fail(SF_ERR_VALIDATION, "sweeps render the whole image");
-    int rc = render_frame(s, cam, nullptr, f, workspace, workspace_bytes, st, st, nullptr);
+    int rc = render_frame(s, cam, nullptr, f, workspace, workspace_bytes, st, st, nullptr, window / 2);
     if (rc) return rc;
     const int W = cam->width, H = cam->height, L = s->L, D = s->D, nl = f->n_levels;
+    // band mode (tile bands of one view): owned rows [oy0, oy1), rendered rows
+    // [ry0, ry1) = the tile rows covering the owned rows +- the filter halo
+    const bool band = f->band_y1 > f->band_y0;
+    const int oy0 = band ? f->band_y0 : 0, oy1 = band ? f->band_y1 : H, halo = band ? window / 2 : 0;
+    const int ry0 = band ? max(0, oy0 - halo) / SF_TILE * SF_TILE : 0;
+    const int ry1 = band ? min(H, (min(H, oy1 + halo) + SF_TILE - 1) / SF_TILE * SF_TILE) : H;
     FrameWs ws;
     carve_frame(workspace, workspace_bytes, s->num_gaussians, W, H, nl, L, s->K, D, f->pair_capacity, &ws);
     LevelSelDev lv;
     lv.n = nl;
     for (int b = 0; b < nl; ++b) lv.lv[b] = f->host_levels[b];
-    const int64_t hw = (int64_t)W * H, qstride = nl * hw;
+    const int64_t hw = (int64_t)W * H, qstride = nl * hw, prow = (int64_t)W * (ry1 - ry0);
     double* raw = f->relevancy_raw;  // (n_prompts, nl, H, W)
+    const float* cmap_rows = f->coeff_map + (size_t)ry0 * W * nl * L;
     // every prompt starts from the frame's counters, as a single query would
     for (int i = 0; i < n_prompts; ++i) {
         cudaMemcpyAsync(stats_i64 + (size_t)i * 16, ws.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
         cudaMemcpyAsync(stats_f64 + (size_t)i * (8 + 2 * nl), ws.stats_f, (8 + 2 * nl) * sizeof(double),
                         cudaMemcpyDeviceToDevice, st);
     }
-    // relevancy: the map read once per chunk of prompts (projected-codebook
-    // columns: chunk prompts + canonicals, within proj_cb's 1 + kMaxCanon)
+    // relevancy of the rendered rows: the map read once per chunk of prompts
+    // (projected-codebook columns: chunk prompts + canonicals, within proj_cb's 1 + kMaxCanon)
     const int chunk = kMaxCanon + 1 - n_canon;
     bool batched = filter_select_fusable(window);
     for (int i0 = 0; i0 < n_prompts && batched; i0 += chunk) {
         const int nq = std::min(chunk, n_prompts - i0);
         launch_project_vectors(s->codebooks, lv, L, D, prompts + (size_t)i0 * D, nq, canon, n_canon, ws.proj_cb, st);
-        if (launch_relevancy_sweep(hw, nl * L, f->coeff_map, ws.proj_cb, nl, L, nq, n_canon, raw + i0 * qstride,
-                                   qstride, st)) {
+        if (launch_relevancy_sweep(prow, nl * L, cmap_rows, ws.proj_cb, nl, L, nq, n_canon,
+                                   raw + i0 * qstride + (size_t)ry0 * W, qstride, hw, st)) {
             batched = false;  // shape outside the sweep kernel: per-prompt passes below
         }
     }
     if (batched) {
-        // filter + statistics + mask of many prompts per launch; partials in
-        // the row-sum buffer (unused by the fused filter)
+        // filter + statistics + mask of many prompts per launch over the owned
+        // rows; partials in the row-sum buffer (unused by the fused filter)
         const size_t per_q = filter_select_batch_ws_bytes(1, nl, H, W) - 256;
         const size_t cap = sizeof(double) * (size_t)qstride - 256;
         const int qb = (int)std::max<size_t>(1, std::min<size_t>(n_prompts, cap / per_q));
@@ -373,23 +381,23 @@ extern "C" int sf_query_sweep(const SfScene* s, const SfCamera* cam, const SfFra
             const int nq = std::min(qb, n_prompts - i0);
             launch_filter_select_batch(nq, nl, H, W, raw + i0 * qstride, window, filtered + i0 * qstride, threshold,
                                        masks ? masks + i0 * hw : nullptr, stats_i64 + (size_t)i0 * 16,
-                                       stats_f64 + (size_t)i0 * (8 + 2 * nl), ws.filter_tmp, st);
+                                       stats_f64 + (size_t)i0 * (8 + 2 * nl), ws.filter_tmp, st, oy0, oy1);
         }
         return check_cuda("sf_query_sweep");
     }
     for (int i = 0; i < n_prompts; ++i) {
         double* ri = raw + i * qstride;
         launch_project_codebook(s->codebooks, lv, L, D, prompts + (size_t)i * D, canon, n_canon, ws.proj_cb, st);
-        launch_relevancy_from_cmap(hw, nl * L, f->coeff_map, ws.proj_cb, nl, L, n_canon, ri, hw, st);
+        launch_relevancy_from_cmap(prow, nl * L, cmap_rows, ws.proj_cb, nl, L, n_canon, ri + (size_t)ry0 * W, hw, st);
         double* fi = filtered + i * qstride;
         uint8_t* mi = masks ? masks + i * hw : nullptr;
         int64_t* si = stats_i64 + (size_t)i * 16;
         double* sf = stats_f64 + (size_t)i * (8 + 2 * nl);
         if (filter_select_fusable(window)) {
-            launch_filter_select(nl, H, W, ri, window, fi, -1, threshold, mi, si, sf, ws.sel_ws, st);
+            launch_filter_select(nl, H, W, ri, window, fi, -1, threshold, mi, si, sf, ws.sel_ws, st, oy0, oy1);
         } else {
-            launch_mean_filter(nl, H, W, ri, window, ws.filter_tmp, fi, st);
-            launch_select_segment(nl, H, W, fi, -1, threshold, mi, si, sf, ws.sel_ws, st);
+            launch_mean_filter(nl, H, W, ri, window, ws.filter_tmp, fi, st, oy0, oy1);
+            launch_select_segment(nl, H, W, fi, -1, threshold, mi, si, sf, ws.sel_ws, st, oy0, oy1);
         }
     }
     return check_cuda("sf_query_sweep");

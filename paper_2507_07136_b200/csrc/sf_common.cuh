@@ -295,7 +295,8 @@ void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const do
 // launch_project_vectors; out (nq, n_levels, P) (prompt-major).  Returns
 // nonzero when the shape is unsupported (n_canon > 8, L % 4, n_ch % 4).
 int launch_relevancy_sweep(int64_t P, int n_ch, const float* cmap, const double* proj, int n_levels, int L,
-                           int nq, int n_canon, double* out, int64_t out_prompt_stride, cudaStream_t st);
+                           int nq, int n_canon, double* out, int64_t out_prompt_stride, int64_t out_level_stride,
+                           cudaStream_t st);
 
 // sf_post.cu
 void launch_project_codebook(const float* codebooks, const LevelSelDev& levels, int L, int D,
@@ -307,7 +308,7 @@ void launch_project_vectors(const float* codebooks, const LevelSelDev& levels, i
 size_t filter_select_batch_ws_bytes(int n_queries, int n_maps, int H, int W);
 void launch_filter_select_batch(int n_queries, int n_maps, int H, int W, const double* raw, int window,
                                 double* filtered, double threshold, uint8_t* masks, int64_t* stats_i64,
-                                double* stats_f64, void* ws, cudaStream_t st);
+                                double* stats_f64, void* ws, cudaStream_t st, int y0 = 0, int y1 = 0);
 void launch_relevancy_f32(int64_t P, int D, const float* f, const double* q, const double* c,
                           int nc, double* out, cudaStream_t st);
 void launch_relevancy_f64(int64_t P, int D, const double* f, const double* q, const double* c,

@@ -442,15 +442,17 @@ size_t filter_select_batch_ws_bytes(int n_queries, int n_maps, int H, int W) {
 
 void launch_filter_select_batch(int n_queries, int n_maps, int H, int W, const double* raw, int window,
                                 double* filtered, double threshold, uint8_t* masks, int64_t* stats_i64,
-                                double* stats_f64, void* ws, cudaStream_t st) {
-    if (n_queries == 0 || W == 0 || H == 0) return;
+                                double* stats_f64, void* ws, cudaStream_t st, int y0, int y1) {
+    if (y1 <= y0) y0 = 0, y1 = H;
+    if (n_queries == 0 || W == 0 || y1 <= y0) return;
     const int r = window / 2;
     MaxMin* partial = (MaxMin*)ws;
-    const int nblk = launch_box2d_stats(n_maps * n_queries, H, W, raw, r, filtered, partial, 0, H, st);
+    const int nblk = launch_box2d_stats(n_maps * n_queries, H, W, raw, r, filtered, partial, y0, y1, st);
     k_finalize_select_wide<<<n_queries, 1024, 0, st>>>(n_maps, nblk, W, partial, -1, stats_i64, stats_f64);
     const int64_t hw = (int64_t)H * W;
     if (masks)
-        launch_mask(hw, filtered, stats_i64, stats_f64, threshold, masks, 0, hw, n_queries, n_maps, st);
+        launch_mask(hw, filtered, stats_i64, stats_f64, threshold, masks, (int64_t)y0 * W, (int64_t)y1 * W, n_queries,
+                    n_maps, st);
 }
 
 void launch_select_segment(int n_maps, int H, int W, const double* maps, int fixed_level,

@@ -385,11 +385,13 @@ class FrameEngine:
 
 
     def sweep(self, cam, levels, out: FrameOutputs, prompts: np.ndarray, canonicals: np.ndarray, *,
-              window: int = 11, threshold: float = 0.5):
+              window: int = 11, threshold: float = 0.5, band=None):
         """Render ``out.coeff_map`` once, then run the query post of every
         prompt over it (sf_query_sweep); returns device tensors
         (filtered (n, levels, H, W) fp64, masks (n, H, W) u8, stats_i64 (n, 16),
-        stats_f64 (n, 8 + 2 levels)) and the host statistics, after one sync."""
+        stats_f64 (n, 8 + 2 levels)) and the host statistics, after one sync.
+        ``band=(y0, y1)``: tile-band mode (only those rows are owned; the
+        statistics cover them and the masks are written there)."""
         cfg = self.ds.config
         dev = self.ds.device
         n, nl = int(prompts.shape[0]), len(levels)
@@ -418,6 +420,8 @@ class FrameEngine:
                 fr.relevancy_raw = N.ptr(raw)
                 fr.stats_i64 = N.ptr(out.stats_i64)
                 fr.stats_f64 = N.ptr(out.stats_f64)
+                if band is not None:
+                    fr.band_y0, fr.band_y1 = int(band[0]), int(band[1])
                 if nl * cfg.K <= 16:
                     fr.chan_by_row = N.ptr(self.channel_plan(levels))
                 N.check(lib.sf_query_sweep(ctypes.byref(self.ds.struct), ctypes.byref(camc), ctypes.byref(fr),

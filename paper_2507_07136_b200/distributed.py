@@ -100,6 +100,44 @@ def global_selection(level_max, level_argmax, level_min, group=None):
     return level, int(gidx[level]), float(gmin[level]), float(gmax[level])
 
 
+def combine_selection_many(level_max, level_argmax, level_min):
+    """combine_selection for many prompts: arrays (bands, prompts, levels) ->
+    one (level, flat index, min, max) per prompt."""
+    mx, am, mn = (np.asarray(a) for a in (level_max, level_argmax, level_min))
+    return [combine_selection(mx[:, i], am[:, i], mn[:, i]) for i in range(mx.shape[1])]
+
+
+def global_selection_many(level_max, level_argmax, level_min, group=None):
+    """global_selection for many prompts at once: (prompts, levels) arrays of this
+    rank's band -> one (level, flat index, min, max) per prompt, with the same
+    two max-all-reduces (of n_prompts x levels int64 keys) for all prompts."""
+    import torch
+    import torch.distributed as dist
+
+    vbits = np.ascontiguousarray(level_max, dtype=np.float64).view(np.int64)
+    idx = np.asarray(level_argmax, dtype=np.int64)
+    mbits = np.ascontiguousarray(level_min, dtype=np.float64).view(np.int64)
+    n, nl = vbits.shape
+    t = torch.tensor(np.concatenate([vbits.ravel(), -mbits.ravel()]), dtype=torch.int64)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    t = t.to(dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    tt = t.cpu().numpy()
+    gmax_bits = tt[:n * nl].reshape(n, nl)
+    gmin_bits = (-tt[n * nl:]).reshape(n, nl)
+    cand = np.where(vbits == gmax_bits, idx, np.iinfo(np.int64).max)
+    ti = torch.tensor(-cand.ravel(), dtype=torch.int64).to(dev)
+    dist.all_reduce(ti, op=dist.ReduceOp.MAX, group=group)
+    gidx = (-ti).cpu().numpy().reshape(n, nl)
+    gmax = gmax_bits.view(np.float64)
+    gmin = gmin_bits.view(np.float64)
+    out = []
+    for i in range(n):
+        level = int(np.argmax(gmax[i]))  # ties -> lowest level (query.py:111-118)
+        out.append((level, int(gidx[i, level]), float(gmin[i, level]), float(gmax[i, level])))
+    return out
+
+
 def gather_results(local: "torch.Tensor", group=None) -> "torch.Tensor":
     """All-gather one equally shaped result tensor per rank (final maps / masks)."""
     import torch
@@ -189,3 +227,69 @@ def _fixed_level_selection(mx, am, mn, level, group):
     one = [mx[level]], [am[level]], [mn[level]]
     _, idx, lo, hi = global_selection(*one, group=group)
     return level, idx, lo, hi
+
+
+@dataclass
+class BandSweep:
+    """One rank's share of a tile-band sharded prompt sweep (config E)."""
+
+    band: Band
+    selections: list          # per prompt: (level, (row, col), lo, hi, degenerate)
+    filtered: object          # (prompts, levels, H, W) fp64; owned rows valid
+    masks: object             # (prompts, H, W) u8; owned rows valid
+
+
+def band_sweep_statistics(engine, cam, levels, prompts, canonicals, world_size: int, rank: int, *,
+                          window: int = 11, threshold: float = 0.5):
+    """Render the band of ``rank`` once and run every prompt over its owned rows:
+    (band, filtered, masks, per-prompt level max / first argmax / min arrays)."""
+    from . import _native as N
+    H, W = int(cam.height), int(cam.width)
+    band = band_rows(H, world_size, rank, halo=int(window) // 2)
+    out = engine.allocate(W, H, levels, coeff_map=True, mask=False)
+    filt, masks, st_i, st_f = engine.sweep(cam, levels, out, np.asarray(prompts, dtype=np.float64),
+                                           np.asarray(canonicals, dtype=np.float64), window=window,
+                                           threshold=threshold, band=(band.y0, band.y1))
+    nl = len(levels)
+    mx = st_f[:, N.STATF_LEVEL_MAX:N.STATF_LEVEL_MAX + nl]
+    mn = st_f[:, N.STATF_LEVEL_MAX + nl:N.STATF_LEVEL_MAX + 2 * nl]
+    am = st_i[:, N.STAT_LEVEL_ARGMAX:N.STAT_LEVEL_ARGMAX + nl]
+    return band, filt, masks, mx, am, mn
+
+
+def finish_band_sweep(band, filt, masks, selections, threshold: float, W: int, H: int) -> BandSweep:
+    """Write each prompt's mask rows of the band with its global selection."""
+    import ctypes
+
+    import torch
+
+    from . import _native as N
+    from .device import stream_ptr
+    lib = N.load()
+    out_sel = []
+    for i, (level, idx, lo, hi) in enumerate(selections):
+        N.check(lib.sf_mask_rows(N.ptr(filt[i]), H, W, int(level), ctypes.c_double(lo), ctypes.c_double(hi),
+                                 ctypes.c_double(threshold), int(band.y0), int(band.y1), N.ptr(masks[i]),
+                                 stream_ptr()))
+        out_sel.append((level, (idx // W, idx % W), lo, hi, not (hi > lo)))
+    torch.cuda.current_stream().synchronize()
+    return BandSweep(band, out_sel, filt, masks)
+
+
+def band_query_sweep(engine, cam, levels, prompts, canonicals, world_size: int, rank: int, *, window: int = 11,
+                     threshold: float = 0.5, group=None) -> BandSweep:
+    """query_sweep over the tile band of ``rank`` (config E: tile bands x prompts):
+    the band is rendered once, every prompt's relevancy / filter / statistics
+    cover the owned rows, one pair of all-reduces selects all prompts' level /
+    point / range (``global_selection_many``), and each prompt's mask rows are
+    written with its global normalisation.  Without a process group the
+    selection is the rank's own (world of 1)."""
+    import torch.distributed as dist
+
+    band, filt, masks, mx, am, mn = band_sweep_statistics(engine, cam, levels, prompts, canonicals, world_size,
+                                                          rank, window=window, threshold=threshold)
+    if dist.is_available() and dist.is_initialized():
+        sel = global_selection_many(mx, am, mn, group=group)
+    else:
+        sel = combine_selection_many(mx[None], am[None], mn[None])
+    return finish_band_sweep(band, filt, masks, sel, threshold, int(cam.width), int(cam.height))

@@ -95,3 +95,57 @@ def test_combine_selection_rules():
     am = [[9, 0], [4, 0]]
     level, idx, _, _ = combine_selection(mx, am, [[0.0, 0.0], [0.0, 0.0]])
     assert level == 0 and idx == 4
+
+
+def _worker_many(rank, world, port, results):
+    import torch.distributed as dist
+
+    from paper_2507_07136_b200.distributed import global_selection_many
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(1)
+    P, H, W = 5, 24, 10
+    maps = rng.random((P, 3, H, W)) * 0.9 + 0.05
+    maps[2, 1, 3, 4] = 0.995       # prompt 2: the max of level 1 in band 0 ...
+    maps[2, 1, 20, 1] = 0.995      # ... tied in band 1 (the lower flat index wins)
+    band = band_rows(H, world, rank, tile=8, halo=0)
+    sub = maps[:, :, band.y0:band.y1].reshape(P, 3, -1)
+    lmax, lmin = sub.max(axis=2), sub.min(axis=2)
+    rows, cols = np.divmod(sub.argmax(axis=2), W)
+    flat = (rows + band.y0) * W + cols
+    results[rank] = global_selection_many(lmax, flat, lmin)
+    dist.destroy_process_group()
+
+
+def test_band_sharded_selection_many_prompts():
+    """global_selection_many (one pair of all-reduces for every prompt of a
+    band sweep) equals the single-process selection prompt by prompt."""
+    from paper_2507_07136_b200.distributed import combine_selection_many
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker_many, args=(world, port, results), nprocs=world, join=True)
+    rng = np.random.default_rng(1)
+    P, H, W = 5, 24, 10
+    maps = rng.random((P, 3, H, W)) * 0.9 + 0.05
+    maps[2, 1, 3, 4] = 0.995
+    maps[2, 1, 20, 1] = 0.995
+    for p in range(P):
+        level = int(np.argmax(maps[p].reshape(3, -1).max(axis=1)))
+        idx = int(np.argmax(maps[p, level]))
+        for r in range(world):
+            lv, ix, mn, mx = results[r][p]
+            assert (lv, ix) == (level, idx)
+            assert mn == maps[p, level].min() and mx == maps[p, level].max()
+    assert results[0][2][:2] == (1, 3 * W + 4)
+    # the host twin over per-band statistics gives the same answers
+    stats = []
+    for r in range(world):
+        band = band_rows(H, world, r, tile=8, halo=0)
+        sub = maps[:, :, band.y0:band.y1].reshape(P, 3, -1)
+        rows, cols = np.divmod(sub.argmax(axis=2), W)
+        stats.append((sub.max(axis=2), (rows + band.y0) * W + cols, sub.min(axis=2)))
+    mx_b, am_b, mn_b = (np.stack(x) for x in zip(*stats))
+    assert combine_selection_many(mx_b, am_b, mn_b) == results[0]

@@ -548,3 +548,35 @@ def test_query_stream_overflow_rerun(rng):
     assert (r.level, r.point) == (one.level, one.point)
     assert np.array_equal(r.mask, one.mask)
     assert all(e.pair_capacity > 64 for e in stream.pipe.engines)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_band_sweep_stitches_to_the_full_sweep(rng, world):
+    """Config E end to end on one GPU: every band renders once and sweeps all
+    prompts over its owned rows; combining the bands' statistics selects each
+    prompt's level / point / range exactly as the full-frame sweep, and the
+    stitched filtered maps and masks equal it bit for bit."""
+    import torch
+    from paper_2507_07136_b200.device import device_scene
+    from paper_2507_07136_b200.distributed import (band_sweep_statistics, combine_selection_many,
+                                                   finish_band_sweep)
+    scene = random_scene(rng, 3000, num_levels=3, L=64, K=4, D=64)
+    cam = make_camera(112, 90)
+    canon = rng.standard_normal((4, 64))
+    prompts = rng.standard_normal((6, 64))
+    levels = (0, 1, 2)
+    eng = device_scene(scene).engine
+    full = sf.query_sweep(scene, cam, [sf.QueryEmbedding(f"q{i}", p) for i, p in enumerate(prompts)], canon)
+    parts = [band_sweep_statistics(eng, cam, levels, prompts, canon, world, r) for r in range(world)]
+    mx, am, mn = (np.stack([p[k] for p in parts]) for k in (3, 4, 5))
+    sel = combine_selection_many(mx, am, mn)
+    W = cam.width
+    for r, (band, filt, masks, *_ ) in enumerate(parts):
+        bs = finish_band_sweep(band, filt, masks, sel, 0.5, W, cam.height)
+        y0, y1 = band.y0, band.y1
+        for i, res in enumerate(full):
+            level, point, lo, hi, degenerate = bs.selections[i]
+            assert (level, point) == (res.level, res.point)
+            for b in range(3):
+                assert np.array_equal(filt[i, b, y0:y1].cpu().numpy(), res.level_maps[b].data[y0:y1])
+            assert np.array_equal(masks[i, y0:y1].cpu().numpy().astype(bool), res.mask[y0:y1])
