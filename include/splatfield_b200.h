@@ -180,6 +180,18 @@ int sf_render_frame_split(const SfScene* scene, const SfCamera* cam, const SfQue
                           void* stream_prepare, void* stream_render, void* handoff_event);
 
 /*
+ * The per-tile lists of the last frame rendered with `workspace` (same shape
+ * arguments as sf_frame_workspace_bytes): tile_offsets (n_tiles+1) u32 and
+ * tile_rows (pairs) u32 scene rows in canonical (depth, id) order per tile --
+ * TileBinning.tile_lists (projection.py:342-376) of the frame itself, for
+ * parity checks of the frame path's binning.  Synchronises `stream`.
+ */
+int sf_frame_tile_lists(int64_t num_gaussians, int32_t width, int32_t height, int32_t n_levels, int32_t L,
+                        int32_t K, int32_t D, int64_t pair_capacity, const void* workspace,
+                        size_t workspace_bytes, uint32_t* tile_offsets, uint32_t* tile_rows, int64_t max_pairs,
+                        void* stream);
+
+/*
  * A sweep of text prompts over one frame (BASELINE config E): the
  * coefficient map is rendered once (frame->coeff_map required; frame must
  * carry no features), then every prompt gets the query_pipeline post --
@@ -248,8 +260,9 @@ int sf_relevancy_f64(int64_t n_pixels, int32_t D, const double* feats, const dou
 int sf_mean_filter(int32_t height, int32_t width, const double* in, int32_t window, double* out,
                    void* workspace, size_t workspace_bytes, void* stream);
 
-/* select_level / localize / segment, query.py:111-145 over n maps (H,W) fp64:
+/* select_level / localize / segment, query.py:111-145 over n (1..32) maps (H,W) fp64:
  * stats_i64[SF_STAT_LEVEL/ROW/COL/DEGENERATE], stats_f64[MIN/MAX/LEVEL_MAX+b];
+ * stats_i64 needs max(16, 8 + n) entries and stats_f64 8 + 2 n (per-map argmax / max / min);
  * mask may be NULL.  fixed_level >= 0 skips selection. */
 size_t sf_select_segment_workspace_bytes(int32_t n_maps, int32_t height, int32_t width);
 int sf_select_segment(int32_t n_maps, int32_t height, int32_t width, const double* maps,

@@ -263,15 +263,14 @@ def splat_sparse(scene, cam, level, **kw):
 
 
 def decode_level(w: np.ndarray, atoms: np.ndarray) -> np.ndarray:
-    """One level of decode, sparse_splat.py:183-199: (..., L) @ (L, D) in float64."""
+    """One level of decode, sparse_splat.py:183-199: the reference's own
+    operation, ``w.reshape(-1, L) @ atoms.astype(float64)`` (numpy / BLAS
+    dgemm, as the reference computes it; or_decode is the plain-C twin)."""
     shp = w.shape
     L = shp[-1]
     w2 = np.ascontiguousarray(w.reshape(-1, L), dtype=np.float64)
-    atoms = np.ascontiguousarray(atoms, dtype=np.float32)
-    D = atoms.shape[1]
-    out = np.empty((w2.shape[0], D))
-    lib().or_decode(w2.shape[0], L, D, _p(w2), L, _p(atoms), _p(out))
-    return out.reshape(shp[:-1] + (D,))
+    out = w2 @ np.asarray(atoms, dtype=np.float32).astype(np.float64)
+    return out.reshape(shp[:-1] + (out.shape[1],))
 
 
 def decode(cmap: OracleCoefficientMap, codebooks):

@@ -60,6 +60,7 @@ EXPORTS = {
                                        ctypes.POINTER(SfQuery), ctypes.POINTER(SfFrame), P, sz, P, P, P]),
     "sf_query_sweep": (ctypes.c_int, [ctypes.POINTER(SfScene), ctypes.POINTER(SfCamera), ctypes.POINTER(SfFrame),
                                       P, i32, P, i32, i32, f64, P, P, P, P, P, sz, P]),
+    "sf_frame_tile_lists": (ctypes.c_int, [i64, i32, i32, i32, i32, i32, i32, i64, P, sz, P, P, i64, P]),
     "sf_project_workspace_bytes": (ctypes.c_int, [i64, ctypes.POINTER(sz)]),
     "sf_project": (ctypes.c_int, [ctypes.POINTER(SfScene), ctypes.POINTER(SfCamera), P, P, P, P, P,
                                   P, P, P, sz, P]),

@@ -325,6 +325,26 @@ extern "C" int sf_render_frame(const SfScene* s, const SfCamera* cam, const SfQu
                         nullptr);
 }
 
+extern "C" int sf_frame_tile_lists(int64_t G, int32_t W, int32_t H, int32_t n_levels, int32_t L, int32_t K,
+                                   int32_t D, int64_t pair_cap, const void* workspace, size_t workspace_bytes,
+                                   uint32_t* tile_offsets, uint32_t* tile_rows, int64_t max_pairs, void* stream) {
+    if (W < 1 || H < 1 || G < 0) return fail(SF_ERR_VALIDATION, "bad frame shape");
+    FrameWs ws;
+    size_t need = carve_frame(const_cast<void*>(workspace), workspace_bytes, G, W, H, n_levels, L, K, D, pair_cap, &ws);
+    if (need > workspace_bytes) return fail(SF_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, need);
+    const int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t total = 0;
+    cudaMemcpyAsync(tile_offsets, ws.tile_offsets, (size_t)(n_tiles + 1) * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                    st);
+    cudaMemcpyAsync(&total, ws.tile_offsets + n_tiles, sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if ((int64_t)total > max_pairs || (int64_t)total > pair_cap)
+        return fail(SF_ERR_WORKSPACE, "%u pairs exceed the output (%lld)", total, (long long)max_pairs);
+    if (total) cudaMemcpyAsync(tile_rows, ws.entries, (size_t)total * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+    return check_cuda("sf_frame_tile_lists");
+}
+
 extern "C" int sf_query_sweep(const SfScene* s, const SfCamera* cam, const SfFrame* f, const double* prompts,
                               int32_t n_prompts, const double* canon, int32_t n_canon, int32_t window,
                               double threshold, double* filtered, uint8_t* masks, int64_t* stats_i64,
@@ -689,7 +709,7 @@ extern "C" int sf_select_segment(int32_t n_maps, int32_t H, int32_t W, const dou
                                  int32_t fixed_level, double threshold, uint8_t* mask,
                                  int64_t* stats_i64, double* stats_f64, void* ws, size_t ws_bytes,
                                  void* stream) {
-    if (n_maps < 1 || n_maps > 32) return fail(SF_ERR_VALIDATION, "at least one level map is required");
+    if (n_maps < 1 || n_maps > 32) return fail(SF_ERR_VALIDATION, "1..32 level maps are required, got %d", n_maps);
     if ((int64_t)H * W == 0) return fail(SF_ERR_VALIDATION, "cannot localize an empty map");
     if (ws_bytes < select_segment_ws_bytes(n_maps, H, W)) return fail(SF_ERR_WORKSPACE, "workspace too small");
     launch_select_segment(n_maps, H, W, maps, fixed_level, threshold, mask, stats_i64, stats_f64, ws,

@@ -384,6 +384,21 @@ class FrameEngine:
             raise SplatfieldError("pair buffer overflow persisted after growing")
 
 
+    def tile_lists(self, W: int, H: int, n_levels: int, n_pairs: int):
+        """The last frame's per-tile lists (offsets, scene rows) from its
+        workspace, as host int64 arrays (parity checks of the frame binning)."""
+        cfg = self.ds.config
+        ws = self.workspace(W, H, n_levels)
+        n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
+        offs = torch.empty(n_tiles + 1, dtype=torch.int32, device=self.ds.device)
+        rows = torch.empty(max(1, n_pairs), dtype=torch.int32, device=self.ds.device)
+        N.check(N.load().sf_frame_tile_lists(self.ds.num_gaussians, W, H, n_levels, cfg.L, cfg.K, cfg.D,
+                                             self.pair_capacity, N.ptr(ws), ws.numel(), N.ptr(offs), N.ptr(rows),
+                                             int(rows.numel()), stream_ptr()))
+        o = offs.cpu().numpy().view(np.uint32).astype(np.int64)
+        r = rows.cpu().numpy().view(np.uint32).astype(np.int64)[:int(o[-1])]
+        return o, r
+
     def sweep(self, cam, levels, out: FrameOutputs, prompts: np.ndarray, canonicals: np.ndarray, *,
               window: int = 11, threshold: float = 0.5, band=None):
         """Render ``out.coeff_map`` once, then run the query post of every

@@ -50,6 +50,11 @@ def band_rows(height: int, world_size: int, rank: int, *, tile: int = 16, halo: 
     if world_size < 1 or not 0 <= rank < world_size:
         raise ValidationError("bad rank / world size")
     tiles_y = (height + tile - 1) // tile
+    if world_size > tiles_y:
+        # every rank raises here, before any collective: a rank with an empty
+        # band would otherwise render nothing (or the whole frame) while the
+        # others wait for it in the selection all-reduce
+        raise ValidationError(f"{world_size} ranks exceed the {tiles_y} tile rows of a {height}-row image")
     t0 = tiles_y * rank // world_size
     t1 = tiles_y * (rank + 1) // world_size
     y0, y1 = min(t0 * tile, height), min(t1 * tile, height)

@@ -154,8 +154,10 @@ def _select(maps, fixed_level: int, threshold: float, want_mask: bool):
     lib = N.load()
     nbytes = lib.sf_select_segment_workspace_bytes(len(ts), h, w)
     ws = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=dev)
-    st_i = torch.zeros(16, dtype=torch.int64, device=dev)
-    st_f = torch.zeros(8 + 32, dtype=torch.float64, device=dev)
+    # k_finalize_select writes stats_i64[8 + m] and stats_f64[8 + n + m] per map m
+    n = len(ts)
+    st_i = torch.zeros(max(16, 8 + n), dtype=torch.int64, device=dev)
+    st_f = torch.zeros(8 + 2 * n, dtype=torch.float64, device=dev)
     mask = torch.empty((h, w), dtype=torch.uint8, device=dev) if want_mask else None
     N.check(lib.sf_select_segment(len(ts), h, w, N.ptr(stacked), fixed_level, float(threshold),
                                   N.ptr(mask), N.ptr(st_i), N.ptr(st_f), N.ptr(ws), ws.numel(),

@@ -149,3 +149,12 @@ def test_band_sharded_selection_many_prompts():
         stats.append((sub.max(axis=2), (rows + band.y0) * W + cols, sub.min(axis=2)))
     mx_b, am_b, mn_b = (np.stack(x) for x in zip(*stats))
     assert combine_selection_many(mx_b, am_b, mn_b) == results[0]
+
+
+def test_band_rows_rejects_more_ranks_than_tile_rows():
+    """Every rank raises before any collective (no empty bands, no hang)."""
+    from paper_2507_07136_b200.errors import ValidationError
+    for r in range(8):
+        with pytest.raises(ValidationError):
+            band_rows(64, 8, r)
+    assert band_rows(64, 4, 3).y1 == 64
