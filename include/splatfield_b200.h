@@ -150,6 +150,12 @@ size_t sf_decode_image_bytes(int32_t n_levels, int32_t L, int32_t K, int32_t D);
 int sf_pack_decode_image(const SfScene* scene, const int32_t* host_levels, int32_t n_levels, void* out,
                          size_t out_bytes, void* stream);
 
+/* Capacity of the exact fp64 replay list (k_blend_fixup_cta) of a W x H
+ * frame: every pixel at most once, so W * H unless lowered for tests by
+ * SF_FIXUP_CAPACITY.  A frame whose stats_i64[SF_STAT_FIXUPS] exceeds it left
+ * pixels uncertified; the host shim raises (it never happens at W * H). */
+int64_t sf_fixup_capacity(int32_t width, int32_t height);
+
 /* Scratch needed by sf_render_frame for this scene/frame shape. */
 int sf_frame_workspace_bytes(int64_t num_gaussians, int32_t width, int32_t height,
                              int32_t n_levels, int32_t L, int32_t K, int32_t D,

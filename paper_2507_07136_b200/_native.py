@@ -53,6 +53,7 @@ class SfFrame(ctypes.Structure):
 
 
 EXPORTS = {
+    "sf_fixup_capacity": (i64, [i32, i32]),
     "sf_frame_workspace_bytes": (ctypes.c_int, [i64, i32, i32, i32, i32, i32, i32, i64, ctypes.POINTER(sz)]),
     "sf_render_frame": (ctypes.c_int, [ctypes.POINTER(SfScene), ctypes.POINTER(SfCamera),
                                        ctypes.POINTER(SfQuery), ctypes.POINTER(SfFrame), P, sz, P]),
@@ -126,6 +127,16 @@ def check(rc: int) -> None:
     if rc == SF_ERR_RESOURCE:
         raise ResourceLimitError(msg)
     raise SplatfieldError(f"native error {rc}: {msg}")
+
+
+def check_fixups(stats, width: int, height: int) -> None:
+    """Raise when a frame listed more ambiguous early-exit pixels than the
+    exact-replay list holds (only possible with SF_FIXUP_CAPACITY lowered):
+    the pixels past the capacity kept an uncertified fp32 decision."""
+    n = int(stats[STAT_FIXUPS])
+    cap = int(load().sf_fixup_capacity(int(width), int(height)))
+    if n > cap:
+        raise SplatfieldError(f"exact-replay capacity exceeded: {n} ambiguous pixels > capacity {cap}")
 
 
 def ptr(t) -> ctypes.c_void_p:

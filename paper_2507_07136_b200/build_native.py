@@ -21,7 +21,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 # Files whose fp64 arithmetic must follow the reference op order bit for bit:
 # no FMA contraction except the explicit fma() calls that mirror BLAS.
 NO_FMAD = {"sf_preprocess.cu", "sf_binning.cu"}
-SOURCES = ["sf_preprocess.cu", "sf_binning.cu", "sf_blend.cu", "sf_post.cu", "sf_decode.cu",
+SOURCES = ["sf_preprocess.cu", "sf_binning.cu", "sf_sort.cu", "sf_blend.cu", "sf_splat_tc.cu", "sf_runtime.cu", "sf_post.cu", "sf_decode.cu",
            "sf_decode_tc.cu", "sf_io.cu", "sf_capi.cu"]
 
 

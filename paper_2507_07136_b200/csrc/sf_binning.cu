@@ -6,7 +6,7 @@
 //  (3) exact ellipse/rectangle test q_min <= 9            projection.py:429-441
 //  (4) stable argsort by tile + searchsorted bounds       projection.py:443-449
 //
-// B200 design.  (1) is a device radix sort of the fp64 depth bits (positive
+// B200 design.  (1) is a device radix sort (sf_sort.cu) of the fp64 depth bits (positive
 // doubles order like their bit patterns) over rows already stored in id
 // order, so a stable sort gives the (depth, id) order exactly; the position
 // in that order is the Gaussian's depth rank r.  (2)+(3) run per rank with
@@ -24,25 +24,11 @@ namespace sf {
 constexpr int kCountCTAs = 296;      // CTAs of the aggregated count pass (2 per SM)
 constexpr int kAggMaxTiles = 16384;  // shared-memory tile histogram limit (64 KB)
 
-size_t depth_sort_cub_bytes(int64_t n) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 64);
-    return bytes;
-}
-size_t id_sort_cub_bytes(int64_t n) { return depth_sort_cub_bytes(n); }
 size_t bin_cta_base_elems(int W, int H) {
     const int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
     return (size_t)kCountCTAs * (size_t)n_tiles;
 }
 
-int depth_sort(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in,
-               uint32_t* vals_out, int64_t n, void* tmp, size_t tmp_bytes, cudaStream_t st) {
-    if (n == 0) return 0;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in,
-                                                    vals_out, (int)n, 0, 64, st);
-    return e == cudaSuccess ? 0 : -1;
-}
 
 // ---------------------------------------------------------------------------
 // inverse of the depth order, and the per-row scatter plan
@@ -369,9 +355,6 @@ __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __
 // per-tile sort of depth ranks (restores canonical order inside each bucket)
 
 constexpr int kSortSmemElems = 8192;
-#ifndef SF_TILE_SORT_BITS
-#define SF_TILE_SORT_BITS 6  // radix digit width of the per-tile block sort (21-bit ranks: 4 passes)
-#endif
 
 __device__ void block_bitonic_sort(uint32_t* s, int N) {
     // N is a power of two; ascending.
@@ -436,34 +419,6 @@ __device__ __forceinline__ int rank_bits(const int64_t* stats) {
     int nbits = 1;
     while (nbits < 32 && ((int64_t)1 << nbits) < nvis) ++nbits;
     return nbits;
-}
-
-// Tiles with n <= 256 * ITEMS: CUB block radix sort in registers/shared memory.
-template <int ITEMS>
-__global__ void __launch_bounds__(256) k_tile_sort_small(const uint32_t* __restrict__ offsets,
-                                                         uint32_t* __restrict__ entries, int lo_exclusive,
-                                                         const int64_t* __restrict__ stats,
-                                                         const uint32_t* __restrict__ rank_to_row) {
-    if (stats[SF_STAT_OVERFLOW]) return;
-    typedef cub::BlockRadixSort<uint32_t, 256, ITEMS, cub::NullType, SF_TILE_SORT_BITS> Sort;
-    __shared__ typename Sort::TempStorage tmp;
-    const int t = blockIdx.x;
-    const uint32_t beg = offsets[t], end = offsets[t + 1];
-    const int n = (int)(end - beg);
-    if (n <= lo_exclusive || n > 256 * ITEMS) return;
-    uint32_t keys[ITEMS];
-    uint32_t* e = entries + beg;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const int idx = threadIdx.x * ITEMS + i;
-        keys[i] = (idx < n) ? e[idx] : 0xffffffffu;
-    }
-    Sort(tmp).Sort(keys, 0, rank_bits(stats));
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const int idx = threadIdx.x * ITEMS + i;
-        if (idx < n) e[idx] = rank_to_row ? __ldg(rank_to_row + keys[i]) : keys[i];
-    }
 }
 
 // Per-tile sort of unique depth ranks, n <= CAP: MSD bucket sort in shared
@@ -628,12 +583,8 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
     const bool agg = cta_base && n_tiles <= kAggMaxTiles && n_items > 0;
     const int64_t per = agg ? (n_items + kCountCTAs - 1) / kCountCTAs : 1;
     if (agg) {
-        static size_t configured = 0;
         const size_t smem = sizeof(uint32_t) * n_tiles;
-        if (smem > configured) {
-            cudaFuncSetAttribute(k_count_pairs_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured = smem;
-        }
+        ensure_smem_attr((const void*)k_count_pairs_agg, smem);
         k_count_pairs_agg<<<kCountCTAs, 512, smem, st>>>(n_items, per, stats, geom, rank_of, g, tile_counts, aux,
                                                          cta_base);
     } else if (blocks) {
@@ -646,12 +597,7 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
                                              entries, agg ? cta_base : nullptr, per);
     // per-tile canonical order: most lists fit the shared-memory bucket sort (<= 4096),
     // the rest go to the larger-capacity kernels (each CTA skips other sizes)
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_tile_sort_bucket<8192, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             2 * 8192 * 4);
-        configured = true;
-    }
+    ensure_smem_attr((const void*)k_tile_sort_bucket<8192, 1024>, 2 * 8192 * 4);
     k_tile_sort_bucket<SF_TS_CAP, SF_TS_NB><<<n_tiles, 256, 2 * SF_TS_CAP * 4, st>>>(tile_offsets, entries, 0, stats,
                                                                                    rank_to_row);
     k_tile_sort_bucket<8192, 1024><<<n_tiles, 256, 2 * 8192 * 4, st>>>(tile_offsets, entries, SF_TS_CAP, stats,

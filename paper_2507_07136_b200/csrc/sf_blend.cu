@@ -38,6 +38,7 @@
 #include <algorithm>
 
 #include "sf_common.cuh"
+#include "sf_blend_dev.cuh"
 
 namespace sf {
 
@@ -56,12 +57,6 @@ constexpr int kStageChan = 3072;     // scatter-plan bytes per stage: 32 records
 constexpr int kChBlock = 192;        // accumulator channels per CTA (smem bound)
 static_assert(kChanWord == kAccPitch * 4, "channel words are accumulator byte offsets");
 
-// fp32 part of a GeomRec (its first 32 bytes): all the blend needs outside
-// the guard band, where the fp64 fields are read from global memory
-struct __align__(16) GeomF32 {
-    float mx_hi, mx_lo, my_hi, my_lo;
-    float a, k, d, opacity;
-};
 
 struct __align__(16) BlendStage {
     GeomF32 g[kBatch];
@@ -121,158 +116,6 @@ struct __align__(16) BlendSmem {
     uint32_t tmem_base;
 };
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
-}
-__device__ __forceinline__ void bar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
-}
-__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_addr(b)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
-                 : "memory");
-}
-// 1-D bulk copy global -> shared, completion on an mbarrier (tx bytes)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(b))
-        : "memory");
-}
-__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-// K-major, 128B-swizzled operand: rows of 128 B, 8-row atoms 1024 B apart
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;
-    d |= (uint64_t)(1024 >> 4) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)2 << 61;
-    return d;
-}
-// D (TMEM) [+]= A (TMEM, tf32, row = lane, K = column) x B (SMEM descriptor)
-__device__ __forceinline__ void mma_tf32_tmem_a(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
-        "}\n" ::"r"(d),
-        "r"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* b) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(b))
-                 : "memory");
-}
-#define SF_X32_REGS(v)                                                                                     \
-    "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),     \
-        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),    \
-        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),   \
-        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
-#define SF_X32_OUTS(v)                                                                                     \
-    "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),        \
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),           \
-        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),         \
-        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),         \
-        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-#define SF_X32_LIST                                                                                        \
-    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27," \
-    "%28,%29,%30,%31}"
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%32], " SF_X32_LIST ";" ::SF_X32_REGS(v), "r"(taddr)
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 " SF_X32_LIST ", [%32];" : SF_X32_OUTS(v) : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%16], "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15};" ::"r"(v[0]),
-        "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(taddr)
-        : "memory");
-}
-// D (TMEM, f32) [+]= A (TMEM, f16 pairs per column, row = lane) x B (SMEM descriptor, f16)
-__device__ __forceinline__ void mma_f16_tmem_a(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-        "}\n" ::"r"(d),
-        "r"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void named_bar_sync(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"((uint64_t)map),
-        "r"(smem_addr(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait() {
-    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ float tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
-
-__device__ __forceinline__ uint64_t gtimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
-__device__ __forceinline__ float rcp_approx(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-// two-branch logistic (query.py:65-84), evaluated branch-free: both branches
-// take exp(-|x|), so a warp with mixed signs runs one exp instead of two
-__device__ __forceinline__ double sigmoid2(double x) {
-    const double e = exp(-fabs(x));
-    return (x >= 0 ? 1.0 : e) / (1.0 + e);
-}
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-                 "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 // Issue the cp.async copies of one batch (nb records) into stage buffer S
 // (called by the 32 lanes of the producer warp; lane j holds record j's row).
@@ -298,74 +141,7 @@ __device__ __forceinline__ void stage_batch(BlendStage& S, const BlendArgs& A, u
     }
     if (lane < nb) S.row[lane] = rows;
 }
-// Warm L2 with the records of a later batch (lane j: record j)
-__device__ __forceinline__ void prefetch_records(const BlendArgs& A, uint32_t r, int cs) {
-    const char* g = reinterpret_cast<const char*>(A.geom + r);
-    const char* c = reinterpret_cast<const char*>(A.chan) + (size_t)r * cs;
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(g));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(c));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(c + cs - 1));
-}
 
-// alpha = min(o exp(-q/2), 0.99) with q <= 9 membership (0 if outside).
-// q is evaluated in fp32 as a (dx + k dy)^2 + d dy^2 (no cancellation),
-// branch-free; inside the guard band around 9 (`amb`) the reference's fp64 q
-// decides instead (blend_alpha_exact, rasterizer.py:161-168).
-__device__ __forceinline__ float blend_alpha_fast(const GeomF32& g, float pxf, float pyf, bool& amb) {
-    constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 / ln 2
-    const float dx = (pxf - g.mx_hi) - g.mx_lo;
-    const float dy = (pyf - g.my_hi) - g.my_lo;
-    const float u = fmaf(g.k, dy, dx);
-    const float ddy = g.d * dy * dy;
-    const float q32 = fmaf(g.a * u, u, ddy);
-    const float su = fabsf(dx) + fabsf(g.k * dy);
-    const float guard = fmaf(1e-5f, fmaf(g.a * su, su, ddy), 1e-5f);
-    amb = fabsf(q32 - 9.f) <= guard;
-    const float al = fminf(g.opacity * exp2f(kNegHalfLog2e * fminf(q32, 9.5f)), 0.99f);
-    return q32 > 9.f ? 0.f : al;
-}
-__device__ __noinline__ float blend_alpha_exact(const GeomF32& g, const GeomRec* __restrict__ g64, double pxd,
-                                                double pyd) {
-    constexpr float kNegHalfLog2e = -0.72134752044448170368f;
-    const GeomRec& G = *g64;  // rare: the reference's fp64 values from global memory
-    double ddx = __dadd_rn(pxd, -G.mx), ddyd = __dadd_rn(pyd, -G.my);
-    double t1 = __dmul_rn(__dmul_rn(G.a64, ddx), ddx);
-    double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, G.b64), ddx), ddyd);
-    double t3 = __dmul_rn(__dmul_rn(G.c64, ddyd), ddyd);
-    double q = __dadd_rn(__dadd_rn(t1, t2), t3);
-    if (!(q <= SF_CUTOFF)) return 0.f;
-    return fminf(g.opacity * exp2f(kNegHalfLog2e * (float)q), 0.99f);
-}
-
-// Conservative patch culling: may any pixel of the 8x4 patch with corner
-// (x0, y0) have q <= 9?  q = a (dx + k dy)^2 + d dy^2 is convex, so its
-// minimum over the pixel-centre rectangle is 0 when the mean lies inside,
-// else on one of the four edges (1-D minimisation with clamping).  fp32 with
-// the same relative guard as blend_alpha; false positives only cost work,
-// blend_alpha still decides every pixel (exactly, inside the guard band).
-__device__ __forceinline__ bool patch_may_hit(const GeomF32& g, float x0, float y0) {
-    const float dx0 = (x0 - g.mx_hi) - g.mx_lo, dx1 = dx0 + 7.f;
-    const float dy0 = (y0 - g.my_hi) - g.my_lo, dy1 = dy0 + 3.f;
-    if (dx0 <= 0.f && dx1 >= 0.f && dy0 <= 0.f && dy1 >= 0.f) return true;
-    const float a = g.a, k = g.k, d = g.d;
-    const float c = fmaf(a * k, k, d);
-    const float s = -(a * k) / c;  // dy* = s * dx on an x edge
-    float best = INFINITY, bs = 0.f;
-    auto eval = [&](float dx, float dy) {
-        const float u = fmaf(k, dy, dx);
-        const float q = fmaf(a * u, u, d * dy * dy);
-        if (q < best) {
-            best = q;
-            const float su = fabsf(dx) + fabsf(k * dy);
-            bs = fmaf(a * su, su, d * dy * dy);
-        }
-    };
-    eval(dx0, fminf(fmaxf(s * dx0, dy0), dy1));
-    eval(dx1, fminf(fmaxf(s * dx1, dy0), dy1));
-    eval(fminf(fmaxf(-k * dy0, dx0), dx1), dy0);
-    eval(fminf(fmaxf(-k * dy1, dx0), dx1), dy1);
-    return best <= 9.f + fmaf(1e-4f, bs, 1e-4f);
-}
 
 __host__ __device__ constexpr int acc_bytes(int nch) { return (nch * kAccPitch * 4 + 15) / 16 * 16; }
 
@@ -1117,12 +893,8 @@ void launch_relevancy_from_cmap(int64_t P, int n_ch, const float* cmap, const do
     if (P == 0) return;
     const size_t smem = sizeof(double) * (size_t)n_levels * L * n_canon;
     const bool vec = (L % 4 == 0) && (n_ch % 4 == 0) && ((uintptr_t)cmap % 16 == 0);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_relevancy_from_cmap<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_relevancy_from_cmap<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
-    }
+    ensure_smem_attr((const void*)k_relevancy_from_cmap<0>, 200 * 1024);
+    ensure_smem_attr((const void*)k_relevancy_from_cmap<4>, 200 * 1024);
     const int blocks = (int)std::min<int64_t>(ceil_div(P, 256), 148 * 8);
     if (vec && n_canon == 4)
         k_relevancy_from_cmap<4><<<blocks, 256, smem, st>>>(P, n_ch, cmap, proj_cb, n_levels, L, n_canon, out,
@@ -1262,11 +1034,7 @@ int launch_relevancy_sweep(int64_t P, int n_ch, const float* cmap, const double*
     if (n_canon < 1 || n_canon > kSwCols || L % 4 || n_ch % 4 || (uintptr_t)cmap % 16 || smem > 200 * 1024)
         return 1;
     if (P == 0 || nq == 0) return 0;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_relevancy_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
-    }
+    ensure_smem_attr((const void*)k_relevancy_sweep, 200 * 1024);
     const int blocks = (int)std::min<int64_t>(ceil_div(P, kSwPx), std::max(1, 148 * 2 / n_levels));  // one wave
     k_relevancy_sweep<<<dim3(blocks, n_levels), kSwThreads, smem, st>>>(P, n_ch, cmap, proj, n_levels, L, nq, n_canon, out,
                                                         out_prompt_stride, out_level_stride);
@@ -1349,15 +1117,25 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_blend_fixup(BlendArgs A) {
             if (lane == 0) excl = 1.0;
             const double Tb = __dmul_rn(T, excl);
             const bool counted = (i < end) && (Tb >= SF_EARLY_EXIT_T) && (al > 0.0);
-            if (counted) {
-                const double e = __dmul_rn(al, Tb);
-                const unsigned char* rec = A.chan + (size_t)r * cs;
+            // Ordered accumulation (deterministic, the reference's order,
+            // sparse_splat.py:144-147): entries in list order, a channel is
+            // owned by lane ch % 32, so each channel's sum runs in depth order.
+            const double e_mine = counted ? __dmul_rn(al, Tb) : 0.0;
+            unsigned live = __ballot_sync(0xffffffffu, counted);
+            while (live) {
+                const int j = __ffs(live) - 1;
+                live &= live - 1;
+                const double e = __shfl_sync(0xffffffffu, e_mine, j);
+                const uint32_t rj = __shfl_sync(0xffffffffu, r, j);
+                const unsigned char* rec = A.chan + (size_t)rj * cs;
                 const uint32_t* words = reinterpret_cast<const uint32_t*>(rec);
                 const float* val = reinterpret_cast<const float*>(rec + voff);
                 for (int k = 0; k < C; ++k) {
                     const int ch = chan_id(words[k]);
-                    if (local) atomicAdd(&wl[ch], e * (double)val[k]);
-                    else atomicAdd(&row[ch], (float)(e * (double)val[k]));
+                    if ((ch & 31) == lane) {
+                        if (local) wl[ch] += e * (double)val[k];
+                        else row[ch] += (float)(e * (double)val[k]);
+                    }
                 }
             }
             T = __dmul_rn(T, __shfl_sync(0xffffffffu, incl, 31));
@@ -1437,16 +1215,16 @@ void launch_dec_codebook_image(const float* codebooks, const LevelSelDev& lv, in
 
 // features (n_levels, H, W, D) fp32 as a 4-D TMA map: boxes of kDecBoxCols
 // columns x 8 x 4 pixels of one level (a warp's fused-decode store box)
-static int make_feature_map(CUtensorMap* map, float* f, int D, int W, int H, int n_levels) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
+int make_feature_map(CUtensorMap* map, float* f, int D, int W, int H, int n_levels) {
+    static const PFN_cuTensorMapEncodeTiled_v12000 enc = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
         cudaDriverEntryPointQueryResult q;
         void* p = nullptr;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
             q != cudaDriverEntryPointSuccess)
-            return -1;
-        enc = (PFN_cuTensorMapEncodeTiled_v12000)p;
-    }
+            return nullptr;
+        return (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }();
+    if (!enc) return -1;
     cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n_levels};
     cuuint64_t strides[3] = {(cuuint64_t)D * 4, (cuuint64_t)W * D * 4, (cuuint64_t)H * W * D * 4};
     cuuint32_t box[4] = {(cuuint32_t)kDecBoxCols, 8, 4, 1};
@@ -1551,11 +1329,7 @@ int launch_splat_transpose(const BlendArgs& a, const float* dW, float* ghat, int
     if (a.n_ch > kChBlock || a.C > kMaxC || a.C % K) return -1;
     const int cs = chan_rec_bytes(a.C);
     const size_t smem = acc_bytes(a.n_ch) + kTrBatch * (sizeof(GeomF32) + 4 + cs + 4 * a.C);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaFuncSetAttribute(k_splat_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
+    ensure_smem_attr((const void*)k_splat_transpose, smem);
     if (a.n_band_tiles > 0) k_splat_transpose<<<2 * a.n_band_tiles, 128, smem, st>>>(a, dW, ghat, K, G);
     return 0;
 }
@@ -1568,6 +1342,9 @@ int launch_splat_transpose(const BlendArgs& a, const float* dW, float* ghat, int
 constexpr int kFxWarps = 8;
 __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) {
     __shared__ double wl[kChBlock];
+    __shared__ double pv[32 * kFxWarps][kMaxC];
+    __shared__ uint8_t chs[32 * kFxWarps][kMaxC];
+    __shared__ uint8_t live_e[32 * kFxWarps];
     __shared__ double wtot[kFxWarps];
     __shared__ double Tround, Tfinal;
     __shared__ unsigned int last_counted;
@@ -1578,6 +1355,7 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
     const int cs = chan_rec_bytes(C);
     const int voff = chan_val_offset(C);
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    const int kper = C / A.n_levels;  // plan slots per level (level-major plan, launch_pack_channels)
     constexpr double thr = SF_EARLY_EXIT_T;
     for (uint32_t idx = blockIdx.x; idx < count; idx += gridDim.x) {
         const uint32_t code = A.fixup_list[idx];
@@ -1626,14 +1404,33 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
             if (lane == 0) excl = 1.0;
             const double Tb = __dmul_rn(__dmul_rn(T, pre), excl);
             const bool live = (i < end) && (Tb >= thr);
-            if (live && al > 0.0) {
+            // Ordered accumulation (deterministic, and the reference's order,
+            // sparse_splat.py:144-147): entry t stages its C channel ids and
+            // products e v; then thread c owns channel c and adds the round's
+            // products to it in list order (only level c / L's K slots can hold c).
+            const bool adds = live && al > 0.0;
+            live_e[tid] = adds ? 1 : 0;
+            if (adds) {
                 const double e = __dmul_rn(al, Tb);
                 const unsigned char* rec = A.chan + (size_t)r * cs;
                 const uint32_t* words = reinterpret_cast<const uint32_t*>(rec);
                 const float* val = reinterpret_cast<const float*>(rec + voff);
-                for (int k = 0; k < C; ++k) atomicAdd(&wl[chan_id(words[k])], e * (double)val[k]);
+                for (int k = 0; k < C; ++k) {
+                    chs[tid][k] = (uint8_t)chan_id(words[k]);
+                    pv[tid][k] = e * (double)val[k];
+                }
             }
             const bool stop = __syncthreads_or((i < end) && !(Tb >= thr));
+            if (tid < A.n_ch) {
+                const int c = tid, k0 = (c / A.L) * kper;
+                double acc = wl[c];
+                for (int j = 0; j < 32 * kFxWarps; ++j) {
+                    if (!live_e[j]) continue;
+                    for (int k = k0; k < k0 + kper; ++k)
+                        if (chs[j][k] == c) acc += pv[j][k];
+                }
+                wl[c] = acc;
+            }
             if (stop) {
                 // final T = T after the last entry still counted (T is non-increasing);
                 // none counted in this round: the T the round started with
@@ -1681,60 +1478,48 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
     }
 }
 
+// k_splat_tc (sf_splat_tc.cu) is the frame path for L = 64, <= 3 levels and
+// 4 or no canonicals; k_blend serves the other shapes (wide / generic channel
+// blocks, other canonical counts).  SF_BLEND_IMPL=legacy forces k_blend
+// (A/B comparisons only).
+bool splat_tc_supported(const BlendArgs& a);
+int launch_splat_tc(const BlendArgs& a, cudaStream_t st);
+
 int launch_blend(const BlendArgs& a, cudaStream_t st) {
     if (a.C > kMaxC) return -2;
     if (a.proj_cb && a.n_ch > kChBlock) return -3;  // fused relevancy needs every channel in one CTA
-    int n_tiles = a.n_band_tiles;
-    int ch_block = a.n_ch < kChBlock ? a.n_ch : kChBlock;
-    int nblk = (a.n_ch + ch_block - 1) / ch_block;
-    const bool dec = a.features != nullptr;
-    CUtensorMap fmap;
-    memset(&fmap, 0, sizeof(fmap));
-    if (dec) {
-        if (!blend_dec_supported(a.n_levels, a.L, a.C / a.n_levels, a.D) || nblk != 1 || !a.dec_b) return -4;
-        if ((uintptr_t)a.features % 16) return -4;
-        if (make_feature_map(&fmap, a.features, a.D, a.W, a.H, a.n_levels)) return -5;
-    }
-    size_t smem = (dec ? 1024 : 0) + acc_bytes(ch_block) + sizeof(BlendSmem);
-    const bool fast = (a.C == 12 && nblk == 1);
-    const int nc = a.proj_cb ? a.n_canon : 0;
-    void (*kern)(BlendArgs, int, const CUtensorMap);
-    int ki;
-    if (dec && !a.proj_cb) { kern = k_blend<12, true, 0, true>; ki = 4; }
-    else if (dec && nc == 4) { kern = k_blend<12, true, 4, true>; ki = 5; }
-    else if (dec) { kern = k_blend<12, true, -1, true>; ki = 6; }
-    else if (fast && !a.proj_cb) { kern = k_blend<12, true, 0, false>; ki = 0; }
-    else if (fast && nc == 4) { kern = k_blend<12, true, 4, false>; ki = 1; }
-    else if (fast) { kern = k_blend<12, true, -1, false>; ki = 2; }
-    else { kern = k_blend<0, false, -1, false>; ki = 3; }
-    static size_t configured[7] = {0, 0, 0, 0, 0, 0, 0};
-    if (smem > configured[ki]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured[ki] = smem;
-    }
-    // development aid: SF_BLEND_TIMELINE=<file> dumps per-CTA %globaltimer stamps
-    // (start, blend done, A in TMEM, end) of every launch
-    static const char* tl_path = getenv("SF_BLEND_TIMELINE");
-    BlendArgs a2 = a;
-    static uint64_t* tl = nullptr;
-    const size_t n_cta = (size_t)2 * n_tiles * nblk;
-    if (tl_path && n_tiles > 0) {
-        if (tl) cudaFree(tl);
-        cudaMalloc(&tl, n_cta * 4 * sizeof(uint64_t));
-        cudaMemsetAsync(tl, 0, n_cta * 4 * sizeof(uint64_t), st);
-        a2.timeline = tl;
-    }
-    if (n_tiles > 0) kern<<<dim3(2 * n_tiles, nblk), kCTAThreads, smem, st>>>(a2, ch_block, fmap);
-    if (tl_path && n_tiles > 0) {
-        uint64_t* h = (uint64_t*)malloc(n_cta * 4 * sizeof(uint64_t));
-        cudaMemcpyAsync(h, tl, n_cta * 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        FILE* fp = fopen(tl_path, "wb");
-        if (fp) {
-            fwrite(h, sizeof(uint64_t), n_cta * 4, fp);
-            fclose(fp);
+    const int n_tiles = a.n_band_tiles;
+    static const bool legacy = [] {
+        const char* e = getenv("SF_BLEND_IMPL");
+        return e && strcmp(e, "legacy") == 0;
+    }();
+    if (!legacy && splat_tc_supported(a)) {
+        const int r = launch_splat_tc(a, st);
+        if (r) return r;
+    } else {
+        int ch_block = a.n_ch < kChBlock ? a.n_ch : kChBlock;
+        int nblk = (a.n_ch + ch_block - 1) / ch_block;
+        const bool dec = a.features != nullptr;
+        CUtensorMap fmap;
+        memset(&fmap, 0, sizeof(fmap));
+        if (dec) {
+            if (!blend_dec_supported(a.n_levels, a.L, a.C / a.n_levels, a.D) || nblk != 1 || !a.dec_b) return -4;
+            if ((uintptr_t)a.features % 16) return -4;
+            if (make_feature_map(&fmap, a.features, a.D, a.W, a.H, a.n_levels)) return -5;
         }
-        free(h);
+        size_t smem = (dec ? 1024 : 0) + acc_bytes(ch_block) + sizeof(BlendSmem);
+        const bool fast = (a.C == 12 && nblk == 1);
+        const int nc = a.proj_cb ? a.n_canon : 0;
+        void (*kern)(BlendArgs, int, const CUtensorMap);
+        if (dec && !a.proj_cb) kern = k_blend<12, true, 0, true>;
+        else if (dec && nc == 4) kern = k_blend<12, true, 4, true>;
+        else if (dec) kern = k_blend<12, true, -1, true>;
+        else if (fast && !a.proj_cb) kern = k_blend<12, true, 0, false>;
+        else if (fast && nc == 4) kern = k_blend<12, true, 4, false>;
+        else if (fast) kern = k_blend<12, true, -1, false>;
+        else kern = k_blend<0, false, -1, false>;
+        if (ensure_smem_attr((const void*)kern, smem)) return -6;
+        if (n_tiles > 0) kern<<<dim3(2 * n_tiles, nblk), kCTAThreads, smem, st>>>(a, ch_block, fmap);
     }
     if (n_tiles > 0 && a.fixup_list && a.early_exit) {
         if (a.n_ch <= kChBlock) k_blend_fixup_cta<<<1184, 32 * kFxWarps, 0, st>>>(a);

@@ -4,6 +4,7 @@
 // reference raises (sparse_splat.py:114-122, query.py:73-90).  All scratch
 // is carved from the caller's workspace; nothing allocates.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -81,7 +82,20 @@ struct FrameWs {
     uint32_t* fixup;  // [0] = count, then the list
 };
 
-static constexpr uint32_t kFixupCapacity = 1u << 20;
+// Exact-replay list capacity: every pixel can be listed at most once, so
+// W * H can never overflow.  SF_FIXUP_CAPACITY (tests only) lowers it to
+// exercise the overflow report: the blend still counts every ambiguous pixel
+// (SF_STAT_FIXUPS), the host raises when the count exceeds the capacity.
+static uint32_t fixup_capacity(int W, int H) {
+    static const long forced = [] {
+        const char* e = getenv("SF_FIXUP_CAPACITY");
+        return e ? atol(e) : -1L;
+    }();
+    const int64_t px = (int64_t)(W > 0 ? W : 1) * (H > 0 ? H : 1);
+    if (forced >= 0 && forced < px) return (uint32_t)forced;
+    return (uint32_t)px;
+}
+extern "C" int64_t sf_fixup_capacity(int32_t W, int32_t H) { return (int64_t)fixup_capacity(W, H); }
 
 static constexpr int kMaxCanon = 64;
 
@@ -98,7 +112,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->keys_out = c.take<uint64_t>(Gp);
     ws->vals_in = c.take<uint32_t>(Gp);
     ws->vals_out = c.take<uint32_t>(Gp);
-    ws->cub_bytes = depth_sort_cub_bytes(Gp);
+    ws->cub_bytes = depth_sort_tmp_bytes(Gp);
     ws->cub_tmp = c.take<char>(ws->cub_bytes);
     ws->stats = c.take<int64_t>(16);
     ws->stats_f = c.take<double>(8 + 2 * kMaxLevels);
@@ -114,7 +128,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->sel_ws = c.take<char>(select_segment_ws_bytes(n_levels, H, W));
     ws->dec_ws = c.take<float>(decode_ws_bytes(L, D) / sizeof(float));
     ws->dec_img = c.take<float>(blend_dec_image_bytes(n_levels, D) / sizeof(float));
-    ws->fixup = c.take<uint32_t>(kFixupCapacity + 1);
+    ws->fixup = c.take<uint32_t>((size_t)fixup_capacity(W, H) + 1);
     return c.off;
 }
 
@@ -254,7 +268,7 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
     a.chan = chan;
     a.fixup_count = ws.fixup;
     a.fixup_list = ws.fixup + 1;
-    a.fixup_capacity = kFixupCapacity;
+    a.fixup_capacity = fixup_capacity(W, H);
     a.stats = ws.stats;
     a.coeff_map = f->coeff_map;
     a.final_t = f->final_t;
@@ -574,7 +588,7 @@ static size_t carve_bin(void* base, size_t cap, int64_t n, int W, int H, int64_t
     w->k1 = c.take<uint64_t>(np);
     w->v0 = c.take<uint32_t>(np);
     w->v1 = c.take<uint32_t>(np);
-    w->cub_bytes = depth_sort_cub_bytes(np);
+    w->cub_bytes = depth_sort_tmp_bytes(np);
     w->cub_tmp = c.take<char>(w->cub_bytes);
     w->stats = c.take<int64_t>(16);
     w->counts = c.take<uint32_t>(2 * n_tiles);

@@ -207,6 +207,11 @@ struct LevelSelDev {
     int lv[kMaxLevels];
 };
 
+// sf_runtime.cu: per-(kernel, device) dynamic shared-memory limit (thread-safe),
+// and the current device's SM count (persistent grids)
+int ensure_smem_attr(const void* func, size_t bytes);
+int device_sm_count();
+
 // ---------------- internal launchers (one .cu each) ----------------
 
 // sf_preprocess.cu
@@ -220,10 +225,10 @@ void launch_project_compact(const SfScene& s, const GeomRec* geom, const uint64_
 size_t project_compact_cub_bytes(int64_t G);
 
 // sf_binning.cu
-size_t depth_sort_cub_bytes(int64_t n);
-int depth_sort(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in,
-               uint32_t* vals_out, int64_t n, void* tmp, size_t tmp_bytes, cudaStream_t st);
-size_t id_sort_cub_bytes(int64_t n);
+// sf_sort.cu: stable LSD radix sort of (u64 key, u32 value); the inputs are scratch
+size_t depth_sort_tmp_bytes(int64_t n);
+int depth_sort(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int64_t n, void* tmp,
+               size_t tmp_bytes, cudaStream_t st);
 // rank_of_row[row] = canonical rank, ~0 for culled rows
 void launch_rank_of_row(int64_t G, const uint32_t* sorted_rows, const int64_t* stats,
                         uint32_t* rank_of_row, cudaStream_t st);

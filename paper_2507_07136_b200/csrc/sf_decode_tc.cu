@@ -402,11 +402,7 @@ int launch_decode(int64_t P, int L, int D, const float* w, int64_t w_stride, con
     const int n_mtiles = (int)((P + tc::BM - 1) / tc::BM);
     if (groups > n_mtiles) groups = n_mtiles;
     const size_t smem = sizeof(tc::Smem) + 1024;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(tc::k_decode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    ensure_smem_attr((const void*)tc::k_decode_tc, smem);
     tc::k_decode_tc<<<groups * nsplit, tc::kThreads, smem, st>>>(ma, mb, mo, P, L, D, nsplit);
     return 0;
 }

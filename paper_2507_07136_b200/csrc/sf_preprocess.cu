@@ -120,11 +120,6 @@ __global__ void __launch_bounds__(256) k_preprocess(SfScene s, SfCamera cam, Geo
     if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(n_visible, (unsigned long long)__popc(ballot));
 }
 
-__global__ void k_zero_i64(int64_t* p, int n) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = 0;
-}
-
 void launch_preprocess(const SfScene& s, const SfCamera& cam, GeomRec* geom, uint64_t* keys,
                        uint32_t* vals, int64_t* stats, cudaStream_t st) {
     if (s.num_gaussians == 0) return;

@@ -184,6 +184,8 @@ class FrameOutputs:
     def host_stats(self):
         if getattr(self, "_host", None) is None:
             self._host = (self.stats_i64.cpu().numpy(), self.stats_f64.cpu().numpy())
+            if int(self._host[0][N.STAT_OVERFLOW]) == 0:
+                N.check_fixups(self._host[0], self.width, self.height)
         return self._host
 
     def stage_ms(self):
@@ -379,6 +381,7 @@ class FrameEngine:
                 st = out._host[0]
                 del keep
                 if int(st[N.STAT_OVERFLOW]) == 0:
+                    N.check_fixups(st, out.width, out.height)
                     return out
                 self.pair_capacity = int(int(st[N.STAT_PAIRS]) * 1.25) + 1024
             raise SplatfieldError("pair buffer overflow persisted after growing")
@@ -449,6 +452,7 @@ class FrameEngine:
                 hsf.copy_(sf, non_blocking=True)
                 fst = out.stats_i64.cpu().numpy()  # synchronises the stream
                 if int(fst[N.STAT_OVERFLOW]) == 0:
+                    N.check_fixups(fst, out.width, out.height)
                     out._host = (fst, out.stats_f64.cpu().numpy())
                     return filt, masks, hsi.numpy()[:n], hsf.numpy()[:n]
                 self.pair_capacity = int(int(fst[N.STAT_PAIRS]) * 1.25) + 1024

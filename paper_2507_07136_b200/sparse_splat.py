@@ -473,6 +473,8 @@ class QueryStream:
         ev, hm, hi, _, _, cam, query = handle
         ev.synchronize()
         st = hi.numpy()
+        if not int(st[N.STAT_OVERFLOW]):
+            N.check_fixups(st, cam.width, cam.height)
         if int(st[N.STAT_OVERFLOW]):
             r = query_pipeline(self.scene, cam, query, self.canonicals, window=self.window,
                                threshold=self.threshold, instrument=False, features=self.features,

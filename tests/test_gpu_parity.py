@@ -126,6 +126,38 @@ def test_fused_decode_matches_fp64_decode_of_the_map(opacity):
     assert np.abs(out.coeff_map.cpu().numpy() - ocm.data).max() <= W_TOL, fix
 
 
+@pytest.mark.parametrize("W,H,G,extent", [(800, 600, 30000, 1.0), (1280, 720, 12000, 0.35)])
+def test_persistent_splat_many_tiles_per_cta(W, H, G, extent):
+    """k_splat_tc's persistent pipeline with many half tiles per CTA (3.7k and
+    7.2k half tiles on 148 SMs): W/A slots alternate, the decode of one tile
+    overlaps the blend of the next, and (extent 0.35) most tiles at the
+    border are empty -- their features are stored as zeros without MMAs.
+    Coefficient map, final T, features and relevancy against the oracle."""
+    import torch
+    from paper_2507_07136_b200.device import QuerySpec, device_scene
+    rng = np.random.default_rng(17)
+    scene = random_scene(rng, G, num_levels=3, L=64, K=4, D=64, image_extent=extent)
+    cam = make_camera(W, H)
+    qv = rng.standard_normal(64)
+    canon = rng.standard_normal((4, 64))
+    eng = device_scene(scene).engine
+    out = eng.allocate(W, H, (0, 1, 2), coeff_map=True, final_t=True, features=True, query=True)
+    eng.run(cam, (0, 1, 2), out, query=QuerySpec(qv, canon, 11, -1, 0.5))
+    torch.cuda.synchronize()
+    ref = O.query_pipeline(scene, cam, qv, canon, window=11, keep_features=True)
+    assert np.abs(out.coeff_map.cpu().numpy() - ref.cmap.data).max() <= W_TOL
+    feats = out.features.cpu().numpy()
+    for b in range(3):
+        f_ref = ref.features[b]
+        assert np.abs(feats[b] - f_ref).max() <= F_REL * np.abs(f_ref).max(), b
+        # pixels no Gaussian reaches decode to exact zeros
+        zero = np.all(ref.cmap.data[:, :, 64 * b:64 * (b + 1)] == 0, axis=2)
+        assert not np.any(feats[b][zero]), b
+    raw = out.relevancy_raw.cpu().numpy()
+    for b in range(3):
+        assert np.abs(raw[b] - ref.raw_maps[b]).max() <= R_TOL
+
+
 @pytest.mark.parametrize("name", golden_names(require_query=True))
 def test_relevancy_ops_vs_reference(name):
     scene, cam, z = load_golden(name)
@@ -367,12 +399,53 @@ def test_frame_pipeline_matches_serial_frames(rng):
         for o in outs:
             got.append((o.features.clone(), o.relevancy_filtered.clone(), o.mask.clone(), o.stats_i64.clone()))
     torch.cuda.synchronize()
+    # bit for bit: the blend (tensor-core sums in a fixed order) and the exact
+    # replay (ordered per-channel sums, no float atomics) are deterministic
+    # (reference tests/test_rasterizer.py:153-158: results independent of workers)
     for k, (f, r, m, st) in enumerate(got):
         o = ref[k % 3]
-        assert (f - o.features).abs().max().item() <= 1e-6 * o.features.abs().max().item()
-        assert (r - o.relevancy_filtered).abs().max().item() <= 1e-12
+        assert torch.equal(f, o.features)
+        assert torch.equal(r, o.relevancy_filtered)
         assert torch.equal(m, o.mask)
         assert torch.equal(st[:8], o.stats_i64[:8])
+
+
+def test_fixup_overflow_raises():
+    """A frame with more early-exit-ambiguous pixels than the exact-replay list
+    holds raises instead of keeping uncertified fp32 decisions.  The list holds
+    W * H by default (cannot overflow); SF_FIXUP_CAPACITY lowers it, so the
+    check runs in a subprocess on an opaque scene that has several ambiguous pixels."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, sys
+sys.path.insert(0, 'tests')
+import paper_2507_07136_b200 as sf
+from paper_2507_07136_b200.errors import SplatfieldError
+from conftest import random_scene, make_camera
+rng = np.random.default_rng(11)
+scene = random_scene(rng, 6000, num_levels=3, L=64, K=4, D=64, opacity_range=(0.8, 0.99))
+cam = make_camera(128, 96)
+try:
+    sf.splat_multilevel(scene, cam, with_stats=True)
+except SplatfieldError as e:
+    assert "exact-replay capacity" in str(e), e
+    print("raised")
+else:
+    print("no-raise")
+"""
+    env = dict(os.environ, SF_FIXUP_CAPACITY="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().endswith("raised"), r.stdout + r.stderr[-2000:]
+    # the same frame at the default capacity replays every ambiguous pixel
+    env.pop("SF_FIXUP_CAPACITY")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("no-raise"), r.stdout + r.stderr[-2000:]
 
 
 def test_render_dense_vs_reference():
