@@ -29,10 +29,10 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_addr(b)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680)  // suspend-time hint: the thread sleeps in hardware until the phase flips
         : "memory");
 }
 
@@ -228,6 +228,29 @@ __device__ __forceinline__ bool patch_may_hit(const GeomF32& g, float x0, float 
     eval(fminf(fmaxf(-k * dy0, dx0), dx1), dy0);
     eval(fminf(fmaxf(-k * dy1, dx0), dx1), dy1);
     return best <= 9.f + fmaf(1e-4f, bs, 1e-4f);
+}
+
+// Guard band of blend_alpha_fast bounded over the whole 8x4 patch: the
+// per-pixel guard 1e-5 (a su^2 + d dy^2) + 1e-5 (su = |dx| + |k dy|) is
+// maximal at the patch's largest |dx| and |dy|, so one value per (entry,
+// patch) is conservative for every pixel (it can only add exact evaluations).
+__device__ __forceinline__ float patch_guard(const GeomF32& g, float x0, float y0) {
+    const float dx0 = (x0 - g.mx_hi) - g.mx_lo, dy0 = (y0 - g.my_hi) - g.my_lo;
+    const float mdx = fmaxf(fabsf(dx0), fabsf(dx0 + 7.f)), mdy = fmaxf(fabsf(dy0), fabsf(dy0 + 3.f));
+    const float su = fmaf(fabsf(g.k), mdy, mdx);
+    return fmaf(1e-5f, fmaf(g.a * su, su, g.d * mdy * mdy), 1e-5f);
+}
+// blend_alpha_fast with a given guard (patch_guard): the same alpha and
+// decision, a (possibly) wider ambiguity band
+__device__ __forceinline__ float blend_alpha_guarded(const GeomF32& g, float pxf, float pyf, float guard, bool& amb) {
+    constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 / ln 2
+    const float dx = (pxf - g.mx_hi) - g.mx_lo;
+    const float dy = (pyf - g.my_hi) - g.my_lo;
+    const float u = fmaf(g.k, dy, dx);
+    const float q32 = fmaf(g.a * u, u, g.d * dy * dy);
+    amb = fabsf(q32 - 9.f) <= guard;
+    const float al = fminf(g.opacity * exp2f(kNegHalfLog2e * fminf(q32, 9.5f)), 0.99f);
+    return q32 > 9.f ? 0.f : al;
 }
 
 // Warm L2 with the records of a later batch (lane j: record j)

@@ -17,7 +17,7 @@
 // scaling keeps the lo parts normal down to 2^-15, below which the absolute
 // error is < 2^-37).  W' = 2^24 W exactly.
 //
-// CTA = one SM (persistent, half tiles blockIdx.x + i gridDim.x), 10 warps:
+// CTA = one SM (persistent, half tiles blockIdx.x + i gridDim.x), 11 warps:
 //   warps 0-3  blend: pixel = TMEM lane (warp w owns lanes 32w..32w+31, an
 //              8x4 patch).  Per batch: conservative patch test (ballot), fp32
 //              alpha with the fp64 guard band, T walk, e -> E rows (fp16
@@ -29,9 +29,12 @@
 //   warp 8     producer: tile lists -> record ring (cp.async), sparse codes
 //              -> dense V^T stage (scatter of 12 hi/lo pairs per entry; the
 //              previous batch's 12 positions are cleared, not the whole stage).
-//   warp 9     MMA issuer (one thread): E V batches into the W slot of the
-//              blending tile, 3-term fp16 decode chunks (A = W from TMEM,
-//              B = codebook chunk by bulk copy) of the previous tile.
+//   warp 9     E V issuer (one thread): each batch's products into the W
+//              slot of the blending tile.
+//   warp 10    decode issuer (one thread): the 3-term fp16 decode chunks
+//              (A = W from TMEM, B = codebook chunk by bulk copy) of the
+//              previous tile.  Both issuers block on mbarriers (no polling);
+//              each one's tcgen05.commit tracks only its own products.
 // TMEM (512 columns): W/A slots [0,192) and [192,384) alternate by tile;
 // two 64-column decode accumulators at [384,512).
 #include <cuda.h>
@@ -49,11 +52,12 @@
 namespace sf {
 namespace tcs {
 
-constexpr int kThreads = 320;
-constexpr int kBlendWarps = 4;   // warps 0-3
-constexpr int kDrainWarp0 = 4;   // warps 4-7
-constexpr int kProdWarp = 8;
-constexpr int kMmaWarp = 9;
+constexpr int kThreads = 480;
+constexpr int kBlendWarps = 8;   // warps 0-7: two per TMEM lane quarter
+constexpr int kDrainWarp0 = 8;   // warps 8-11
+constexpr int kProdWarp = 12;
+constexpr int kMmaWarp = 13;   // E V issuer (one thread)
+constexpr int kDecWarp = 14;   // decode issuer (one thread)
 constexpr int kStages = 3;
 constexpr int kBatch = 32;
 constexpr int kMaxLevels = 3;
@@ -69,7 +73,7 @@ constexpr int kEBytes = 128 * kBatch * 2;         // 8 KB per part
 constexpr int kVBytes = kMaxCh * kBatch * 2;      // 12 KB per part
 constexpr float kScale = 4096.f;                  // 2^12 on E, V and the decode's A
 constexpr float kInvW = 1.f / 16777216.f;         // W = W' 2^-24
-constexpr uint32_t kMaxC = 16;
+constexpr uint32_t kMaxC = 12;  // channels per Gaussian (levels x K); more: legacy k_blend
 
 struct __align__(1024) Smem {
     unsigned char bring[kBStages][kChunkBytes];  // decode B ring (SW128, 1024-aligned)
@@ -81,6 +85,11 @@ struct __align__(1024) Smem {
     GeomF32 g[kStages][kBatch];
     uint32_t row[kStages][kBatch];
     double pd[kMaxCh * 4];  // fused relevancy: Pd_j = P_q - P_cj per (level, l)
+    uint32_t ering[8][kBatch];          // producer: tile-list entries, 5 batches ahead
+    unsigned char cring[3][kBatch][96]; // producer: the entries' sparse codes (plan records), 2 batches ahead
+    float guard[kBlendWarps][kBatch];   // per blend warp: its batch entries' patch guard bands
+    float alpha[4][2][16 * 32];         // per blend warp (quarter, hb): alphas of its <= 16 candidates x 32 pixels
+    float4 hand[4][2][32];              // pair hand-off: (T, T before last, error bound, count | done)
     int nb[kStages];
     int done_count;
     uint32_t contrib[2];   // per W slot: bit w = blend warp w's pixels got a contribution
@@ -91,6 +100,8 @@ struct __align__(1024) Smem {
     uint64_t b_full[kBStages], acc_full[2], acc_empty[2];
     uint32_t tmem_base;
 };
+
+static_assert(sizeof(Smem) + 1024 <= 232448, "shared memory exceeds the 227 KB opt-in limit");
 
 __device__ __forceinline__ bool bar_test(uint64_t* b, uint32_t parity) {
     uint32_t ok;
@@ -148,11 +159,35 @@ __device__ __forceinline__ uint32_t ns_off(int r, int k) {
 // the role's position, readable by the host while the kernel runs
 __device__ __forceinline__ void progress(const BlendArgs& A, int role, uint32_t a, uint32_t b) {
     if (A.timeline)
-        *reinterpret_cast<volatile uint64_t*>(A.timeline + (size_t)blockIdx.x * 16 + role) =
+        *reinterpret_cast<volatile uint64_t*>(A.timeline + (size_t)blockIdx.x * 128 + role) =
             ((uint64_t)a << 32) | (uint64_t)b | (1ull << 63);
 }
 
-template <int NC, bool DEC>
+// per-tile event timeline of CTA 0 (same aid): stamp[tile][event] at [148 * 128 + 16 * tile + event]
+__device__ __forceinline__ void tl_stamp(const BlendArgs& A, int tile_it, int ev) {
+    if (A.timeline && blockIdx.x == 0 && tile_it < 256)
+        A.timeline[148 * 128 + 16 * tile_it + ev] = clock64();
+}
+// cycle accounting (same aid): slot i of the CTA's 64 counters at [16, 80) of its 128
+__device__ __forceinline__ void prof_add(const BlendArgs& A, int i, uint64_t v) {
+    if (A.timeline) A.timeline[(size_t)blockIdx.x * 128 + 16 + i] += v;
+}
+#define SF_PROG(...)                       \
+    do {                                   \
+        if constexpr (prof) progress(__VA_ARGS__); \
+    } while (0)
+#define SF_STAMP(...)                      \
+    do {                                   \
+        if constexpr (prof) tl_stamp(__VA_ARGS__); \
+    } while (0)
+#define SF_TIMED(acc, stmt)                     \
+    do {                                        \
+        const uint64_t t0_ = prof ? clock64() : 0; \
+        stmt;                                   \
+        if (prof) acc += clock64() - t0_;       \
+    } while (0)
+
+template <int NC, bool DEC, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __grid_constant__ CUtensorMap fmap) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t mis = (1024u - (smem_addr(smem_raw) & 1023u)) & 1023u;
@@ -208,59 +243,95 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
     __syncthreads();
     tc_after();
     const uint32_t tm = S.tmem_base;
+    constexpr bool prof = PROF;  // the SF_TC_PROGRESS development variant: progress, cycle counters, timeline
+    const uint64_t t_start = prof ? clock64() : 0;
+    uint64_t w0 = 0, w1 = 0, w2 = 0;  // per-role wait counters (SF_TC_PROGRESS only)
 
     if (warp == kProdWarp) {
         // ---------------- producer: records -> ring, sparse codes -> V^T ----------------
+        // A cp.async software pipeline (no load latency in the loop): the tile
+        // list's entries are issued 5 batches ahead (ering), the entries' sparse
+        // codes 2 batches ahead (cring), the geometry records of batch bi with
+        // the stage's rec_full barrier.  Commit group G_bi = everything issued
+        // in iteration bi; wait_group 2 at its end lands G_{bi-2}: batch bi's
+        // codes, and the entries of batch bi + 3 that iteration bi + 1 reads.
         const int C = A.C;
         const int cs = chan_rec_bytes(C), voff = chan_val_offset(C);
+        const int cq = cs / 16;
         const uint32_t vh0 = smem_addr(&S.vhi[0][0]), vl0 = smem_addr(&S.vlo[0][0]);
         // channel ids (u8) this lane wrote into the stage used 1, 2, 3 batches ago
-        uint32_t old0[4] = {~0u, ~0u, ~0u, ~0u}, old1[4] = {~0u, ~0u, ~0u, ~0u}, old2[4] = {~0u, ~0u, ~0u, ~0u};
+        uint32_t old0[3] = {~0u, ~0u, ~0u}, old1[3] = {~0u, ~0u, ~0u}, old2[3] = {~0u, ~0u, ~0u};
+        auto cp4 = [&](void* dst, const void* src) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+        };
+        auto load_codes = [&](int slot3, uint32_t row) {
+            const unsigned char* src = A.chan + (size_t)row * cs;
+            unsigned char* dst = &S.cring[slot3][lane][0];
+            for (int q = 0; q < cq; ++q) cp_async16(dst + 16 * q, src + 16 * q);
+        };
         int bs = 0;
         for (int it = 0; it < n_my; ++it) {
             const int ht = (int)blockIdx.x + it * (int)gridDim.x;
             const int tile = A.tile0 + (ht >> 1);
             const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
-            auto entry = [&](uint32_t i) -> uint32_t { return i < end ? __ldg(A.entries + i) : 0u; };
-            auto load_chan = [&](uint32_t r, bool ok, uint4 (&w)[4], float4 (&v)[4]) {
-                const unsigned char* rec = A.chan + (size_t)r * cs;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const bool in = ok && 4 * q < C;
-                    w[q] = in ? __ldg(reinterpret_cast<const uint4*>(rec) + q) : make_uint4(0, 0, 0, 0);
-                    v[q] = in ? __ldg(reinterpret_cast<const float4*>(rec + voff) + q) : make_float4(0, 0, 0, 0);
+            if (lane == 0) SF_STAMP(A, it, 9);
+            {
+                // warm L2 with the next tile's first entries (its prologue reads them)
+                const int ht2 = ht + (int)gridDim.x;
+                if (ht2 < n_half && lane < 4) {
+                    const int t2 = A.tile0 + (ht2 >> 1);
+                    const uint32_t b2 = A.tile_offsets[t2] + 32u * lane;
+                    if (b2 < A.tile_offsets[t2 + 1]) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.entries + b2));
                 }
-            };
-            uint32_t e_cur = entry(beg + lane), e_next = entry(beg + kBatch + lane);
-            if (beg + lane < end) prefetch_records(A, e_cur, cs);
-            uint4 wc[4], wn[4];
-            float4 vc[4], vn[4];
-            load_chan(e_cur, beg + lane < end, wc, vc);
+            }
+            // prologue: entries of batches 0..4, then the codes of batches 0, 1
+#pragma unroll
+            for (int k = 0; k < 5; ++k)
+                if (beg + 32u * k + lane < end) cp4(&S.ering[k][lane], A.entries + beg + 32u * k + lane);
+            cp_async_commit();
+            cp_async_wait<0>();
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (beg + 32u * k + lane < end) {
+                    const uint32_t r = S.ering[k][lane];
+                    load_codes(k, r);
+                    prefetch_records(A, r, cs);
+                }
+                cp_async_commit();
+            }
             for (int bi = 0;; ++bi) {
                 const int s = bs % kStages;
                 const uint32_t base = beg + (uint32_t)bi * kBatch;
-                const uint32_t e_n2 = entry(base + 2 * kBatch + lane);
-                if (base + kBatch + lane < end) prefetch_records(A, e_next, cs);
-                if (bs >= kStages) bar_wait(&S.ev_empty[s], ((bs / kStages) - 1) & 1);
+                if (bs >= kStages) SF_TIMED(w0, bar_wait(&S.ev_empty[s], ((bs / kStages) - 1) & 1));
                 const bool all_done = *reinterpret_cast<volatile int*>(&S.done_count) == kBlendWarps * (it + 1);
                 const int nb = (base < end && !all_done) ? (int)min((uint32_t)kBatch, end - base) : 0;
+                const uint32_t row = S.ering[bi & 7][lane];
                 if (lane < nb) {
-                    cp_async16(&S.g[s][lane], A.geom + e_cur);
-                    cp_async16(reinterpret_cast<char*>(&S.g[s][lane]) + 16, reinterpret_cast<const char*>(A.geom + e_cur) + 16);
-                    S.row[s][lane] = e_cur;
+                    cp_async16(&S.g[s][lane], A.geom + row);
+                    cp_async16(reinterpret_cast<char*>(&S.g[s][lane]) + 16, reinterpret_cast<const char*>(A.geom + row) + 16);
+                    S.row[s][lane] = row;
                 }
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&S.rec_full[s]))
                              : "memory");
                 if (lane == 0) S.nb[s] = nb;
                 __syncwarp();
                 if (lane == 0) bar_arrive(&S.rec_full[s]);
-                // the next batch's codes load while this batch's V^T is built
-                const bool nxt_ok = nb == kBatch && base + kBatch + lane < end;
-                load_chan(e_next, nxt_ok, wn, vn);
+                if (nb == kBatch) {
+                    // entries of batch bi + 5 (slot of batch bi - 3, consumed); codes of batch bi + 2
+                    if (base + 5u * kBatch + lane < end)
+                        cp4(&S.ering[(bi + 5) & 7][lane], A.entries + base + 5u * kBatch + lane);
+                    if (base + 2u * kBatch + lane < end) {
+                        const uint32_t r2 = S.ering[(bi + 2) & 7][lane];
+                        load_codes((bi + 2) % 3, r2);
+                        prefetch_records(A, r2, cs);
+                    }
+                }
+                cp_async_commit();
+                cp_async_wait<2>();  // G_{bi-2}: this batch's codes
                 const uint32_t vh = vh0 + s * kVBytes, vl = vl0 + s * kVBytes;
                 // clear what this lane wrote into the stage last time (column k = lane)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < 3; ++q) {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const uint32_t n = (old0[q] >> (8 * e)) & 0xFFu;
@@ -271,12 +342,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                         }
                     }
                 }
-                uint32_t nw[4] = {~0u, ~0u, ~0u, ~0u};
+                uint32_t nw[3] = {~0u, ~0u, ~0u};
                 if (lane < nb) {
-                    const uint32_t wv[16] = {wc[0].x, wc[0].y, wc[0].z, wc[0].w, wc[1].x, wc[1].y, wc[1].z, wc[1].w,
-                                             wc[2].x, wc[2].y, wc[2].z, wc[2].w, wc[3].x, wc[3].y, wc[3].z, wc[3].w};
-                    const float fv[16] = {vc[0].x, vc[0].y, vc[0].z, vc[0].w, vc[1].x, vc[1].y, vc[1].z, vc[1].w,
-                                          vc[2].x, vc[2].y, vc[2].z, vc[2].w, vc[3].x, vc[3].y, vc[3].z, vc[3].w};
+                    const unsigned char* rec = &S.cring[bi % 3][lane][0];
+                    uint32_t wv[12];
+                    float fv[12];
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const uint4 w4 = q * 4 < C ? *reinterpret_cast<const uint4*>(rec + 16 * q) : make_uint4(0, 0, 0, 0);
+                        const float4 v4 =
+                            q * 4 < C ? *reinterpret_cast<const float4*>(rec + voff + 16 * q) : make_float4(0, 0, 0, 0);
+                        wv[4 * q] = w4.x, wv[4 * q + 1] = w4.y, wv[4 * q + 2] = w4.z, wv[4 * q + 3] = w4.w;
+                        fv[4 * q] = v4.x, fv[4 * q + 1] = v4.y, fv[4 * q + 2] = v4.z, fv[4 * q + 3] = v4.w;
+                    }
 #pragma unroll
                     for (int c = 0; c < (int)kMaxC; c += 2) {
                         if (c < C) {
@@ -300,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < 3; ++q) {
                     old0[q] = old1[q];
                     old1[q] = old2[q];
                     old2[q] = nw[q];
@@ -309,24 +387,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 __syncwarp();
                 if (lane == 0) bar_arrive(&S.ev_full[s]);
                 ++bs;
-                if (lane == 0) progress(A, 0, (uint32_t)it, (uint32_t)bs);
-                if (nb == 0) break;
-                e_cur = e_next;
-                e_next = e_n2;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) wc[q] = wn[q], vc[q] = vn[q];
+                if (lane == 0) SF_PROG(A, 0, (uint32_t)it, (uint32_t)bs);
+                if (nb == 0) {
+                    if (lane == 0) SF_STAMP(A, it, 10);
+                    break;
+                }
             }
+            cp_async_wait<0>();
         }
     } else if (warp < kBlendWarps) {
         // ---------------- blend warps: E rows per batch, W epilogue per tile ----------------
-        const int cw = warp;
+        // Warps w and w + 4 share TMEM lane quarter w & 3 (32 pixels, an 8x4
+        // patch).  Warp hb = w >> 2 owns entries [16 hb, 16 hb + 16) of every
+        // batch: both evaluate their alphas at once, then walk the
+        // transmittance in depth order -- hb 0, hand the pixel state (T, T
+        // before the last contribution, error bound, count / done) to hb 1
+        // through shared memory and a named barrier, hb 1 walks, hands back.
+        const int cw = warp & 3, hb = warp >> 2;
         const int m = 32 * cw + lane;  // MMA row = TMEM lane = pixel slot in the half tile
         const uint32_t lane_off = (uint32_t)(32 * cw) << 16;
         const uint32_t eh0 = smem_addr(&S.ehi[0][0]) + (uint32_t)((m >> 3) * 512 + (m & 7) * 16);
         const uint32_t el0 = smem_addr(&S.elo[0][0]) + (uint32_t)((m >> 3) * 512 + (m & 7) * 16);
         const bool rel = NC == 4 && A.proj_cb != nullptr;
+        const bool early_exit = A.early_exit != 0;
+        float* gsm = S.guard[warp];
+        float* asc = S.alpha[cw][hb];          // [16][32] alphas of this warp's candidates
+        float4* hand_out = S.hand[cw][hb];     // state this warp posts
+        const float4* hand_in = S.hand[cw][hb ^ 1];
+        const int bar_ab = 1 + cw, bar_ba = 5 + cw;  // named barriers of the pair (64 threads)
+        const int bar_rd = 9 + cw;                    // hb 0 has read the tile's W for the relevancy
+        const int e0 = 16 * hb;                       // first batch entry of this warp
         int bs = 0;
-        uint32_t zero_mask = 0;  // stages whose E rows of this warp are all zero
+        uint32_t zero_mask = 0;  // stages whose E half-rows of this warp are all zero
         for (int it = 0; it < n_my; ++it) {
             const int ht = (int)blockIdx.x + it * (int)gridDim.x;
             const int slot = it & 1;
@@ -341,85 +433,139 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             float T = 1.f, eb = 0.f, Tprev = 1.f;
             int ncontrib = 0, nbatches = 0;
             bool done = !inside;
-            bool warp_done = __all_sync(0xffffffffu, done);
-            bool counted = warp_done;
-            if (warp_done && lane == 0) atomicAdd(&S.done_count, 1);
+            if (hb == 0 && lane == 0) SF_STAMP(A, it, 0);
+            bool all_done = __all_sync(0xffffffffu, done);
+            bool counted = all_done;
+            if (all_done && lane == 0) atomicAdd(&S.done_count, 1);
+            float Tr = 1.f;  // running transmittance over every entry (T: after the last counted one)
+            auto recv = [&](int id) {
+                named_bar_sync(id, 64);
+                const float4 st = hand_in[lane];
+                T = st.x, Tprev = st.y, eb = st.z;
+                const int c = __float_as_int(st.w);
+                ncontrib = c & 0x7FFFFFFF;
+                done = c < 0;
+                Tr = done ? 0.f : T;  // once done nothing counts again; else Tr == T
+            };
+            auto post = [&](int id) {
+                hand_out[lane] = make_float4(T, Tprev, eb, __int_as_float(ncontrib | (done ? (int)0x80000000 : 0)));
+                asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
+            };
             for (;;) {
                 const int s = bs % kStages;
-                bar_wait(&S.rec_full[s], (bs / kStages) & 1);
+                SF_TIMED(w0, bar_wait(&S.rec_full[s], (bs / kStages) & 1));
                 const int nb = *reinterpret_cast<volatile int*>(&S.nb[s]);
                 if (nb == 0) {
+                    if (hb == 0 && nbatches > 0) recv(bar_ba);  // the tile's final state
                     __syncwarp();
                     if (lane == 0) bar_arrive(&S.ev_full[s]);
                     ++bs;
                     break;
                 }
-                ++nbatches;
-                const uint32_t eh = eh0 + s * kEBytes, el = el0 + s * kEBytes;
-                if (!warp_done) {
-                    const GeomF32* G = S.g[s];
-                    const uint32_t wcand = __ballot_sync(0xffffffffu, lane < nb && patch_may_hit(G[lane], pdx0, pdy0));
+                const uint32_t eh = eh0 + s * kEBytes + 256 * hb, el = el0 + s * kEBytes + 256 * hb;
+                const GeomF32* G = S.g[s];
+                // ---- alphas of this warp's candidates (before the hand-off) ----
+                const uint64_t ta0 = prof ? clock64() : 0;
+                uint32_t wmask = 0;
+                if (!all_done) {
+                    bool hit = false;
+                    if (lane < 16 && e0 + lane < nb) {
+                        hit = patch_may_hit(G[e0 + lane], pdx0, pdy0);
+                        gsm[lane] = patch_guard(G[e0 + lane], pdx0, pdy0);
+                    }
+                    wmask = __ballot_sync(0xffffffffu, hit);
+                    __syncwarp();
+                    int c0 = 0;
+#pragma unroll 1
+                    for (uint32_t wm = wmask; wm; c0 += 8) {
+                        int jj[8];
 #pragma unroll
-                    for (int g4 = 0; g4 < 4; ++g4) {
-                        const uint32_t byte = (wcand >> (8 * g4)) & 0xFFu;
-                        uint32_t hw[4] = {0u, 0u, 0u, 0u}, lw[4] = {0u, 0u, 0u, 0u};
-                        if (byte) {
-                            float alv[8];
-                            uint32_t amb = 0;
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) {
-                                bool gb = false;
-                                alv[u] = ((byte >> u) & 1u) ? blend_alpha_fast(G[8 * g4 + u], pxf, pyf, gb) : 0.f;
-                                amb |= (gb ? 1u : 0u) << u;
-                            }
-                            if (__any_sync(0xffffffffu, amb != 0)) {
-                                for (int u = 0; u < 8; ++u)
-                                    if (amb & (1u << u))
-                                        alv[u] = blend_alpha_exact(G[8 * g4 + u], A.geom + S.row[s][8 * g4 + u], pxd, pyd);
-                            }
-                            float ev[8];
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) {
-                                const float al = alv[u];
-                                const bool live = al > 0.f && !done;
-                                ev[u] = live ? al * T : 0.f;
-                                if (live) {
-                                    Tprev = T;
-                                    T = fmaf(-al, T, T);
-                                    eb = fmaf(al, rcp_approx(1.f - al), eb);  // 1 - al in [0.01, 1]
-                                    ++ncontrib;
-                                    if (A.early_exit && T < (float)SF_EARLY_EXIT_T) done = true;
-                                }
-                            }
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) split2(ev[2 * i] * kScale, ev[2 * i + 1] * kScale, hw[i], lw[i]);
+                        for (int u = 0; u < 8; ++u) {
+                            jj[u] = wm ? __ffs(wm) - 1 : -1;
+                            wm &= wm - 1;
                         }
-                        sts128(eh + 128 * g4, hw[0], hw[1], hw[2], hw[3]);
-                        sts128(el + 128 * g4, lw[0], lw[1], lw[2], lw[3]);
-                    }
-                    zero_mask &= ~(1u << s);
-                } else if (!((zero_mask >> s) & 1u)) {
+                        float alv[8];
+                        bool anyamb = false;
+                        uint32_t amb = 0;
 #pragma unroll
-                    for (int g4 = 0; g4 < 4; ++g4) {
-                        sts128(eh + 128 * g4, 0u, 0u, 0u, 0u);
-                        sts128(el + 128 * g4, 0u, 0u, 0u, 0u);
+                        for (int u = 0; u < 8; ++u) {
+                            const int j = jj[u] & 15;
+                            bool gb = false;
+                            alv[u] = blend_alpha_guarded(G[e0 + j], pxf, pyf, gsm[j], gb);
+                            gb = gb && jj[u] >= 0;
+                            amb |= (gb ? 1u : 0u) << u;
+                            anyamb |= gb;
+                        }
+                        if (__any_sync(0xffffffffu, anyamb)) {
+#pragma unroll 1
+                            for (int u = 0; u < 8; ++u)
+                                if (amb & (1u << u))
+                                    alv[u] = blend_alpha_exact(G[e0 + jj[u]], A.geom + S.row[s][e0 + jj[u]], pxd, pyd);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (c0 + u < 16) asc[(c0 + u) * 32 + lane] = alv[u];
                     }
-                    zero_mask |= 1u << s;
                 }
+                // ---- E half-row: zero, then the candidates' e (hi, lo) ----
+                if (wmask || !((zero_mask >> s) & 1u)) {
+                    sts128(eh, 0u, 0u, 0u, 0u);
+                    sts128(eh + 128, 0u, 0u, 0u, 0u);
+                    sts128(el, 0u, 0u, 0u, 0u);
+                    sts128(el + 128, 0u, 0u, 0u, 0u);
+                }
+                zero_mask = wmask ? (zero_mask & ~(1u << s)) : (zero_mask | (1u << s));
+                // ---- hand-off in, transmittance walk in depth order, hand-off out ----
+                if (prof) w1 += clock64() - ta0;
+                if (hb == 1) SF_TIMED(w0, recv(bar_ab));
+                else if (nbatches > 0) SF_TIMED(w0, recv(bar_ba));
+                const uint64_t tw0 = prof ? clock64() : 0;
+                {
+                    int c = 0;
+#pragma unroll 4
+                    for (uint32_t wm = wmask; wm; ++c) {
+                        const int j = __ffs(wm) - 1;
+                        wm &= wm - 1;
+                        // Tr runs through every entry (one FMA per entry carries the
+                        // loop); an entry counts iff alpha > 0 and Tr before it >= 1e-4
+                        // (T only falls, so that is the reference's early exit, and the
+                        // counted entries see exactly the transmittance they saw before)
+                        const float al = asc[c * 32 + lane];
+                        const bool live = al > 0.f && inside && (!early_exit || Tr >= (float)SF_EARLY_EXIT_T);
+                        const float alive = live ? al : 0.f;
+                        const float e = alive * Tr;
+                        Tprev = live ? Tr : Tprev;
+                        Tr = fmaf(-al, Tr, Tr);
+                        T = live ? Tr : T;
+                        eb = fmaf(alive, rcp_approx(1.f - alive), eb);  // 1 - alive in [0.01, 1]
+                        ncontrib += live ? 1 : 0;
+                        const float x = e * kScale;
+                        const __half h = __float2half_rn(x);
+                        const __half l = __float2half_rn(x - __half2float(h));
+                        const uint32_t o = (uint32_t)((j >> 3) * 128 + (j & 7) * 2);
+                        sts16(eh + o, __half_as_ushort(h));
+                        sts16(el + o, __half_as_ushort(l));
+                    }
+                }
+                done = !inside || (early_exit && Tr < (float)SF_EARLY_EXIT_T);
+                post(hb == 0 ? bar_ab : bar_ba);
+                if (prof) w2 += clock64() - tw0;
+                ++nbatches;
                 proxy_fence();
                 __syncwarp();
                 if (lane == 0) bar_arrive(&S.ev_full[s]);
                 ++bs;
-                if (!warp_done && __all_sync(0xffffffffu, done)) {
-                    warp_done = true;
+                if (!all_done && __all_sync(0xffffffffu, done)) {
+                    all_done = true;
                     if (!counted && lane == 0) atomicAdd(&S.done_count, 1);
                     counted = true;
                 }
             }
             if (!counted && lane == 0) atomicAdd(&S.done_count, 1);
+            if (hb == 0 && lane == 0) SF_STAMP(A, it, 1);
 
-            // ---- per-tile epilogue ----
-            if (inside && A.early_exit && A.fixup_list) {
+            // ---- per-tile epilogue: hb 0 takes columns [0, 32) of each level, hb 1 [32, 64) ----
+            if (hb == 0 && inside && A.early_exit && A.fixup_list) {
                 // early-exit decisions fp32 cannot certify: replayed in fp64 by k_blend_fixup_cta
                 const float tol = fmaf(4e-6f, eb, fmaf(3e-7f, (float)ncontrib, 2e-6f));
                 const float thr = (float)SF_EARLY_EXIT_T;
@@ -429,27 +575,79 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     if (k < A.fixup_capacity) A.fixup_list[k] = ((uint32_t)tile << 8) | (uint32_t)(half * 128 + m);
                 }
             }
-            if (A.final_t && inside) A.final_t[(size_t)py * A.W + px] = T;
+            if (hb == 0 && A.final_t && inside) A.final_t[(size_t)py * A.W + px] = T;
             const bool any = __any_sync(0xffffffffu, ncontrib > 0);
-            if (lane == 0) progress(A, 1 + cw, (uint32_t)it, 0x10000u | (uint32_t)bs);
-            bar_wait(&S.w_full[slot], (it >> 1) & 1);
-            if (lane == 0) progress(A, 1 + cw, (uint32_t)it, 0x20000u | (uint32_t)bs);
+            if (lane == 0 && hb == 0) SF_PROG(A, 1 + cw, (uint32_t)it, 0x10000u | (uint32_t)bs);
+            SF_TIMED(w0, bar_wait(&S.w_full[slot], (it >> 1) & 1));
+            if (lane == 0 && hb == 0) SF_PROG(A, 1 + cw, (uint32_t)it, 0x20000u | (uint32_t)bs);
             // published only now: the W slot's previous tile (it - 2) has been
             // fully decoded (its slot_free preceded this tile's E V products),
-            // so the MMA issuer has read that tile's flag
-            if (lane == 0) {
+            // so the decode issuer has read that tile's flag
+            if (hb == 0 && lane == 0) {
                 if (any) atomicOr(&S.contrib[slot], 1u << cw);
                 else atomicAnd(&S.contrib[slot], ~(1u << cw));
             }
             tc_after();
-            const uint32_t wcol = tm + lane_off + (uint32_t)(slot * kSlotCols);
+            const uint32_t wslot = tm + lane_off + (uint32_t)(slot * kSlotCols);
             const size_t pix = (size_t)py * A.W + px;
-            for (int b = 0; b < n_levels; ++b) {
-                double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
+            // Compact code: this part runs once per tile per warp, so its
+            // instructions are fetched cold -- loops stay rolled.
+            // (1) hb 0: relevancy over all 64 columns of each level (before hb 1
+            //     converts its columns in place), 8 columns per step.
+            if (hb == 0 && rel && nbatches) {
 #pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
+                for (int b = 0; b < n_levels; ++b) {
+                    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
+#pragma unroll 1
+                    for (int c = 0; c < 64; c += 8) {
+                        uint32_t v[8];
+                        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                                       "=r"(v[7])
+                                     : "r"(wslot + (uint32_t)(64 * b + c)));
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        const double* P = S.pd + (size_t)(64 * b + c) * 4;
+#pragma unroll
+                        for (int i = 0; i < 8; i += 2) {
+                            const double2 a01 = *reinterpret_cast<const double2*>(P + 4 * i);
+                            const double2 a23 = *reinterpret_cast<const double2*>(P + 4 * i + 2);
+                            const double2 b01 = *reinterpret_cast<const double2*>(P + 4 * i + 4);
+                            const double2 b23 = *reinterpret_cast<const double2*>(P + 4 * i + 6);
+                            const double x = (double)(__uint_as_float(v[i]) * kInvW);
+                            const double y = (double)(__uint_as_float(v[i + 1]) * kInvW);
+                            d0 = fma(x, a01.x, d0), d1 = fma(x, a01.y, d1), d2 = fma(x, a23.x, d2), d3 = fma(x, a23.y, d3);
+                            f0 = fma(y, b01.x, f0), f1 = fma(y, b01.y, f1), f2 = fma(y, b23.x, f2), f3 = fma(y, b23.y, f3);
+                        }
+                    }
+                    d0 += f0, d1 += f1, d2 += f2, d3 += f3;
+                    // sigmoid is monotone: min_j sigmoid(d_j) = sigmoid(min_j d_j)
+                    if (inside)
+                        A.relevancy_raw[(size_t)b * A.W * A.H + pix] =
+                            sigmoid2(np_minimum(np_minimum(d0, d1), np_minimum(d2, d3)));
+                }
+            } else if (hb == 0 && rel && inside) {
+#pragma unroll 1
+                for (int b = 0; b < n_levels; ++b) A.relevancy_raw[(size_t)b * A.W * A.H + pix] = 0.5;  // W = 0
+            }
+            if (rel) {
+                // hb 1 may overwrite its columns once hb 0 has read them
+                if (hb == 0) {
+                    tc_before();
+                    __syncwarp();
+                    asm volatile("bar.arrive %0, 64;" ::"r"(bar_rd) : "memory");
+                } else {
+                    named_bar_sync(bar_rd, 64);
+                    tc_after();
+                }
+            }
+            // (2) each warp: its 32 columns of each level -> coefficient map (if
+            //     requested) and, fused decode, the A operand (fp16 hi/lo pairs of
+            //     W 2^12) in place
+            if (DEC || A.coeff_map) {
+#pragma unroll 1
+                for (int b = 0; b < n_levels; ++b) {
+                    const uint32_t col = wslot + (uint32_t)(64 * b + 32 * hb);
                     uint32_t v[32];
-                    const uint32_t col = wcol + (uint32_t)(64 * b + 32 * h);
                     if (nbatches) {
                         tmem_ld32(col, v);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -457,47 +655,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = 0u;
                     }
-                    float w[32];
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) w[i] = __uint_as_float(v[i]) * kInvW;
-                    if (rel) {
-                        const double* P = S.pd + (size_t)(64 * b + 32 * h) * 4;
-#pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
-                            const double2 a01 = *reinterpret_cast<const double2*>(P + 4 * i);
-                            const double2 a23 = *reinterpret_cast<const double2*>(P + 4 * i + 2);
-                            const double2 b01 = *reinterpret_cast<const double2*>(P + 4 * i + 4);
-                            const double2 b23 = *reinterpret_cast<const double2*>(P + 4 * i + 6);
-                            const double x = (double)w[i], y = (double)w[i + 1];
-                            d0 = fma(x, a01.x, d0), d1 = fma(x, a01.y, d1), d2 = fma(x, a23.x, d2), d3 = fma(x, a23.y, d3);
-                            f0 = fma(y, b01.x, f0), f1 = fma(y, b01.y, f1), f2 = fma(y, b23.x, f2), f3 = fma(y, b23.y, f3);
-                        }
-                    }
                     if (A.coeff_map && inside) {
-                        float4* dst = reinterpret_cast<float4*>(A.coeff_map + pix * n_ch + 64 * b + 32 * h);
+                        float4* dst = reinterpret_cast<float4*>(A.coeff_map + pix * n_ch + 64 * b + 32 * hb);
 #pragma unroll
                         for (int i = 0; i < 8; ++i)
-                            __stcs(dst + i, make_float4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]));
+                            __stcs(dst + i, make_float4(__uint_as_float(v[4 * i]) * kInvW, __uint_as_float(v[4 * i + 1]) * kInvW,
+                                                        __uint_as_float(v[4 * i + 2]) * kInvW,
+                                                        __uint_as_float(v[4 * i + 3]) * kInvW));
                     }
                     if (DEC) {
+                        // W' 2^-24 2^12 = W' 2^-12: hi / lo of W 2^12
                         uint32_t hi[16], lo[16];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) split2(w[2 * i] * kScale, w[2 * i + 1] * kScale, hi[i], lo[i]);
+                        for (int i = 0; i < 16; ++i)
+                            split2(__uint_as_float(v[2 * i]) * (kInvW * kScale), __uint_as_float(v[2 * i + 1]) * (kInvW * kScale),
+                                   hi[i], lo[i]);
                         tmem_st16(col, hi);
                         tmem_st16(col + 16, lo);
                     }
-                }
-                if (rel && inside) {
-                    d0 += f0, d1 += f1, d2 += f2, d3 += f3;
-                    // sigmoid is monotone: min_j sigmoid(d_j) = sigmoid(min_j d_j)
-                    A.relevancy_raw[(size_t)b * A.W * A.H + pix] =
-                        sigmoid2(np_minimum(np_minimum(d0, d1), np_minimum(d2, d3)));
                 }
             }
             if (DEC) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_before();
             __syncwarp();
             if (lane == 0) bar_arrive(DEC ? &S.a_ready[slot] : &S.slot_free[slot]);
+            if (hb == 0 && lane == 0) SF_STAMP(A, it, 2);
         }
     } else if (warp < kDrainWarp0 + 4) {
         // ---------------- drain warps: accumulators -> swizzled boxes -> TMA stores ----------------
@@ -516,9 +698,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 const int tile = A.tile0 + (ht >> 1), half = ht & 1;
                 const int w8 = half * 4 + q;
                 const int bx = (tile % A.tiles_x) * SF_TILE + (w8 & 1) * 8, by = (tile / A.tiles_x) * SF_TILE + (w8 >> 1) * 4;
-                if (lane == 0) progress(A, 5 + q, (uint32_t)it, 0x10000u | (uint32_t)Gd);
-                bar_wait(&S.dq_full[slot], (it >> 1) & 1);
-                if (lane == 0) progress(A, 5 + q, (uint32_t)it, 0x20000u | (uint32_t)Gd);
+                if (lane == 0) SF_PROG(A, 5 + q, (uint32_t)it, 0x10000u | (uint32_t)Gd);
+                SF_TIMED(w0, bar_wait(&S.dq_full[slot], (it >> 1) & 1));
+                if (lane == 0) SF_PROG(A, 5 + q, (uint32_t)it, 0x20000u | (uint32_t)Gd);
+                if (q == 0 && lane == 0) SF_STAMP(A, it, 6);
                 const bool contrib = *reinterpret_cast<volatile uint32_t*>(&S.dq_info[slot]) != 0u;
                 __syncwarp();
                 if (lane == 0) bar_arrive(&S.dq_empty[slot]);
@@ -544,8 +727,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 }
                 for (int g = 0; g < nchunk; ++g, ++Gd) {
                     const int t = Gd & 1, b = g / dchunks, c = g - b * dchunks;
-                    if (lane == 0) progress(A, 5 + q, (uint32_t)it, 0x30000u | (uint32_t)Gd);
-                    bar_wait(&S.acc_full[t], (Gd >> 1) & 1);
+                    if (lane == 0) SF_PROG(A, 5 + q, (uint32_t)it, 0x30000u | (uint32_t)Gd);
+                    SF_TIMED(w1, bar_wait(&S.acc_full[t], (Gd >> 1) & 1));
                     if (q == 0 && lane == 0) {
                         // chunk Gd's MMAs are complete: its codebook stage takes chunk Gd + 2
                         const int sg = Gd % kBStages;
@@ -565,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     const float sc = b == 0 ? scl[0] : (b == 1 ? scl[1] : scl[2]);
 #pragma unroll
                     for (int i = 0; i < 64; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
-                    if (lane == 0) bulk_wait_read<0>();  // the previous chunk's stores have left the boxes
+                    if (lane == 0) SF_TIMED(w2, bulk_wait_read<0>());  // the previous chunk's stores have left the boxes
                     __syncwarp();
 #pragma unroll
                     for (int qq = 0; qq < 2; ++qq) {
@@ -584,6 +767,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                         tma_store_4d(&fmap, wbox, c * kDecN, bx, by, b);
                         tma_store_4d(&fmap, wbox + kBoxBytes, c * kDecN + kBoxCols, bx, by, b);
                         bulk_commit();
+                        if (q == 0 && g == nchunk - 1) SF_STAMP(A, it, 7);
+                        if (q == 0 && g == 0) SF_STAMP(A, it, 8);
                     }
                 }
             }
@@ -594,104 +779,102 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             }
         }
     } else if (warp == kMmaWarp && lane == 0) {
-        // ---------------- MMA issuer ----------------
+        // ---------------- E V issuer: the blend products, batch by batch ----------------
         const uint32_t idesc_ev = (1u << 4) | ((uint32_t)(n_ch >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        const uint32_t idesc_dec = (1u << 4) | ((uint32_t)(kDecN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        const unsigned char* img = reinterpret_cast<const unsigned char*>(A.dec_b);
-        if (DEC) {
-            for (int g = 0; g < kBStages; ++g) {
-                bar_expect_tx(&S.b_full[g], kChunkBytes);
-                bulk_g2s(S.bring[g], img + (size_t)(g % nchunk) * kChunkBytes, kChunkBytes, &S.b_full[g]);
-            }
-        }
         const uint32_t eh0 = smem_addr(&S.ehi[0][0]), el0 = smem_addr(&S.elo[0][0]);
         const uint32_t vh0 = smem_addr(&S.vhi[0][0]), vl0 = smem_addr(&S.vlo[0][0]);
-        const uint64_t bdesc0 = sw128_desc(smem_addr(S.bring[0]));
-        int te = 0, be = 0;
-        bool first = true;
-        int td = 0, cd = 0, Gd = 0;
-        bool dactive = false;
-        while (te < n_my || (DEC && td < n_my)) {
-            bool prog = false;
-            if (DEC && td < te) {
-                if (!dactive && bar_test(&S.a_ready[td & 1], (td >> 1) & 1) &&
-                    (td < 2 || bar_test(&S.dq_empty[td & 1], ((td >> 1) - 1) & 1))) {
-                    tc_after();
-                    // the drains learn the tile's kind in order, through their own ring
-                    const uint32_t c = *reinterpret_cast<volatile uint32_t*>(&S.contrib[td & 1]);
-                    S.dq_info[td & 1] = c;
-                    bar_arrive(&S.dq_full[td & 1]);
-                    if (c != 0u) {
-                        dactive = true;
-                        cd = 0;
-                    } else {
-                        bar_arrive(&S.slot_free[td & 1]);  // nothing to multiply: the slot is free now
-                        ++td;
-                    }
-                    prog = true;
-                }
-                if (dactive) {
-                    const int s = Gd % kBStages, t = Gd & 1;
-                    if (bar_test(&S.b_full[s], (Gd / kBStages) & 1) &&
-                        (Gd < 2 || bar_test(&S.acc_empty[t], ((Gd >> 1) - 1) & 1))) {
-                        tc_after();
-                        const int b = cd / dchunks;
-                        const uint32_t d = tm + (uint32_t)(kAccCol0 + t * kDecN);
-                        const uint64_t bd = bdesc0 + (uint64_t)((s * kChunkBytes) >> 4);
-                        const uint32_t a0 = tm + (uint32_t)((td & 1) * kSlotCols + 64 * b);
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {  // K steps of 16: Al Bh + Ah Bl + Ah Bh
-                            const uint64_t bh = bd + 2 * k, bl = bh + ((kChunkBytes / 2) >> 4);
-                            const uint32_t ah = a0 + (uint32_t)(32 * (k >> 1) + 8 * (k & 1)), al = ah + 16;
-                            mma_f16_tmem_a(d, al, bh, idesc_dec, k > 0 ? 1u : 0u);
-                            mma_f16_tmem_a(d, ah, bl, idesc_dec, 1u);
-                            mma_f16_tmem_a(d, ah, bh, idesc_dec, 1u);
-                        }
-                        mma_commit(&S.acc_full[t]);
-                        ++Gd;
-                        if (++cd == nchunk) {
-                            mma_commit(&S.slot_free[td & 1]);
-                            ++td;
-                            dactive = false;
-                        }
-                        prog = true;
-                    }
-                }
-            }
-            if (te < n_my) {
+        int be = 0;
+        for (int te = 0; te < n_my; ++te) {
+            bool first = true;
+            for (;;) {
                 const int s = be % kStages;
-                const bool slot_ok = !first || te < 2 || bar_test(&S.slot_free[te & 1], ((te >> 1) - 1) & 1);
-                if (slot_ok && bar_test(&S.ev_full[s], (be / kStages) & 1)) {
-                    tc_after();
-                    const int nb = *reinterpret_cast<volatile int*>(&S.nb[s]);
-                    if (nb) {
-                        const uint32_t d = tm + (uint32_t)((te & 1) * kSlotCols);
-#pragma unroll
-                        for (int k = 0; k < 2; ++k) {
-                            const uint32_t o = 256u * k;
-                            const uint64_t ah = ns_desc(eh0 + s * kEBytes + o), al = ns_desc(el0 + s * kEBytes + o);
-                            const uint64_t bh = ns_desc(vh0 + s * kVBytes + o), bl = ns_desc(vl0 + s * kVBytes + o);
-                            mma_f16_ss(d, ah, bh, idesc_ev, (first && k == 0) ? 0u : 1u);
-                            mma_f16_ss(d, ah, bl, idesc_ev, 1u);
-                            mma_f16_ss(d, al, bh, idesc_ev, 1u);
-                        }
-                        mma_commit(&S.ev_empty[s]);
-                        first = false;
-                    } else {
-                        // end of the tile's stream: W complete once the issued MMAs are
-                        if (!first) mma_commit(&S.w_full[te & 1]);
-                        else bar_arrive(&S.w_full[te & 1]);
-                        bar_arrive(&S.ev_empty[s]);
-                        ++te;
-                        first = true;
-                    }
-                    ++be;
-                    prog = true;
+                SF_TIMED(w0, bar_wait(&S.ev_full[s], (be / kStages) & 1));
+                const int nb = *reinterpret_cast<volatile int*>(&S.nb[s]);
+                ++be;
+                // The slot's previous tile (te - 2) must be fully decoded before
+                // this tile writes it -- also when the tile has no batch at all:
+                // w_full(te) lets the blend warps convert into the slot and
+                // publish a_ready(te), which must not complete a second phase of
+                // a_ready[slot] before the decode issuer consumed a_ready(te - 2).
+                if (first && te >= 2) SF_TIMED(w1, bar_wait(&S.slot_free[te & 1], ((te >> 1) - 1) & 1));
+                if (nb == 0) {
+                    // end of the tile's stream: W complete once the issued products are
+                    if (!first) mma_commit(&S.w_full[te & 1]);
+                    else bar_arrive(&S.w_full[te & 1]);
+                    SF_STAMP(A, te, 3);
+                    bar_arrive(&S.ev_empty[s]);
+                    break;
                 }
+                tc_after();
+                const uint32_t d = tm + (uint32_t)((te & 1) * kSlotCols);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const uint32_t o = 256u * k;
+                    const uint64_t ah = ns_desc(eh0 + s * kEBytes + o), al = ns_desc(el0 + s * kEBytes + o);
+                    const uint64_t bh = ns_desc(vh0 + s * kVBytes + o), bl = ns_desc(vl0 + s * kVBytes + o);
+                    mma_f16_ss(d, ah, bh, idesc_ev, (first && k == 0) ? 0u : 1u);
+                    mma_f16_ss(d, ah, bl, idesc_ev, 1u);
+                    mma_f16_ss(d, al, bh, idesc_ev, 1u);
+                }
+                mma_commit(&S.ev_empty[s]);
+                first = false;
             }
-            if (!prog) __nanosleep(20);
-            else progress(A, 9, ((uint32_t)te << 16) | (uint32_t)td, ((uint32_t)be << 16) | (uint32_t)Gd);
+            SF_PROG(A, 9, (uint32_t)te, (uint32_t)be);
         }
+    } else if (DEC && warp == kDecWarp && lane == 0) {
+        // ---------------- decode issuer: 3-term fp16 chunks of each converted tile ----------------
+        const uint32_t idesc_dec = (1u << 4) | ((uint32_t)(kDecN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        const unsigned char* img = reinterpret_cast<const unsigned char*>(A.dec_b);
+        for (int g = 0; g < kBStages; ++g) {
+            bar_expect_tx(&S.b_full[g], kChunkBytes);
+            bulk_g2s(S.bring[g], img + (size_t)(g % nchunk) * kChunkBytes, kChunkBytes, &S.b_full[g]);
+        }
+        const uint64_t bdesc0 = sw128_desc(smem_addr(S.bring[0]));
+        int Gd = 0;
+        for (int td = 0; td < n_my; ++td) {
+            SF_TIMED(w0, bar_wait(&S.a_ready[td & 1], (td >> 1) & 1));
+            if (td >= 2) SF_TIMED(w0, bar_wait(&S.dq_empty[td & 1], ((td >> 1) - 1) & 1));
+            tc_after();
+            SF_STAMP(A, td, 4);
+            // the drains learn the tile's kind in order, through their own ring
+            const uint32_t c = *reinterpret_cast<volatile uint32_t*>(&S.contrib[td & 1]);
+            S.dq_info[td & 1] = c;
+            bar_arrive(&S.dq_full[td & 1]);
+            if (c == 0u) {
+                bar_arrive(&S.slot_free[td & 1]);  // nothing to multiply: the slot is free now
+                continue;
+            }
+            for (int cd = 0; cd < nchunk; ++cd, ++Gd) {
+                const int s = Gd % kBStages, t = Gd & 1;
+                SF_TIMED(w1, bar_wait(&S.b_full[s], (Gd / kBStages) & 1));
+                if (Gd >= 2) SF_TIMED(w2, bar_wait(&S.acc_empty[t], ((Gd >> 1) - 1) & 1));
+                tc_after();
+                const int b = cd / dchunks;
+                const uint32_t d = tm + (uint32_t)(kAccCol0 + t * kDecN);
+                const uint64_t bd = bdesc0 + (uint64_t)((s * kChunkBytes) >> 4);
+                const uint32_t a0 = tm + (uint32_t)((td & 1) * kSlotCols + 64 * b);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {  // K steps of 16: Al Bh + Ah Bl + Ah Bh
+                    const uint64_t bh = bd + 2 * k, bl = bh + ((kChunkBytes / 2) >> 4);
+                    const uint32_t ah = a0 + (uint32_t)(32 * (k >> 1) + 8 * (k & 1)), al = ah + 16;
+                    mma_f16_tmem_a(d, al, bh, idesc_dec, k > 0 ? 1u : 0u);
+                    mma_f16_tmem_a(d, ah, bl, idesc_dec, 1u);
+                    mma_f16_tmem_a(d, ah, bh, idesc_dec, 1u);
+                }
+                mma_commit(&S.acc_full[t]);
+            }
+            mma_commit(&S.slot_free[td & 1]);
+            SF_STAMP(A, td, 5);
+            SF_PROG(A, 10, (uint32_t)td, (uint32_t)Gd);
+        }
+    }
+    if (prof && lane == 0) {
+        // 4 counters per warp: blend 0..31, drain 32..47, producer 48, E V issuer 52, decode issuer 56
+        const int slot = 4 * warp;
+        prof_add(A, slot + 0, clock64() - t_start);
+        prof_add(A, slot + 1, w0);
+        prof_add(A, slot + 2, w1);
+        prof_add(A, slot + 3, w2);
     }
     __syncwarp();
     tc_before();
@@ -699,6 +882,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
     if (warp == 0) {
         tc_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+        if (lane == 0) SF_PROG(A, 11, 1u, 1u);
     }
 }
 
@@ -725,19 +909,24 @@ int launch_splat_tc(const BlendArgs& a, cudaStream_t st) {
     memset(&fmap, 0, sizeof(fmap));
     if (dec && make_feature_map(&fmap, a.features, a.D, a.W, a.H, a.n_levels)) return -5;
     const bool rel = a.proj_cb != nullptr;
+    static const unsigned long long prog = [] {
+        const char* e = getenv("SF_TC_PROGRESS");
+        return e ? strtoull(e, nullptr, 10) : 0ull;
+    }();
     void (*kern)(BlendArgs, const CUtensorMap);
-    if (dec) kern = rel ? tcs::k_splat_tc<4, true> : tcs::k_splat_tc<0, true>;
-    else kern = rel ? tcs::k_splat_tc<4, false> : tcs::k_splat_tc<0, false>;
+    if (prog) {
+        if (dec) kern = rel ? tcs::k_splat_tc<4, true, true> : tcs::k_splat_tc<0, true, true>;
+        else kern = rel ? tcs::k_splat_tc<4, false, true> : tcs::k_splat_tc<0, false, true>;
+    } else {
+        if (dec) kern = rel ? tcs::k_splat_tc<4, true, false> : tcs::k_splat_tc<0, true, false>;
+        else kern = rel ? tcs::k_splat_tc<4, false, false> : tcs::k_splat_tc<0, false, false>;
+    }
     const size_t smem = splat_tc_smem_bytes();
     if (ensure_smem_attr((const void*)kern, smem)) return -6;
     const int n_half = 2 * a.n_band_tiles;
     if (n_half <= 0) return 0;
     const int grid = std::min(n_half, device_sm_count());
     BlendArgs a2 = a;
-    static const unsigned long long prog = [] {
-        const char* e = getenv("SF_TC_PROGRESS");
-        return e ? strtoull(e, nullptr, 10) : 0ull;
-    }();
     a2.timeline = prog ? reinterpret_cast<uint64_t*>(prog) : nullptr;
     kern<<<grid, tcs::kThreads, smem, st>>>(a2, fmap);
     return 0;

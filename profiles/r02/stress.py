@@ -13,31 +13,32 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
-prog = torch.zeros(148 * 16, dtype=torch.int64).pin_memory()
-os.environ["SF_TC_PROGRESS"] = str(prog.data_ptr())
+prog = torch.zeros(148 * 128 + 16 * 256, dtype=torch.int64).pin_memory()
+if not os.environ.get("STRESS_NOPROG"):
+    os.environ["SF_TC_PROGRESS"] = str(prog.data_ptr())
 
 import paper_2507_07136_b200 as sf  # noqa: E402
 from paper_2507_07136_b200 import synthetic  # noqa: E402
 from paper_2507_07136_b200.device import QuerySpec, device_scene  # noqa: E402
 
-ROLES = ["prod", "bl0", "bl1", "bl2", "bl3", "dr0", "dr1", "dr2", "dr3", "mma"]
+ROLES = ["prod", "bl0", "bl1", "bl2", "bl3", "dr0", "dr1", "dr2", "dr3", "ev", "dec", "done"]
 
 
 def dump(n_cta):
-    p = prog.numpy().reshape(148, 16)
+    p = prog.numpy()[:148 * 128].reshape(148, 128)
     for c in range(n_cta):
         row = []
-        for r in range(10):
+        for r in range(12):
             v = int(p[c, r]) & ((1 << 63) - 1)
             a, b = v >> 32, v & 0xFFFFFFFF
-            if r == 9:
-                row.append(f"mma te={a >> 16} td={a & 0xFFFF} be={b >> 16} Gd={b & 0xFFFF}")
+            if r >= 9:
+                row.append(f"{ROLES[r]} t={a} n={b}")
             else:
                 row.append(f"{ROLES[r]} it={a} st={b >> 16} n={b & 0xFFFF}")
         print(c, " | ".join(row))
 
 
-def run(G, W, H, timeout=60.0):
+def run(G, W, H, timeout=float(os.environ.get("STRESS_TIMEOUT", "60"))):
     scene = synthetic.make_scene(G)
     cam = synthetic.make_camera(W, H)
     qv, canon = synthetic.make_query()
@@ -49,6 +50,7 @@ def run(G, W, H, timeout=60.0):
     spec = QuerySpec(qv, canon, 11, -1, 0.5)
     torch.cuda.synchronize()
     prog.zero_()
+    torch.cuda.synchronize()
     t0 = time.time()
     keep = eng.enqueue(cam, levels, out, query=spec)
     ev = torch.cuda.Event()
@@ -66,6 +68,51 @@ def run(G, W, H, timeout=60.0):
     print(f"ok G={G} {W}x{H} in {time.time() - t0:.2f}s pairs={st[1]} fixups={st[7]} level={st[3]}", flush=True)
     f = out.features
     print("  features finite:", bool(torch.isfinite(f).all().item()), "max", f.abs().max().item(), flush=True)
+    if not os.environ.get("STRESS_NOPROG"):
+        prof_report(min(148, 2 * ((W + 15) // 16) * ((H + 15) // 16)))
+        timeline_report()
+
+
+def timeline_report():
+    """CTA 0's per-tile events (cycles relative to the first), us at 1.965 GHz."""
+    t = prog.numpy()[148 * 128:].reshape(256, 16).astype(np.int64)
+    names = ["blend_start", "blend_end", "epi_done", "ev_wfull", "dec_start", "dec_end", "drain_start",
+             "drain_last", "drain_first", "prod_start", "prod_end"]
+    n = int((t[:, 0] > 0).sum())
+    t0 = t[0, 0]
+    print("  tile " + " ".join(f"{x[:11]:>11s}" for x in names))
+    for i in list(range(min(n, 6))) + list(range(max(6, n - 3), n)):
+        print(f"  {i:4d} " + " ".join(f"{(t[i, e] - t0) / 1965.0:11.2f}" if t[i, e] else f"{'-':>11s}" for e in range(11)))
+    if n > 10:
+        d = np.diff(t[:n, :11], axis=0) / 1965.0
+        print("  mean per-tile period (us): " + " ".join(f"{x[:6]}={v:.2f}" for x, v in zip(names, d.mean(axis=0))))
+
+
+def prof_report(n_cta):
+    """Cycle accounting per role (mean over CTAs, in % of the role's total)."""
+    p = prog.numpy()[:148 * 128].reshape(148, 128)[:n_cta, 16:].astype(np.float64)
+    names = {0: "blend", 16: "drain", 32: "producer", 36: "ev_issuer", 40: "dec_issuer"}
+    labels = {"blend": ("waits", "alpha", "walk"), "drain": ("dq_full", "acc_full", "bulk_read(lane0)"),
+              "producer": ("ev_empty", "-", "-"), "ev_issuer": ("ev_full", "slot_free", "-"),
+              "dec_issuer": ("a_ready/dq", "b_full", "acc_empty")}
+    for base, nm in names.items():
+        warps = 8 if base == 0 else (4 if base == 32 else 1)
+        tot = p[:, base:base + 4 * warps:4].sum(axis=1)
+        print(f"  {nm:9s} total {tot.mean() / 1e3:9.1f} kcyc/CTA", end="")
+        for k in range(3):
+            v = p[:, base + 1 + k:base + 4 * warps:4].sum(axis=1)
+            lab = labels[nm][k]
+            if lab == "-":
+                continue
+            if lab == "progress_iters":
+                print(f"  {lab} {v.mean():.0f}", end="")
+            elif lab == "cand":
+                raw = prog.numpy()[:148 * 128].reshape(148, 128)[:n_cta, 16:80][:, base + 1 + k:base + 4 * warps:4].astype(np.int64)
+                cand, ent = (raw >> 32).sum(), (raw & 0xFFFFFFFF).sum()
+                print(f"  candidates {cand / max(ent, 1):.2f} of {ent / n_cta / warps:.0f} entries/warp", end="")
+            else:
+                print(f"  {lab} {100 * v.mean() / max(tot.mean(), 1):5.1f}%", end="")
+        print()
 
 
 if __name__ == "__main__":
