@@ -315,6 +315,12 @@ int sf_abi_version(void); /* 2: SfFrame band fields; 3: fused decode (coeff_map 
  * 0 if the decode runs as a separate tcgen05 GEMM over the coefficient map. */
 int sf_decode_fused(int32_t n_levels, int32_t L, int32_t K, int32_t D);
 
+/* 1 if a query frame of this shape computes the relevancy inside the blend
+ * kernel; 0 if from the coefficient map in HBM (then SfFrame.coeff_map is
+ * required with an SfQuery).  Replaces the relevancy_map call of
+ * query_pipeline (splatfield/sparse_splat.py:281-283, query.py:65-84). */
+int sf_relevancy_fused(int32_t n_levels, int32_t L, int32_t K, int32_t n_canon);
+
 #ifdef __cplusplus
 }
 #endif

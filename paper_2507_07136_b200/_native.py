@@ -87,6 +87,7 @@ EXPORTS = {
     "sf_last_error": (ctypes.c_char_p, []),
     "sf_abi_version": (ctypes.c_int, []),
     "sf_decode_fused": (ctypes.c_int, [i32, i32, i32, i32]),
+    "sf_relevancy_fused": (ctypes.c_int, [i32, i32, i32, i32]),
     "sf_decode_image_bytes": (sz, [i32, i32, i32, i32]),
     "sf_pack_decode_image": (ctypes.c_int, [ctypes.POINTER(SfScene), P, i32, P, sz, P]),
     "sf_lsv2_unpack": (ctypes.c_int, [P, i64, i32, i32, i32, P, P, P, P, P, P, P, P, P]),

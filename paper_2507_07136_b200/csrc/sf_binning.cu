@@ -31,21 +31,7 @@ size_t bin_cta_base_elems(int W, int H) {
 
 
 // ---------------------------------------------------------------------------
-// inverse of the depth order, and the per-row scatter plan
-// (sparse_splat.py:126-132 cat_idx / cat_vals)
-
-__global__ void __launch_bounds__(256) k_rank_of_row(int64_t G, const uint32_t* __restrict__ sorted_rows,
-                                                     const int64_t* __restrict__ stats,
-                                                     uint32_t* __restrict__ rank_of_row) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= G) return;
-    rank_of_row[sorted_rows[r]] = (r < stats[SF_STAT_VISIBLE]) ? (uint32_t)r : 0xffffffffu;
-}
-
-void launch_rank_of_row(int64_t G, const uint32_t* sorted_rows, const int64_t* stats, uint32_t* rank_of_row,
-                        cudaStream_t st) {
-    if (G) k_rank_of_row<<<ceil_div(G, 256), 256, 0, st>>>(G, sorted_rows, stats, rank_of_row);
-}
+// per-row scatter plan (sparse_splat.py:126-132 cat_idx / cat_vals)
 
 __global__ void __launch_bounds__(256) k_pack_channels(int64_t G, const uint16_t* __restrict__ cidx,
                                                        const float* __restrict__ cval, int K, int L,
@@ -130,12 +116,13 @@ __device__ __forceinline__ bool tile_hit(const MahalPre& p, int tx, int ty, cons
     return min_mahal_sq_to_rect_pre(p, lx, ly, hx, hy) <= SF_CUTOFF;
 }
 
-__device__ __forceinline__ bool item_rank(int64_t i, const int64_t* stats, const uint32_t* rank_of, uint32_t& r) {
-    if (rank_of) {
-        r = rank_of[i];
-        return r != 0xffffffffu;
-    }
+// The item an entry names: frame mode (row_keys != null) -- item i is scene
+// row i, visible iff its depth key is not the culled sentinel, and the entry
+// is the row (put in (depth, row) order by k_tile_sort_depth); sf_bin mode --
+// item i has canonical rank i (i < stats[VISIBLE]) and the entry is i.
+__device__ __forceinline__ bool item_rank(int64_t i, const int64_t* stats, const uint64_t* row_keys, uint32_t& r) {
     r = (uint32_t)i;
+    if (row_keys) return __ldg(row_keys + i) != ~0ull;
     return i < stats[SF_STAT_VISIBLE];
 }
 
@@ -147,12 +134,12 @@ __device__ __forceinline__ bool item_rank(int64_t i, const int64_t* stats, const
 // kept too, so the emit pass repeats no fp64 arithmetic.
 __global__ void __launch_bounds__(256, 4) k_count_pairs(int64_t N, const int64_t* __restrict__ stats,
                                                      const GeomRec* __restrict__ geom,
-                                                     const uint32_t* __restrict__ rank_of,
+                                                     const uint64_t* __restrict__ row_keys,
                                                      TileGrid g, uint32_t* __restrict__ tile_counts,
                                                      BinAux* __restrict__ aux) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t r;
-    if (i >= N || !item_rank(i, stats, rank_of, r)) return;
+    if (i >= N || !item_rank(i, stats, row_keys, r)) return;
     Proj64 p = geom_proj(geom[i]);
     int tx0, tx1, ty0, ty1;
     cand_rect(p, g, tx0, tx1, ty0, ty1);
@@ -196,7 +183,7 @@ __global__ void __launch_bounds__(256, 4) k_count_pairs(int64_t N, const int64_t
 // per pair, with the same emit-time arithmetic.
 __global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t per, const int64_t* __restrict__ stats,
                                                          const GeomRec* __restrict__ geom,
-                                                         const uint32_t* __restrict__ rank_of, TileGrid g,
+                                                         const uint64_t* __restrict__ row_keys, TileGrid g,
                                                          uint32_t* __restrict__ tile_counts, BinAux* __restrict__ aux,
                                                          uint32_t* __restrict__ cta_base) {
     extern __shared__ uint32_t hist[];
@@ -206,7 +193,7 @@ __global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t p
     const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(N, i0 + per);
     for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
         uint32_t r;
-        if (!item_rank(i, stats, rank_of, r)) continue;
+        if (!item_rank(i, stats, row_keys, r)) continue;
         Proj64 p = geom_proj(geom[i]);
         int tx0, tx1, ty0, ty1;
         cand_rect(p, g, tx0, tx1, ty0, ty1);
@@ -313,7 +300,7 @@ __device__ __forceinline__ void emit_one(int j, int t, uint32_t r, const BinAux&
 
 __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __restrict__ stats,
                                                     const GeomRec* __restrict__ geom,
-                                                    const uint32_t* __restrict__ rank_of, TileGrid g,
+                                                    const uint64_t* __restrict__ row_keys, TileGrid g,
                                                     const BinAux* __restrict__ aux,
                                                     const uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ cursor,
@@ -322,7 +309,7 @@ __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __
     if (stats[SF_STAT_OVERFLOW]) return;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t r;
-    if (i >= N || !item_rank(i, stats, rank_of, r)) return;
+    if (i >= N || !item_rank(i, stats, row_keys, r)) return;
     BinAux a;
     {
         const uint4* src = reinterpret_cast<const uint4*>(aux + i);
@@ -570,10 +557,217 @@ __global__ void __launch_bounds__(256) k_tile_sort_large(const uint32_t* __restr
     }
 }
 
-void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint32_t* rank_of,
-                    const uint32_t* rank_to_row, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
-                    uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
-                    BinAux* aux, uint32_t* cta_base, int tile_row0, int tile_row1, cudaStream_t st) {
+// ---------------------------------------------------------------------------
+// Frame mode: per-tile sort of ROWS by (depth key, row).  Reference order
+// lexsort((ids, depths)) (projection.py:396) restricted to one tile, then the
+// stable argsort by tile (projection.py:443-449) keeps it inside each list:
+// so sorting each tile's rows by (fp64 depth, id) gives the reference's lists
+// without ranking all Gaussians globally.  Depth keys are the fp64 depth bits
+// (positive doubles order like their bits; sf_preprocess.cu) and rows are in
+// id order, so (key, row) compares exactly like (depth, id).  The keys of a
+// tile are gathered from the L2-resident key array (8 B per entry).
+//
+// Sort: MSD bucket pass in shared memory -- bucket = floor((key - min) *
+// NB / span) in fp64 (rounding is monotone, so buckets stay in key order),
+// histogram, scan, scatter of entry indices, insertion sort inside each
+// bucket on (key, row).  Strongly clustered tiles (a bucket over kMaxBucket
+// entries) take a bitonic sort of the indices instead.
+template <int CAP>
+struct TileSortDepth {
+    static constexpr size_t kSmem = (size_t)CAP * (8 + 4 + 2);
+};
+
+__device__ __forceinline__ bool key_row_less(uint64_t ka, uint32_t ra, uint64_t kb, uint32_t rb) {
+    return ka < kb || (ka == kb && ra < rb);
+}
+
+template <int CAP, int NB>
+__global__ void __launch_bounds__(256) k_tile_sort_depth(const uint32_t* __restrict__ offsets,
+                                                         uint32_t* __restrict__ entries, int lo_exclusive,
+                                                         const int64_t* __restrict__ stats,
+                                                         const uint64_t* __restrict__ row_keys) {
+    static_assert(CAP <= 65536 && NB % 256 == 0, "index width / scan split");
+    if (stats[SF_STAT_OVERFLOW]) return;
+    extern __shared__ __align__(16) unsigned char ts_smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(ts_smem);           // CAP
+    uint32_t* rows = reinterpret_cast<uint32_t*>(keys + CAP);       // CAP
+    uint16_t* order = reinterpret_cast<uint16_t*>(rows + CAP);      // CAP
+    __shared__ uint32_t start[NB + 1];
+    __shared__ uint32_t cursor[NB];
+    __shared__ unsigned long long s_min, s_max;
+    __shared__ int s_big;
+    const int t = blockIdx.x;
+    const uint32_t beg = offsets[t], end = offsets[t + 1];
+    const int n = (int)(end - beg);
+    if (n <= lo_exclusive || n > CAP) return;
+    uint32_t* e = entries + beg;
+    if (threadIdx.x == 0) {
+        s_min = ~0ull;
+        s_max = 0ull;
+        s_big = 0;
+    }
+    for (int b = threadIdx.x; b < NB; b += blockDim.x) cursor[b] = 0;
+    __syncthreads();
+    unsigned long long mn = ~0ull, mx = 0ull;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t r = e[i];
+        const uint64_t k = __ldg(row_keys + r);
+        rows[i] = r;
+        keys[i] = k;
+        mn = min(mn, (unsigned long long)k);
+        mx = max(mx, (unsigned long long)k);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&s_min, mn);
+        atomicMax(&s_max, mx);
+    }
+    __syncthreads();
+    const uint64_t kmin = s_min;
+    const double bscale = (double)NB / ((double)(s_max - kmin) + 1.0);
+    auto bucket_of = [&](uint64_t k) { return min(NB - 1, (int)((double)(k - kmin) * bscale)); };
+    for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cursor[bucket_of(keys[i])], 1u);
+    __syncthreads();
+    {
+        typedef cub::BlockScan<uint32_t, 256> Scan;
+        __shared__ typename Scan::TempStorage tmp;
+        constexpr int PER = NB / 256;
+        uint32_t c[PER], sum = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            c[j] = cursor[threadIdx.x * PER + j];
+            sum += c[j];
+        }
+        uint32_t ex;
+        Scan(tmp).ExclusiveSum(sum, ex);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int b = threadIdx.x * PER + j;
+            start[b] = ex;
+            cursor[b] = ex;
+            if (c[j] > (uint32_t)kMaxBucket) s_big = 1;
+            ex += c[j];
+        }
+        if (threadIdx.x == 255) start[NB] = ex;
+    }
+    __syncthreads();
+    if (s_big) {
+        // clustered keys: bitonic sort of the indices on (key, row)
+        int N = 2;
+        while (N < n) N <<= 1;
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+            order[i] = (uint16_t)i;
+            if (i >= n) {
+                keys[i] = ~0ull;
+                rows[i] = 0xffffffffu;
+            }
+        }
+        __syncthreads();
+        for (int k = 2; k <= N; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int p = threadIdx.x; p < (N >> 1); p += blockDim.x) {
+                    const int i = 2 * j * (p / j) + (p % j), ixj = i + j;
+                    const bool up = (i & k) == 0;
+                    const uint16_t a = order[i], b = order[ixj];
+                    if (key_row_less(keys[b], rows[b], keys[a], rows[a]) == up) {
+                        order[i] = b;
+                        order[ixj] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    } else {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&cursor[bucket_of(keys[i])], 1u)] = (uint16_t)i;
+        __syncthreads();
+        for (int b = threadIdx.x; b < NB; b += blockDim.x) {
+            const int b0 = (int)start[b], b1 = (int)start[b + 1];
+            for (int i = b0 + 1; i < b1; ++i) {
+                const uint16_t x = order[i];
+                const uint64_t kx = keys[x];
+                const uint32_t rx = rows[x];
+                int j = i - 1;
+                while (j >= b0 && key_row_less(kx, rx, keys[order[j]], rows[order[j]])) {
+                    order[j + 1] = order[j];
+                    --j;
+                }
+                order[j + 1] = x;
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) e[i] = rows[order[i]];
+}
+
+// Lists over 8192 entries (pathological overlap): a stable LSD split sort in
+// global scratch, first on the row bits, then on the 64 key bits.
+__global__ void __launch_bounds__(256) k_tile_sort_depth_large(const uint32_t* __restrict__ offsets,
+                                                               uint32_t* __restrict__ entries,
+                                                               uint32_t* __restrict__ scratch, int lo_exclusive,
+                                                               const int64_t* __restrict__ stats,
+                                                               const uint64_t* __restrict__ row_keys) {
+    if (stats[SF_STAT_OVERFLOW]) return;
+    typedef cub::BlockScan<int, 256> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int s_zero;
+    const int t = blockIdx.x;
+    const uint32_t beg = offsets[t], end = offsets[t + 1];
+    const int n = (int)(end - beg);
+    if (n <= lo_exclusive) return;
+    uint32_t* src = entries + beg;
+    uint32_t* dst = scratch + beg;
+    uint32_t rmax = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) rmax = max(rmax, src[i]);
+    rmax = __reduce_max_sync(0xffffffffu, rmax);
+    __shared__ uint32_t s_rmax;
+    if (threadIdx.x == 0) s_rmax = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_rmax, rmax);
+    __syncthreads();
+    int row_bits = 1;
+    while (row_bits < 32 && (s_rmax >> row_bits)) ++row_bits;
+    for (int pass = 0; pass < row_bits + 64; ++pass) {
+        auto bit_of = [&](uint32_t r) -> uint32_t {
+            return pass < row_bits ? (r >> pass) & 1u : (uint32_t)(__ldg(row_keys + r) >> (pass - row_bits)) & 1u;
+        };
+        int z = 0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) z += !bit_of(src[i]);
+        int zsum;
+        Scan(tmp).ExclusiveSum(z, z, zsum);
+        if (threadIdx.x == 0) s_zero = zsum;
+        __syncthreads();
+        int base0 = 0, base1 = s_zero;
+        for (int s0 = 0; s0 < n; s0 += blockDim.x) {
+            const int i = s0 + threadIdx.x;
+            const bool valid = i < n;
+            const uint32_t v = valid ? src[i] : 0u;
+            const int isz = (valid && !bit_of(v)) ? 1 : 0;
+            int ex, tot;
+            Scan(tmp).ExclusiveSum(isz, ex, tot);
+            if (valid) dst[isz ? base0 + ex : base1 + ((int)threadIdx.x - ex)] = v;
+            base0 += tot;
+            base1 += min((int)blockDim.x, n - s0) - tot;
+            __syncthreads();
+        }
+        uint32_t* tt = src;
+        src = dst;
+        dst = tt;
+        __syncthreads();
+    }
+    // row_bits + 64 passes: the result is in the entries when the count is even
+    if (src != entries + beg)
+        for (int i = threadIdx.x; i < n; i += blockDim.x) entries[beg + i] = src[i];
+}
+
+void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint64_t* row_keys, int W,
+                    int H, int64_t pair_capacity, uint32_t* tile_counts, uint32_t* tile_offsets, uint32_t* tile_cursor,
+                    uint32_t* entries, uint32_t* sort_scratch, BinAux* aux, uint32_t* cta_base, int tile_row0,
+                    int tile_row1, cudaStream_t st) {
     TileGrid g{W, H, (W + SF_TILE - 1) / SF_TILE, (H + SF_TILE - 1) / SF_TILE, 0, 0};
     g.ty_lo = tile_row0;
     g.ty_hi = (tile_row1 > tile_row0 ? tile_row1 : g.tiles_y) - 1;
@@ -585,24 +779,36 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
     if (agg) {
         const size_t smem = sizeof(uint32_t) * n_tiles;
         ensure_smem_attr((const void*)k_count_pairs_agg, smem);
-        k_count_pairs_agg<<<kCountCTAs, 512, smem, st>>>(n_items, per, stats, geom, rank_of, g, tile_counts, aux,
+        k_count_pairs_agg<<<kCountCTAs, 512, smem, st>>>(n_items, per, stats, geom, row_keys, g, tile_counts, aux,
                                                          cta_base);
     } else if (blocks) {
-        k_count_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, tile_counts, aux);
+        k_count_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, row_keys, g, tile_counts, aux);
     }
     k_tile_scan<<<1, 1024, 0, st>>>(n_tiles, tile_counts, tile_offsets, tile_cursor, pair_capacity,
                                     const_cast<int64_t*>(stats));
     if (blocks)
-        k_emit_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, rank_of, g, aux, tile_offsets, tile_cursor,
+        k_emit_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, row_keys, g, aux, tile_offsets, tile_cursor,
                                              entries, agg ? cta_base : nullptr, per);
-    // per-tile canonical order: most lists fit the shared-memory bucket sort (<= 4096),
-    // the rest go to the larger-capacity kernels (each CTA skips other sizes)
+    if (row_keys) {
+        // frame mode: each tile's rows into (depth, row) order -- the canonical
+        // order, since scene rows are id-ordered; no global depth sort
+        constexpr size_t s1 = TileSortDepth<4096>::kSmem, s2 = TileSortDepth<8192>::kSmem;
+        ensure_smem_attr((const void*)k_tile_sort_depth<4096, 1024>, s1);
+        ensure_smem_attr((const void*)k_tile_sort_depth<8192, 2048>, s2);
+        k_tile_sort_depth<4096, 1024><<<n_tiles, 256, s1, st>>>(tile_offsets, entries, 0, stats, row_keys);
+        k_tile_sort_depth<8192, 2048><<<n_tiles, 256, s2, st>>>(tile_offsets, entries, 4096, stats, row_keys);
+        k_tile_sort_depth_large<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192, stats, row_keys);
+        return;
+    }
+    // sf_bin mode: unique ranks; most lists fit the shared-memory bucket sort
+    // (<= 4096), the rest go to the larger-capacity kernels (each CTA skips
+    // other sizes)
     ensure_smem_attr((const void*)k_tile_sort_bucket<8192, 1024>, 2 * 8192 * 4);
     k_tile_sort_bucket<SF_TS_CAP, SF_TS_NB><<<n_tiles, 256, 2 * SF_TS_CAP * 4, st>>>(tile_offsets, entries, 0, stats,
-                                                                                   rank_to_row);
+                                                                                   nullptr);
     k_tile_sort_bucket<8192, 1024><<<n_tiles, 256, 2 * 8192 * 4, st>>>(tile_offsets, entries, SF_TS_CAP, stats,
-                                                                       rank_to_row);
-    k_tile_sort_large<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192, stats, rank_to_row);
+                                                                       nullptr);
+    k_tile_sort_large<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192, stats, nullptr);
 }
 
 }  // namespace sf

@@ -1344,7 +1344,8 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
     __shared__ double wl[kChBlock];
     __shared__ double pv[32 * kFxWarps][kMaxC];
     __shared__ uint8_t chs[32 * kFxWarps][kMaxC];
-    __shared__ uint8_t live_e[32 * kFxWarps];
+    __shared__ uint16_t live_list[32 * kFxWarps];  // the round's adding entries, in list order
+    __shared__ int wcnt[kFxWarps];
     __shared__ double wtot[kFxWarps];
     __shared__ double Tround, Tfinal;
     __shared__ unsigned int last_counted;
@@ -1409,7 +1410,8 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
             // products e v; then thread c owns channel c and adds the round's
             // products to it in list order (only level c / L's K slots can hold c).
             const bool adds = live && al > 0.0;
-            live_e[tid] = adds ? 1 : 0;
+            const uint32_t abal = __ballot_sync(0xffffffffu, adds);
+            if (lane == 0) wcnt[wid] = __popc(abal);
             if (adds) {
                 const double e = __dmul_rn(al, Tb);
                 const unsigned char* rec = A.chan + (size_t)r * cs;
@@ -1421,11 +1423,20 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
                 }
             }
             const bool stop = __syncthreads_or((i < end) && !(Tb >= thr));
+            // compact the adding entries (usually a small fraction of the round)
+            int n_add = 0, woff = 0;
+#pragma unroll
+            for (int v = 0; v < kFxWarps; ++v) {
+                woff += v < wid ? wcnt[v] : 0;
+                n_add += wcnt[v];
+            }
+            if (adds) live_list[woff + __popc(abal & ((1u << lane) - 1u))] = (uint16_t)tid;
+            __syncthreads();
             if (tid < A.n_ch) {
                 const int c = tid, k0 = (c / A.L) * kper;
                 double acc = wl[c];
-                for (int j = 0; j < 32 * kFxWarps; ++j) {
-                    if (!live_e[j]) continue;
+                for (int u = 0; u < n_add; ++u) {
+                    const int j = live_list[u];
                     for (int k = k0; k < k0 + kper; ++k)
                         if (chs[j][k] == c) acc += pv[j][k];
                 }

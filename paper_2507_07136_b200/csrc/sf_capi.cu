@@ -52,19 +52,31 @@ extern "C" int sf_decode_fused(int32_t n_levels, int32_t L, int32_t K, int32_t D
     return blend_dec_supported(n_levels, L, K, D) ? 1 : 0;
 }
 
+// Relevancy is fused into the blend epilogue while the coefficient tile is on
+// chip.  It is computed from the map in HBM instead (so the frame needs a
+// coefficient map buffer) when the channels span several blend CTAs, or when
+// the tensor-core splat (L = 64, <= 3 levels, <= 12 channels per Gaussian)
+// renders the frame and the canonical count is not its fused 4: every query
+// frame of a shape then uses the same splat kernel, hence the same W.
+static bool relevancy_fused(int n_levels, int L, int K, int n_canon) {
+    const int n_ch = n_levels * L;
+    if (n_ch > 192) return false;
+    const bool tc = L == 64 && n_levels <= 3 && n_levels * K <= 12;
+    return !tc || n_canon == 4;
+}
+
+extern "C" int sf_relevancy_fused(int32_t n_levels, int32_t L, int32_t K, int32_t n_canon) {
+    return relevancy_fused(n_levels, L, K, n_canon) ? 1 : 0;
+}
+
 // ---------------------------------------------------------------------------
 // frame workspace layout
 
 struct FrameWs {
-    uint32_t* rank_of_row;
     BinAux* aux;
     uint32_t* cta_base;
-    uint64_t* keys_in;
-    uint64_t* keys_out;
+    uint64_t* keys_in;  // per row: fp64 depth bits, ~0 = culled
     uint32_t* vals_in;
-    uint32_t* vals_out;
-    void* cub_tmp;
-    size_t cub_bytes;
     int64_t* stats;
     double* stats_f;
     GeomRec* geom;
@@ -105,15 +117,10 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     int64_t Gp = G > 0 ? G : 1;
     int n_tiles = ((W + SF_TILE - 1) / SF_TILE) * ((H + SF_TILE - 1) / SF_TILE);
     int C = n_levels * K;
-    ws->rank_of_row = c.take<uint32_t>(Gp);
     ws->aux = c.take<BinAux>(Gp);
     ws->cta_base = c.take<uint32_t>(bin_cta_base_elems(W, H));
     ws->keys_in = c.take<uint64_t>(Gp);
-    ws->keys_out = c.take<uint64_t>(Gp);
     ws->vals_in = c.take<uint32_t>(Gp);
-    ws->vals_out = c.take<uint32_t>(Gp);
-    ws->cub_bytes = depth_sort_tmp_bytes(Gp);
-    ws->cub_tmp = c.take<char>(ws->cub_bytes);
     ws->stats = c.take<int64_t>(16);
     ws->stats_f = c.take<double>(8 + 2 * kMaxLevels);
     ws->geom = c.take<GeomRec>(Gp);
@@ -185,7 +192,8 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
     // decode fused into the blend CTAs whenever the shape allows (features
     // then never need the coefficient map in HBM)
     const bool fused_dec = f->features && blend_dec_supported(f->n_levels, L, K, D);
-    bool need_cmap = (f->features != nullptr && !fused_dec) || (q && n_ch > 192);
+    const bool rel_from_map = q && !relevancy_fused(f->n_levels, L, K, q->n_canonicals);
+    bool need_cmap = (f->features != nullptr && !fused_dec) || rel_from_map;
     if (need_cmap && !f->coeff_map) return fail(SF_ERR_VALIDATION, "coefficient map buffer required");
     // band mode: owned rows [y0, y1), rendered rows = tile rows covering the
     // owned rows +- the mean-filter halo
@@ -222,12 +230,9 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
         launch_pack_channels(*s, lv, ws.chan, st_prep);
         chan = ws.chan;
     }
-    // K2
-    if (depth_sort(ws.keys_in, ws.keys_out, ws.vals_in, ws.vals_out, G, ws.cub_tmp, ws.cub_bytes, st_prep))
-        return check_cuda("depth sort");
-    launch_rank_of_row(G, ws.vals_out, ws.stats, ws.rank_of_row, st_prep);
-    // K3/K4: (tile, depth rank) lists, stored as scene rows
-    launch_binning(G, ws.stats, ws.geom, ws.rank_of_row, ws.vals_out, W, H, f->pair_capacity, ws.tile_counts,
+    // K2-K4: per-tile lists of scene rows in (depth, id) order -- the depth
+    // order is established per tile (k_tile_sort_depth), not globally
+    launch_binning(G, ws.stats, ws.geom, ws.keys_in, W, H, f->pair_capacity, ws.tile_counts,
                    ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, ws.cta_base, tr0, tr1, st_prep);
     if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
                                    ws.proj_cb, st_prep);
@@ -275,7 +280,6 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
     // relevancy: fused into the blend epilogue while the coefficient tile is
     // in shared memory; from the map in HBM only when the channels span
     // several blend CTAs
-    const bool rel_from_map = q && n_ch > 192;
     a.proj_cb = (q && !rel_from_map) ? ws.proj_cb : nullptr;
     a.n_levels = f->n_levels;
     a.L = L;
@@ -627,7 +631,7 @@ extern "C" int sf_bin(int64_t n, const double* means2d, const double* inv_covs, 
         depth_sort(w.k0, w.k1, w.v1, w.v0, n, w.cub_tmp, w.cub_bytes, st);
     }
     k_bin_finish<<<blocks, 256, 0, st>>>(n, w.v0, w.proj, w.geom, order, w.stats);
-    launch_binning(n, w.stats, w.geom, nullptr, nullptr, W, H, pair_cap, w.counts, w.offsets, w.cursor,
+    launch_binning(n, w.stats, w.geom, nullptr, W, H, pair_cap, w.counts, w.offsets, w.cursor,
                    (uint32_t*)tile_entries, w.scratch, w.aux, w.cta_base, 0, 0, st);
     k_offsets_to_i64<<<ceil_div(n_tiles + 1, 256), 256, 0, st>>>(n_tiles, w.offsets, tile_offsets);
     if (stats_i64) cudaMemcpyAsync(stats_i64, w.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);

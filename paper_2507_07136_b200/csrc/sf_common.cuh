@@ -229,14 +229,12 @@ size_t project_compact_cub_bytes(int64_t G);
 size_t depth_sort_tmp_bytes(int64_t n);
 int depth_sort(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int64_t n, void* tmp,
                size_t tmp_bytes, cudaStream_t st);
-// rank_of_row[row] = canonical rank, ~0 for culled rows
-void launch_rank_of_row(int64_t G, const uint32_t* sorted_rows, const int64_t* stats,
-                        uint32_t* rank_of_row, cudaStream_t st);
 // per-row scatter plan (channel ids + values) of the selected levels
 void launch_pack_channels(const SfScene& s, const LevelSelDev& levels, unsigned char* chan, cudaStream_t st);
-// Binning over n_items geometry records.  rank_of == null: record i has
-// canonical rank i (i < stats[VISIBLE]); else rank_of[i] (~0 = culled).
-// rank_to_row != null: the sorted per-tile ranks are replaced by rows.
+// Binning over n_items geometry records.  row_keys == null (sf_bin): record
+// i has canonical rank i (i < stats[VISIBLE]) and the lists hold ranks.
+// row_keys != null (frame): record i is scene row i, culled iff row_keys[i]
+// == ~0, and each list's rows are sorted by (row_keys[row], row).
 // tile_counts holds 2 * n_tiles counters; aux one BinAux per item.
 constexpr int kBinSlots = 8;
 struct __align__(16) BinAux {
@@ -244,8 +242,8 @@ struct __align__(16) BinAux {
     uint16_t tx0, ty0, w, h;     // candidate rectangle
     uint32_t pos[kBinSlots];     // in-tile position of the first kBinSlots hits
 };
-void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint32_t* rank_of,
-                    const uint32_t* rank_to_row, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
+void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint64_t* row_keys, int W,
+                    int H, int64_t pair_capacity, uint32_t* tile_counts,
                     uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
                     BinAux* aux, uint32_t* cta_base, int tile_row0, int tile_row1, cudaStream_t st);
 // per-(count CTA, tile) range bases of the aggregated count pass

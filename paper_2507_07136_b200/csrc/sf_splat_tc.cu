@@ -168,6 +168,11 @@ __device__ __forceinline__ void tl_stamp(const BlendArgs& A, int tile_it, int ev
     if (A.timeline && blockIdx.x == 0 && tile_it < 256)
         A.timeline[148 * 128 + 16 * tile_it + ev] = clock64();
 }
+// per-chunk decode timeline of CTA 0 (same aid): stamp[chunk][event] at [148 * 128 + 16 * 256 + 8 * Gd + event]
+__device__ __forceinline__ void ch_stamp(const BlendArgs& A, int gd, int ev) {
+    if (A.timeline && blockIdx.x == 0 && gd < 2048)
+        A.timeline[148 * 128 + 16 * 256 + 8 * gd + ev] = clock64();
+}
 // cycle accounting (same aid): slot i of the CTA's 64 counters at [16, 80) of its 128
 __device__ __forceinline__ void prof_add(const BlendArgs& A, int i, uint64_t v) {
     if (A.timeline) A.timeline[(size_t)blockIdx.x * 128 + 16 + i] += v;
@@ -179,6 +184,10 @@ __device__ __forceinline__ void prof_add(const BlendArgs& A, int i, uint64_t v) 
 #define SF_STAMP(...)                      \
     do {                                   \
         if constexpr (prof) tl_stamp(__VA_ARGS__); \
+    } while (0)
+#define SF_CSTAMP(...)                     \
+    do {                                   \
+        if constexpr (prof) ch_stamp(__VA_ARGS__); \
     } while (0)
 #define SF_TIMED(acc, stmt)                     \
     do {                                        \
@@ -729,6 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     const int t = Gd & 1, b = g / dchunks, c = g - b * dchunks;
                     if (lane == 0) SF_PROG(A, 5 + q, (uint32_t)it, 0x30000u | (uint32_t)Gd);
                     SF_TIMED(w1, bar_wait(&S.acc_full[t], (Gd >> 1) & 1));
+                    if (q == 0 && lane == 0) SF_CSTAMP(A, Gd, 0);
                     if (q == 0 && lane == 0) {
                         // chunk Gd's MMAs are complete: its codebook stage takes chunk Gd + 2
                         const int sg = Gd % kBStages;
@@ -745,10 +755,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     tc_before();
                     __syncwarp();
                     if (lane == 0) bar_arrive(&S.acc_empty[t]);
+                    if (q == 0 && lane == 0) SF_CSTAMP(A, Gd, 1);
                     const float sc = b == 0 ? scl[0] : (b == 1 ? scl[1] : scl[2]);
 #pragma unroll
                     for (int i = 0; i < 64; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
                     if (lane == 0) SF_TIMED(w2, bulk_wait_read<0>());  // the previous chunk's stores have left the boxes
+                    if (q == 0 && lane == 0) SF_CSTAMP(A, Gd, 2);
                     __syncwarp();
 #pragma unroll
                     for (int qq = 0; qq < 2; ++qq) {
@@ -767,6 +779,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                         tma_store_4d(&fmap, wbox, c * kDecN, bx, by, b);
                         tma_store_4d(&fmap, wbox + kBoxBytes, c * kDecN + kBoxCols, bx, by, b);
                         bulk_commit();
+                        if (q == 0) SF_CSTAMP(A, Gd, 3);
                         if (q == 0 && g == nchunk - 1) SF_STAMP(A, it, 7);
                         if (q == 0 && g == 0) SF_STAMP(A, it, 8);
                     }
@@ -849,6 +862,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 SF_TIMED(w1, bar_wait(&S.b_full[s], (Gd / kBStages) & 1));
                 if (Gd >= 2) SF_TIMED(w2, bar_wait(&S.acc_empty[t], ((Gd >> 1) - 1) & 1));
                 tc_after();
+                SF_CSTAMP(A, Gd, 4);
                 const int b = cd / dchunks;
                 const uint32_t d = tm + (uint32_t)(kAccCol0 + t * kDecN);
                 const uint64_t bd = bdesc0 + (uint64_t)((s * kChunkBytes) >> 4);
@@ -862,6 +876,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     mma_f16_tmem_a(d, ah, bh, idesc_dec, 1u);
                 }
                 mma_commit(&S.acc_full[t]);
+                SF_CSTAMP(A, Gd, 5);
             }
             mma_commit(&S.slot_free[td & 1]);
             SF_STAMP(A, td, 5);

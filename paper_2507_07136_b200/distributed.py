@@ -206,9 +206,11 @@ def band_query(engine, cam, levels, spec, world_size: int, rank: int, group=None
     H = int(cam.height)
     band = band_rows(H, world_size, rank, halo=int(spec.window) // 2)
     if out is None:
-        # the coefficient map is only materialised when the channels span several
-        # blend CTAs (relevancy is then computed from the map, sf_capi.cu)
-        wide = len(levels) * int(engine.ds.config.L) > 192
+        # the coefficient map is only materialised when the relevancy is not
+        # fused into the blend (it is then computed from the map, sf_capi.cu)
+        from . import _native as N
+        cfg = engine.ds.config
+        wide = not N.load().sf_relevancy_fused(len(levels), int(cfg.L), int(cfg.K), int(len(spec.canonicals)))
         out = engine.allocate(int(cam.width), H, levels, coeff_map=wide, features=False, query=True)
     engine.run(cam, levels, out, query=spec, band=(band.y0, band.y1))
     mx, am, mn = band_statistics(out, len(levels))

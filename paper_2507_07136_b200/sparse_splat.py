@@ -293,7 +293,8 @@ def query_pipeline(scene, cam, query: QueryEmbedding, canonicals, *, window: int
         raise ValidationError("coefficient index >= L")
     eager = features == "eager"
     fused = bool(N.load().sf_decode_fused(len(levels), cfg.L, cfg.K, cfg.D))
-    need_cmap = (eager and not fused) or len(levels) * cfg.L > 192
+    rel_fused = bool(N.load().sf_relevancy_fused(len(levels), cfg.L, cfg.K, canon.shape[0]))
+    need_cmap = (eager and not fused) or not rel_fused
     eng = ds.engine if engine is None else engine  # serve.py: one engine + stream per concurrent request
     out = eng.allocate(W, H, levels, coeff_map=need_cmap, features=eager, query=True)
     spec = QuerySpec(query.vector, canon, window, fixed, threshold)
@@ -437,7 +438,8 @@ class QueryStream:
             raise ValidationError("coefficient index >= L")
         eager = features == "eager"
         fused = bool(N.load().sf_decode_fused(len(self.levels), cfg.L, cfg.K, cfg.D))
-        need_cmap = (eager and not fused) or len(self.levels) * cfg.L > 192
+        rel_fused = bool(N.load().sf_relevancy_fused(len(self.levels), cfg.L, cfg.K, canon.shape[0]))
+        need_cmap = (eager and not fused) or not rel_fused
         self.pipe = FramePipeline(self.ds, self.W, self.H, self.levels, coeff_map=need_cmap, features=eager,
                                   query=True)
         self.canon_dev = torch.from_numpy(canon).to(self.ds.device)

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
-prog = torch.zeros(148 * 128 + 16 * 256, dtype=torch.int64).pin_memory()
+prog = torch.zeros(148 * 128 + 16 * 256 + 8 * 2048, dtype=torch.int64).pin_memory()
 if not os.environ.get("STRESS_NOPROG"):
     os.environ["SF_TC_PROGRESS"] = str(prog.data_ptr())
 
@@ -71,11 +71,12 @@ def run(G, W, H, timeout=float(os.environ.get("STRESS_TIMEOUT", "60"))):
     if not os.environ.get("STRESS_NOPROG"):
         prof_report(min(148, 2 * ((W + 15) // 16) * ((H + 15) // 16)))
         timeline_report()
+        chunk_report()
 
 
 def timeline_report():
     """CTA 0's per-tile events (cycles relative to the first), us at 1.965 GHz."""
-    t = prog.numpy()[148 * 128:].reshape(256, 16).astype(np.int64)
+    t = prog.numpy()[148 * 128:148 * 128 + 16 * 256].reshape(256, 16).astype(np.int64)
     names = ["blend_start", "blend_end", "epi_done", "ev_wfull", "dec_start", "dec_end", "drain_start",
              "drain_last", "drain_first", "prod_start", "prod_end"]
     n = int((t[:, 0] > 0).sum())
@@ -86,6 +87,25 @@ def timeline_report():
     if n > 10:
         d = np.diff(t[:n, :11], axis=0) / 1965.0
         print("  mean per-tile period (us): " + " ".join(f"{x[:6]}={v:.2f}" for x, v in zip(names, d.mean(axis=0))))
+
+
+def chunk_report():
+    """CTA 0's per-chunk decode events: issuer start/commit, drain 0 acc_full/ld/bulk/store (cycles)."""
+    c = prog.numpy()[148 * 128 + 16 * 256:].reshape(2048, 8).astype(np.int64)
+    n = int((c[:, 4] > 0).sum())
+    if n < 4:
+        return
+    t0 = c[0, 4]
+    names = ["acc_full", "ld_done", "bulk_ok", "stored", "iss_start", "iss_end"]
+    print("  chunk " + " ".join(f"{x:>9s}" for x in names) + "   (cycles from chunk 0 issue)")
+    for i in list(range(min(n, 30))) + list(range(max(30, n - 30), n)):
+        print(f"  {i:5d} " + " ".join(f"{c[i, e] - t0:9d}" if c[i, e] else f"{'-':>9s}" for e in [0, 1, 2, 3, 4, 5]))
+    d = c[:n]
+    ok = (d[:, [0, 1, 2, 3, 4, 5]] > 0).all(axis=1)
+    d = d[ok]
+    print("  mean: issue->commit %.0f, issue->acc_full %.0f, acc_full->ld_done %.0f, ld_done->bulk_ok %.0f, bulk_ok->stored %.0f cycles; chunk period %.0f" % (
+        (d[:, 5] - d[:, 4]).mean(), (d[:, 0] - d[:, 4]).mean(), (d[:, 1] - d[:, 0]).mean(), (d[:, 2] - d[:, 1]).mean(),
+        (d[:, 3] - d[:, 2]).mean(), np.median(np.diff(d[:, 4]))))
 
 
 def prof_report(n_cta):
