@@ -321,6 +321,42 @@ int sf_decode_fused(int32_t n_levels, int32_t L, int32_t K, int32_t D);
  * query_pipeline (splatfield/sparse_splat.py:281-283, query.py:65-84). */
 int sf_relevancy_fused(int32_t n_levels, int32_t L, int32_t K, int32_t n_canon);
 
+/* ---- training step (splatfield/train.py; kernels in csrc/sf_train.cu) ----
+ * Parameters live in HBM in device row order: logits (levels, G, L) fp64,
+ * codebooks (levels, L, D) fp64.  All sums run in a fixed order. */
+
+/* softmax -> top-K -> renormalise per (row, level) into the scatter plan
+ * (sf_channel_plan_bytes bytes); replaces normalize_batch (train.py:131-139). */
+int sf_train_plan(int64_t G, int32_t levels, int32_t L, int32_t K, const double* logits, void* plan, void* stream);
+/* loss partial blocks per level of a frame of HW pixels; codebook-gradient splits */
+int64_t sf_train_loss_blocks(int64_t HW);
+int32_t sf_train_cb_splits(void);
+/* F = W atoms, r = (F - T) mask, loss partials (levels * blocks, 2) = (sum r^2,
+ * sum (1 - cos) mask), dF = 2 scale r + cos_w scale dcos, dW = dF atoms^T
+ * (forward_loss train.py:201-279, backward train.py:303-329).  wmap / dW:
+ * (HW, levels L) fp32; targets / dF: (levels, HW, D) fp64; mask (HW) fp64 or
+ * NULL; pix_stats (levels, HW, 3) fp64, required when cos_w != 0. */
+int sf_train_residual(int64_t HW, int32_t levels, int32_t L, int32_t D, const float* wmap, const double* atoms,
+                      const double* targets, const double* mask, double scale, double cos_w, double* pix_stats,
+                      double* dF, float* dW, double* loss_part, void* stream);
+/* dL/datoms = W^T dF (train.py:321); part: sf_train_cb_splits x levels x L x D */
+int sf_train_cbgrad(int64_t HW, int32_t levels, int32_t L, int32_t D, const float* wmap, const double* dF,
+                    double* part, double* grad_cb, void* stream);
+int64_t sf_train_logit_blocks(int64_t G, int32_t levels);
+int64_t sf_train_adam_blocks(int64_t n);
+/* top-K softmax backward from ghat (levels, G, K) fp32 (the transpose splat's
+ * output, SfFrame.grad_values); grad_out (levels, G, L) or NULL; with t > 0
+ * and m, v: Adam step t on the logits in place (train.py:79-107, 331-340).
+ * norm_part: sf_train_logit_blocks squared-gradient partials. */
+int sf_train_logits(int64_t G, int32_t levels, int32_t L, int32_t K, double* logits, const float* ghat,
+                    double* grad_out, double* m, double* v, double lr, double beta1, double beta2, double eps,
+                    int64_t t, double* norm_part, void* stream);
+/* Adam step t on n parameters (t = 0: only the squared-gradient partials) */
+int sf_train_adam(int64_t n, double* param, const double* grad, double* m, double* v, double lr, double beta1,
+                  double beta2, double eps, int64_t t, double* norm_part, void* stream);
+/* out[j] = sum_i part[i * stride + j] in order, j < width */
+int sf_train_reduce(int64_t n, int32_t stride, int32_t width, const double* part, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,6 +90,16 @@ EXPORTS = {
     "sf_relevancy_fused": (ctypes.c_int, [i32, i32, i32, i32]),
     "sf_decode_image_bytes": (sz, [i32, i32, i32, i32]),
     "sf_pack_decode_image": (ctypes.c_int, [ctypes.POINTER(SfScene), P, i32, P, sz, P]),
+    "sf_train_plan": (ctypes.c_int, [i64, i32, i32, i32, P, P, P]),
+    "sf_train_loss_blocks": (i64, [i64]),
+    "sf_train_cb_splits": (i32, []),
+    "sf_train_residual": (ctypes.c_int, [i64, i32, i32, i32, P, P, P, P, f64, f64, P, P, P, P, P]),
+    "sf_train_cbgrad": (ctypes.c_int, [i64, i32, i32, i32, P, P, P, P, P]),
+    "sf_train_logit_blocks": (i64, [i64, i32]),
+    "sf_train_adam_blocks": (i64, [i64]),
+    "sf_train_logits": (ctypes.c_int, [i64, i32, i32, i32, P, P, P, P, P, f64, f64, f64, f64, i64, P, P]),
+    "sf_train_adam": (ctypes.c_int, [i64, P, P, P, P, f64, f64, f64, f64, i64, P, P]),
+    "sf_train_reduce": (ctypes.c_int, [i64, i32, i32, P, P, P]),
     "sf_lsv2_unpack": (ctypes.c_int, [P, i64, i32, i32, i32, P, P, P, P, P, P, P, P, P]),
 }
 

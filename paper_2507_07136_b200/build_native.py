@@ -22,7 +22,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 # no FMA contraction except the explicit fma() calls that mirror BLAS.
 NO_FMAD = {"sf_preprocess.cu", "sf_binning.cu"}
 SOURCES = ["sf_preprocess.cu", "sf_binning.cu", "sf_sort.cu", "sf_blend.cu", "sf_splat_tc.cu", "sf_runtime.cu", "sf_post.cu", "sf_decode.cu",
-           "sf_decode_tc.cu", "sf_io.cu", "sf_capi.cu"]
+           "sf_decode_tc.cu", "sf_io.cu", "sf_train.cu", "sf_capi.cu"]
 
 
 def nvcc() -> str:

@@ -17,6 +17,8 @@
 // (tile id | depth rank), i.e. the reference's per-tile lists, bit for bit.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "sf_common.cuh"
 
 namespace sf {
@@ -238,14 +240,21 @@ __global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t p
 
 // Exclusive scan over tiles (single CTA): offsets, emit cursors (past the
 // slot-positioned entries), pair total.
+// Also lists the tiles whose lists exceed kShortList entries (big[0] = count,
+// big[1..] = tile ids) for the long-list sorts.
+constexpr int kShortList = 4096;
 __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t* __restrict__ counts,
                                                     uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ cursor,
-                                                    int64_t pair_capacity, int64_t* stats) {
+                                                    int64_t pair_capacity, int64_t* stats,
+                                                    uint32_t* __restrict__ big) {
     typedef cub::BlockScan<unsigned long long, 1024> Scan;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ unsigned long long carry;
-    if (threadIdx.x == 0) carry = 0;
+    if (threadIdx.x == 0) {
+        carry = 0;
+        big[0] = 0u;
+    }
     __syncthreads();
     // 8 consecutive tiles per thread and pass: one block scan covers 8192 tiles
     constexpr int kPer = 8;
@@ -268,6 +277,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
             if (t < n_tiles) {
                 offsets[t] = (uint32_t)ex;
                 cursor[t] = (uint32_t)(ex + c0[k]);
+                if (c[k] > (unsigned long long)kShortList) big[1 + atomicAdd(&big[0], 1u)] = (uint32_t)t;
             }
             ex += c[k];
         }
@@ -582,12 +592,34 @@ __device__ __forceinline__ bool key_row_less(uint64_t ka, uint32_t ra, uint64_t 
 }
 
 template <int CAP, int NB>
+__device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __restrict__ offsets,
+                                                    uint32_t* __restrict__ entries, int lo_exclusive,
+                                                    const uint64_t* __restrict__ row_keys);
+
+template <int CAP, int NB>
 __global__ void __launch_bounds__(256) k_tile_sort_depth(const uint32_t* __restrict__ offsets,
                                                          uint32_t* __restrict__ entries, int lo_exclusive,
                                                          const int64_t* __restrict__ stats,
-                                                         const uint64_t* __restrict__ row_keys) {
+                                                         const uint64_t* __restrict__ row_keys,
+                                                         const uint32_t* __restrict__ big) {
     static_assert(CAP <= 65536 && NB % 256 == 0, "index width / scan split");
     if (stats[SF_STAT_OVERFLOW]) return;
+    if (!big) {
+        tile_sort_depth_one<CAP, NB>(blockIdx.x, offsets, entries, lo_exclusive, row_keys);
+        return;
+    }
+    // long lists only: the tiles k_tile_scan listed
+    const int nb = (int)big[0];
+    for (int i = blockIdx.x; i < nb; i += gridDim.x) {
+        tile_sort_depth_one<CAP, NB>((int)big[1 + i], offsets, entries, lo_exclusive, row_keys);
+        __syncthreads();
+    }
+}
+
+template <int CAP, int NB>
+__device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __restrict__ offsets,
+                                                    uint32_t* __restrict__ entries, int lo_exclusive,
+                                                    const uint64_t* __restrict__ row_keys) {
     extern __shared__ __align__(16) unsigned char ts_smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(ts_smem);           // CAP
     uint32_t* rows = reinterpret_cast<uint32_t*>(keys + CAP);       // CAP
@@ -596,7 +628,6 @@ __global__ void __launch_bounds__(256) k_tile_sort_depth(const uint32_t* __restr
     __shared__ uint32_t cursor[NB];
     __shared__ unsigned long long s_min, s_max;
     __shared__ int s_big;
-    const int t = blockIdx.x;
     const uint32_t beg = offsets[t], end = offsets[t + 1];
     const int n = (int)(end - beg);
     if (n <= lo_exclusive || n > CAP) return;
@@ -706,16 +737,29 @@ __global__ void __launch_bounds__(256) k_tile_sort_depth(const uint32_t* __restr
 
 // Lists over 8192 entries (pathological overlap): a stable LSD split sort in
 // global scratch, first on the row bits, then on the 64 key bits.
+__device__ __noinline__ void tile_sort_depth_split(int t, const uint32_t* __restrict__ offsets,
+                                                   uint32_t* __restrict__ entries, uint32_t* __restrict__ scratch,
+                                                   int lo_exclusive, const uint64_t* __restrict__ row_keys);
 __global__ void __launch_bounds__(256) k_tile_sort_depth_large(const uint32_t* __restrict__ offsets,
                                                                uint32_t* __restrict__ entries,
                                                                uint32_t* __restrict__ scratch, int lo_exclusive,
                                                                const int64_t* __restrict__ stats,
-                                                               const uint64_t* __restrict__ row_keys) {
+                                                               const uint64_t* __restrict__ row_keys,
+                                                               const uint32_t* __restrict__ big) {
     if (stats[SF_STAT_OVERFLOW]) return;
+    const int nb = (int)big[0];
+    for (int i = blockIdx.x; i < nb; i += gridDim.x) {
+        tile_sort_depth_split((int)big[1 + i], offsets, entries, scratch, lo_exclusive, row_keys);
+        __syncthreads();
+    }
+}
+
+__device__ __noinline__ void tile_sort_depth_split(int t, const uint32_t* __restrict__ offsets,
+                                                   uint32_t* __restrict__ entries, uint32_t* __restrict__ scratch,
+                                                   int lo_exclusive, const uint64_t* __restrict__ row_keys) {
     typedef cub::BlockScan<int, 256> Scan;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ int s_zero;
-    const int t = blockIdx.x;
     const uint32_t beg = offsets[t], end = offsets[t + 1];
     const int n = (int)(end - beg);
     if (n <= lo_exclusive) return;
@@ -784,8 +828,9 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
     } else if (blocks) {
         k_count_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, row_keys, g, tile_counts, aux);
     }
+    uint32_t* big = tile_cursor + n_tiles;  // long-list tiles (tile_cursor holds 2 n_tiles + 1)
     k_tile_scan<<<1, 1024, 0, st>>>(n_tiles, tile_counts, tile_offsets, tile_cursor, pair_capacity,
-                                    const_cast<int64_t*>(stats));
+                                    const_cast<int64_t*>(stats), big);
     if (blocks)
         k_emit_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, row_keys, g, aux, tile_offsets, tile_cursor,
                                              entries, agg ? cta_base : nullptr, per);
@@ -795,9 +840,15 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
         constexpr size_t s1 = TileSortDepth<4096>::kSmem, s2 = TileSortDepth<8192>::kSmem;
         ensure_smem_attr((const void*)k_tile_sort_depth<4096, 1024>, s1);
         ensure_smem_attr((const void*)k_tile_sort_depth<8192, 2048>, s2);
-        k_tile_sort_depth<4096, 1024><<<n_tiles, 256, s1, st>>>(tile_offsets, entries, 0, stats, row_keys);
-        k_tile_sort_depth<8192, 2048><<<n_tiles, 256, s2, st>>>(tile_offsets, entries, 4096, stats, row_keys);
-        k_tile_sort_depth_large<<<n_tiles, 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192, stats, row_keys);
+        // one CTA per tile for the common lists; the rare longer ones by a
+        // one-wave grid striding over the tiles (CTAs skip other sizes)
+        const int sms = device_sm_count();
+        static_assert(kShortList == 4096, "short-list capacity");
+        k_tile_sort_depth<4096, 1024><<<n_tiles, 256, s1, st>>>(tile_offsets, entries, 0, stats, row_keys, nullptr);
+        k_tile_sort_depth<8192, 2048><<<std::min(n_tiles, sms), 256, s2, st>>>(tile_offsets, entries, 4096, stats,
+                                                                              row_keys, big);
+        k_tile_sort_depth_large<<<std::min(n_tiles, sms), 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192,
+                                                                        stats, row_keys, big);
         return;
     }
     // sf_bin mode: unique ranks; most lists fit the shared-memory bucket sort

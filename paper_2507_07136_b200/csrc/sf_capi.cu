@@ -32,6 +32,15 @@ static int check_cuda(const char* where) {
 
 extern "C" const char* sf_last_error(void) { return g_err; }
 
+namespace sf {
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+}  // namespace sf
+
 extern "C" void* sf_event_create(void) {
     cudaEvent_t e = nullptr;
     if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
@@ -127,7 +136,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->chan = c.take<unsigned char>((size_t)Gp * chan_rec_bytes(C));
     ws->tile_counts = c.take<uint32_t>(2 * n_tiles);
     ws->tile_offsets = c.take<uint32_t>(n_tiles + 1);
-    ws->tile_cursor = c.take<uint32_t>(n_tiles);
+    ws->tile_cursor = c.take<uint32_t>(2 * n_tiles + 1);  // + the long-list tile list (launch_binning)
     ws->entries = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
     ws->scratch = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
     ws->proj_cb = c.take<double>((size_t)n_levels * L * (1 + kMaxCanon));
@@ -599,7 +608,7 @@ static size_t carve_bin(void* base, size_t cap, int64_t n, int W, int H, int64_t
     w->aux = c.take<BinAux>(np);
     w->cta_base = c.take<uint32_t>(bin_cta_base_elems(W, H));
     w->offsets = c.take<uint32_t>(n_tiles + 1);
-    w->cursor = c.take<uint32_t>(n_tiles);
+    w->cursor = c.take<uint32_t>(2 * n_tiles + 1);
     w->scratch = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
     return c.off;
 }

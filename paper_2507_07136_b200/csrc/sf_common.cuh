@@ -210,6 +210,8 @@ struct LevelSelDev {
 // sf_runtime.cu: per-(kernel, device) dynamic shared-memory limit (thread-safe),
 // and the current device's SM count (persistent grids)
 int ensure_smem_attr(const void* func, size_t bytes);
+// message for sf_last_error (sf_capi.cu)
+void set_error(const char* fmt, ...);
 int device_sm_count();
 
 // ---------------- internal launchers (one .cu each) ----------------

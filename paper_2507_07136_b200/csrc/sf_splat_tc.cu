@@ -94,6 +94,8 @@ struct __align__(1024) Smem {
     int done_count;
     uint32_t contrib[2];   // per W slot: bit w = blend warp w's pixels got a contribution
     uint32_t dq_info[2];   // MMA -> drains, per tile in order: contrib of the tile
+    uint32_t ev_tag[kStages];  // batch sequence number + 1 when some blend warp had a candidate in it
+    uint32_t tile_tag[2];      // per W slot: tile iteration + 1 when some batch of the tile had a candidate
     uint64_t rec_full[kStages], ev_full[kStages], ev_empty[kStages];
     uint64_t w_full[2], a_ready[2], slot_free[2];
     uint64_t dq_full[2], dq_empty[2];
@@ -227,6 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
         for (int i = 0; i < kBStages; ++i) bar_init(&S.b_full[i], 1);
         S.done_count = 0;
         S.contrib[0] = S.contrib[1] = 0u;
+        for (int i = 0; i < kStages; ++i) S.ev_tag[i] = 0u;
+        S.tile_tag[0] = S.tile_tag[1] = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // V stages start (and, between batches, are returned to) all zero
@@ -323,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&S.rec_full[s]))
                              : "memory");
                 if (lane == 0) S.nb[s] = nb;
+                if (prof && nb) ++w1;
                 __syncwarp();
                 if (lane == 0) bar_arrive(&S.rec_full[s]);
                 if (nb == kBatch) {
@@ -441,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             const float pdx0 = (float)(x0 + (w8 & 1) * 8), pdy0 = (float)(y0 + (w8 >> 1) * 4);
             float T = 1.f, eb = 0.f, Tprev = 1.f;
             int ncontrib = 0, nbatches = 0;
+            bool tile_hit = false;  // some batch of this tile had a candidate for this warp
             bool done = !inside;
             if (hb == 0 && lane == 0) SF_STAMP(A, it, 0);
             bool all_done = __all_sync(0xffffffffu, done);
@@ -560,6 +566,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 post(hb == 0 ? bar_ab : bar_ba);
                 if (prof) w2 += clock64() - tw0;
                 ++nbatches;
+                // batches without a candidate in any warp have E = 0: the issuer skips them
+                if (wmask && lane == 0) S.ev_tag[s] = (uint32_t)bs + 1u;
+                tile_hit |= wmask != 0u;
                 proxy_fence();
                 __syncwarp();
                 if (lane == 0) bar_arrive(&S.ev_full[s]);
@@ -572,6 +581,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             }
             if (!counted && lane == 0) atomicAdd(&S.done_count, 1);
             if (hb == 0 && lane == 0) SF_STAMP(A, it, 1);
+            // W holds products iff some warp had a candidate in some batch (else
+            // the issuer skipped every batch and the slot is stale): the 8 blend
+            // warps agree on that through the tile tag
+            if (tile_hit && lane == 0) S.tile_tag[slot] = (uint32_t)it + 1u;
+            named_bar_sync(13, 32 * kBlendWarps);
+            const bool wvalid = *reinterpret_cast<volatile uint32_t*>(&S.tile_tag[slot]) == (uint32_t)it + 1u;
 
             // ---- per-tile epilogue: hb 0 takes columns [0, 32) of each level, hb 1 [32, 64) ----
             if (hb == 0 && inside && A.early_exit && A.fixup_list) {
@@ -603,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             // instructions are fetched cold -- loops stay rolled.
             // (1) hb 0: relevancy over all 64 columns of each level (before hb 1
             //     converts its columns in place), 8 columns per step.
-            if (hb == 0 && rel && nbatches) {
+            if (hb == 0 && rel && wvalid) {
 #pragma unroll 1
                 for (int b = 0; b < n_levels; ++b) {
                     double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
@@ -657,7 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 for (int b = 0; b < n_levels; ++b) {
                     const uint32_t col = wslot + (uint32_t)(64 * b + 32 * hb);
                     uint32_t v[32];
-                    if (nbatches) {
+                    if (wvalid) {
                         tmem_ld32(col, v);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     } else {
@@ -817,6 +832,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     SF_STAMP(A, te, 3);
                     bar_arrive(&S.ev_empty[s]);
                     break;
+                }
+                if (*reinterpret_cast<volatile uint32_t*>(&S.ev_tag[s]) != (uint32_t)(be - 1) + 1u) {
+                    // no blend warp had a candidate: E = 0, nothing to add
+                    bar_arrive(&S.ev_empty[s]);
+                    if (prof) ++w2;
+                    continue;
                 }
                 tc_after();
                 const uint32_t d = tm + (uint32_t)((te & 1) * kSlotCols);

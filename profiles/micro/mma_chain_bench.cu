@@ -31,12 +31,12 @@ __device__ __forceinline__ void issue(uint32_t tm, uint64_t ad, uint64_t bd, uin
 
 template <bool ATMEM, int NACC>
 __global__ void k(int iters, int N, int bg, unsigned long long* out) {
-    __shared__ __align__(1024) unsigned char sm[40 * 1024];
+    extern __shared__ __align__(1024) unsigned char sm[];  // B: [0, 32 KB), A: [32 KB, 48 KB)
     __shared__ uint32_t tbase;
     __shared__ __align__(8) uint64_t bar;
     __shared__ volatile int stop;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < 40 * 1024 / 4; i += blockDim.x) ((uint32_t*)sm)[i] = 0;
+    for (int i = threadIdx.x; i < 48 * 1024 / 4; i += blockDim.x) ((uint32_t*)sm)[i] = 0;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sa(&tbase)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -93,7 +93,8 @@ template <bool ATMEM, int NACC>
 void run(int N, int bg, unsigned long long* d) {
     const int iters = 2048;
     unsigned long long h[2];
-    k<ATMEM, NACC><<<1, 160>>>(iters, N, bg, d);
+    cudaFuncSetAttribute(k<ATMEM, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    k<ATMEM, NACC><<<1, 160, 64 * 1024>>>(iters, N, bg, d);
     cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
     printf("N=%3d A=%s acc=%d bg=%d: %6.1f cyc/mma (floor %d)\n", N, ATMEM ? "TMEM" : "SMEM", NACC, bg,
            (double)h[0] / iters, 128 * N / 256);

@@ -113,7 +113,7 @@ def prof_report(n_cta):
     p = prog.numpy()[:148 * 128].reshape(148, 128)[:n_cta, 16:].astype(np.float64)
     names = {0: "blend", 16: "drain", 32: "producer", 36: "ev_issuer", 40: "dec_issuer"}
     labels = {"blend": ("waits", "alpha", "walk"), "drain": ("dq_full", "acc_full", "bulk_read(lane0)"),
-              "producer": ("ev_empty", "-", "-"), "ev_issuer": ("ev_full", "slot_free", "-"),
+              "producer": ("ev_empty", "batches", "-"), "ev_issuer": ("ev_full", "slot_free", "skipped_batches"),
               "dec_issuer": ("a_ready/dq", "b_full", "acc_empty")}
     for base, nm in names.items():
         warps = 8 if base == 0 else (4 if base == 32 else 1)
@@ -124,7 +124,11 @@ def prof_report(n_cta):
             lab = labels[nm][k]
             if lab == "-":
                 continue
-            if lab == "progress_iters":
+            if lab == "batches":
+                print(f"  batches {v.mean():.0f}/CTA", end="")
+            elif lab == "skipped_batches":
+                print(f"  skipped batches {v.mean():.0f}/CTA", end="")
+            elif lab == "progress_iters":
                 print(f"  {lab} {v.mean():.0f}", end="")
             elif lab == "cand":
                 raw = prog.numpy()[:148 * 128].reshape(148, 128)[:n_cta, 16:80][:, base + 1 + k:base + 4 * warps:4].astype(np.int64)
