@@ -579,9 +579,10 @@ __global__ void __launch_bounds__(256) k_tile_sort_large(const uint32_t* __restr
 //
 // Sort: MSD bucket pass in shared memory -- bucket = floor((key - min) *
 // NB / span) in fp64 (rounding is monotone, so buckets stay in key order),
-// histogram, scan, scatter of entry indices, insertion sort inside each
-// bucket on (key, row).  Strongly clustered tiles (a bucket over kMaxBucket
-// entries) take a bitonic sort of the indices instead.
+// histogram, scan, scatter of entry indices into their buckets; then every
+// entry's final position is its bucket's start plus the number of bucket
+// members ordering before it on (key, row) -- each entry independently, so
+// there is no serial insertion chain (keys are unique as (key, row) pairs).
 template <int CAP>
 struct TileSortDepth {
     static constexpr size_t kSmem = (size_t)CAP * (8 + 4 + 2);
@@ -623,11 +624,10 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
     extern __shared__ __align__(16) unsigned char ts_smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(ts_smem);           // CAP
     uint32_t* rows = reinterpret_cast<uint32_t*>(keys + CAP);       // CAP
-    uint16_t* order = reinterpret_cast<uint16_t*>(rows + CAP);      // CAP
+    uint16_t* order = reinterpret_cast<uint16_t*>(rows + CAP);      // CAP: entry indices grouped by bucket
     __shared__ uint32_t start[NB + 1];
     __shared__ uint32_t cursor[NB];
     __shared__ unsigned long long s_min, s_max;
-    __shared__ int s_big;
     const uint32_t beg = offsets[t], end = offsets[t + 1];
     const int n = (int)(end - beg);
     if (n <= lo_exclusive || n > CAP) return;
@@ -635,18 +635,28 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
     if (threadIdx.x == 0) {
         s_min = ~0ull;
         s_max = 0ull;
-        s_big = 0;
     }
     for (int b = threadIdx.x; b < NB; b += blockDim.x) cursor[b] = 0;
+    // rows (coalesced), then their keys (L2 gathers, 8 in flight per thread)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) rows[i] = e[i];
     __syncthreads();
     unsigned long long mn = ~0ull, mx = 0ull;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const uint32_t r = e[i];
-        const uint64_t k = __ldg(row_keys + r);
-        rows[i] = r;
-        keys[i] = k;
-        mn = min(mn, (unsigned long long)k);
-        mx = max(mx, (unsigned long long)k);
+    for (int i0 = threadIdx.x; i0 < n; i0 += 8 * blockDim.x) {
+        uint64_t k[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            k[u] = i < n ? __ldg(row_keys + rows[i]) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            if (i < n) {
+                keys[i] = k[u];
+                mn = min(mn, (unsigned long long)k[u]);
+                mx = max(mx, (unsigned long long)k[u]);
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -681,58 +691,29 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
             const int b = threadIdx.x * PER + j;
             start[b] = ex;
             cursor[b] = ex;
-            if (c[j] > (uint32_t)kMaxBucket) s_big = 1;
             ex += c[j];
         }
         if (threadIdx.x == 255) start[NB] = ex;
     }
     __syncthreads();
-    if (s_big) {
-        // clustered keys: bitonic sort of the indices on (key, row)
-        int N = 2;
-        while (N < n) N <<= 1;
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
-            order[i] = (uint16_t)i;
-            if (i >= n) {
-                keys[i] = ~0ull;
-                rows[i] = 0xffffffffu;
-            }
-        }
-        __syncthreads();
-        for (int k = 2; k <= N; k <<= 1) {
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int p = threadIdx.x; p < (N >> 1); p += blockDim.x) {
-                    const int i = 2 * j * (p / j) + (p % j), ixj = i + j;
-                    const bool up = (i & k) == 0;
-                    const uint16_t a = order[i], b = order[ixj];
-                    if (key_row_less(keys[b], rows[b], keys[a], rows[a]) == up) {
-                        order[i] = b;
-                        order[ixj] = a;
-                    }
-                }
-                __syncthreads();
-            }
-        }
-    } else {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&cursor[bucket_of(keys[i])], 1u)] = (uint16_t)i;
-        __syncthreads();
-        for (int b = threadIdx.x; b < NB; b += blockDim.x) {
-            const int b0 = (int)start[b], b1 = (int)start[b + 1];
-            for (int i = b0 + 1; i < b1; ++i) {
-                const uint16_t x = order[i];
-                const uint64_t kx = keys[x];
-                const uint32_t rx = rows[x];
-                int j = i - 1;
-                while (j >= b0 && key_row_less(kx, rx, keys[order[j]], rows[order[j]])) {
-                    order[j + 1] = order[j];
-                    --j;
-                }
-                order[j + 1] = x;
-            }
-        }
-    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&cursor[bucket_of(keys[i])], 1u)] = (uint16_t)i;
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) e[i] = rows[order[i]];
+    // final position = bucket start + the members of the bucket that order
+    // before the entry on (key, row): independent per entry (no serial chain);
+    // the rows are in shared memory, so the list is overwritten in place
+    for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        const int i = order[p];
+        const uint64_t ki = keys[i];
+        const uint32_t ri = rows[i];
+        const int b = bucket_of(ki);
+        const int q0 = (int)start[b], q1 = (int)start[b + 1];
+        int r = q0;
+        for (int q = q0; q < q1; ++q) {
+            const int j = order[q];
+            r += key_row_less(keys[j], rows[j], ki, ri) ? 1 : 0;
+        }
+        e[r] = ri;
+    }
 }
 
 // Lists over 8192 entries (pathological overlap): a stable LSD split sort in

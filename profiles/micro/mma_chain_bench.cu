@@ -36,7 +36,7 @@ __global__ void k(int iters, int N, int bg, unsigned long long* out) {
     __shared__ __align__(8) uint64_t bar;
     __shared__ volatile int stop;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < 48 * 1024 / 4; i += blockDim.x) ((uint32_t*)sm)[i] = 0;
+    for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((uint32_t*)sm)[i] = 0;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sa(&tbase)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -70,7 +70,19 @@ __global__ void k(int iters, int N, int bg, unsigned long long* out) {
             out[0] = (unsigned long long)(t1 - t0);
             stop = 1;
         }
-    } else if (bg && warp >= 1 && warp <= 4) {
+    } else if (bg == 2 && warp >= 1) {
+        // background: shared-memory load/store traffic (like the blend warps'), on [48 KB, 64 KB)
+        uint32_t a = sa(sm + 48 * 1024) + (uint32_t)((threadIdx.x * 16) & 16383);
+        uint32_t x = threadIdx.x, acc = 0;
+        for (int i = 0; !stop; ++i) {
+            uint32_t v0, v1, v2, v3;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3) : "r"(a));
+            acc += v0 ^ v3;
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a ^ 512u), "r"(x), "r"(acc), "r"(v1), "r"(v2));
+            a = sa(sm + 48 * 1024) + (uint32_t)(((threadIdx.x + i * 37) * 16) & 16383);
+        }
+        if (acc == 12345) out[1] = acc;
+    } else if (bg == 1 && warp >= 1 && warp <= 4) {
         // background: TMEM reads of the accumulator area's lane quarter (like the drains)
         uint32_t v[32], acc = 0;
         const int q = warp - 1;
@@ -94,7 +106,7 @@ void run(int N, int bg, unsigned long long* d) {
     const int iters = 2048;
     unsigned long long h[2];
     cudaFuncSetAttribute(k<ATMEM, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    k<ATMEM, NACC><<<1, 160, 64 * 1024>>>(iters, N, bg, d);
+    k<ATMEM, NACC><<<1, bg == 2 ? 512 : 160, 64 * 1024>>>(iters, N, bg, d);
     cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
     printf("N=%3d A=%s acc=%d bg=%d: %6.1f cyc/mma (floor %d)\n", N, ATMEM ? "TMEM" : "SMEM", NACC, bg,
            (double)h[0] / iters, 128 * N / 256);
@@ -103,7 +115,7 @@ void run(int N, int bg, unsigned long long* d) {
 int main() {
     unsigned long long* d;
     cudaMalloc(&d, 16);
-    for (int bg : {0, 1})
+    for (int bg : {0, 1, 2})
         for (int N : {64, 128, 256}) {
             run<true, 1>(N, bg, d);
             if (N <= 128) run<true, 2>(N, bg, d);

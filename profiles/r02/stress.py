@@ -111,7 +111,8 @@ def chunk_report():
 def prof_report(n_cta):
     """Cycle accounting per role (mean over CTAs, in % of the role's total)."""
     p = prog.numpy()[:148 * 128].reshape(148, 128)[:n_cta, 16:].astype(np.float64)
-    names = {0: "blend", 16: "drain", 32: "producer", 36: "ev_issuer", 40: "dec_issuer"}
+    # 4 counters per warp (slot 4 * warp): blend warps 0-7, drains 8-11, producer 12, E V issuer 13, decode issuer 14
+    names = {0: "blend", 32: "drain", 48: "producer", 52: "ev_issuer", 56: "dec_issuer"}
     labels = {"blend": ("waits", "alpha", "walk"), "drain": ("dq_full", "acc_full", "bulk_read(lane0)"),
               "producer": ("ev_empty", "batches", "-"), "ev_issuer": ("ev_full", "slot_free", "skipped_batches"),
               "dec_issuer": ("a_ready/dq", "b_full", "acc_empty")}
