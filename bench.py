@@ -42,20 +42,15 @@ CONFIGS = {
     "C": (2_000_000, 1440, 1080),
     "E": (5_000_000, 1920, 1080),
 }
-# Kernels launched per query frame (sf_render_frame), from the ncu launch list in
-# profiles/r01_launches_latest.csv: preprocess, CUB onesweep depth sort (10),
-# rank_of_row, count, tile scan, emit, 3 tile-sort kernels, project codebook,
-# blend, blend fixup, 3 x (codebook split + tcgen05 decode), 2 x box filter,
-# reduce, finalize, mask.
-KERNELS_PER_FRAME = 32
-# With the decode fused into the blend (profiles/r01_launches_fused.csv): preprocess,
-# CUB onesweep depth sort (10), rank_of_row, count, tile scan, emit, 3 tile-sort
-# kernels, project codebook, blend (+ decode), fixup, fused box filter + statistics,
-# finalize, mask (the codebook image is cached per level selection).
-KERNELS_PER_FRAME_FUSED = 24
+# Kernels launched per query frame (sf_render_frame) with the decode fused into
+# the splat (round 2 launch list, profiles/r02/evidence/): preprocess, count,
+# tile scan, emit, 3 per-tile depth sorts, project codebook, splat (+ decode),
+# fixup, fused box filter + statistics, finalize, mask.  The single-GPU path
+# counts them live (count_kernels_per_frame); this constant serves the N > 1 line.
+KERNELS_PER_FRAME_FUSED = 13
 
 
-NCU_SUMMARY = "r01_ncu_fused.txt"
+NCU_SUMMARY = "r02_ncu_splat.txt"
 
 
 def ncu_traffic(kernel: str = "decode", summary: str = "r01_ncu_summary.txt"):
@@ -368,6 +363,23 @@ def main():
     return run_single(args)
 
 
+def count_kernels_per_frame(enqueue, pipe) -> int:
+    """Kernels one pipelined frame launches, counted by the CUDA profiler on an
+    untimed frame (every one is this repo's: the frame path calls no library
+    kernels; memsets and copies are not counted)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        pipe.begin()
+        enqueue()
+        pipe.end()
+        torch.cuda.synchronize()
+    kern = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+            and "memset" not in e.name.lower() and "memcpy" not in e.name.lower()]
+    return len(kern)
+
+
 def run_single(args):
     import numpy as np
     import torch
@@ -406,6 +418,7 @@ def run_single(args):
     for _ in range(args.warmup):
         pipe.enqueue(cam, levels, query=spec, qdev=qdev)
     pipe.end()
+    launches_per_frame = count_kernels_per_frame(lambda: pipe.enqueue(cam, levels, query=spec, qdev=qdev), pipe)
     stage = []
     for _ in range(3):
         step(timing=True)
@@ -449,8 +462,9 @@ def run_single(args):
     # SURVEY 8(d) algorithmic bytes of the fused blend + decode: the scene read
     # once (116 B per visible Gaussian), the codebooks, the fp32 features written
     alg_bytes = 3 * P * 512 * 4 + vis * 116 + 3 * 64 * 512 * 4
-    dom_kernel = "k_blend<DEC> (blend + fused relevancy + fused 3-term fp16 tcgen05 decode, one frame)"
-    traffic = ncu_traffic("blend_dec", NCU_SUMMARY)
+    dom_kernel = ("tcs::k_splat_tc<4,DEC> (persistent splat: E V blend products + fused relevancy + "
+                  "3-term fp16 decode on tcgen05, one frame)")
+    traffic = ncu_traffic("splat_tc", NCU_SUMMARY)
     hbm_peak, peak_kind = peaks()
     achieved = alg_bytes / (b_ms / 1e3) / 1e9
 
@@ -499,7 +513,7 @@ def run_single(args):
         "parity": parity,
         "e2e": e2e,
         "query_sweep": sweep,
-        "gpu_launches": KERNELS_PER_FRAME_FUSED * args.steps,
+        "gpu_launches": launches_per_frame * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 
+#include "sf_blend_dev.cuh"
 #include "sf_common.cuh"
 
 namespace sf {
@@ -292,6 +293,26 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
     }
 }
 
+// Half-tile flags of a tile hit (frame mode): bit h is set when the 16 x 8
+// pixel half h (rows 8h .. 8h + 7) may see the Gaussian.  With the conic
+// written q = a (dx + k dy)^2 + d dy^2 (GeomF32), every point with q <= 9 has
+// |dy| <= 3 / sqrt(d): the flag tests the half's pixel rows against that
+// y-extent (widened by 1e-3 relative + 1e-3 px for the fp32 evaluation), so
+// an entry without its half's flag has alpha = 0 at every pixel there.
+struct HalfTest {
+    float my, ry;
+};
+__device__ __forceinline__ HalfTest half_test_of(const GeomF32& g) {
+    const float ry = 3.f * rsqrtf(g.d);
+    return HalfTest{g.my_hi + g.my_lo, fmaf(ry, 1e-3f, ry) + 1e-3f};
+}
+__device__ __forceinline__ uint32_t half_tile_flags(const HalfTest& g, int x0, int y0) {
+    (void)x0;
+    const float lo = g.my - g.ry, hi = g.my + g.ry;
+    const float y = (float)y0;
+    return ((hi >= y && lo <= y + 7.f) ? 1u : 0u) | ((hi >= y + 8.f && lo <= y + 15.f) ? 2u : 0u);
+}
+
 __device__ __forceinline__ void emit_one(int j, int t, uint32_t r, const BinAux& a,
                                          const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ base,
                                          uint32_t* __restrict__ cursor, uint32_t* __restrict__ entries) {
@@ -330,13 +351,20 @@ __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __
     const int w = a.w;
     int j = 0;
     const uint32_t* base = cta_base ? cta_base + (size_t)(i / per) * (g.tiles_x * g.tiles_y) : nullptr;
+    // frame mode: which half tiles of the hit tile the splat's patch tests may
+    // see the Gaussian in (entry bits 31 / 30; moved to the flag array by the sort)
+    HalfTest ht;
+    if (row_keys) ht = half_test_of(*reinterpret_cast<const GeomF32*>(geom + i));
+    auto tagged = [&](int tx, int ty) -> uint32_t {
+        return row_keys ? r | (half_tile_flags(ht, tx * SF_TILE, ty * SF_TILE) << kEntryFlagShift) : r;
+    };
     if (w * (int)a.h <= 64) {
         unsigned long long mask = a.mask;
         while (mask) {
             const int bit = __ffsll((long long)mask) - 1;
             mask &= mask - 1;
             const int tx = a.tx0 + bit % w, ty = a.ty0 + bit / w;
-            emit_one(j++, ty * g.tiles_x + tx, r, a, offsets, base, cursor, entries);
+            emit_one(j++, ty * g.tiles_x + tx, tagged(tx, ty), a, offsets, base, cursor, entries);
         }
         return;
     }
@@ -345,7 +373,7 @@ __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __
     const MahalPre mp = mahal_pre(p.mx, p.my, p.a, p.b, p.c);
     for (int ty = a.ty0; ty < a.ty0 + (int)a.h; ++ty)
         for (int tx = a.tx0; tx < a.tx0 + w; ++tx)
-            if (tile_hit(mp, tx, ty, g)) emit_one(j++, ty * g.tiles_x + tx, r, a, offsets, base, cursor, entries);
+            if (tile_hit(mp, tx, ty, g)) emit_one(j++, ty * g.tiles_x + tx, tagged(tx, ty), a, offsets, base, cursor, entries);
 }
 
 // ---------------------------------------------------------------------------
@@ -595,24 +623,26 @@ __device__ __forceinline__ bool key_row_less(uint64_t ka, uint32_t ra, uint64_t 
 template <int CAP, int NB>
 __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ entries, int lo_exclusive,
-                                                    const uint64_t* __restrict__ row_keys);
+                                                    const uint64_t* __restrict__ row_keys,
+                                                    uint8_t* __restrict__ flags);
 
 template <int CAP, int NB>
 __global__ void __launch_bounds__(256) k_tile_sort_depth(const uint32_t* __restrict__ offsets,
                                                          uint32_t* __restrict__ entries, int lo_exclusive,
                                                          const int64_t* __restrict__ stats,
                                                          const uint64_t* __restrict__ row_keys,
-                                                         const uint32_t* __restrict__ big) {
+                                                         const uint32_t* __restrict__ big,
+                                                         uint8_t* __restrict__ flags) {
     static_assert(CAP <= 65536 && NB % 256 == 0, "index width / scan split");
     if (stats[SF_STAT_OVERFLOW]) return;
     if (!big) {
-        tile_sort_depth_one<CAP, NB>(blockIdx.x, offsets, entries, lo_exclusive, row_keys);
+        tile_sort_depth_one<CAP, NB>(blockIdx.x, offsets, entries, lo_exclusive, row_keys, flags);
         return;
     }
     // long lists only: the tiles k_tile_scan listed
     const int nb = (int)big[0];
     for (int i = blockIdx.x; i < nb; i += gridDim.x) {
-        tile_sort_depth_one<CAP, NB>((int)big[1 + i], offsets, entries, lo_exclusive, row_keys);
+        tile_sort_depth_one<CAP, NB>((int)big[1 + i], offsets, entries, lo_exclusive, row_keys, flags);
         __syncthreads();
     }
 }
@@ -620,38 +650,40 @@ __global__ void __launch_bounds__(256) k_tile_sort_depth(const uint32_t* __restr
 template <int CAP, int NB>
 __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ entries, int lo_exclusive,
-                                                    const uint64_t* __restrict__ row_keys) {
+                                                    const uint64_t* __restrict__ row_keys,
+                                                    uint8_t* __restrict__ flags) {
     extern __shared__ __align__(16) unsigned char ts_smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(ts_smem);           // CAP
     uint32_t* rows = reinterpret_cast<uint32_t*>(keys + CAP);       // CAP
     uint16_t* order = reinterpret_cast<uint16_t*>(rows + CAP);      // CAP: entry indices grouped by bucket
     __shared__ uint32_t start[NB + 1];
     __shared__ uint32_t cursor[NB];
-    __shared__ unsigned long long s_min, s_max;
+    __shared__ unsigned long long w_min[8], w_max[8];  // per warp (256 threads)
     const uint32_t beg = offsets[t], end = offsets[t + 1];
     const int n = (int)(end - beg);
     if (n <= lo_exclusive || n > CAP) return;
     uint32_t* e = entries + beg;
-    if (threadIdx.x == 0) {
-        s_min = ~0ull;
-        s_max = 0ull;
-    }
     for (int b = threadIdx.x; b < NB; b += blockDim.x) cursor[b] = 0;
-    // rows (coalesced), then their keys (L2 gathers, 8 in flight per thread)
-    for (int i = threadIdx.x; i < n; i += blockDim.x) rows[i] = e[i];
-    __syncthreads();
+    // rows (coalesced) and their keys (L2 gathers), 8 in flight per thread
     unsigned long long mn = ~0ull, mx = 0ull;
     for (int i0 = threadIdx.x; i0 < n; i0 += 8 * blockDim.x) {
+        uint32_t r[8];
         uint64_t k[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int i = i0 + u * blockDim.x;
-            k[u] = i < n ? __ldg(row_keys + rows[i]) : 0ull;
+            r[u] = i < n ? e[i] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            k[u] = i < n ? __ldg(row_keys + (r[u] & kEntryRowMask)) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int i = i0 + u * blockDim.x;
             if (i < n) {
+                rows[i] = r[u];
                 keys[i] = k[u];
                 mn = min(mn, (unsigned long long)k[u]);
                 mx = max(mx, (unsigned long long)k[u]);
@@ -664,12 +696,17 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
         mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
     if ((threadIdx.x & 31) == 0) {
-        atomicMin(&s_min, mn);
-        atomicMax(&s_max, mx);
+        w_min[threadIdx.x >> 5] = mn;
+        w_max[threadIdx.x >> 5] = mx;
     }
     __syncthreads();
-    const uint64_t kmin = s_min;
-    const double bscale = (double)NB / ((double)(s_max - kmin) + 1.0);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        mn = min(mn, w_min[w]);
+        mx = max(mx, w_max[w]);
+    }
+    const uint64_t kmin = mn;
+    const double bscale = (double)NB / ((double)(mx - kmin) + 1.0);
     auto bucket_of = [&](uint64_t k) { return min(NB - 1, (int)((double)(k - kmin) * bscale)); };
     for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cursor[bucket_of(keys[i])], 1u);
     __syncthreads();
@@ -701,18 +738,20 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
     // final position = bucket start + the members of the bucket that order
     // before the entry on (key, row): independent per entry (no serial chain);
     // the rows are in shared memory, so the list is overwritten in place
+    // (rows compare without their half-tile flags; the flags go to their own array)
     for (int p = threadIdx.x; p < n; p += blockDim.x) {
         const int i = order[p];
         const uint64_t ki = keys[i];
-        const uint32_t ri = rows[i];
+        const uint32_t ri = rows[i] & kEntryRowMask;
         const int b = bucket_of(ki);
         const int q0 = (int)start[b], q1 = (int)start[b + 1];
         int r = q0;
         for (int q = q0; q < q1; ++q) {
             const int j = order[q];
-            r += key_row_less(keys[j], rows[j], ki, ri) ? 1 : 0;
+            r += key_row_less(keys[j], rows[j] & kEntryRowMask, ki, ri) ? 1 : 0;
         }
         e[r] = ri;
+        flags[beg + r] = (uint8_t)(rows[i] >> kEntryFlagShift);
     }
 }
 
@@ -720,24 +759,27 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
 // global scratch, first on the row bits, then on the 64 key bits.
 __device__ __noinline__ void tile_sort_depth_split(int t, const uint32_t* __restrict__ offsets,
                                                    uint32_t* __restrict__ entries, uint32_t* __restrict__ scratch,
-                                                   int lo_exclusive, const uint64_t* __restrict__ row_keys);
+                                                   int lo_exclusive, const uint64_t* __restrict__ row_keys,
+                                                   uint8_t* __restrict__ flags);
 __global__ void __launch_bounds__(256) k_tile_sort_depth_large(const uint32_t* __restrict__ offsets,
                                                                uint32_t* __restrict__ entries,
                                                                uint32_t* __restrict__ scratch, int lo_exclusive,
                                                                const int64_t* __restrict__ stats,
                                                                const uint64_t* __restrict__ row_keys,
-                                                               const uint32_t* __restrict__ big) {
+                                                               const uint32_t* __restrict__ big,
+                                                               uint8_t* __restrict__ flags) {
     if (stats[SF_STAT_OVERFLOW]) return;
     const int nb = (int)big[0];
     for (int i = blockIdx.x; i < nb; i += gridDim.x) {
-        tile_sort_depth_split((int)big[1 + i], offsets, entries, scratch, lo_exclusive, row_keys);
+        tile_sort_depth_split((int)big[1 + i], offsets, entries, scratch, lo_exclusive, row_keys, flags);
         __syncthreads();
     }
 }
 
 __device__ __noinline__ void tile_sort_depth_split(int t, const uint32_t* __restrict__ offsets,
                                                    uint32_t* __restrict__ entries, uint32_t* __restrict__ scratch,
-                                                   int lo_exclusive, const uint64_t* __restrict__ row_keys) {
+                                                   int lo_exclusive, const uint64_t* __restrict__ row_keys,
+                                                   uint8_t* __restrict__ flags) {
     typedef cub::BlockScan<int, 256> Scan;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ int s_zero;
@@ -747,7 +789,7 @@ __device__ __noinline__ void tile_sort_depth_split(int t, const uint32_t* __rest
     uint32_t* src = entries + beg;
     uint32_t* dst = scratch + beg;
     uint32_t rmax = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) rmax = max(rmax, src[i]);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) rmax = max(rmax, src[i] & kEntryRowMask);
     rmax = __reduce_max_sync(0xffffffffu, rmax);
     __shared__ uint32_t s_rmax;
     if (threadIdx.x == 0) s_rmax = 0;
@@ -758,6 +800,7 @@ __device__ __noinline__ void tile_sort_depth_split(int t, const uint32_t* __rest
     while (row_bits < 32 && (s_rmax >> row_bits)) ++row_bits;
     for (int pass = 0; pass < row_bits + 64; ++pass) {
         auto bit_of = [&](uint32_t r) -> uint32_t {
+            r &= kEntryRowMask;
             return pass < row_bits ? (r >> pass) & 1u : (uint32_t)(__ldg(row_keys + r) >> (pass - row_bits)) & 1u;
         };
         int z = 0;
@@ -784,13 +827,17 @@ __device__ __noinline__ void tile_sort_depth_split(int t, const uint32_t* __rest
         dst = tt;
         __syncthreads();
     }
-    // row_bits + 64 passes: the result is in the entries when the count is even
-    if (src != entries + beg)
-        for (int i = threadIdx.x; i < n; i += blockDim.x) entries[beg + i] = src[i];
+    // plain rows to the entries, half-tile flags to their array
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t v = src[i];
+        flags[beg + i] = (uint8_t)(v >> kEntryFlagShift);
+        entries[beg + i] = v & kEntryRowMask;
+    }
 }
 
-void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint64_t* row_keys, int W,
-                    int H, int64_t pair_capacity, uint32_t* tile_counts, uint32_t* tile_offsets, uint32_t* tile_cursor,
+void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint64_t* row_keys,
+                    uint8_t* entry_flags, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
+                    uint32_t* tile_offsets, uint32_t* tile_cursor,
                     uint32_t* entries, uint32_t* sort_scratch, BinAux* aux, uint32_t* cta_base, int tile_row0,
                     int tile_row1, cudaStream_t st) {
     TileGrid g{W, H, (W + SF_TILE - 1) / SF_TILE, (H + SF_TILE - 1) / SF_TILE, 0, 0};
@@ -822,14 +869,15 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
         ensure_smem_attr((const void*)k_tile_sort_depth<4096, 1024>, s1);
         ensure_smem_attr((const void*)k_tile_sort_depth<8192, 2048>, s2);
         // one CTA per tile for the common lists; the rare longer ones by a
-        // one-wave grid striding over the tiles (CTAs skip other sizes)
+        // one-wave grid striding over the tiles k_tile_scan listed
         const int sms = device_sm_count();
         static_assert(kShortList == 4096, "short-list capacity");
-        k_tile_sort_depth<4096, 1024><<<n_tiles, 256, s1, st>>>(tile_offsets, entries, 0, stats, row_keys, nullptr);
+        k_tile_sort_depth<4096, 1024><<<n_tiles, 256, s1, st>>>(tile_offsets, entries, 0, stats, row_keys, nullptr,
+                                                                 entry_flags);
         k_tile_sort_depth<8192, 2048><<<std::min(n_tiles, sms), 256, s2, st>>>(tile_offsets, entries, 4096, stats,
-                                                                              row_keys, big);
+                                                                              row_keys, big, entry_flags);
         k_tile_sort_depth_large<<<std::min(n_tiles, sms), 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192,
-                                                                        stats, row_keys, big);
+                                                                        stats, row_keys, big, entry_flags);
         return;
     }
     // sf_bin mode: unique ranks; most lists fit the shared-memory bucket sort

@@ -94,6 +94,7 @@ struct FrameWs {
     uint32_t* tile_offsets;
     uint32_t* tile_cursor;
     uint32_t* entries;
+    uint8_t* entry_flags;  // per entry: half-tile flags (bit 0 top, bit 1 bottom half)
     uint32_t* scratch;
     double* proj_cb;
     double* filter_tmp;
@@ -138,6 +139,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->tile_offsets = c.take<uint32_t>(n_tiles + 1);
     ws->tile_cursor = c.take<uint32_t>(2 * n_tiles + 1);  // + the long-list tile list (launch_binning)
     ws->entries = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
+    ws->entry_flags = c.take<uint8_t>(pair_cap > 0 ? pair_cap : 1);
     ws->scratch = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
     ws->proj_cb = c.take<double>((size_t)n_levels * L * (1 + kMaxCanon));
     ws->filter_tmp = c.take<double>((size_t)n_levels * W * H);
@@ -160,7 +162,7 @@ static int validate_scene_cam(const SfScene* s, const SfCamera* cam) {
     if (cam->width < 1 || cam->height < 1) return fail(SF_ERR_VALIDATION, "image size must be >= 1 pixel");
     if (!(cam->fx > 0) || !(cam->fy > 0)) return fail(SF_ERR_VALIDATION, "focal lengths must be > 0");
     if (!(cam->near_plane > 0)) return fail(SF_ERR_VALIDATION, "near plane must be > 0");
-    if (s->num_gaussians < 0 || s->num_gaussians >= (int64_t)1 << 31)
+    if (s->num_gaussians < 0 || s->num_gaussians >= (int64_t)1 << kEntryFlagShift)
         return fail(SF_ERR_VALIDATION, "num_gaussians out of range");
     return SF_OK;
 }
@@ -241,7 +243,7 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
     }
     // K2-K4: per-tile lists of scene rows in (depth, id) order -- the depth
     // order is established per tile (k_tile_sort_depth), not globally
-    launch_binning(G, ws.stats, ws.geom, ws.keys_in, W, H, f->pair_capacity, ws.tile_counts,
+    launch_binning(G, ws.stats, ws.geom, ws.keys_in, ws.entry_flags, W, H, f->pair_capacity, ws.tile_counts,
                    ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, ws.cta_base, tr0, tr1, st_prep);
     if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
                                    ws.proj_cb, st_prep);
@@ -278,6 +280,7 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
     a.early_exit = f->early_exit;
     a.tile_offsets = ws.tile_offsets;
     a.entries = ws.entries;
+    a.entry_flags = ws.entry_flags;
     a.geom = ws.geom;
     a.chan = chan;
     a.fixup_count = ws.fixup;
@@ -640,7 +643,7 @@ extern "C" int sf_bin(int64_t n, const double* means2d, const double* inv_covs, 
         depth_sort(w.k0, w.k1, w.v1, w.v0, n, w.cub_tmp, w.cub_bytes, st);
     }
     k_bin_finish<<<blocks, 256, 0, st>>>(n, w.v0, w.proj, w.geom, order, w.stats);
-    launch_binning(n, w.stats, w.geom, nullptr, W, H, pair_cap, w.counts, w.offsets, w.cursor,
+    launch_binning(n, w.stats, w.geom, nullptr, nullptr, W, H, pair_cap, w.counts, w.offsets, w.cursor,
                    (uint32_t*)tile_entries, w.scratch, w.aux, w.cta_base, 0, 0, st);
     k_offsets_to_i64<<<ceil_div(n_tiles + 1, 256), 256, 0, st>>>(n_tiles, w.offsets, tile_offsets);
     if (stats_i64) cudaMemcpyAsync(stats_i64, w.stats, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);

@@ -233,6 +233,12 @@ int depth_sort(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_
                size_t tmp_bytes, cudaStream_t st);
 // per-row scatter plan (channel ids + values) of the selected levels
 void launch_pack_channels(const SfScene& s, const LevelSelDev& levels, unsigned char* chan, cudaStream_t st);
+// Frame-mode tile entries leave the emit pass as row | half-tile flags << 30
+// (bit 30: the top 16x8 half may see the Gaussian, bit 31: the bottom half);
+// the per-tile sort moves the flags to a byte array parallel to the entries,
+// so every consumer of the sorted lists reads plain rows.
+constexpr int kEntryFlagShift = 30;
+constexpr uint32_t kEntryRowMask = (1u << kEntryFlagShift) - 1u;
 // Binning over n_items geometry records.  row_keys == null (sf_bin): record
 // i has canonical rank i (i < stats[VISIBLE]) and the lists hold ranks.
 // row_keys != null (frame): record i is scene row i, culled iff row_keys[i]
@@ -244,8 +250,8 @@ struct __align__(16) BinAux {
     uint16_t tx0, ty0, w, h;     // candidate rectangle
     uint32_t pos[kBinSlots];     // in-tile position of the first kBinSlots hits
 };
-void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint64_t* row_keys, int W,
-                    int H, int64_t pair_capacity, uint32_t* tile_counts,
+void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, const uint64_t* row_keys,
+                    uint8_t* entry_flags, int W, int H, int64_t pair_capacity, uint32_t* tile_counts,
                     uint32_t* tile_offsets, uint32_t* tile_cursor, uint32_t* entries, uint32_t* sort_scratch,
                     BinAux* aux, uint32_t* cta_base, int tile_row0, int tile_row1, cudaStream_t st);
 // per-(count CTA, tile) range bases of the aggregated count pass
@@ -260,6 +266,7 @@ struct BlendArgs {
     int early_exit;
     const uint32_t* tile_offsets;
     const uint32_t* entries;
+    const uint8_t* entry_flags;  // frame lists: half-tile flags per entry (launch_binning), or null
     const GeomRec* geom;
     const unsigned char* chan;
     const int64_t* stats;  // overflow flag gate

@@ -85,7 +85,7 @@ struct __align__(1024) Smem {
     GeomF32 g[kStages][kBatch];
     uint32_t row[kStages][kBatch];
     double pd[kMaxCh * 4];  // fused relevancy: Pd_j = P_q - P_cj per (level, l)
-    uint32_t ering[8][kBatch];          // producer: tile-list entries, 5 batches ahead
+    uint32_t ering[8][kBatch];          // producer: the half tile's filtered entries, 3 batches ahead
     unsigned char cring[3][kBatch][96]; // producer: the entries' sparse codes (plan records), 2 batches ahead
     float guard[kBlendWarps][kBatch];   // per blend warp: its batch entries' patch guard bands
     float alpha[4][2][16 * 32];         // per blend warp (quarter, hb): alphas of its <= 16 candidates x 32 pixels
@@ -95,6 +95,7 @@ struct __align__(1024) Smem {
     uint32_t contrib[2];   // per W slot: bit w = blend warp w's pixels got a contribution
     uint32_t dq_info[2];   // MMA -> drains, per tile in order: contrib of the tile
     uint32_t ev_tag[kStages];  // batch sequence number + 1 when some blend warp had a candidate in it
+    uint32_t ev_union[kStages];  // profiling variant: entries of the batch that are some warp's candidate
     uint32_t tile_tag[2];      // per W slot: tile iteration + 1 when some batch of the tile had a candidate
     uint64_t rec_full[kStages], ev_full[kStages], ev_empty[kStages];
     uint64_t w_full[2], a_ready[2], slot_free[2];
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
         for (int i = 0; i < kBStages; ++i) bar_init(&S.b_full[i], 1);
         S.done_count = 0;
         S.contrib[0] = S.contrib[1] = 0u;
-        for (int i = 0; i < kStages; ++i) S.ev_tag[i] = 0u;
+        for (int i = 0; i < kStages; ++i) S.ev_tag[i] = S.ev_union[i] = 0u;
         S.tile_tag[0] = S.tile_tag[1] = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -262,21 +263,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
 
     if (warp == kProdWarp) {
         // ---------------- producer: records -> ring, sparse codes -> V^T ----------------
-        // A cp.async software pipeline (no load latency in the loop): the tile
-        // list's entries are issued 5 batches ahead (ering), the entries' sparse
+        // The half tile's entries: the tile list filtered by the half-tile
+        // flags (launch_binning: an entry without its half's flag has alpha = 0
+        // at every pixel of the half) and compacted into ering, kept 3 batches
+        // ahead; raw chunks of 32 entries are loaded two chunks ahead in
+        // registers.  A cp.async pipeline for the rest: the entries' sparse
         // codes 2 batches ahead (cring), the geometry records of batch bi with
         // the stage's rec_full barrier.  Commit group G_bi = everything issued
         // in iteration bi; wait_group 2 at its end lands G_{bi-2}: batch bi's
-        // codes, and the entries of batch bi + 3 that iteration bi + 1 reads.
+        // codes.
         const int C = A.C;
         const int cs = chan_rec_bytes(C), voff = chan_val_offset(C);
         const int cq = cs / 16;
         const uint32_t vh0 = smem_addr(&S.vhi[0][0]), vl0 = smem_addr(&S.vlo[0][0]);
         // channel ids (u8) this lane wrote into the stage used 1, 2, 3 batches ago
         uint32_t old0[3] = {~0u, ~0u, ~0u}, old1[3] = {~0u, ~0u, ~0u}, old2[3] = {~0u, ~0u, ~0u};
-        auto cp4 = [&](void* dst, const void* src) {
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-        };
         auto load_codes = [&](int slot3, uint32_t row) {
             const unsigned char* src = A.chan + (size_t)row * cs;
             unsigned char* dst = &S.cring[slot3][lane][0];
@@ -297,15 +298,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     if (b2 < A.tile_offsets[t2 + 1]) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.entries + b2));
                 }
             }
-            // prologue: entries of batches 0..4, then the codes of batches 0, 1
-#pragma unroll
-            for (int k = 0; k < 5; ++k)
-                if (beg + 32u * k + lane < end) cp4(&S.ering[k][lane], A.entries + beg + 32u * k + lane);
-            cp_async_commit();
-            cp_async_wait<0>();
+            // filtered entry stream of this half tile
+            const uint32_t hbit = 1u << (ht & 1);
+            uint32_t rp = beg, nf = 0;  // next raw index, filtered entries so far
+            uint32_t r0, f0, r1, f1;    // raw chunks at rp and rp + 32 (row, flags)
+            auto load_raw = [&](uint32_t i, uint32_t& row, uint32_t& fl) {
+                row = 0u;
+                fl = 0u;
+                if (i < end) {
+                    row = __ldg(A.entries + i);
+                    fl = A.entry_flags ? (uint32_t)__ldg(A.entry_flags + i) : 3u;
+                }
+            };
+            load_raw(beg + lane, r0, f0);
+            load_raw(beg + 32u + lane, r1, f1);
+            auto fill = [&](uint32_t target) {
+                while (nf < target && rp < end) {
+                    uint32_t r2, f2;
+                    load_raw(rp + 64u + lane, r2, f2);
+                    if (lane == 0 && rp + 256u < end) {
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.entries + rp + 256u));
+                        if (A.entry_flags) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.entry_flags + rp + 256u));
+                    }
+                    const bool keep = rp + lane < end && (f0 & hbit) != 0u;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+                    if (keep) {
+                        const uint32_t q = nf + (uint32_t)__popc(bal & ((1u << lane) - 1u));
+                        S.ering[(q >> 5) & 7][q & 31] = r0;
+                    }
+                    nf += (uint32_t)__popc(bal);
+                    rp += 32u;
+                    r0 = r1, f0 = f1, r1 = r2, f1 = f2;
+                }
+                __syncwarp();
+            };
+            // prologue: filtered entries of batches 0..2, then the codes of batches 0, 1
+            fill(3u * kBatch);
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
-                if (beg + 32u * k + lane < end) {
+                if (32u * k + lane < nf) {
                     const uint32_t r = S.ering[k][lane];
                     load_codes(k, r);
                     prefetch_records(A, r, cs);
@@ -314,10 +345,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             }
             for (int bi = 0;; ++bi) {
                 const int s = bs % kStages;
-                const uint32_t base = beg + (uint32_t)bi * kBatch;
+                const uint32_t base = (uint32_t)bi * kBatch;  // in the filtered stream
                 if (bs >= kStages) SF_TIMED(w0, bar_wait(&S.ev_empty[s], ((bs / kStages) - 1) & 1));
                 const bool all_done = *reinterpret_cast<volatile int*>(&S.done_count) == kBlendWarps * (it + 1);
-                const int nb = (base < end && !all_done) ? (int)min((uint32_t)kBatch, end - base) : 0;
+                if (!all_done) fill(base + 3u * kBatch);  // batches bi .. bi + 2 (fewer at the list's end)
+                const int nb = (base < nf && !all_done) ? (int)min((uint32_t)kBatch, nf - base) : 0;
                 const uint32_t row = S.ering[bi & 7][lane];
                 if (lane < nb) {
                     cp_async16(&S.g[s][lane], A.geom + row);
@@ -328,13 +360,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                              : "memory");
                 if (lane == 0) S.nb[s] = nb;
                 if (prof && nb) ++w1;
+                if (prof) w2 += (uint64_t)nb;  // entries streamed
                 __syncwarp();
                 if (lane == 0) bar_arrive(&S.rec_full[s]);
                 if (nb == kBatch) {
-                    // entries of batch bi + 5 (slot of batch bi - 3, consumed); codes of batch bi + 2
-                    if (base + 5u * kBatch + lane < end)
-                        cp4(&S.ering[(bi + 5) & 7][lane], A.entries + base + 5u * kBatch + lane);
-                    if (base + 2u * kBatch + lane < end) {
+                    // codes of batch bi + 2
+                    if (base + 2u * kBatch + lane < nf) {
                         const uint32_t r2 = S.ering[(bi + 2) & 7][lane];
                         load_codes((bi + 2) % 3, r2);
                         prefetch_records(A, r2, cs);
@@ -568,6 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 ++nbatches;
                 // batches without a candidate in any warp have E = 0: the issuer skips them
                 if (wmask && lane == 0) S.ev_tag[s] = (uint32_t)bs + 1u;
+                if (prof && wmask && lane == 0) atomicOr(&S.ev_union[s], wmask << (16 * hb));
                 tile_hit |= wmask != 0u;
                 proxy_fence();
                 __syncwarp();
@@ -833,10 +865,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     bar_arrive(&S.ev_empty[s]);
                     break;
                 }
+                if (prof) {
+                    w2 += (uint64_t)__popc(*reinterpret_cast<volatile uint32_t*>(&S.ev_union[s]));
+                    S.ev_union[s] = 0u;
+                }
                 if (*reinterpret_cast<volatile uint32_t*>(&S.ev_tag[s]) != (uint32_t)(be - 1) + 1u) {
                     // no blend warp had a candidate: E = 0, nothing to add
                     bar_arrive(&S.ev_empty[s]);
-                    if (prof) ++w2;
                     continue;
                 }
                 tc_after();

@@ -46,7 +46,7 @@ def run(G, W, H, timeout=float(os.environ.get("STRESS_TIMEOUT", "60"))):
     eng = ds.engine
     eng.pair_capacity = max(eng.pair_capacity, 48 * G)
     levels = (0, 1, 2)
-    out = eng.allocate(W, H, levels, coeff_map=False, features=True, query=True)
+    out = eng.allocate(W, H, levels, coeff_map=False, features=not os.environ.get("STRESS_NOFEAT"), query=True)
     spec = QuerySpec(qv, canon, 11, -1, 0.5)
     torch.cuda.synchronize()
     prog.zero_()
@@ -67,7 +67,8 @@ def run(G, W, H, timeout=float(os.environ.get("STRESS_TIMEOUT", "60"))):
     st = out.stats_i64.cpu().numpy()
     print(f"ok G={G} {W}x{H} in {time.time() - t0:.2f}s pairs={st[1]} fixups={st[7]} level={st[3]}", flush=True)
     f = out.features
-    print("  features finite:", bool(torch.isfinite(f).all().item()), "max", f.abs().max().item(), flush=True)
+    if f is not None:
+        print("  features finite:", bool(torch.isfinite(f).all().item()), "max", f.abs().max().item(), flush=True)
     if not os.environ.get("STRESS_NOPROG"):
         prof_report(min(148, 2 * ((W + 15) // 16) * ((H + 15) // 16)))
         timeline_report()
@@ -85,6 +86,12 @@ def timeline_report():
     for i in list(range(min(n, 6))) + list(range(max(6, n - 3), n)):
         print(f"  {i:4d} " + " ".join(f"{(t[i, e] - t0) / 1965.0:11.2f}" if t[i, e] else f"{'-':>11s}" for e in range(11)))
     if n > 10:
+        blend = (t[:n, 1] - t[:n, 0]) / 1965.0
+        epi = (t[:n, 2] - t[:n, 1]) / 1965.0
+        dec = [(t[i, 5] - t[i, 4]) / 1965.0 for i in range(n) if t[i, 5] and t[i, 4]]
+        print(f"  per tile (us): blend mean {blend.mean():.2f} median {np.median(blend):.2f} max {blend.max():.2f}; "
+              f"blend_end->epi_done mean {epi.mean():.2f}; decode issue span mean {np.mean(dec) if dec else 0:.2f} "
+              f"over {len(dec)} non-empty tiles of {n}")
         d = np.diff(t[:n, :11], axis=0) / 1965.0
         print("  mean per-tile period (us): " + " ".join(f"{x[:6]}={v:.2f}" for x, v in zip(names, d.mean(axis=0))))
 
@@ -114,7 +121,7 @@ def prof_report(n_cta):
     # 4 counters per warp (slot 4 * warp): blend warps 0-7, drains 8-11, producer 12, E V issuer 13, decode issuer 14
     names = {0: "blend", 32: "drain", 48: "producer", 52: "ev_issuer", 56: "dec_issuer"}
     labels = {"blend": ("waits", "alpha", "walk"), "drain": ("dq_full", "acc_full", "bulk_read(lane0)"),
-              "producer": ("ev_empty", "batches", "-"), "ev_issuer": ("ev_full", "slot_free", "skipped_batches"),
+              "producer": ("ev_empty", "batches", "entries"), "ev_issuer": ("ev_full", "slot_free", "candidate_entries"),
               "dec_issuer": ("a_ready/dq", "b_full", "acc_empty")}
     for base, nm in names.items():
         warps = 8 if base == 0 else (4 if base == 32 else 1)
@@ -125,7 +132,9 @@ def prof_report(n_cta):
             lab = labels[nm][k]
             if lab == "-":
                 continue
-            if lab == "batches":
+            if lab in ("entries", "candidate_entries"):
+                print(f"  {lab} {v.mean():.0f}/CTA", end="")
+            elif lab == "batches":
                 print(f"  batches {v.mean():.0f}/CTA", end="")
             elif lab == "skipped_batches":
                 print(f"  skipped batches {v.mean():.0f}/CTA", end="")
