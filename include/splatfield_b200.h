@@ -119,6 +119,11 @@ typedef struct SfFrame {
      * level -- and nothing after it. */
     const float* grad_coeff_map;
     float* grad_values;
+    /* 1: blend with the projection and tile lists the previous frame of this
+     * workspace built (same scene, camera, image and shape; no SfQuery; a
+     * chan_by_row plan is required) -- render_dense's channel passes and the
+     * training backward reuse the forward frame's binning.  0: full frame. */
+    int32_t reuse_lists;
 } SfFrame;
 
 /* stats_i64 slots */
@@ -308,7 +313,7 @@ int sf_lsv2_unpack(const void* records, int64_t num_gaussians, int32_t num_level
                    float* positions, float* rotations, float* scales, float* opacities, float* colors,
                    uint16_t* coeff_indices, float* coeff_values, uint32_t* flags, void* stream);
 
-int sf_abi_version(void); /* 2: SfFrame band fields; 3: fused decode (coeff_map optional with features) */
+int sf_abi_version(void); /* 2: SfFrame band fields; 3: fused decode (coeff_map optional with features); 4: SfFrame.reuse_lists, training entry points */
 
 /* 1 if sf_render_frame decodes features inside the blend kernel for this
  * shape (then SfFrame.coeff_map may be NULL when features are requested);

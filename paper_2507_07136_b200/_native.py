@@ -49,7 +49,7 @@ class SfFrame(ctypes.Structure):
                 ("coeff_map", P), ("final_t", P), ("features", P), ("relevancy_raw", P),
                 ("relevancy_filtered", P), ("mask", P), ("stats_i64", P), ("stats_f64", P),
                 ("events", P * 5), ("chan_by_row", P), ("band_y0", i32), ("band_y1", i32),
-                ("dec_image", P), ("grad_coeff_map", P), ("grad_values", P)]
+                ("dec_image", P), ("grad_coeff_map", P), ("grad_values", P), ("reuse_lists", i32)]
 
 
 EXPORTS = {

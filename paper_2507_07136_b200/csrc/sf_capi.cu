@@ -55,7 +55,7 @@ extern "C" float sf_event_elapsed_ms(void* a, void* b) {
     if (cudaEventElapsedTime(&ms, (cudaEvent_t)a, (cudaEvent_t)b) != cudaSuccess) return -1.f;
     return ms;
 }
-extern "C" int sf_abi_version(void) { return 3; }
+extern "C" int sf_abi_version(void) { return 4; }
 
 extern "C" int sf_decode_fused(int32_t n_levels, int32_t L, int32_t K, int32_t D) {
     return blend_dec_supported(n_levels, L, K, D) ? 1 : 0;
@@ -229,22 +229,29 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
 
     const int64_t G = s->num_gaussians;
     if (f->events[0]) cudaEventRecord((cudaEvent_t)f->events[0], st_prep);
-    cudaMemsetAsync(ws.stats, 0, 16 * sizeof(int64_t), st_prep);
-    cudaMemsetAsync(ws.stats_f, 0, (8 + 2 * kMaxLevels) * sizeof(double), st_prep);
-    cudaMemsetAsync(ws.fixup, 0, sizeof(uint32_t), st_prep);
-    // K1
-    launch_preprocess(*s, *cam, ws.geom, ws.keys_in, ws.vals_in, ws.stats, st_prep);
-    // per-row scatter plan: a scene constant for a level selection, so callers
-    // may pass a cached copy (sf_pack_channels)
-    const unsigned char* chan = f->chan_by_row;
-    if (!chan) {
-        launch_pack_channels(*s, lv, ws.chan, st_prep);
-        chan = ws.chan;
+    if (f->reuse_lists && q) return fail(SF_ERR_VALIDATION, "reuse_lists is for frames without a query");
+    if (!f->reuse_lists) {
+        cudaMemsetAsync(ws.stats, 0, 16 * sizeof(int64_t), st_prep);
+        cudaMemsetAsync(ws.stats_f, 0, (8 + 2 * kMaxLevels) * sizeof(double), st_prep);
     }
-    // K2-K4: per-tile lists of scene rows in (depth, id) order -- the depth
-    // order is established per tile (k_tile_sort_depth), not globally
-    launch_binning(G, ws.stats, ws.geom, ws.keys_in, ws.entry_flags, W, H, f->pair_capacity, ws.tile_counts,
-                   ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, ws.cta_base, tr0, tr1, st_prep);
+    cudaMemsetAsync(ws.fixup, 0, sizeof(uint32_t), st_prep);
+    const unsigned char* chan = f->chan_by_row;
+    if (!chan && f->reuse_lists) return fail(SF_ERR_VALIDATION, "reuse_lists needs a scatter plan (chan_by_row)");
+    if (!f->reuse_lists) {
+        // K1
+        launch_preprocess(*s, *cam, ws.geom, ws.keys_in, ws.vals_in, ws.stats, st_prep);
+        // per-row scatter plan: a scene constant for a level selection, so callers
+        // may pass a cached copy (sf_pack_channels)
+        if (!chan) {
+            launch_pack_channels(*s, lv, ws.chan, st_prep);
+            chan = ws.chan;
+        }
+        // K2-K4: per-tile lists of scene rows in (depth, id) order -- the depth
+        // order is established per tile (k_tile_sort_depth), not globally
+        launch_binning(G, ws.stats, ws.geom, ws.keys_in, ws.entry_flags, W, H, f->pair_capacity, ws.tile_counts,
+                       ws.tile_offsets, ws.tile_cursor, ws.entries, ws.scratch, ws.aux, ws.cta_base, tr0, tr1,
+                       st_prep);
+    }
     if (q) launch_project_codebook(s->codebooks, lv, L, D, q->vector, q->canonicals, q->n_canonicals,
                                    ws.proj_cb, st_prep);
     if (f->grad_coeff_map) {

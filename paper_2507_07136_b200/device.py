@@ -136,14 +136,44 @@ _scene_cache: dict = {}
 _cache_lock = threading.Lock()
 
 
+_SCENE_ARRAYS = ("positions", "rotations", "scales", "opacities", "colors", "coeff_indices", "coeff_values", "ids")
+
+
+def _fingerprint(scene) -> tuple:
+    """Identity of a scene's arrays and codebooks (object, data pointer, shape,
+    dtype): reassigning any of them re-uploads.  In-place edits keep the
+    identity -- call ``invalidate(scene)`` after those (the reference treats
+    scenes as immutable; so does the serving path).  ~10 us per call."""
+    parts = []
+    for name in _SCENE_ARRAYS:
+        a = getattr(scene, name, None)
+        if isinstance(a, np.ndarray):
+            parts.append((name, id(a), a.__array_interface__["data"][0], a.shape, a.dtype.str))
+        else:
+            parts.append((name, id(a)))
+    cbs = tuple(getattr(scene, "codebooks", ()))
+    for cb in cbs:
+        a = cb.atoms
+        parts.append((id(cb), id(a), a.__array_interface__["data"][0] if isinstance(a, np.ndarray) else 0))
+    return tuple(parts) + ((len(cbs), id(scene.config)),)
+
+
+def invalidate(scene) -> None:
+    """Drop the cached device copy of ``scene`` (after editing its arrays in place)."""
+    with _cache_lock:
+        _scene_cache.pop(id(scene), None)
+
+
 def device_scene(scene) -> DeviceScene:
-    """Upload ``scene`` once and return its cached device copy."""
+    """Upload ``scene`` once and return its cached device copy (re-uploaded
+    when the scene's arrays or codebooks changed, see ``_fingerprint``)."""
     if isinstance(scene, DeviceScene):
         return scene
     key = id(scene)
+    fp = _fingerprint(scene)
     with _cache_lock:
         hit = _scene_cache.get(key)
-        if hit is not None and hit[0]() is scene:
+        if hit is not None and hit[0]() is scene and hit[2] == fp:
             return hit[1]
     ds = DeviceScene(scene)
     with _cache_lock:
@@ -151,7 +181,7 @@ def device_scene(scene) -> DeviceScene:
             ref = weakref.ref(scene, lambda _r, k=key: _scene_cache.pop(k, None))
         except TypeError:  # not weak-referenceable: cache without eviction hook
             ref = (lambda s=scene: s)
-        _scene_cache[key] = (ref, ds)
+        _scene_cache[key] = (ref, ds, fp)
     return ds
 
 
@@ -212,7 +242,9 @@ class FrameEngine:
         self.pair_capacity = max(1 << 16, 6 * g)
         self._ws = None
         self._ws_key = None
-        self._lock = threading.Lock()
+        # re-entrant: render_dense holds it across its channel passes, which
+        # reuse the first pass's tile lists (SfFrame.reuse_lists)
+        self._lock = threading.RLock()
         self._events = None
         self._handoff = None
         self._plans = {}
@@ -284,7 +316,7 @@ class FrameEngine:
 
     def enqueue(self, cam, levels, out: FrameOutputs, *, query: QuerySpec | None = None,
                 early_exit: bool = True, qdev=None, timing: bool = False, band=None, prep_stream=None,
-                dense=None):
+                dense=None, reuse_lists: bool = False):
         """Launch one frame on the current stream (no host synchronisation).
 
         ``band=(y0, y1)``: tile-band mode -- only pixel rows [y0, y1) are owned
@@ -292,7 +324,9 @@ class FrameEngine:
         ``prep_stream``: run projection / sort / binning there instead
         (sf_render_frame_split); the rest stays on the current stream.
         ``dense=(plan, C)``: blend C <= 16 dense channels per Gaussian from a
-        ready scatter plan (render_dense) instead of the scene's coefficients."""
+        ready scatter plan (render_dense) instead of the scene's coefficients.
+        ``reuse_lists``: skip projection and binning and blend with the lists
+        the previous frame of this workspace built (same camera and shape)."""
         cfg = self.ds.config
         camc = camera_struct(cam)
         W, H = camc.width, camc.height
@@ -321,6 +355,7 @@ class FrameEngine:
         fr.stats_f64 = N.ptr(out.stats_f64)
         if band is not None:
             fr.band_y0, fr.band_y1 = int(band[0]), int(band[1])
+        fr.reuse_lists = 1 if reuse_lists else 0
         if dense is not None:
             fr.chan_by_row = N.ptr(dense[0])
         elif len(levels) * cfg.K <= 16:

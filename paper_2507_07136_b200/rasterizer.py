@@ -129,21 +129,26 @@ def render_dense(scene, cam, channels="color", *, tag: str | None = None,
     vals = values if (ds.orig_rows is None or device_rows) else values[ds.orig_rows.cpu().numpy()]
     vals = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float32)).to(dev)
     out = torch.zeros((H, W, c), dtype=torch.float32, device=dev)
-    final_t = torch.ones((H, W), dtype=torch.float32, device=dev)
-    pairs = 0
-    for c0 in range(0, c, DENSE_CHANNELS_PER_PASS):
-        cc = min(DENSE_CHANNELS_PER_PASS, c - c0)
-        half = (4 * cc + 15) // 16 * 4  # words per record half (chan_val_offset / 4)
-        plan = torch.zeros((max(g, 1), 2 * half), dtype=torch.int32, device=dev)
-        plan[:, :cc] = torch.arange(cc, dtype=torch.int32, device=dev) * 516  # accumulator byte offsets
-        if g:
-            plan[:g, half:half + cc] = vals[:, c0:c0 + cc].contiguous().view(torch.int32)
-        fo = eng.allocate(W, H, (0,), coeff_map=False, final_t=True, mask=False)
-        fo.coeff_map = torch.empty((H, W, cc), dtype=torch.float32, device=dev)
-        eng.run(cam, (0,), fo, early_exit=early_exit, dense=(plan, cc))
-        out[:, :, c0:c0 + cc] = fo.coeff_map
-        final_t = fo.final_t
-        pairs = int(fo.host_stats()[0][1])
+    # every pass blends 16 plan channels (unused ones carry zero values), so the
+    # workspace layout is the same for all passes: the first pass projects and
+    # bins, the others reuse its tile lists (SfFrame.reuse_lists).  C = 0 still
+    # runs one pass: final T and the pair count come from a real frame.
+    cc = DENSE_CHANNELS_PER_PASS
+    half = (4 * cc + 15) // 16 * 4  # words per record half (chan_val_offset / 4)
+    fo = eng.allocate(W, H, (0,), coeff_map=False, final_t=True, mask=False)
+    fo.coeff_map = torch.empty((H, W, cc), dtype=torch.float32, device=dev)
+    with eng._lock:
+        for i, c0 in enumerate(range(0, max(c, 1), cc)):
+            n = min(cc, c - c0)
+            plan = torch.zeros((max(g, 1), 2 * half), dtype=torch.int32, device=dev)
+            plan[:, :cc] = torch.arange(cc, dtype=torch.int32, device=dev) * 516  # accumulator byte offsets
+            if g and n > 0:
+                plan[:g, half:half + n] = vals[:, c0:c0 + n].contiguous().view(torch.int32)
+            eng.run(cam, (0,), fo, early_exit=early_exit, dense=(plan, cc), reuse_lists=i > 0)
+            if n > 0:
+                out[:, :, c0:c0 + n] = fo.coeff_map[:, :, :n]
+    final_t = fo.final_t
+    pairs = int(fo.host_stats()[0][1])
     data = out.double()
     if bg is not None:
         data = data + final_t.double()[:, :, None] * torch.from_numpy(bg).to(dev)[None, None, :]

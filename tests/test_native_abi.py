@@ -43,7 +43,7 @@ def test_ctypes_binding_covers_header(lib_path):
     for name in declared_functions():
         assert name in N.EXPORTS, name
         assert getattr(lib, name) is not None
-    assert lib.sf_abi_version() == 3
+    assert lib.sf_abi_version() == 4
     assert lib.sf_decode_fused(3, 64, 4, 512) == 1
     assert lib.sf_decode_fused(3, 32, 4, 512) == 0
 
