@@ -119,6 +119,43 @@ __device__ __forceinline__ bool tile_hit(const MahalPre& p, int tx, int ty, cons
     return min_mahal_sq_to_rect_pre(p, lx, ly, hx, hy) <= SF_CUTOFF;
 }
 
+// tile_hit with an fp32 pre-test.  The rectangle is taken relative to the
+// mean with exact fp64 differences; the four edge minima of the reference's
+// quadratic (the same clipped points) are evaluated in fp32, and the result
+// decides when it clears 9 by more than 1e-5 of the largest term magnitude
+// met (+1e-6) -- fp32 rounding of these few operations stays below 1e-6 of
+// it.  Otherwise (and for the mean inside the rectangle) the decision is the
+// exact fp64 one, so the lists stay byte-identical.
+struct MahalPre32 {
+    float a, c, boc, boa, twob;
+};
+__device__ __forceinline__ MahalPre32 mahal_pre32(const MahalPre& p) {
+    return MahalPre32{(float)p.a, (float)p.c, (float)p.boc, (float)p.boa, (float)p.twob};
+}
+__device__ __forceinline__ bool tile_hit_fast(const MahalPre& p, const MahalPre32& f, int tx, int ty,
+                                              const TileGrid& g) {
+    const double lx = (double)(tx * SF_TILE), ly = (double)(ty * SF_TILE);
+    const double hx = np_minimum(lx + (double)SF_TILE, (double)g.W) - 1;
+    const double hy = np_minimum(ly + (double)SF_TILE, (double)g.H) - 1;
+    if ((p.mx >= lx) && (p.mx <= hx) && (p.my >= ly) && (p.my <= hy)) return true;  // q = 0 <= 9
+    const float x0 = (float)(lx - p.mx), x1 = (float)(hx - p.mx);
+    const float y0 = (float)(ly - p.my), y1 = (float)(hy - p.my);
+    float best = INFINITY, mag = 0.f;
+    auto ev = [&](float dx, float dy) {
+        const float t1 = f.a * dx * dx, t2 = f.twob * dx * dy, t3 = f.c * dy * dy;
+        best = fminf(best, t1 + t2 + t3);
+        mag = fmaxf(mag, t1 + fabsf(t2) + t3);
+    };
+    ev(x0, fminf(fmaxf(-f.boc * x0, y0), y1));
+    ev(x1, fminf(fmaxf(-f.boc * x1, y0), y1));
+    ev(fminf(fmaxf(-f.boa * y0, x0), x1), y0);
+    ev(fminf(fmaxf(-f.boa * y1, x0), x1), y1);
+    const float tol = 1e-5f * mag + 1e-6f;
+    if (best + tol < (float)SF_CUTOFF) return true;
+    if (best - tol > (float)SF_CUTOFF) return false;
+    return min_mahal_sq_to_rect_pre(p, lx, ly, hx, hy) <= SF_CUTOFF;
+}
+
 // The item an entry names: frame mode (row_keys != null) -- item i is scene
 // row i, visible iff its depth key is not the culled sentinel, and the entry
 // is the row (put in (depth, row) order by k_tile_sort_depth); sf_bin mode --
@@ -147,6 +184,7 @@ __global__ void __launch_bounds__(256, 4) k_count_pairs(int64_t N, const int64_t
     int tx0, tx1, ty0, ty1;
     cand_rect(p, g, tx0, tx1, ty0, ty1);
     const MahalPre mp = mahal_pre(p.mx, p.my, p.a, p.b, p.c);
+    const MahalPre32 mf = mahal_pre32(mp);
     const int n_tiles = g.tiles_x * g.tiles_y;
     BinAux a;
     a.mask = 0;
@@ -159,7 +197,7 @@ __global__ void __launch_bounds__(256, 4) k_count_pairs(int64_t N, const int64_t
     int bit = 0, nh = 0;
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx, ++bit)
-            if (tile_hit(mp, tx, ty, g)) {
+            if (tile_hit_fast(mp, mf, tx, ty, g)) {
                 const int t = ty * g.tiles_x + tx;
                 if (nh < kBinSlots) {
                     const uint32_t pos = atomicAdd(&tile_counts[t], 1u);
@@ -201,6 +239,7 @@ __global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t p
         int tx0, tx1, ty0, ty1;
         cand_rect(p, g, tx0, tx1, ty0, ty1);
         const MahalPre mp = mahal_pre(p.mx, p.my, p.a, p.b, p.c);
+        const MahalPre32 mf = mahal_pre32(mp);
         BinAux a;
         a.mask = 0;
         a.tx0 = (uint16_t)tx0;
@@ -212,7 +251,7 @@ __global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t p
         int bit = 0, nh = 0;
         for (int ty = ty0; ty <= ty1; ++ty)
             for (int tx = tx0; tx <= tx1; ++tx, ++bit) {
-                if (tile_hit(mp, tx, ty, g)) {
+                if (tile_hit_fast(mp, mf, tx, ty, g)) {
                     const int t = ty * g.tiles_x + tx;
                     if (nh < kBinSlots) {
                         const uint32_t pos = atomicAdd(&hist[t], 1u);

@@ -1342,6 +1342,7 @@ int launch_splat_transpose(const BlendArgs& a, const float* dW, float* ghat, int
 constexpr int kFxWarps = 8;
 __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) {
     __shared__ double wl[kChBlock];
+    __shared__ float wf[kChBlock];
     __shared__ double pv[32 * kFxWarps][kMaxC];
     __shared__ uint8_t chs[32 * kFxWarps][kMaxC];
     __shared__ uint16_t live_list[32 * kFxWarps];  // the round's adding entries, in list order
@@ -1373,21 +1374,37 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
         __syncthreads();
         const double pxd = (double)px, pyd = (double)py;
         const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
+        // the next round's entry is loaded (and its record prefetched) one round ahead
+        uint32_t r_next = (beg + (uint32_t)tid < end) ? A.entries[beg + tid] : 0u;
         for (uint32_t r0 = beg; r0 < end; r0 += 32 * kFxWarps) {
             const double T = Tround;
             const uint32_t i = r0 + (uint32_t)(wid * 32 + lane);
             double al = 0.0;
-            uint32_t r = 0;
+            uint32_t r = r_next;
+            {
+                const uint32_t i2 = i + 32 * kFxWarps;
+                r_next = i2 < end ? A.entries[i2] : 0u;
+                if (i2 < end) {
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(A.geom + r_next));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(A.geom + r_next) + 64));
+                }
+            }
             if (i < end) {
-                r = A.entries[i];
                 const GeomRec* g = A.geom + r;
-                double ddx = __dadd_rn(pxd, -g->mx), ddy = __dadd_rn(pyd, -g->my);
-                double t1 = __dmul_rn(__dmul_rn(g->a64, ddx), ddx);
-                double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, g->b64), ddx), ddy);
-                double t3 = __dmul_rn(__dmul_rn(g->c64, ddy), ddy);
-                double q = __dadd_rn(__dadd_rn(t1, t2), t3);
-                if (q <= SF_CUTOFF)
-                    al = np_minimum(__dmul_rn((double)g->opacity, exp(__dmul_rn(-0.5, q))), SF_ALPHA_CLAMP);
+                // fp32 pre-test: outside its guard band q32 > 9 certifies q > 9
+                // (alpha = 0), so only the entries that touch the pixel take
+                // the fp64 path (the fp32 record is 32 of the 80 bytes)
+                bool amb = false;
+                const float a32 = blend_alpha_fast(*reinterpret_cast<const GeomF32*>(g), (float)px, (float)py, amb);
+                if (a32 > 0.f || amb) {
+                    double ddx = __dadd_rn(pxd, -g->mx), ddy = __dadd_rn(pyd, -g->my);
+                    double t1 = __dmul_rn(__dmul_rn(g->a64, ddx), ddx);
+                    double t2 = __dmul_rn(__dmul_rn(__dmul_rn(2.0, g->b64), ddx), ddy);
+                    double t3 = __dmul_rn(__dmul_rn(g->c64, ddy), ddy);
+                    double q = __dadd_rn(__dadd_rn(t1, t2), t3);
+                    if (q <= SF_CUTOFF)
+                        al = np_minimum(__dmul_rn((double)g->opacity, exp(__dmul_rn(-0.5, q))), SF_ALPHA_CLAMP);
+                }
             }
             const double f = __dadd_rn(1.0, -al);
             double incl = f;
@@ -1465,13 +1482,35 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
         if (tid == 0 && A.final_t) A.final_t[pix] = (float)Tend;
         if (A.features) {
             // the fused decode used the fp32 tile: redo this pixel's features from
-            // the exact coefficients (fp32 FMA over L terms, ~4e-6 relative)
-            for (int bn = tid; bn < A.n_levels * A.D; bn += blockDim.x) {
-                const int b = bn / A.D, n = bn - b * A.D;
-                const float* cb = A.codebooks + (size_t)A.lv.lv[b] * A.L * A.D + n;
-                float fv = 0.f;
-                for (int l = 0; l < A.L; ++l) fv = fmaf((float)wl[b * A.L + l], __ldg(cb + (size_t)l * A.D), fv);
-                A.features[(size_t)b * A.feat_level_stride + pix * A.D + n] = fv;
+            // the exact coefficients (fp32 FMA over L terms, ~4e-6 relative);
+            // 8 outputs per thread at a time, as independent FMA chains
+            for (int c = tid; c < A.n_ch; c += blockDim.x) wf[c] = (float)wl[c];
+            __syncthreads();
+            const int total = A.n_levels * A.D;
+            for (int base = tid; base < total; base += 8 * blockDim.x) {
+                float fv[8];
+                const float* cbp[8];
+                int wo[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int bn = min(base + k * (int)blockDim.x, total - 1);
+                    const int b = bn / A.D, n = bn - b * A.D;
+                    cbp[k] = A.codebooks + (size_t)A.lv.lv[b] * A.L * A.D + n;
+                    wo[k] = b * A.L;
+                    fv[k] = 0.f;
+                }
+                for (int l = 0; l < A.L; ++l) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) fv[k] = fmaf(wf[wo[k] + l], __ldg(cbp[k] + (size_t)l * A.D), fv[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int bn = base + k * (int)blockDim.x;
+                    if (bn < total) {
+                        const int b = bn / A.D, n = bn - b * A.D;
+                        A.features[(size_t)b * A.feat_level_stride + pix * A.D + n] = fv[k];
+                    }
+                }
             }
         }
         if (A.proj_cb && A.relevancy_raw && tid < A.n_levels) {

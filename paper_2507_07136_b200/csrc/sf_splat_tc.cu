@@ -52,12 +52,13 @@
 namespace sf {
 namespace tcs {
 
-constexpr int kThreads = 480;
+constexpr int kThreads = 512;
 constexpr int kBlendWarps = 8;   // warps 0-7: two per TMEM lane quarter
 constexpr int kDrainWarp0 = 8;   // warps 8-11
 constexpr int kProdWarp = 12;
 constexpr int kMmaWarp = 13;   // E V issuer (one thread)
 constexpr int kDecWarp = 14;   // decode issuer (one thread)
+constexpr int kLoadWarp = 15;  // codebook chunk loader (one thread)
 constexpr int kStages = 3;
 constexpr int kBatch = 32;
 constexpr int kMaxLevels = 3;
@@ -100,7 +101,8 @@ struct __align__(1024) Smem {
     uint64_t rec_full[kStages], ev_full[kStages], ev_empty[kStages];
     uint64_t w_full[2], a_ready[2], slot_free[2];
     uint64_t dq_full[2], dq_empty[2];
-    uint64_t b_full[kBStages], acc_full[2], acc_empty[2];
+    uint64_t b_full[kBStages], b_empty[kBStages], acc_full[2], acc_empty[2];
+    int dec_total;  // decode issuer -> loader: chunks decoded in all (-1 while running)
     uint32_t tmem_base;
 };
 
@@ -227,7 +229,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             bar_init(&S.dq_full[i], 1);
             bar_init(&S.dq_empty[i], 4);
         }
-        for (int i = 0; i < kBStages; ++i) bar_init(&S.b_full[i], 1);
+        for (int i = 0; i < kBStages; ++i) {
+            bar_init(&S.b_full[i], 1);
+            bar_init(&S.b_empty[i], 1);
+        }
+        S.dec_total = -1;
         S.done_count = 0;
         S.contrib[0] = S.contrib[1] = 0u;
         for (int i = 0; i < kStages; ++i) S.ev_tag[i] = S.ev_union[i] = 0u;
@@ -786,14 +792,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     if (lane == 0) SF_PROG(A, 5 + q, (uint32_t)it, 0x30000u | (uint32_t)Gd);
                     SF_TIMED(w1, bar_wait(&S.acc_full[t], (Gd >> 1) & 1));
                     if (q == 0 && lane == 0) SF_CSTAMP(A, Gd, 0);
-                    if (q == 0 && lane == 0) {
-                        // chunk Gd's MMAs are complete: its codebook stage takes chunk Gd + 2
-                        const int sg = Gd % kBStages;
-                        bar_expect_tx(&S.b_full[sg], kChunkBytes);
-                        bulk_g2s(S.bring[sg],
-                                 reinterpret_cast<const unsigned char*>(A.dec_b) + (size_t)((Gd + kBStages) % nchunk) * kChunkBytes,
-                                 kChunkBytes, &S.b_full[sg]);
-                    }
                     tc_after();
                     uint32_t v[64];
                     tmem_ld32(tm + lane_off + (uint32_t)(kAccCol0 + t * kDecN), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
@@ -833,10 +831,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 }
             }
             if (lane == 0) bulk_wait_read<0>();
-            if (q == 0 && lane == 0) {
-                // the two codebook loads still in flight (chunks Gd, Gd + 1) land before exit
-                for (int G = Gd; G < Gd + kBStages; ++G) bar_wait(&S.b_full[G % kBStages], (G / kBStages) & 1);
-            }
         }
     } else if (warp == kMmaWarp && lane == 0) {
         // ---------------- E V issuer: the blend products, batch by batch ----------------
@@ -893,11 +887,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
     } else if (DEC && warp == kDecWarp && lane == 0) {
         // ---------------- decode issuer: 3-term fp16 chunks of each converted tile ----------------
         const uint32_t idesc_dec = (1u << 4) | ((uint32_t)(kDecN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        const unsigned char* img = reinterpret_cast<const unsigned char*>(A.dec_b);
-        for (int g = 0; g < kBStages; ++g) {
-            bar_expect_tx(&S.b_full[g], kChunkBytes);
-            bulk_g2s(S.bring[g], img + (size_t)(g % nchunk) * kChunkBytes, kChunkBytes, &S.b_full[g]);
-        }
         const uint64_t bdesc0 = sw128_desc(smem_addr(S.bring[0]));
         int Gd = 0;
         for (int td = 0; td < n_my; ++td) {
@@ -932,12 +921,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     mma_f16_tmem_a(d, ah, bh, idesc_dec, 1u);
                 }
                 mma_commit(&S.acc_full[t]);
+                mma_commit(&S.b_empty[s]);  // the chunk's codebook stage is free once its MMAs are
                 SF_CSTAMP(A, Gd, 5);
             }
             mma_commit(&S.slot_free[td & 1]);
             SF_STAMP(A, td, 5);
             SF_PROG(A, 10, (uint32_t)td, (uint32_t)Gd);
         }
+        *reinterpret_cast<volatile int*>(&S.dec_total) = Gd;
+    } else if (DEC && warp == kLoadWarp && lane == 0) {
+        // ---------------- codebook loader: chunk g + kBStages into the stage chunk g frees ----------------
+        // (decoupled from the drains, which read the accumulators later; every
+        // non-empty tile decodes chunks 0 .. nchunk - 1 in order, so global
+        // chunk G needs image chunk G % nchunk)
+        const unsigned char* img = reinterpret_cast<const unsigned char*>(A.dec_b);
+        for (int g = 0; g < kBStages; ++g) {
+            bar_expect_tx(&S.b_full[g], kChunkBytes);
+            bulk_g2s(S.bring[g], img + (size_t)(g % nchunk) * kChunkBytes, kChunkBytes, &S.b_full[g]);
+        }
+        int G = 0;
+        for (;;) {
+            const int sg = G % kBStages;
+            if (bar_test(&S.b_empty[sg], (G / kBStages) & 1)) {
+                bar_expect_tx(&S.b_full[sg], kChunkBytes);
+                bulk_g2s(S.bring[sg], img + (size_t)((G + kBStages) % nchunk) * kChunkBytes, kChunkBytes, &S.b_full[sg]);
+                ++G;
+                continue;
+            }
+            const int total = *reinterpret_cast<volatile int*>(&S.dec_total);
+            if (total >= 0 && G >= total) break;
+            __nanosleep(32);
+        }
+        // the loads of chunks G .. G + kBStages - 1 were never consumed: they land before exit
+        for (int g = G; g < G + kBStages; ++g) bar_wait(&S.b_full[g % kBStages], (g / kBStages) & 1);
     }
     if (prof && lane == 0) {
         // 4 counters per warp: blend 0..31, drain 32..47, producer 48, E V issuer 52, decode issuer 56
