@@ -363,6 +363,35 @@ def main():
     return run_single(args)
 
 
+def tf32_peak() -> dict:
+    """Dense TF32 tensor throughput on this GPU (cuBLAS 8192^3, median of 5):
+    the denominator for the decode GEMM's tensor roofline (the
+    frame's decode is 2 H W 3 64 512 = 305.8 GFLOP at config C, issued 3x by
+    the 3-term split)."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        for _ in range(2):
+            a @ b
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = sorted(ts)[2]
+        return {"tf32_dense_tflops": 2 * n ** 3 / (ms / 1e3) / 1e12, "probe": "torch.matmul fp32 8192^3, allow_tf32",
+                "decode_gflop_per_frame": 2 * 1440 * 1080 * 3 * 64 * 512 / 1e9}
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 def count_kernels_per_frame(enqueue, pipe) -> int:
     """Kernels one pipelined frame launches, counted by the CUDA profiler on an
     untimed frame (every one is this repo's: the frame path calls no library
@@ -477,6 +506,12 @@ def run_single(args):
     orbit = measure_orbit(args, ds, levels, spec, qdev, W, H, fused, 0, 1, None)
     del pipe
     torch.cuda.empty_cache()
+    # config E's own load on one GPU: 5M Gaussians at 1920x1080, 32 prompts
+    config_e = None
+    if not args.no_sweep and args.config == "C":
+        config_e = measure_band_sweep(args, 1, 0, None)
+        torch.cuda.empty_cache()
+    tf32 = tf32_peak()
 
     parity, cpu = None, None
     if not args.no_cpu_baseline:
@@ -513,6 +548,8 @@ def run_single(args):
         "parity": parity,
         "e2e": e2e,
         "query_sweep": sweep,
+        "config_e_sweep": config_e,
+        "tensor_peak": tf32,
         "gpu_launches": launches_per_frame * args.steps,
         "clocks": clocks,
     }
@@ -763,9 +800,10 @@ def run_multi(args, world, rank, local, dist):
     dist.destroy_process_group()
 
 
-def measure_band_sweep(args, world, rank, dist):
+def measure_band_sweep(args, world, rank, dist=None):
     """Config E: 5M Gaussians at 1920x1080, 32 prompts, one tile band per rank
-    (distributed.band_query_sweep); sweeps per second over all ranks."""
+    (distributed.band_query_sweep); sweeps per second over all ranks.  With
+    dist=None (one GPU) the single band is the whole view."""
     import numpy as np
     import torch
 
@@ -781,13 +819,16 @@ def measure_band_sweep(args, world, rank, dist):
     for _ in range(2):
         band_query_sweep(eng, cam, (0, 1, 2), prompts, canon, world, rank)
     n = max(3, args.steps // 4)
-    dist.barrier()
+    if dist is not None:
+        dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(n):
         bs = band_query_sweep(eng, cam, (0, 1, 2), prompts, canon, world, rank)
     torch.cuda.synchronize()
-    dt = _max_over_ranks(time.perf_counter() - t0, dist)
+    dt = time.perf_counter() - t0
+    if dist is not None:
+        dt = _max_over_ranks(dt, dist)
     del bs, eng
     torch.cuda.empty_cache()
     return {"sweeps_per_s": n / dt, "prompt_frames_per_s": 32 * n / dt, "ms_per_sweep": 1e3 * dt / n,
