@@ -35,6 +35,7 @@ def _compile(src: str, log_dir: str) -> tuple[str, str]:
     flags = list(COMMON)
     if src in NO_FMAD:
         flags.append("-fmad=false")
+    flags += os.environ.get("SF_NVCC_DEFINES", "").split()  # development experiments only
     cmd = [nvcc(), "-c", os.path.join(CSRC, src), "-o", out] + flags
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(os.path.join(log_dir, src + ".log"), "w") as f:

@@ -101,7 +101,7 @@ struct FrameWs {
     void* sel_ws;
     float* dec_ws;
     float* dec_img;   // fused decode: pre-swizzled tf32 hi/lo codebook chunks
-    uint32_t* fixup;  // [0] = count, then the list
+    uint32_t* fixup;  // [0] = count, [1] = the splat's half-tile claim counter, [2, 4) pad, then the list
 };
 
 // Exact-replay list capacity: every pixel can be listed at most once, so
@@ -146,7 +146,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->sel_ws = c.take<char>(select_segment_ws_bytes(n_levels, H, W));
     ws->dec_ws = c.take<float>(decode_ws_bytes(L, D) / sizeof(float));
     ws->dec_img = c.take<float>(blend_dec_image_bytes(n_levels, D) / sizeof(float));
-    ws->fixup = c.take<uint32_t>((size_t)fixup_capacity(W, H) + 1);
+    ws->fixup = c.take<uint32_t>((size_t)fixup_capacity(W, H) + 4);
     return c.off;
 }
 
@@ -234,7 +234,7 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
         cudaMemsetAsync(ws.stats, 0, 16 * sizeof(int64_t), st_prep);
         cudaMemsetAsync(ws.stats_f, 0, (8 + 2 * kMaxLevels) * sizeof(double), st_prep);
     }
-    cudaMemsetAsync(ws.fixup, 0, sizeof(uint32_t), st_prep);
+    cudaMemsetAsync(ws.fixup, 0, 4 * sizeof(uint32_t), st_prep);
     const unsigned char* chan = f->chan_by_row;
     if (!chan && f->reuse_lists) return fail(SF_ERR_VALIDATION, "reuse_lists needs a scatter plan (chan_by_row)");
     if (!f->reuse_lists) {
@@ -291,7 +291,8 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
     a.geom = ws.geom;
     a.chan = chan;
     a.fixup_count = ws.fixup;
-    a.fixup_list = ws.fixup + 1;
+    a.sched = ws.fixup + 1;
+    a.fixup_list = ws.fixup + 4;
     a.fixup_capacity = fixup_capacity(W, H);
     a.stats = ws.stats;
     a.coeff_map = f->coeff_map;

@@ -273,6 +273,7 @@ struct BlendArgs {
     uint32_t* fixup_list;  // (tile << 8 | pixel slot) of pixels whose early-exit decision is ambiguous
     uint32_t* fixup_count;
     uint32_t fixup_capacity;
+    uint32_t* sched;       // [0]: next half tile to claim (tensor-core splat), zeroed per frame
     float* coeff_map;      // (H,W,n_ch) or null
     float* final_t;        // (H,W) or null
     // fused projected-codebook relevancy (optional)

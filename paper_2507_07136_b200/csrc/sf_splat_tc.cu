@@ -92,6 +92,9 @@ struct __align__(1024) Smem {
     float alpha[4][2][16 * 32];         // per blend warp (quarter, hb): alphas of its <= 16 candidates x 32 pixels
     float4 hand[4][2][32];              // pair hand-off: (T, T before last, error bound, count | done)
     int nb[kStages];
+    int sched[8];    // producer -> blend warps / E V issuer: half tile of iteration it (-1: no more)
+    int a_ht[2];     // blend warps -> decode issuer, per W slot: the converted tile's half tile
+    int dq_ht[2];    // decode issuer -> drains, per tile in order: half tile (-1: no more)
     int done_count;
     uint32_t contrib[2];   // per W slot: bit w = blend warp w's pixels got a contribution
     uint32_t dq_info[2];   // MMA -> drains, per tile in order: contrib of the tile
@@ -108,16 +111,18 @@ struct __align__(1024) Smem {
 
 static_assert(sizeof(Smem) + 1024 <= 232448, "shared memory exceeds the 227 KB opt-in limit");
 
-__device__ __forceinline__ bool bar_test(uint64_t* b, uint32_t parity) {
+// wait for the phase up to about `ns` nanoseconds (the thread sleeps in
+// hardware until the phase completes or the hint expires): true if it completed
+__device__ __forceinline__ bool bar_wait_for(uint64_t* b, uint32_t parity, uint32_t ns) {
     uint32_t ok;
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         "selp.u32 %0, 1, 0, p;\n"
         "}\n"
         : "=r"(ok)
-        : "r"(smem_addr(b)), "r"(parity)
+        : "r"(smem_addr(b)), "r"(parity), "r"(ns)
         : "memory");
     return ok != 0;
 }
@@ -212,7 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
     const int n_levels = A.n_levels, n_ch = A.n_ch;
     const int dchunks = DEC ? A.D / kDecN : 0;  // chunks per level
     const int nchunk = n_levels * dchunks;      // decode chunks per half tile
-    const int n_my = (int)blockIdx.x < n_half ? (n_half - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    // Half tiles are claimed dynamically (A.sched[0], zeroed per frame): a CTA
+    // takes the next one when its producer starts streaming a tile, so SMs
+    // that drew light tiles take more (tile cost varies ~100x across a frame).
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -290,19 +297,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             for (int q = 0; q < cq; ++q) cp_async16(dst + 16 * q, src + 16 * q);
         };
         int bs = 0;
-        for (int it = 0; it < n_my; ++it) {
-            const int ht = (int)blockIdx.x + it * (int)gridDim.x;
-            const int tile = A.tile0 + (ht >> 1);
-            const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
+        auto claim = [&]() -> int {
+            uint32_t x = 0;
+            if (lane == 0) x = atomicAdd(A.sched, 1u);
+            x = __shfl_sync(0xffffffffu, x, 0);
+            return x < (uint32_t)n_half ? (int)x : -1;
+        };
+        int ht_next = claim();
+        for (int it = 0;; ++it) {
+            // the tile after this one is claimed now, so its first entries can be warmed in L2
+            const int ht = ht_next;
+            ht_next = ht >= 0 ? claim() : -1;
+            if (lane == 0) S.sched[it & 7] = ht;  // published by the tile's first rec_full arrive
+            // ht < 0: no more tiles -- one empty batch (nb = 0) tells every role
+            const int tile = ht >= 0 ? A.tile0 + (ht >> 1) : 0;
+            const uint32_t beg = ht >= 0 ? A.tile_offsets[tile] : 0u, end = ht >= 0 ? A.tile_offsets[tile + 1] : 0u;
             if (lane == 0) SF_STAMP(A, it, 9);
-            {
-                // warm L2 with the next tile's first entries (its prologue reads them)
-                const int ht2 = ht + (int)gridDim.x;
-                if (ht2 < n_half && lane < 4) {
-                    const int t2 = A.tile0 + (ht2 >> 1);
-                    const uint32_t b2 = A.tile_offsets[t2] + 32u * lane;
-                    if (b2 < A.tile_offsets[t2 + 1]) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.entries + b2));
-                }
+            if (ht_next >= 0 && lane < 4) {
+                const int t2 = A.tile0 + (ht_next >> 1);
+                const uint32_t b2 = A.tile_offsets[t2] + 32u * lane;
+                if (b2 < A.tile_offsets[t2 + 1]) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.entries + b2));
             }
             // filtered entry stream of this half tile
             const uint32_t hbit = 1u << (ht & 1);
@@ -445,6 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 }
             }
             cp_async_wait<0>();
+            if (ht < 0) break;
         }
     } else if (warp < kBlendWarps) {
         // ---------------- blend warps: E rows per batch, W epilogue per tile ----------------
@@ -466,13 +481,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
         float4* hand_out = S.hand[cw][hb];     // state this warp posts
         const float4* hand_in = S.hand[cw][hb ^ 1];
         const int bar_ab = 1 + cw, bar_ba = 5 + cw;  // named barriers of the pair (64 threads)
-        const int bar_rd = 9 + cw;                    // hb 0 has read the tile's W for the relevancy
+        const int bar_rd = 9 + cw;                    // hb 0 has read hb 1's partial relevancy dots
         const int e0 = 16 * hb;                       // first batch entry of this warp
         int bs = 0;
         uint32_t zero_mask = 0;  // stages whose E half-rows of this warp are all zero
-        for (int it = 0; it < n_my; ++it) {
-            const int ht = (int)blockIdx.x + it * (int)gridDim.x;
+        for (int it = 0;; ++it) {
             const int slot = it & 1;
+            // the tile's first batch carries its half-tile index (S.sched)
+            SF_TIMED(w0, bar_wait(&S.rec_full[bs % kStages], (bs / kStages) & 1));
+            const int ht = *reinterpret_cast<volatile int*>(&S.sched[it & 7]);
+            if (ht < 0) {
+                // no more tiles: pass the empty batch on; once the E V issuer has
+                // released this W slot (as for any tile), tell the decode issuer
+                __syncwarp();
+                if (lane == 0) bar_arrive(&S.ev_full[bs % kStages]);
+                ++bs;
+                SF_TIMED(w0, bar_wait(&S.w_full[slot], (it >> 1) & 1));
+                if (lane == 0) {
+                    S.a_ht[slot] = -1;
+                    bar_arrive(DEC ? &S.a_ready[slot] : &S.slot_free[slot]);
+                }
+                break;
+            }
             const int tile = A.tile0 + (ht >> 1), half = ht & 1;
             const int x0 = (tile % A.tiles_x) * SF_TILE, y0 = (tile / A.tiles_x) * SF_TILE;
             const int w8 = half * 4 + cw;
@@ -485,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             int ncontrib = 0, nbatches = 0;
             bool tile_hit = false;  // some batch of this tile had a candidate for this warp
             bool done = !inside;
-            if (hb == 0 && lane == 0) SF_STAMP(A, it, 0);
+            if (warp == 0 && lane == 0) SF_STAMP(A, it, 0);
             bool all_done = __all_sync(0xffffffffu, done);
             bool counted = all_done;
             if (all_done && lane == 0) atomicAdd(&S.done_count, 1);
@@ -618,12 +648,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 }
             }
             if (!counted && lane == 0) atomicAdd(&S.done_count, 1);
-            if (hb == 0 && lane == 0) SF_STAMP(A, it, 1);
+            if (warp == 0 && lane == 0) SF_STAMP(A, it, 1);
             // W holds products iff some warp had a candidate in some batch (else
             // the issuer skipped every batch and the slot is stale): the 8 blend
             // warps agree on that through the tile tag
             if (tile_hit && lane == 0) S.tile_tag[slot] = (uint32_t)it + 1u;
             named_bar_sync(13, 32 * kBlendWarps);
+            if (warp == 0 && lane == 0) SF_STAMP(A, it, 11);
             const bool wvalid = *reinterpret_cast<volatile uint32_t*>(&S.tile_tag[slot]) == (uint32_t)it + 1u;
 
             // ---- per-tile epilogue: hb 0 takes columns [0, 32) of each level, hb 1 [32, 64) ----
@@ -641,6 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             const bool any = __any_sync(0xffffffffu, ncontrib > 0);
             if (lane == 0 && hb == 0) SF_PROG(A, 1 + cw, (uint32_t)it, 0x10000u | (uint32_t)bs);
             SF_TIMED(w0, bar_wait(&S.w_full[slot], (it >> 1) & 1));
+            if (warp == 0 && lane == 0) SF_STAMP(A, it, 12);
             if (lane == 0 && hb == 0) SF_PROG(A, 1 + cw, (uint32_t)it, 0x20000u | (uint32_t)bs);
             // published only now: the W slot's previous tile (it - 2) has been
             // fully decoded (its slot_free preceded this tile's E V products),
@@ -654,57 +686,55 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             const size_t pix = (size_t)py * A.W + px;
             // Compact code: this part runs once per tile per warp, so its
             // instructions are fetched cold -- loops stay rolled.
-            // (1) hb 0: relevancy over all 64 columns of each level (before hb 1
-            //     converts its columns in place), 8 columns per step.
-            if (hb == 0 && rel && wvalid) {
+            // Each warp works on its own 32 columns of each level only (no
+            // cross-warp TMEM dependency): its half of the fused relevancy dot
+            // products (fp64, W (P_q - P_cj)), the coefficient map (if
+            // requested) and, fused decode, the in-place A operand.  The pair's
+            // partial dots meet in the quarter's rows of E stages 0-1 (no MMA
+            // reads E between w_full and the next tile's batches).
+            auto xslot = [&](int h, int b) -> double* {
+                const int g = 3 * h + b;  // 6 groups of 32 px x 4 doubles: ehi[0], elo[0], ehi[1] quarter rows
+                unsigned char* base = (g >> 1) == 0 ? (unsigned char*)&S.ehi[0][0]
+                                                    : ((g >> 1) == 1 ? (unsigned char*)&S.elo[0][0] : (unsigned char*)&S.ehi[1][0]);
+                return reinterpret_cast<double*>(base + cw * 2048 + (g & 1) * 1024) + 4 * lane;
+            };
+            // (1) the warp's partial relevancy dots over its own 32 columns of
+            //     each level, 8 columns per step (compact code)
+            if (rel) {
 #pragma unroll 1
                 for (int b = 0; b < n_levels; ++b) {
                     double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
+                    if (wvalid) {
 #pragma unroll 1
-                    for (int c = 0; c < 64; c += 8) {
-                        uint32_t v[8];
-                        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                                       "=r"(v[7])
-                                     : "r"(wslot + (uint32_t)(64 * b + c)));
-                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        const double* P = S.pd + (size_t)(64 * b + c) * 4;
+                        for (int c = 32 * hb; c < 32 * hb + 32; c += 8) {
+                            uint32_t v[8];
+                            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                                           "=r"(v[7])
+                                         : "r"(wslot + (uint32_t)(64 * b + c)));
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                            const double* P = S.pd + (size_t)(64 * b + c) * 4;
 #pragma unroll
-                        for (int i = 0; i < 8; i += 2) {
-                            const double2 a01 = *reinterpret_cast<const double2*>(P + 4 * i);
-                            const double2 a23 = *reinterpret_cast<const double2*>(P + 4 * i + 2);
-                            const double2 b01 = *reinterpret_cast<const double2*>(P + 4 * i + 4);
-                            const double2 b23 = *reinterpret_cast<const double2*>(P + 4 * i + 6);
-                            const double x = (double)(__uint_as_float(v[i]) * kInvW);
-                            const double y = (double)(__uint_as_float(v[i + 1]) * kInvW);
-                            d0 = fma(x, a01.x, d0), d1 = fma(x, a01.y, d1), d2 = fma(x, a23.x, d2), d3 = fma(x, a23.y, d3);
-                            f0 = fma(y, b01.x, f0), f1 = fma(y, b01.y, f1), f2 = fma(y, b23.x, f2), f3 = fma(y, b23.y, f3);
+                            for (int i = 0; i < 8; i += 2) {
+                                const double2 a01 = *reinterpret_cast<const double2*>(P + 4 * i);
+                                const double2 a23 = *reinterpret_cast<const double2*>(P + 4 * i + 2);
+                                const double2 b01 = *reinterpret_cast<const double2*>(P + 4 * i + 4);
+                                const double2 b23 = *reinterpret_cast<const double2*>(P + 4 * i + 6);
+                                const double x = (double)(__uint_as_float(v[i]) * kInvW);
+                                const double y = (double)(__uint_as_float(v[i + 1]) * kInvW);
+                                d0 = fma(x, a01.x, d0), d1 = fma(x, a01.y, d1), d2 = fma(x, a23.x, d2), d3 = fma(x, a23.y, d3);
+                                f0 = fma(y, b01.x, f0), f1 = fma(y, b01.y, f1), f2 = fma(y, b23.x, f2), f3 = fma(y, b23.y, f3);
+                            }
                         }
                     }
-                    d0 += f0, d1 += f1, d2 += f2, d3 += f3;
-                    // sigmoid is monotone: min_j sigmoid(d_j) = sigmoid(min_j d_j)
-                    if (inside)
-                        A.relevancy_raw[(size_t)b * A.W * A.H + pix] =
-                            sigmoid2(np_minimum(np_minimum(d0, d1), np_minimum(d2, d3)));
-                }
-            } else if (hb == 0 && rel && inside) {
-#pragma unroll 1
-                for (int b = 0; b < n_levels; ++b) A.relevancy_raw[(size_t)b * A.W * A.H + pix] = 0.5;  // W = 0
-            }
-            if (rel) {
-                // hb 1 may overwrite its columns once hb 0 has read them
-                if (hb == 0) {
-                    tc_before();
-                    __syncwarp();
-                    asm volatile("bar.arrive %0, 64;" ::"r"(bar_rd) : "memory");
-                } else {
-                    named_bar_sync(bar_rd, 64);
-                    tc_after();
+                    double2* o = reinterpret_cast<double2*>(xslot(hb, b));
+                    o[0] = make_double2(d0 + f0, d1 + f1);
+                    o[1] = make_double2(d2 + f2, d3 + f3);
                 }
             }
-            // (2) each warp: its 32 columns of each level -> coefficient map (if
-            //     requested) and, fused decode, the A operand (fp16 hi/lo pairs of
-            //     W 2^12) in place
+            if (warp == 0 && lane == 0) SF_STAMP(A, it, 13);
+            // (2) its 32 columns of each level -> coefficient map (if requested)
+            //     and, fused decode, the A operand (fp16 hi/lo pairs of W 2^12) in place
             if (DEC || A.coeff_map) {
 #pragma unroll 1
                 for (int b = 0; b < n_levels; ++b) {
@@ -740,8 +770,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             if (DEC) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_before();
             __syncwarp();
-            if (lane == 0) bar_arrive(DEC ? &S.a_ready[slot] : &S.slot_free[slot]);
-            if (hb == 0 && lane == 0) SF_STAMP(A, it, 2);
+            if (lane == 0) {
+                S.a_ht[slot] = ht;
+                bar_arrive(DEC ? &S.a_ready[slot] : &S.slot_free[slot]);
+            }
+            if (warp == 0 && lane == 0) SF_STAMP(A, it, 14);
+            if (rel) {
+                // hb 1 -> hb 0: partial dots posted (bar_ba, as after a batch walk);
+                // hb 0 -> hb 1: read (bar_rd), hb 1 may write E again
+                if (hb == 1) {
+                    asm volatile("bar.arrive %0, 64;" ::"r"(bar_ba) : "memory");
+                    named_bar_sync(bar_rd, 64);
+                } else {
+                    named_bar_sync(bar_ba, 64);
+#pragma unroll 1
+                    for (int b = 0; b < n_levels; ++b) {
+                        const double2* p0 = reinterpret_cast<const double2*>(xslot(0, b));
+                        const double2* p1 = reinterpret_cast<const double2*>(xslot(1, b));
+                        const double2 a01 = p0[0], a23 = p0[1], b01 = p1[0], b23 = p1[1];
+                        // sigmoid is monotone: min_j sigmoid(d_j) = sigmoid(min_j d_j)
+                        const double dm =
+                            np_minimum(np_minimum(a01.x + b01.x, a01.y + b01.y), np_minimum(a23.x + b23.x, a23.y + b23.y));
+                        if (inside) A.relevancy_raw[(size_t)b * A.W * A.H + pix] = sigmoid2(dm);
+                    }
+                    asm volatile("bar.arrive %0, 64;" ::"r"(bar_rd) : "memory");
+                }
+                zero_mask &= ~3u;  // the partials overwrote E rows of stages 0 and 1
+            }
+            if (warp == 0 && lane == 0) SF_STAMP(A, it, 2);
         }
     } else if (warp < kDrainWarp0 + 4) {
         // ---------------- drain warps: accumulators -> swizzled boxes -> TMA stores ----------------
@@ -754,19 +810,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             for (int b = 0; b < kMaxLevels; ++b) scl[b] = (b < n_levels ? A.dec_scale[b] : 1.f) / kScale;
             int Gd = 0;
             bool box_zero = false;
-            for (int it = 0; it < n_my; ++it) {
-                const int ht = (int)blockIdx.x + it * (int)gridDim.x;
+            for (int it = 0;; ++it) {
                 const int slot = it & 1;
-                const int tile = A.tile0 + (ht >> 1), half = ht & 1;
-                const int w8 = half * 4 + q;
-                const int bx = (tile % A.tiles_x) * SF_TILE + (w8 & 1) * 8, by = (tile / A.tiles_x) * SF_TILE + (w8 >> 1) * 4;
                 if (lane == 0) SF_PROG(A, 5 + q, (uint32_t)it, 0x10000u | (uint32_t)Gd);
                 SF_TIMED(w0, bar_wait(&S.dq_full[slot], (it >> 1) & 1));
                 if (lane == 0) SF_PROG(A, 5 + q, (uint32_t)it, 0x20000u | (uint32_t)Gd);
                 if (q == 0 && lane == 0) SF_STAMP(A, it, 6);
+                const int ht = *reinterpret_cast<volatile int*>(&S.dq_ht[slot]);
                 const bool contrib = *reinterpret_cast<volatile uint32_t*>(&S.dq_info[slot]) != 0u;
                 __syncwarp();
                 if (lane == 0) bar_arrive(&S.dq_empty[slot]);
+                if (ht < 0) break;
+                const int tile = A.tile0 + (ht >> 1), half = ht & 1;
+                const int w8 = half * 4 + q;
+                const int bx = (tile % A.tiles_x) * SF_TILE + (w8 & 1) * 8, by = (tile / A.tiles_x) * SF_TILE + (w8 >> 1) * 4;
                 if (!contrib) {
                     // no contribution anywhere in the half tile: its features are zero
                     if (!box_zero) {
@@ -780,8 +837,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     if (lane == 0) {
                         for (int g = 0; g < nchunk; ++g) {
                             const int b = g / dchunks, c = g - b * dchunks;
+#ifndef SF_NOSTORE  // experiment only: no feature stores
                             tma_store_4d(&fmap, wbox, c * kDecN, bx, by, b);
                             tma_store_4d(&fmap, wbox + kBoxBytes, c * kDecN + kBoxCols, bx, by, b);
+#endif
                         }
                         bulk_commit();
                     }
@@ -821,8 +880,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     proxy_fence();
                     __syncwarp();
                     if (lane == 0) {
+#ifndef SF_NOSTORE
                         tma_store_4d(&fmap, wbox, c * kDecN, bx, by, b);
                         tma_store_4d(&fmap, wbox + kBoxBytes, c * kDecN + kBoxCols, bx, by, b);
+#endif
                         bulk_commit();
                         if (q == 0) SF_CSTAMP(A, Gd, 3);
                         if (q == 0 && g == nchunk - 1) SF_STAMP(A, it, 7);
@@ -838,12 +899,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
         const uint32_t eh0 = smem_addr(&S.ehi[0][0]), el0 = smem_addr(&S.elo[0][0]);
         const uint32_t vh0 = smem_addr(&S.vhi[0][0]), vl0 = smem_addr(&S.vlo[0][0]);
         int be = 0;
-        for (int te = 0; te < n_my; ++te) {
+        for (int te = 0;; ++te) {
             bool first = true;
+            int ht = 0;
             for (;;) {
                 const int s = be % kStages;
                 SF_TIMED(w0, bar_wait(&S.ev_full[s], (be / kStages) & 1));
                 const int nb = *reinterpret_cast<volatile int*>(&S.nb[s]);
+                if (first) ht = *reinterpret_cast<volatile int*>(&S.sched[te & 7]);
                 ++be;
                 // The slot's previous tile (te - 2) must be fully decoded before
                 // this tile writes it -- also when the tile has no batch at all:
@@ -883,21 +946,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 first = false;
             }
             SF_PROG(A, 9, (uint32_t)te, (uint32_t)be);
+            if (ht < 0) break;  // the terminal empty tile
         }
     } else if (DEC && warp == kDecWarp && lane == 0) {
         // ---------------- decode issuer: 3-term fp16 chunks of each converted tile ----------------
         const uint32_t idesc_dec = (1u << 4) | ((uint32_t)(kDecN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         const uint64_t bdesc0 = sw128_desc(smem_addr(S.bring[0]));
         int Gd = 0;
-        for (int td = 0; td < n_my; ++td) {
+        for (int td = 0;; ++td) {
             SF_TIMED(w0, bar_wait(&S.a_ready[td & 1], (td >> 1) & 1));
             if (td >= 2) SF_TIMED(w0, bar_wait(&S.dq_empty[td & 1], ((td >> 1) - 1) & 1));
             tc_after();
             SF_STAMP(A, td, 4);
-            // the drains learn the tile's kind in order, through their own ring
-            const uint32_t c = *reinterpret_cast<volatile uint32_t*>(&S.contrib[td & 1]);
+            // the drains learn the tile (and its kind) in order, through their own ring
+            const int ht = *reinterpret_cast<volatile int*>(&S.a_ht[td & 1]);
+            const uint32_t c = ht >= 0 ? *reinterpret_cast<volatile uint32_t*>(&S.contrib[td & 1]) : 0u;
             S.dq_info[td & 1] = c;
+            S.dq_ht[td & 1] = ht;
             bar_arrive(&S.dq_full[td & 1]);
+            if (ht < 0) break;
             if (c == 0u) {
                 bar_arrive(&S.slot_free[td & 1]);  // nothing to multiply: the slot is free now
                 continue;
@@ -942,7 +1009,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
         int G = 0;
         for (;;) {
             const int sg = G % kBStages;
-            if (bar_test(&S.b_empty[sg], (G / kBStages) & 1)) {
+            // sleeps until the stage frees (no polling: this warp shares an SMSP
+            // with a blend pair); wakes now and then to see whether the decode ended
+            if (bar_wait_for(&S.b_empty[sg], (G / kBStages) & 1, 20000)) {
                 bar_expect_tx(&S.b_full[sg], kChunkBytes);
                 bulk_g2s(S.bring[sg], img + (size_t)((G + kBStages) % nchunk) * kChunkBytes, kChunkBytes, &S.b_full[sg]);
                 ++G;
@@ -950,7 +1019,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             }
             const int total = *reinterpret_cast<volatile int*>(&S.dec_total);
             if (total >= 0 && G >= total) break;
-            __nanosleep(32);
         }
         // the loads of chunks G .. G + kBStages - 1 were never consumed: they land before exit
         for (int g = G; g < G + kBStages; ++g) bar_wait(&S.b_full[g % kBStages], (g / kBStages) & 1);
@@ -978,6 +1046,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
 size_t splat_tc_smem_bytes() { return sizeof(tcs::Smem) + 1024; }
 
 bool splat_tc_supported(const BlendArgs& a) {
+    if (!a.sched) return false;
     if (a.L != 64 || a.n_levels < 1 || a.n_levels > tcs::kMaxLevels || a.n_ch != 64 * a.n_levels) return false;
     if (a.C < 1 || a.C > (int)tcs::kMaxC) return false;
     if (a.proj_cb && a.n_canon != 4) return false;
@@ -1012,7 +1081,11 @@ int launch_splat_tc(const BlendArgs& a, cudaStream_t st) {
     if (ensure_smem_attr((const void*)kern, smem)) return -6;
     const int n_half = 2 * a.n_band_tiles;
     if (n_half <= 0) return 0;
-    const int grid = std::min(n_half, device_sm_count());
+    static const int grid_env = [] {  // development aid: fewer CTAs than SMs (SF_TC_GRID)
+        const char* e = getenv("SF_TC_GRID");
+        return e ? atoi(e) : 0;
+    }();
+    const int grid = std::min(n_half, grid_env > 0 ? grid_env : device_sm_count());
     BlendArgs a2 = a;
     a2.timeline = prog ? reinterpret_cast<uint64_t*>(prog) : nullptr;
     kern<<<grid, tcs::kThreads, smem, st>>>(a2, fmap);

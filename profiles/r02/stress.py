@@ -94,6 +94,13 @@ def timeline_report():
               f"over {len(dec)} non-empty tiles of {n}")
         d = np.diff(t[:n, :11], axis=0) / 1965.0
         print("  mean per-tile period (us): " + " ".join(f"{x[:6]}={v:.2f}" for x, v in zip(names, d.mean(axis=0))))
+        ok = (t[:n, 11] > 0) & (t[:n, 12] > 0) & (t[:n, 13] > 0) & (t[:n, 14] > 0)
+        if ok.any():
+            tt = t[:n][ok]
+            parts = [("loop->bar13", 1, 11), ("bar13->w_full", 11, 12), ("relevancy", 12, 13), ("convert", 13, 14),
+                     ("rel_final", 14, 2)]
+            print("  epilogue (us, warp 0, mean over %d tiles): " % ok.sum()
+                  + " ".join(f"{nm} {((tt[:, b] - tt[:, a]) / 1965.0).mean():.2f}" for nm, a, b in parts))
 
 
 def chunk_report():
@@ -123,6 +130,9 @@ def prof_report(n_cta):
     labels = {"blend": ("waits", "alpha", "walk"), "drain": ("dq_full", "acc_full", "bulk_read(lane0)"),
               "producer": ("ev_empty", "batches", "entries"), "ev_issuer": ("ev_full", "slot_free", "candidate_entries"),
               "dec_issuer": ("a_ready/dq", "b_full", "acc_empty")}
+    dur = p[:, 0]  # warp 0's elapsed cycles (persistent CTAs start together)
+    print(f"  CTA duration (warp 0, kcyc): min {dur.min() / 1e3:.0f} mean {dur.mean() / 1e3:.0f} max {dur.max() / 1e3:.0f}"
+          f" (max/mean {dur.max() / max(dur.mean(), 1):.3f})")
     for base, nm in names.items():
         warps = 8 if base == 0 else (4 if base == 32 else 1)
         tot = p[:, base:base + 4 * warps:4].sum(axis=1)
