@@ -281,19 +281,22 @@ __global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t p
 // Exclusive scan over tiles (single CTA): offsets, emit cursors (past the
 // slot-positioned entries), pair total.
 // Also lists the tiles whose lists exceed kShortList entries (big[0] = count,
-// big[1..] = tile ids) for the long-list sorts.
+// big[1..] = tile ids) for the long-list sorts, and those with kTinyList <
+// n <= kShortList in mid (same layout) for the mid-size sort.
 constexpr int kShortList = 4096;
+constexpr int kTinyList = 2048;
 __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t* __restrict__ counts,
                                                     uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ cursor,
                                                     int64_t pair_capacity, int64_t* stats,
-                                                    uint32_t* __restrict__ big) {
+                                                    uint32_t* __restrict__ big, uint32_t* __restrict__ mid) {
     typedef cub::BlockScan<unsigned long long, 1024> Scan;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ unsigned long long carry;
     if (threadIdx.x == 0) {
         carry = 0;
         big[0] = 0u;
+        mid[0] = 0u;
     }
     __syncthreads();
     // 8 consecutive tiles per thread and pass: one block scan covers 8192 tiles
@@ -318,6 +321,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
                 offsets[t] = (uint32_t)ex;
                 cursor[t] = (uint32_t)(ex + c0[k]);
                 if (c[k] > (unsigned long long)kShortList) big[1 + atomicAdd(&big[0], 1u)] = (uint32_t)t;
+                else if (c[k] > (unsigned long long)kTinyList) mid[1 + atomicAdd(&mid[0], 1u)] = (uint32_t)t;
             }
             ex += c[k];
         }
@@ -368,7 +372,10 @@ __device__ __forceinline__ void emit_one(int j, int t, uint32_t r, const BinAux&
     entries[pos] = r;
 }
 
-__global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __restrict__ stats,
+#ifndef SF_EMIT_MINB
+#define SF_EMIT_MINB 4
+#endif
+__global__ void __launch_bounds__(256, SF_EMIT_MINB) k_emit_pairs(int64_t N, const int64_t* __restrict__ stats,
                                                     const GeomRec* __restrict__ geom,
                                                     const uint64_t* __restrict__ row_keys, TileGrid g,
                                                     const BinAux* __restrict__ aux,
@@ -412,7 +419,8 @@ __global__ void __launch_bounds__(256) k_emit_pairs(int64_t N, const int64_t* __
     const MahalPre mp = mahal_pre(p.mx, p.my, p.a, p.b, p.c);
     for (int ty = a.ty0; ty < a.ty0 + (int)a.h; ++ty)
         for (int tx = a.tx0; tx < a.tx0 + w; ++tx)
-            if (tile_hit(mp, tx, ty, g)) emit_one(j++, ty * g.tiles_x + tx, tagged(tx, ty), a, offsets, base, cursor, entries);
+            if (tile_hit(mp, tx, ty, g))
+                emit_one(j++, ty * g.tiles_x + tx, tagged(tx, ty), a, offsets, base, cursor, entries);
 }
 
 // ---------------------------------------------------------------------------
@@ -644,60 +652,68 @@ __global__ void __launch_bounds__(256) k_tile_sort_large(const uint32_t* __restr
 // id order, so (key, row) compares exactly like (depth, id).  The keys of a
 // tile are gathered from the L2-resident key array (8 B per entry).
 //
-// Sort: MSD bucket pass in shared memory -- bucket = floor((key - min) *
-// NB / span) in fp64 (rounding is monotone, so buckets stay in key order),
+// Sort: MSD bucket pass in shared memory -- as many buckets as list slots,
+// bucket = (key - min) >> shift (monotone, so buckets stay in key order),
 // histogram, scan, scatter of entry indices into their buckets; then every
 // entry's final position is its bucket's start plus the number of bucket
 // members ordering before it on (key, row) -- each entry independently, so
 // there is no serial insertion chain (keys are unique as (key, row) pairs).
 template <int CAP>
 struct TileSortDepth {
-    static constexpr size_t kSmem = (size_t)CAP * (8 + 4 + 2);
+    // keys, rows, bucket order (CAP each), bucket starts and cursors (NB = CAP)
+    static constexpr size_t kSmem = (size_t)CAP * (8 + 4 + 2) + (size_t)(2 * CAP + 1) * 4;
 };
 
 __device__ __forceinline__ bool key_row_less(uint64_t ka, uint32_t ra, uint64_t kb, uint32_t rb) {
     return ka < kb || (ka == kb && ra < rb);
 }
 
-template <int CAP, int NB>
+#ifndef SF_TS_EXP
+#define SF_TS_EXP 0
+#endif
+template <int CAP, int NB, int NT>
 __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ entries, int lo_exclusive,
                                                     const uint64_t* __restrict__ row_keys,
                                                     uint8_t* __restrict__ flags);
 
-template <int CAP, int NB>
-__global__ void __launch_bounds__(256) k_tile_sort_depth(const uint32_t* __restrict__ offsets,
+// NT threads per CTA: the mid-size and long lists use 512 (shared memory caps
+// the CTAs per SM, so more warps per CTA hide the key-gather latency)
+template <int CAP, int NB, int NT>
+__global__ void __launch_bounds__(NT) k_tile_sort_depth(const uint32_t* __restrict__ offsets,
                                                          uint32_t* __restrict__ entries, int lo_exclusive,
                                                          const int64_t* __restrict__ stats,
                                                          const uint64_t* __restrict__ row_keys,
                                                          const uint32_t* __restrict__ big,
                                                          uint8_t* __restrict__ flags) {
-    static_assert(CAP <= 65536 && NB % 256 == 0, "index width / scan split");
+    static_assert(CAP <= 65536 && NB % NT == 0, "index width / scan split");
     if (stats[SF_STAT_OVERFLOW]) return;
     if (!big) {
-        tile_sort_depth_one<CAP, NB>(blockIdx.x, offsets, entries, lo_exclusive, row_keys, flags);
+        tile_sort_depth_one<CAP, NB, NT>(blockIdx.x, offsets, entries, lo_exclusive, row_keys, flags);
         return;
     }
     // long lists only: the tiles k_tile_scan listed
     const int nb = (int)big[0];
     for (int i = blockIdx.x; i < nb; i += gridDim.x) {
-        tile_sort_depth_one<CAP, NB>((int)big[1 + i], offsets, entries, lo_exclusive, row_keys, flags);
+        tile_sort_depth_one<CAP, NB, NT>((int)big[1 + i], offsets, entries, lo_exclusive, row_keys, flags);
         __syncthreads();
     }
 }
 
-template <int CAP, int NB>
+template <int CAP, int NB, int NT>
 __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ entries, int lo_exclusive,
                                                     const uint64_t* __restrict__ row_keys,
                                                     uint8_t* __restrict__ flags) {
+    constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char ts_smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(ts_smem);           // CAP
     uint32_t* rows = reinterpret_cast<uint32_t*>(keys + CAP);       // CAP
     uint16_t* order = reinterpret_cast<uint16_t*>(rows + CAP);      // CAP: entry indices grouped by bucket
-    __shared__ uint32_t start[NB + 1];
-    __shared__ uint32_t cursor[NB];
-    __shared__ unsigned long long w_min[8], w_max[8];  // per warp (256 threads)
+    uint32_t* start = reinterpret_cast<uint32_t*>(order + CAP);     // NB + 1
+    uint32_t* cursor = start + NB + 1;                              // NB
+    static_assert(NB == CAP && CAP % 4 == 0, "one bucket per entry slot; 4-byte aligned bucket arrays");
+    __shared__ unsigned long long w_min[NW], w_max[NW];  // per warp
     const uint32_t beg = offsets[t], end = offsets[t + 1];
     const int n = (int)(end - beg);
     if (n <= lo_exclusive || n > CAP) return;
@@ -740,19 +756,22 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
     }
     __syncthreads();
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < NW; ++w) {
         mn = min(mn, w_min[w]);
         mx = max(mx, w_max[w]);
     }
     const uint64_t kmin = mn;
-    const double bscale = (double)NB / ((double)(mx - kmin) + 1.0);
-    auto bucket_of = [&](uint64_t k) { return min(NB - 1, (int)((double)(k - kmin) * bscale)); };
+    // bucket = (key - min) >> shift, the smallest shift that maps the span
+    // below NB: monotone in the key, between NB / 2 and NB buckets used
+    const uint64_t span = mx - kmin;
+    const int shift = max(0, 64 - __clzll((long long)span) - __ffs(NB) + 1);
+    auto bucket_of = [&](uint64_t k) { return (int)((k - kmin) >> shift); };
     for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cursor[bucket_of(keys[i])], 1u);
     __syncthreads();
     {
-        typedef cub::BlockScan<uint32_t, 256> Scan;
+        typedef cub::BlockScan<uint32_t, NT> Scan;
         __shared__ typename Scan::TempStorage tmp;
-        constexpr int PER = NB / 256;
+        constexpr int PER = NB / NT;
         uint32_t c[PER], sum = 0;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
@@ -769,7 +788,7 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
             cursor[b] = ex;
             ex += c[j];
         }
-        if (threadIdx.x == 255) start[NB] = ex;
+        if (threadIdx.x == NT - 1) start[NB] = ex;
     }
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) order[atomicAdd(&cursor[bucket_of(keys[i])], 1u)] = (uint16_t)i;
@@ -785,10 +804,14 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
         const int b = bucket_of(ki);
         const int q0 = (int)start[b], q1 = (int)start[b + 1];
         int r = q0;
+#if SF_TS_EXP == 2  // experiment only (wrong order): no in-bucket ranking
+        r = p;
+#else
         for (int q = q0; q < q1; ++q) {
             const int j = order[q];
             r += key_row_less(keys[j], rows[j] & kEntryRowMask, ki, ri) ? 1 : 0;
         }
+#endif
         e[r] = ri;
         flags[beg + r] = (uint8_t)(rows[i] >> kEntryFlagShift);
     }
@@ -895,25 +918,31 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
     } else if (blocks) {
         k_count_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, row_keys, g, tile_counts, aux);
     }
-    uint32_t* big = tile_cursor + n_tiles;  // long-list tiles (tile_cursor holds 2 n_tiles + 1)
+    uint32_t* big = tile_cursor + n_tiles;  // long-list tiles (tile_cursor holds 3 n_tiles + 2)
+    uint32_t* mid = big + n_tiles + 1;      // mid-size lists
     k_tile_scan<<<1, 1024, 0, st>>>(n_tiles, tile_counts, tile_offsets, tile_cursor, pair_capacity,
-                                    const_cast<int64_t*>(stats), big);
+                                    const_cast<int64_t*>(stats), big, mid);
     if (blocks)
         k_emit_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, row_keys, g, aux, tile_offsets, tile_cursor,
                                              entries, agg ? cta_base : nullptr, per);
     if (row_keys) {
         // frame mode: each tile's rows into (depth, row) order -- the canonical
         // order, since scene rows are id-ordered; no global depth sort
-        constexpr size_t s1 = TileSortDepth<4096>::kSmem, s2 = TileSortDepth<8192>::kSmem;
-        ensure_smem_attr((const void*)k_tile_sort_depth<4096, 1024>, s1);
-        ensure_smem_attr((const void*)k_tile_sort_depth<8192, 2048>, s2);
-        // one CTA per tile for the common lists; the rare longer ones by a
-        // one-wave grid striding over the tiles k_tile_scan listed
+        constexpr size_t s0 = TileSortDepth<2048>::kSmem, s1 = TileSortDepth<4096>::kSmem,
+                         s2 = TileSortDepth<8192>::kSmem;
+        ensure_smem_attr((const void*)k_tile_sort_depth<2048, 2048, 256>, s0);
+        ensure_smem_attr((const void*)k_tile_sort_depth<4096, 4096, 512>, s1);
+        ensure_smem_attr((const void*)k_tile_sort_depth<8192, 8192, 512>, s2);
+        // one CTA per tile for the common lists (<= 2048 entries: 28 KB of
+        // shared memory, 6 CTAs per SM); the longer ones by grids striding
+        // over the tiles k_tile_scan listed
         const int sms = device_sm_count();
-        static_assert(kShortList == 4096, "short-list capacity");
-        k_tile_sort_depth<4096, 1024><<<n_tiles, 256, s1, st>>>(tile_offsets, entries, 0, stats, row_keys, nullptr,
-                                                                 entry_flags);
-        k_tile_sort_depth<8192, 2048><<<std::min(n_tiles, sms), 256, s2, st>>>(tile_offsets, entries, 4096, stats,
+        static_assert(kShortList == 4096 && kTinyList == 2048, "list-size classes");
+        k_tile_sort_depth<2048, 2048, 256><<<n_tiles, 256, s0, st>>>(tile_offsets, entries, 0, stats, row_keys, nullptr,
+                                                                entry_flags);
+        k_tile_sort_depth<4096, 4096, 512><<<std::min(n_tiles, 3 * sms), 512, s1, st>>>(tile_offsets, entries, 2048, stats,
+                                                                                  row_keys, mid, entry_flags);
+        k_tile_sort_depth<8192, 8192, 512><<<std::min(n_tiles, sms), 512, s2, st>>>(tile_offsets, entries, 4096, stats,
                                                                               row_keys, big, entry_flags);
         k_tile_sort_depth_large<<<std::min(n_tiles, sms), 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192,
                                                                         stats, row_keys, big, entry_flags);

@@ -1340,7 +1340,10 @@ int launch_splat_transpose(const BlendArgs& a, const float* dW, float* ghat, int
 // steps.  T before an entry = T before the round x the product of the earlier
 // warps' (1 - alpha) x the warp's exclusive prefix product.
 constexpr int kFxWarps = 8;
-__global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) {
+#ifndef SF_FX_EXP
+#define SF_FX_EXP 0
+#endif
+__global__ void __launch_bounds__(32 * kFxWarps, 3) k_blend_fixup_cta(BlendArgs A) {
     __shared__ double wl[kChBlock];
     __shared__ float wf[kChBlock];
     __shared__ double pv[32 * kFxWarps][kMaxC];
@@ -1376,7 +1379,7 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
         const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
         // the next round's entry is loaded (and its record prefetched) one round ahead
         uint32_t r_next = (beg + (uint32_t)tid < end) ? A.entries[beg + tid] : 0u;
-        for (uint32_t r0 = beg; r0 < end; r0 += 32 * kFxWarps) {
+        for (uint32_t r0 = beg; r0 < (SF_FX_EXP == 2 ? beg : end); r0 += 32 * kFxWarps) {
             const double T = Tround;
             const uint32_t i = r0 + (uint32_t)(wid * 32 + lane);
             double al = 0.0;
@@ -1480,7 +1483,7 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
         if (A.coeff_map)
             for (int c = tid; c < A.n_ch; c += blockDim.x) A.coeff_map[pix * A.n_ch + c] = (float)wl[c];
         if (tid == 0 && A.final_t) A.final_t[pix] = (float)Tend;
-        if (A.features) {
+        if (A.features && SF_FX_EXP != 1) {  // (SF_FX_EXP: timing experiments only)
             // the fused decode used the fp32 tile: redo this pixel's features from
             // the exact coefficients (fp32 FMA over L terms, ~4e-6 relative);
             // 8 outputs per thread at a time, as independent FMA chains
@@ -1499,7 +1502,21 @@ __global__ void __launch_bounds__(32 * kFxWarps) k_blend_fixup_cta(BlendArgs A) 
                     wo[k] = b * A.L;
                     fv[k] = 0.f;
                 }
-                for (int l = 0; l < A.L; ++l) {
+                // 4 codebook rows in flight per chain (the loads are L2 hits:
+                // latency, not bandwidth, bounds this loop)
+                int l = 0;
+                for (; l + 4 <= A.L; l += 4) {
+                    float cv[4][8];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) cv[u][k] = __ldg(cbp[k] + (size_t)(l + u) * A.D);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) fv[k] = fmaf(wf[wo[k] + l + u], cv[u][k], fv[k]);
+                }
+                for (; l < A.L; ++l) {
 #pragma unroll
                     for (int k = 0; k < 8; ++k) fv[k] = fmaf(wf[wo[k] + l], __ldg(cbp[k] + (size_t)l * A.D), fv[k]);
                 }

@@ -18,7 +18,10 @@
 
 namespace sf {
 
-__global__ void __launch_bounds__(256) k_preprocess(SfScene s, SfCamera cam, GeomRec* __restrict__ geom,
+#ifndef SF_PRE_MINB
+#define SF_PRE_MINB 5
+#endif
+__global__ void __launch_bounds__(256, SF_PRE_MINB) k_preprocess(SfScene s, SfCamera cam, GeomRec* __restrict__ geom,
                                                     uint64_t* __restrict__ keys,
                                                     uint32_t* __restrict__ vals,
                                                     unsigned long long* __restrict__ n_visible) {
