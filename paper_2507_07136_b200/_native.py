@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libsplatfield_b200.so")
 SF_OK, SF_ERR_VALIDATION, SF_ERR_RESOURCE, SF_ERR_CUDA, SF_ERR_WORKSPACE = 0, 1, 2, 3, 4
 STAT_VISIBLE, STAT_PAIRS, STAT_OVERFLOW, STAT_LEVEL, STAT_ROW, STAT_COL, STAT_DEGENERATE = range(7)
 STAT_FIXUPS, STAT_LEVEL_ARGMAX = 7, 8  # STAT_LEVEL_ARGMAX + b: band-owned first argmax of block b
+CHAN_WORD = 129 * 4  # scatter-plan channel word = channel x this (sf_common.cuh kChanWord)
 STATF_MIN, STATF_MAX, STATF_LEVEL_MAX = 0, 1, 8  # STATF_LEVEL_MAX + n_levels + b: block b min
 
 P = ctypes.c_void_p

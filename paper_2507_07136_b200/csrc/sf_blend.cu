@@ -1483,7 +1483,10 @@ __global__ void __launch_bounds__(32 * kFxWarps, 3) k_blend_fixup_cta(BlendArgs 
         if (A.coeff_map)
             for (int c = tid; c < A.n_ch; c += blockDim.x) A.coeff_map[pix * A.n_ch + c] = (float)wl[c];
         if (tid == 0 && A.final_t) A.final_t[pix] = (float)Tend;
-        if (A.features && SF_FX_EXP != 1) {  // (SF_FX_EXP: timing experiments only)
+        if (A.features && A.fixup_w && idx < A.fixup_w_capacity) {
+            // the features are redone by k_fixup_decode for all replayed pixels at once
+            for (int c = tid; c < A.n_ch; c += blockDim.x) A.fixup_w[(size_t)idx * A.n_ch + c] = (float)wl[c];
+        } else if (A.features && SF_FX_EXP != 1) {  // (SF_FX_EXP: timing experiments only)
             // the fused decode used the fp32 tile: redo this pixel's features from
             // the exact coefficients (fp32 FMA over L terms, ~4e-6 relative);
             // 8 outputs per thread at a time, as independent FMA chains
@@ -1545,6 +1548,87 @@ __global__ void __launch_bounds__(32 * kFxWarps, 3) k_blend_fixup_cta(BlendArgs 
     }
 }
 
+// Features of the replayed pixels from their exact coefficients (fixup_w,
+// written by k_blend_fixup_cta): per CTA 32 pixels x 64 columns of one level,
+// the codebook slice and the pixels' coefficients staged in shared memory;
+// each output is the same fp32 FMA chain over l as the per-pixel recompute.
+// Work items (pixel block, level, column block) are strided over a fixed grid
+// (the pixel count is only known on the device).
+int device_sm_count();
+constexpr int kFdPix = 32, kFdCols = 64;
+__global__ void __launch_bounds__(256, 4) k_fixup_decode(BlendArgs A) {
+    __shared__ __align__(16) float cb[64][kFdCols];   // L <= 64 rows of the level's codebook slice
+    __shared__ float wrow[kFdPix][65];  // the block's pixels' coefficients of the level (padded)
+    __shared__ size_t pixs[kFdPix];
+    const uint32_t count = min(min(*A.fixup_count, A.fixup_capacity), A.fixup_w_capacity);
+    const int nblk = (int)((count + kFdPix - 1) / kFdPix), ncb = A.D / kFdCols;
+    const int items = nblk * A.n_levels * ncb;
+    const int L = A.L;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int pb = it / (A.n_levels * ncb), rem = it - pb * A.n_levels * ncb;
+        const int b = rem / ncb, n0 = (rem - b * ncb) * kFdCols;
+        const float* src = A.codebooks + (size_t)A.lv.lv[b] * L * A.D + n0;
+        {
+            // all loads in flight before the shared-memory stores (L2 latency, not bandwidth)
+            float cv[16], wv[8];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int i = threadIdx.x + u * 256, l = i / kFdCols;
+                cv[u] = l < L ? __ldg(src + (size_t)l * A.D + (i % kFdCols)) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = threadIdx.x + u * 256, p = i / 64, l = i % 64;
+                const uint32_t idx = (uint32_t)(pb * kFdPix + p);
+                wv[u] = (idx < count && l < L) ? A.fixup_w[(size_t)idx * A.n_ch + b * L + l] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int i = threadIdx.x + u * 256;
+                cb[i / kFdCols][i % kFdCols] = cv[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = threadIdx.x + u * 256;
+                wrow[i / 64][i % 64] = wv[u];
+            }
+        }
+        if (threadIdx.x < kFdPix) {
+            const uint32_t idx = (uint32_t)(pb * kFdPix + threadIdx.x);
+            size_t pix = ~(size_t)0;
+            if (idx < count) {
+                const uint32_t code = A.fixup_list[idx];
+                const int tile = (int)(code >> 8), slot = (int)(code & 255u);
+                const int w8 = slot >> 5, l8 = slot & 31;
+                const int px = (tile % A.tiles_x) * SF_TILE + (w8 & 1) * 8 + (l8 & 7);
+                const int py = (tile / A.tiles_x) * SF_TILE + (w8 >> 1) * 4 + (l8 >> 3);
+                pix = (size_t)py * A.W + px;
+            }
+            pixs[threadIdx.x] = pix;
+        }
+        __syncthreads();
+        // thread: pixel t / 8, columns 8 (t % 8) .. + 8
+        const int p = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 8;
+        float fv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fv[k] = 0.f;
+#pragma unroll 8
+        for (int l = 0; l < L; ++l) {
+            const float w = wrow[p][l];
+            const float4 q0 = *reinterpret_cast<const float4*>(&cb[l][c0]);  // 16-byte loads: conflict-free rows
+            const float4 q1 = *reinterpret_cast<const float4*>(&cb[l][c0 + 4]);
+            fv[0] = fmaf(w, q0.x, fv[0]), fv[1] = fmaf(w, q0.y, fv[1]), fv[2] = fmaf(w, q0.z, fv[2]), fv[3] = fmaf(w, q0.w, fv[3]);
+            fv[4] = fmaf(w, q1.x, fv[4]), fv[5] = fmaf(w, q1.y, fv[5]), fv[6] = fmaf(w, q1.z, fv[6]), fv[7] = fmaf(w, q1.w, fv[7]);
+        }
+        if (pixs[p] != ~(size_t)0) {
+            float4* dst = reinterpret_cast<float4*>(A.features + (size_t)b * A.feat_level_stride + pixs[p] * A.D + n0 + c0);
+            dst[0] = make_float4(fv[0], fv[1], fv[2], fv[3]);
+            dst[1] = make_float4(fv[4], fv[5], fv[6], fv[7]);
+        }
+        __syncthreads();
+    }
+}
+
 // k_splat_tc (sf_splat_tc.cu) is the frame path for L = 64, <= 3 levels and
 // 4 or no canonicals; k_blend serves the other shapes (wide / generic channel
 // blocks, other canonical counts).  SF_BLEND_IMPL=legacy forces k_blend
@@ -1589,7 +1673,10 @@ int launch_blend(const BlendArgs& a, cudaStream_t st) {
         if (n_tiles > 0) kern<<<dim3(2 * n_tiles, nblk), kCTAThreads, smem, st>>>(a, ch_block, fmap);
     }
     if (n_tiles > 0 && a.fixup_list && a.early_exit) {
-        if (a.n_ch <= kChBlock) k_blend_fixup_cta<<<1184, 32 * kFxWarps, 0, st>>>(a);
+        if (a.n_ch <= kChBlock) {
+            k_blend_fixup_cta<<<1184, 32 * kFxWarps, 0, st>>>(a);
+            if (a.features && a.fixup_w) k_fixup_decode<<<4 * device_sm_count(), 256, 0, st>>>(a);
+        }
         else k_blend_fixup<<<296, 32 * kFixWarps, 0, st>>>(a);
     }
     return 0;  // (relevancy for n_ch > one channel block: launch_relevancy_from_cmap by the caller)

@@ -101,6 +101,7 @@ struct FrameWs {
     void* sel_ws;
     float* dec_ws;
     float* dec_img;   // fused decode: pre-swizzled tf32 hi/lo codebook chunks
+    float* fixw;      // exact coefficients of replayed pixels for k_fixup_decode (kFixWPixels x channels)
     uint32_t* fixup;  // [0] = count, [1] = the splat's half-tile claim counter, [2, 4) pad, then the list
 };
 
@@ -120,6 +121,9 @@ static uint32_t fixup_capacity(int W, int H) {
 extern "C" int64_t sf_fixup_capacity(int32_t W, int32_t H) { return (int64_t)fixup_capacity(W, H); }
 
 static constexpr int kMaxCanon = 64;
+// replayed pixels whose features k_fixup_decode redoes in one batch (more: the
+// replay kernel redoes them itself)
+static constexpr uint32_t kFixWPixels = 16384;
 
 static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n_levels, int L,
                           int K, int D, int64_t pair_cap, FrameWs* ws) {
@@ -147,6 +151,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->dec_ws = c.take<float>(decode_ws_bytes(L, D) / sizeof(float));
     ws->dec_img = c.take<float>(blend_dec_image_bytes(n_levels, D) / sizeof(float));
     ws->fixup = c.take<uint32_t>((size_t)fixup_capacity(W, H) + 4);
+    ws->fixw = c.take<float>(D > 0 ? (size_t)kFixWPixels * n_levels * L : 1);
     return c.off;
 }
 
@@ -319,6 +324,10 @@ static int render_frame(const SfScene* s, const SfCamera* cam, const SfQuery* q,
         a.dec_scale = (const float*)((const char*)dec_img + blend_dec_image_bytes(f->n_levels, D) - 64);
         a.codebooks = s->codebooks;
         a.lv = lv;
+        if (L <= 64 && D % 64 == 0) {
+            a.fixup_w = ws.fixw;
+            a.fixup_w_capacity = kFixWPixels;
+        }
     }
     if (f->events[4]) cudaEventRecord((cudaEvent_t)f->events[4], st);
     if (launch_blend(a, st)) return fail(SF_ERR_VALIDATION, "blend configuration unsupported");

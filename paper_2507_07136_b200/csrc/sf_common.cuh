@@ -274,6 +274,8 @@ struct BlendArgs {
     uint32_t* fixup_count;
     uint32_t fixup_capacity;
     uint32_t* sched;       // [0]: next half tile to claim (tensor-core splat), zeroed per frame
+    float* fixup_w;        // exact coefficients of the replayed pixels (fused decode), or null
+    uint32_t fixup_w_capacity;
     float* coeff_map;      // (H,W,n_ch) or null
     float* final_t;        // (H,W) or null
     // fused projected-codebook relevancy (optional)

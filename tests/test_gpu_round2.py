@@ -66,3 +66,39 @@ def test_render_dense_zero_channels_is_a_real_frame(rng):
     assert stats.pairs_blended == ref.pairs_blended > 0
     np.testing.assert_allclose(stats.final_transmittance, ref.final_transmittance, atol=1e-6)
     assert stats.final_transmittance.min() < 1.0
+
+
+@pytest.mark.gpu
+def test_device_topk_and_adam_match_numpy():
+    """materialize / normalize_coefficients (k_train_plan) and OptimState.step
+    (k_train_adam) against numpy restatements of train.py:79-139."""
+    import paper_2507_07136_b200 as sf
+    from paper_2507_07136_b200 import train as T
+    rng = np.random.default_rng(5)
+    lg = rng.standard_normal((2, 300, 64)) * 3
+    lg[0, 0, 9] = lg[0, 0, 5]  # an exact tie: the lower index first (stable argsort of -p)
+    idx, vals = T._device_topk(lg, 4)
+    p = np.exp(lg - lg.max(-1, keepdims=True))
+    p /= p.sum(-1, keepdims=True)
+    ref = np.sort(np.argsort(-p, axis=-1, kind="stable")[..., :4], axis=-1)
+    assert np.array_equal(idx, ref)
+    kept = np.take_along_axis(p, ref, -1)
+    kept /= kept.sum(-1, keepdims=True)
+    assert np.abs(vals - kept).max() <= 1e-6
+    c = sf.normalize_coefficients(lg[1, 7], 4)
+    assert np.array_equal(c.indices, ref[1, 7]) and np.abs(c.values - kept[1, 7]).max() <= 1e-6
+    # Adam: two steps on both parameter groups
+    fld = T.TrainableField(logits=lg.copy(), codebooks=rng.standard_normal((2, 64, 8)))
+    opt = T.OptimState(0.05, 0.02, 0.9, 0.999, 1e-8)
+    ref_p = [fld.logits.copy(), fld.codebooks.copy()]
+    m = [np.zeros_like(x) for x in ref_p]
+    v = [np.zeros_like(x) for x in ref_p]
+    for t in (1, 2):
+        g = T.Gradients(logits=rng.standard_normal(lg.shape), codebooks=rng.standard_normal((2, 64, 8)))
+        opt.step(fld, g)
+        for k, (gr, lr) in enumerate(((g.logits, 0.05), (g.codebooks, 0.02))):
+            m[k] += (1 - 0.9) * (gr - m[k])
+            v[k] += (1 - 0.999) * (gr * gr - v[k])
+            ref_p[k] -= lr * (m[k] / (1 - 0.9 ** t)) / (np.sqrt(v[k] / (1 - 0.999 ** t)) + 1e-8)
+    assert np.abs(fld.logits - ref_p[0]).max() <= 1e-12
+    assert np.abs(fld.codebooks - ref_p[1]).max() <= 1e-12
