@@ -17,24 +17,28 @@
 // scaling keeps the lo parts normal down to 2^-15, below which the absolute
 // error is < 2^-37).  W' = 2^24 W exactly.
 //
-// CTA = one SM (persistent, half tiles blockIdx.x + i gridDim.x), 11 warps:
-//   warps 0-3  blend: pixel = TMEM lane (warp w owns lanes 32w..32w+31, an
-//              8x4 patch).  Per batch: conservative patch test (ballot), fp32
-//              alpha with the fp64 guard band, T walk, e -> E rows (fp16
-//              hi/lo, 16-byte stores).  Per tile: W from TMEM, fused
-//              relevancy (fp64), final T, early-exit ambiguity list, and the
-//              in-place conversion of W into the decode's A operand.
-//   warps 4-7  drain (DEC): accumulator -> registers -> 128B-swizzled boxes ->
-//              TMA stores of features[level][y][x][col].
-//   warp 8     producer: tile lists -> record ring (cp.async), sparse codes
-//              -> dense V^T stage (scatter of 12 hi/lo pairs per entry; the
-//              previous batch's 12 positions are cleared, not the whole stage).
-//   warp 9     E V issuer (one thread): each batch's products into the W
+// CTA = one SM (persistent; half tiles claimed dynamically through A.sched),
+// 16 warps:
+//   warps 0-7  blend: two per TMEM lane quarter (an 8x4 pixel patch); warp
+//              hb = w >> 2 takes entries [16 hb, 16 hb + 16) of each batch.
+//              Per batch: conservative patch test (ballot), fp32 alpha with
+//              the fp64 guard band, the transmittance walk handed between the
+//              pair, e -> E rows (fp16 hi/lo).  Per tile: W from TMEM (each
+//              warp its own 32 columns per level), fused relevancy (fp64; the
+//              pair's partial dots meet in E stage memory), final T, the
+//              early-exit ambiguity list, and the in-place conversion of W
+//              into the decode's A operand.
+//   warps 8-11 drains (fused decode): accumulator -> registers -> 128B-swizzled
+//              boxes -> TMA stores of features[level][y][x][col].
+//   warp 12    producer: claims half tiles; tile lists -> record ring
+//              (cp.async), sparse codes -> dense V^T stage (the previous
+//              batch's 12 positions are cleared, not the whole stage).
+//   warp 13    E V issuer (one thread): each batch's products into the W
 //              slot of the blending tile.
-//   warp 10    decode issuer (one thread): the 3-term fp16 decode chunks
-//              (A = W from TMEM, B = codebook chunk by bulk copy) of the
-//              previous tile.  Both issuers block on mbarriers (no polling);
-//              each one's tcgen05.commit tracks only its own products.
+//   warp 14    decode issuer (one thread): the 3-term fp16 decode chunks
+//              (A = W from TMEM, B = codebook chunk) of the previous tile.
+//   warp 15    codebook chunk loader (one thread, sleeps on its mbarrier).
+//   Issuers block on mbarriers; each tcgen05.commit tracks only its own products.
 // TMEM (512 columns): W/A slots [0,192) and [192,384) alternate by tile;
 // two 64-column decode accumulators at [384,512).
 #include <cuda.h>

@@ -94,6 +94,11 @@ def timeline_report():
               f"over {len(dec)} non-empty tiles of {n}")
         d = np.diff(t[:n, :11], axis=0) / 1965.0
         print("  mean per-tile period (us): " + " ".join(f"{x[:6]}={v:.2f}" for x, v in zip(names, d.mean(axis=0))))
+        dr = (t[:n, 11] > 0) & (t[:n, 2] > 0) & (t[:n, 12] == 0)
+        if dr.any():  # fused decode: the drains run the W epilogue (stamps 11 = w_full, 2 = done)
+            tt = t[:n][dr]
+            print("  drain epilogue (us, drain 0, mean over %d tiles): blend_end->w_full %.2f, epilogue %.2f" % (
+                dr.sum(), ((tt[:, 11] - tt[:, 1]) / 1965.0).mean(), ((tt[:, 2] - tt[:, 11]) / 1965.0).mean()))
         ok = (t[:n, 11] > 0) & (t[:n, 12] > 0) & (t[:n, 13] > 0) & (t[:n, 14] > 0)
         if ok.any():
             tt = t[:n][ok]
