@@ -668,9 +668,6 @@ __device__ __forceinline__ bool key_row_less(uint64_t ka, uint32_t ra, uint64_t 
     return ka < kb || (ka == kb && ra < rb);
 }
 
-#ifndef SF_TS_EXP
-#define SF_TS_EXP 0
-#endif
 template <int CAP, int NB, int NT>
 __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ entries, int lo_exclusive,
@@ -804,14 +801,10 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
         const int b = bucket_of(ki);
         const int q0 = (int)start[b], q1 = (int)start[b + 1];
         int r = q0;
-#if SF_TS_EXP == 2  // experiment only (wrong order): no in-bucket ranking
-        r = p;
-#else
         for (int q = q0; q < q1; ++q) {
             const int j = order[q];
             r += key_row_less(keys[j], rows[j] & kEntryRowMask, ki, ri) ? 1 : 0;
         }
-#endif
         e[r] = ri;
         flags[beg + r] = (uint8_t)(rows[i] >> kEntryFlagShift);
     }

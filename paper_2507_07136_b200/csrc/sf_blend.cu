@@ -1340,9 +1340,6 @@ int launch_splat_transpose(const BlendArgs& a, const float* dW, float* ghat, int
 // steps.  T before an entry = T before the round x the product of the earlier
 // warps' (1 - alpha) x the warp's exclusive prefix product.
 constexpr int kFxWarps = 8;
-#ifndef SF_FX_EXP
-#define SF_FX_EXP 0
-#endif
 __global__ void __launch_bounds__(32 * kFxWarps, 3) k_blend_fixup_cta(BlendArgs A) {
     __shared__ double wl[kChBlock];
     __shared__ float wf[kChBlock];
@@ -1379,7 +1376,7 @@ __global__ void __launch_bounds__(32 * kFxWarps, 3) k_blend_fixup_cta(BlendArgs 
         const uint32_t beg = A.tile_offsets[tile], end = A.tile_offsets[tile + 1];
         // the next round's entry is loaded (and its record prefetched) one round ahead
         uint32_t r_next = (beg + (uint32_t)tid < end) ? A.entries[beg + tid] : 0u;
-        for (uint32_t r0 = beg; r0 < (SF_FX_EXP == 2 ? beg : end); r0 += 32 * kFxWarps) {
+        for (uint32_t r0 = beg; r0 < end; r0 += 32 * kFxWarps) {
             const double T = Tround;
             const uint32_t i = r0 + (uint32_t)(wid * 32 + lane);
             double al = 0.0;
@@ -1486,7 +1483,7 @@ __global__ void __launch_bounds__(32 * kFxWarps, 3) k_blend_fixup_cta(BlendArgs 
         if (A.features && A.fixup_w && idx < A.fixup_w_capacity) {
             // the features are redone by k_fixup_decode for all replayed pixels at once
             for (int c = tid; c < A.n_ch; c += blockDim.x) A.fixup_w[(size_t)idx * A.n_ch + c] = (float)wl[c];
-        } else if (A.features && SF_FX_EXP != 1) {  // (SF_FX_EXP: timing experiments only)
+        } else if (A.features) {
             // the fused decode used the fp32 tile: redo this pixel's features from
             // the exact coefficients (fp32 FMA over L terms, ~4e-6 relative);
             // 8 outputs per thread at a time, as independent FMA chains
