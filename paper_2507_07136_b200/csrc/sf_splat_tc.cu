@@ -515,26 +515,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             const float pxf = (float)px, pyf = (float)py;
             const double pxd = (double)px, pyd = (double)py;
             const float pdx0 = (float)(x0 + (w8 & 1) * 8), pdy0 = (float)(y0 + (w8 >> 1) * 4);
-            float T = 1.f, eb = 0.f, Tprev = 1.f;
-            int ncontrib = 0, nbatches = 0;
+            // this warp's entries only: T after / before its last counted entry,
+            // error bound, count, batch of that entry + 1 (merged at the tile end)
+            float Tw = 1.f, Tpw = 1.f, ebw = 0.f;
+            int nw = 0, lastw = 0, nbatches = 0;
+            float Trun = 1.f;  // hb 0: the running transmittance entering the batch
             bool tile_hit = false;  // some batch of this tile had a candidate for this warp
             bool done = !inside;
             if (warp == 0 && lane == 0) SF_STAMP(A, it, 0);
             bool all_done = __all_sync(0xffffffffu, done);
             bool counted = all_done;
             if (all_done && lane == 0) atomicAdd(&S.done_count, 1);
-            float Tr = 1.f;  // running transmittance over every entry (T: after the last counted one)
-            auto recv = [&](int id) {
+            // the pair's hand-off carries only the running transmittance: each warp
+            // folds prod (1 - a) over its candidates into its alpha phase and passes
+            // T_in prod on at once, before its own walk (the walk is off the chain)
+            auto recv = [&](int id) -> float {
                 named_bar_sync(id, 64);
-                const float4 st = hand_in[lane];
-                T = st.x, Tprev = st.y, eb = st.z;
-                const int c = __float_as_int(st.w);
-                ncontrib = c & 0x7FFFFFFF;
-                done = c < 0;
-                Tr = done ? 0.f : T;  // once done nothing counts again; else Tr == T
+                return hand_in[lane].x;
             };
-            auto post = [&](int id) {
-                hand_out[lane] = make_float4(T, Tprev, eb, __int_as_float(ncontrib | (done ? (int)0x80000000 : 0)));
+            auto post = [&](int id, float t) {
+                hand_out[lane].x = t;
                 asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
             };
             for (;;) {
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 SF_TIMED(w0, bar_wait(&S.rec_full[s], (bs / kStages) & 1));
                 const int nb = *reinterpret_cast<volatile int*>(&S.nb[s]);
                 if (nb == 0) {
-                    if (hb == 0 && nbatches > 0) recv(bar_ba);  // the tile's final state
+                    if (hb == 0 && nbatches > 0) Trun = recv(bar_ba);  // the running T after the tile
                     __syncwarp();
                     if (lane == 0) bar_arrive(&S.ev_full[s]);
                     ++bs;
@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 // ---- alphas of this warp's candidates (before the hand-off) ----
                 const uint64_t ta0 = prof ? clock64() : 0;
                 uint32_t wmask = 0;
+                float P = 1.f;  // prod (1 - a) over this warp's candidates, in depth order
                 if (!all_done) {
                     bool hit = false;
                     if (lane < 16 && e0 + lane < nb) {
@@ -589,8 +590,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                                     alv[u] = blend_alpha_exact(G[e0 + jj[u]], A.geom + S.row[s][e0 + jj[u]], pxd, pyd);
                         }
 #pragma unroll
-                        for (int u = 0; u < 8; ++u)
+                        for (int u = 0; u < 8; ++u) {
                             if (c0 + u < 16) asc[(c0 + u) * 32 + lane] = alv[u];
+                            if (jj[u] >= 0) P = fmaf(-alv[u], P, P);
+                        }
                     }
                 }
                 // ---- E half-row: zero, then the candidates' e (hi, lo) ----
@@ -603,8 +606,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 zero_mask = wmask ? (zero_mask & ~(1u << s)) : (zero_mask | (1u << s));
                 // ---- hand-off in, transmittance walk in depth order, hand-off out ----
                 if (prof) w1 += clock64() - ta0;
-                if (hb == 1) SF_TIMED(w0, recv(bar_ab));
-                else if (nbatches > 0) SF_TIMED(w0, recv(bar_ba));
+                float Tr;  // running transmittance before this warp's entries of the batch
+                if (hb == 1) {
+                    SF_TIMED(w0, Tr = recv(bar_ab));
+                } else {
+                    if (nbatches > 0) SF_TIMED(w0, Trun = recv(bar_ba));
+                    Tr = Trun;
+                }
+                post(hb == 0 ? bar_ab : bar_ba, Tr * P);
                 const uint64_t tw0 = prof ? clock64() : 0;
                 {
                     int c = 0;
@@ -620,11 +629,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                         const bool live = al > 0.f && inside && (!early_exit || Tr >= (float)SF_EARLY_EXIT_T);
                         const float alive = live ? al : 0.f;
                         const float e = alive * Tr;
-                        Tprev = live ? Tr : Tprev;
+                        Tpw = live ? Tr : Tpw;
                         Tr = fmaf(-al, Tr, Tr);
-                        T = live ? Tr : T;
-                        eb = fmaf(alive, rcp_approx(1.f - alive), eb);  // 1 - alive in [0.01, 1]
-                        ncontrib += live ? 1 : 0;
+                        Tw = live ? Tr : Tw;
+                        ebw = fmaf(alive, rcp_approx(1.f - alive), ebw);  // 1 - alive in [0.01, 1]
+                        nw += live ? 1 : 0;
+                        lastw = live ? nbatches + 1 : lastw;
                         const float x = e * kScale;
                         const __half h = __float2half_rn(x);
                         const __half l = __float2half_rn(x - __half2float(h));
@@ -634,7 +644,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     }
                 }
                 done = !inside || (early_exit && Tr < (float)SF_EARLY_EXIT_T);
-                post(hb == 0 ? bar_ab : bar_ba);
                 if (prof) w2 += clock64() - tw0;
                 ++nbatches;
                 // batches without a candidate in any warp have E = 0: the issuer skips them
@@ -662,18 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             const bool wvalid = *reinterpret_cast<volatile uint32_t*>(&S.tile_tag[slot]) == (uint32_t)it + 1u;
 
             // ---- per-tile epilogue: hb 0 takes columns [0, 32) of each level, hb 1 [32, 64) ----
-            if (hb == 0 && inside && A.early_exit && A.fixup_list) {
-                // early-exit decisions fp32 cannot certify: replayed in fp64 by k_blend_fixup_cta
-                const float tol = fmaf(4e-6f, eb, fmaf(3e-7f, (float)ncontrib, 2e-6f));
-                const float thr = (float)SF_EARLY_EXIT_T;
-                const bool amb = done ? (Tprev < thr * (1.f + tol) || T > thr * (1.f - tol)) : (T < thr * (1.f + tol));
-                if (amb) {
-                    const uint32_t k = atomicAdd(A.fixup_count, 1u);
-                    if (k < A.fixup_capacity) A.fixup_list[k] = ((uint32_t)tile << 8) | (uint32_t)(half * 128 + m);
-                }
-            }
-            if (hb == 0 && A.final_t && inside) A.final_t[(size_t)py * A.W + px] = T;
-            const bool any = __any_sync(0xffffffffu, ncontrib > 0);
+            const bool any = __any_sync(0xffffffffu, nw > 0);  // this warp's entries contributed somewhere
             if (lane == 0 && hb == 0) SF_PROG(A, 1 + cw, (uint32_t)it, 0x10000u | (uint32_t)bs);
             SF_TIMED(w0, bar_wait(&S.w_full[slot], (it >> 1) & 1));
             if (warp == 0 && lane == 0) SF_STAMP(A, it, 12);
@@ -681,9 +679,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             // published only now: the W slot's previous tile (it - 2) has been
             // fully decoded (its slot_free preceded this tile's E V products),
             // so the decode issuer has read that tile's flag
-            if (hb == 0 && lane == 0) {
-                if (any) atomicOr(&S.contrib[slot], 1u << cw);
-                else atomicAnd(&S.contrib[slot], ~(1u << cw));
+            if (lane == 0) {
+                if (any) atomicOr(&S.contrib[slot], 1u << warp);
+                else atomicAnd(&S.contrib[slot], ~(1u << warp));
             }
             tc_after();
             const uint32_t wslot = tm + lane_off + (uint32_t)(slot * kSlotCols);
@@ -779,14 +777,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 bar_arrive(DEC ? &S.a_ready[slot] : &S.slot_free[slot]);
             }
             if (warp == 0 && lane == 0) SF_STAMP(A, it, 14);
-            if (rel) {
-                // hb 1 -> hb 0: partial dots posted (bar_ba, as after a batch walk);
-                // hb 0 -> hb 1: read (bar_rd), hb 1 may write E again
-                if (hb == 1) {
-                    asm volatile("bar.arrive %0, 64;" ::"r"(bar_ba) : "memory");
-                    named_bar_sync(bar_rd, 64);
-                } else {
-                    named_bar_sync(bar_ba, 64);
+            // hb 1 -> hb 0 (bar_ba, as after a batch): its per-pixel state and,
+            // fused relevancy, its partial dots; hb 0 -> hb 1 (bar_rd): read,
+            // hb 1 may write E / post again
+            if (hb == 1) {
+                hand_out[lane] = make_float4(Tw, Tpw, ebw, __int_as_float((nw << 12) | lastw));
+                asm volatile("bar.arrive %0, 64;" ::"r"(bar_ba) : "memory");
+                named_bar_sync(bar_rd, 64);
+            } else {
+                named_bar_sync(bar_ba, 64);
+                const float4 st1 = hand_in[lane];
+                if (rel) {
 #pragma unroll 1
                     for (int b = 0; b < n_levels; ++b) {
                         const double2* p0 = reinterpret_cast<const double2*>(xslot(0, b));
@@ -797,10 +798,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                             np_minimum(np_minimum(a01.x + b01.x, a01.y + b01.y), np_minimum(a23.x + b23.x, a23.y + b23.y));
                         if (inside) A.relevancy_raw[(size_t)b * A.W * A.H + pix] = sigmoid2(dm);
                     }
-                    asm volatile("bar.arrive %0, 64;" ::"r"(bar_rd) : "memory");
                 }
-                zero_mask &= ~3u;  // the partials overwrote E rows of stages 0 and 1
+                asm volatile("bar.arrive %0, 64;" ::"r"(bar_rd) : "memory");
+                // the pixel's state: the later of the two warps' last counted entries
+                // (same batch: hb 1's entries come after hb 0's)
+                const int c1 = __float_as_int(st1.w), n1 = c1 >> 12, last1 = c1 & 0xFFF;
+                const bool one = n1 > 0 && last1 >= lastw;
+                const float T = one ? st1.x : Tw, Tprev = one ? st1.y : Tpw;
+                const float eb = ebw + st1.z;
+                const int ncontrib = nw + n1;
+                const float thr = (float)SF_EARLY_EXIT_T;
+                const bool pdone = !inside || (early_exit && Trun < thr);
+                if (inside && early_exit && A.fixup_list) {
+                    // early-exit decisions fp32 cannot certify: replayed in fp64 by k_blend_fixup_cta
+                    const float tol = fmaf(4e-6f, eb, fmaf(3e-7f, (float)ncontrib, 2e-6f));
+                    const bool amb = pdone ? (Tprev < thr * (1.f + tol) || T > thr * (1.f - tol)) : (T < thr * (1.f + tol));
+                    if (amb) {
+                        const uint32_t k = atomicAdd(A.fixup_count, 1u);
+                        if (k < A.fixup_capacity) A.fixup_list[k] = ((uint32_t)tile << 8) | (uint32_t)(half * 128 + m);
+                    }
+                }
+                if (A.final_t && inside) A.final_t[pix] = T;
             }
+            if (rel) zero_mask &= ~3u;  // the partials overwrote E rows of stages 0 and 1
             if (warp == 0 && lane == 0) SF_STAMP(A, it, 2);
         }
     } else if (warp < kDrainWarp0 + 4) {
