@@ -584,7 +584,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                             anyamb |= gb;
                         }
                         if (__any_sync(0xffffffffu, anyamb)) {
-#pragma unroll 1
+                            // rare; unrolled so alv stays in registers (a rolled loop
+                            // indexes it dynamically and spills it on the common path)
+#pragma unroll
                             for (int u = 0; u < 8; ++u)
                                 if (amb & (1u << u))
                                     alv[u] = blend_alpha_exact(G[e0 + jj[u]], A.geom + S.row[s][e0 + jj[u]], pxd, pyd);
