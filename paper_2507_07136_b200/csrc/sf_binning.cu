@@ -229,6 +229,9 @@ __global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t p
                                                          uint32_t* __restrict__ cta_base) {
     extern __shared__ uint32_t hist[];
     const int n_tiles = g.tiles_x * g.tiles_y;
+    // the in-tile slots of the thread's current item (shared memory, not registers:
+    // the fp64 tile test already needs most of the register budget)
+    __shared__ uint32_t spos[512][kBinSlots];
     for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) hist[t] = 0;
     __syncthreads();
     const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(N, i0 + per);
@@ -240,31 +243,27 @@ __global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t p
         cand_rect(p, g, tx0, tx1, ty0, ty1);
         const MahalPre mp = mahal_pre(p.mx, p.my, p.a, p.b, p.c);
         const MahalPre32 mf = mahal_pre32(mp);
-        BinAux a;
-        a.mask = 0;
-        a.tx0 = (uint16_t)tx0;
-        a.ty0 = (uint16_t)ty0;
-        a.w = (uint16_t)(tx1 - tx0 + 1);
-        a.h = (uint16_t)max(0, ty1 - ty0 + 1);
-#pragma unroll
-        for (int k = 0; k < kBinSlots; ++k) a.pos[k] = 0;
+        unsigned long long mask = 0;
+        uint32_t* pos_k = spos[threadIdx.x];
         int bit = 0, nh = 0;
         for (int ty = ty0; ty <= ty1; ++ty)
             for (int tx = tx0; tx <= tx1; ++tx, ++bit) {
                 if (tile_hit_fast(mp, mf, tx, ty, g)) {
                     const int t = ty * g.tiles_x + tx;
-                    if (nh < kBinSlots) {
-                        const uint32_t pos = atomicAdd(&hist[t], 1u);
-#pragma unroll
-                        for (int k = 0; k < kBinSlots; ++k)
-                            if (k == nh) a.pos[k] = pos;
-                    } else {
-                        atomicAdd(&tile_counts[n_tiles + t], 1u);
-                    }
+                    if (nh < kBinSlots) pos_k[nh] = atomicAdd(&hist[t], 1u);
+                    else atomicAdd(&tile_counts[n_tiles + t], 1u);
                     ++nh;
-                    if (bit < 64) a.mask |= 1ull << bit;
+                    if (bit < 64) mask |= 1ull << bit;
                 }
             }
+        BinAux a;
+        a.mask = mask;
+        a.tx0 = (uint16_t)tx0;
+        a.ty0 = (uint16_t)ty0;
+        a.w = (uint16_t)(tx1 - tx0 + 1);
+        a.h = (uint16_t)max(0, ty1 - ty0 + 1);
+#pragma unroll
+        for (int k = 0; k < kBinSlots; ++k) a.pos[k] = k < nh ? pos_k[k] : 0u;
         const uint4* src = reinterpret_cast<const uint4*>(&a);
         uint4* dst = reinterpret_cast<uint4*>(aux + i);
 #pragma unroll
@@ -303,12 +302,13 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
     constexpr int kPer = 8;
     for (int base = 0; base < n_tiles; base += 1024 * kPer) {
         const int t0 = base + threadIdx.x * kPer;
-        unsigned long long c0[kPer], c[kPer], sum = 0;
+        uint32_t c0[kPer], c[kPer];  // per-tile counts fit 32 bits (the pair total may not)
+        unsigned long long sum = 0;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const int t = t0 + k;
-            c0[k] = (t < n_tiles) ? counts[t] : 0;
-            c[k] = (t < n_tiles) ? c0[k] + counts[n_tiles + t] : 0;
+            c0[k] = (t < n_tiles) ? counts[t] : 0u;
+            c[k] = (t < n_tiles) ? c0[k] + counts[n_tiles + t] : 0u;
             sum += c[k];
         }
         unsigned long long ex, tot;
