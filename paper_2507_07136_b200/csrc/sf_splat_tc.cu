@@ -76,7 +76,7 @@ constexpr int kBoxCols = 32;
 constexpr int kBoxBytes = 8 * 4 * kBoxCols * 4;  // 8 x 4 pixels x 32 fp32
 constexpr int kEBytes = 128 * kBatch * 2;         // 8 KB per part
 constexpr int kVBytes = kMaxCh * kBatch * 2;      // 12 KB per part
-constexpr float kScale = 4096.f;                  // 2^12 on E, V and the decode's A
+constexpr float kScale = 4096.f;                  // 2^12 on E and V (keeps their fp16 lo parts normal)
 constexpr float kInvW = 1.f / 16777216.f;         // W = W' 2^-24
 constexpr uint32_t kMaxC = 12;  // channels per Gaussian (levels x K); more: legacy k_blend
 
@@ -760,11 +760,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                                                         __uint_as_float(v[4 * i + 3]) * kInvW));
                     }
                     if (DEC) {
-                        // W' 2^-24 2^12 = W' 2^-12: hi / lo of W 2^12
+                        // W = W' 2^-24: hi / lo of W itself (F = A B needs no rescale in the
+                        // drains; a subnormal fp16 part costs < 3e-8 absolute per coefficient)
                         uint32_t hi[16], lo[16];
 #pragma unroll
                         for (int i = 0; i < 16; ++i)
-                            split2(__uint_as_float(v[2 * i]) * (kInvW * kScale), __uint_as_float(v[2 * i + 1]) * (kInvW * kScale),
+                            split2(__uint_as_float(v[2 * i]) * kInvW, __uint_as_float(v[2 * i + 1]) * kInvW,
                                    hi[i], lo[i]);
                         tmem_st16(col, hi);
                         tmem_st16(col + 16, lo);
@@ -833,7 +834,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             unsigned char* wbox = S.box[q][0];
             float scl[kMaxLevels];
 #pragma unroll
-            for (int b = 0; b < kMaxLevels; ++b) scl[b] = (b < n_levels ? A.dec_scale[b] : 1.f) / kScale;
+            for (int b = 0; b < kMaxLevels; ++b) scl[b] = b < n_levels ? A.dec_scale[b] : 1.f;  // 1 unless the atoms needed scaling
             int Gd = 0;
             bool box_zero = false;
             for (int it = 0;; ++it) {
@@ -887,8 +888,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     if (lane == 0) bar_arrive(&S.acc_empty[t]);
                     if (q == 0 && lane == 0) SF_CSTAMP(A, Gd, 1);
                     const float sc = b == 0 ? scl[0] : (b == 1 ? scl[1] : scl[2]);
+                    if (sc != 1.f) {  // warp-uniform; only for atoms outside the fp16-friendly range
 #pragma unroll
-                    for (int i = 0; i < 64; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
+                        for (int i = 0; i < 64; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * sc);
+                    }
                     if (lane == 0) SF_TIMED(w2, bulk_wait_read<0>());  // the previous chunk's stores have left the boxes
                     if (q == 0 && lane == 0) SF_CSTAMP(A, Gd, 2);
                     __syncwarp();
