@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                         const float x = e * kScale;
                         const __half h = __float2half_rn(x);
                         const __half l = __float2half_rn(x - __half2float(h));
-                        const uint32_t o = (uint32_t)((j >> 3) * 128 + (j & 7) * 2);
+                        const uint32_t o = (uint32_t)(2 * j + (j >> 3) * 112);  // (j >> 3) 128 + (j & 7) 2
                         sts16(eh + o, __half_as_ushort(h));
                         sts16(el + o, __half_as_ushort(l));
                     }
@@ -790,19 +790,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             } else {
                 named_bar_sync(bar_ba, 64);
                 const float4 st1 = hand_in[lane];
+                double dm[kMaxLevels] = {0.0, 0.0, 0.0};
                 if (rel) {
-#pragma unroll 1
-                    for (int b = 0; b < n_levels; ++b) {
-                        const double2* p0 = reinterpret_cast<const double2*>(xslot(0, b));
-                        const double2* p1 = reinterpret_cast<const double2*>(xslot(1, b));
-                        const double2 a01 = p0[0], a23 = p0[1], b01 = p1[0], b23 = p1[1];
-                        // sigmoid is monotone: min_j sigmoid(d_j) = sigmoid(min_j d_j)
-                        const double dm =
-                            np_minimum(np_minimum(a01.x + b01.x, a01.y + b01.y), np_minimum(a23.x + b23.x, a23.y + b23.y));
-                        if (inside) A.relevancy_raw[(size_t)b * A.W * A.H + pix] = sigmoid2(dm);
+#pragma unroll
+                    for (int b = 0; b < kMaxLevels; ++b) {
+                        if (b < n_levels) {
+                            const double2* p0 = reinterpret_cast<const double2*>(xslot(0, b));
+                            const double2* p1 = reinterpret_cast<const double2*>(xslot(1, b));
+                            const double2 a01 = p0[0], a23 = p0[1], b01 = p1[0], b23 = p1[1];
+                            dm[b] = np_minimum(np_minimum(a01.x + b01.x, a01.y + b01.y), np_minimum(a23.x + b23.x, a23.y + b23.y));
+                        }
                     }
                 }
-                asm volatile("bar.arrive %0, 64;" ::"r"(bar_rd) : "memory");
+                asm volatile("bar.arrive %0, 64;" ::"r"(bar_rd) : "memory");  // hb 1 may go on while hb 0 finishes
+                if (rel && inside) {
+                    // sigmoid is monotone: min_j sigmoid(d_j) = sigmoid(min_j d_j)
+#pragma unroll 1
+                    for (int b = 0; b < n_levels; ++b) {
+                        const double d = b == 0 ? dm[0] : (b == 1 ? dm[1] : dm[2]);
+                        A.relevancy_raw[(size_t)b * A.W * A.H + pix] = sigmoid2(d);
+                    }
+                }
                 // the pixel's state: the later of the two warps' last counted entries
                 // (same batch: hb 1's entries come after hb 0's)
                 const int c1 = __float_as_int(st1.w), n1 = c1 >> 12, last1 = c1 & 0xFFF;
