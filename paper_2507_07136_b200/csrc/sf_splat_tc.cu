@@ -109,7 +109,9 @@ struct __align__(1024) Smem {
     uint64_t w_full[2], a_ready[2], slot_free[2];
     uint64_t dq_full[2], dq_empty[2];
     uint64_t b_full[kBStages], b_empty[kBStages], acc_full[2], acc_empty[2];
+    uint64_t dec_done;  // the decode issuer's products have all completed
     int dec_total;  // decode issuer -> loader: chunks decoded in all (-1 while running)
+    int loader_g;   // loader -> decode issuer: the chunk whose stage it waits for
     uint32_t tmem_base;
 };
 
@@ -244,7 +246,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             bar_init(&S.b_full[i], 1);
             bar_init(&S.b_empty[i], 1);
         }
+        bar_init(&S.dec_done, 1);
         S.dec_total = -1;
+        S.loader_g = -1;
         S.done_count = 0;
         S.contrib[0] = S.contrib[1] = 0u;
         for (int i = 0; i < kStages; ++i) S.ev_tag[i] = S.ev_union[i] = 0u;
@@ -1032,7 +1036,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
             SF_STAMP(A, td, 5);
             SF_PROG(A, 10, (uint32_t)td, (uint32_t)Gd);
         }
+        // wake the loader: once every product has completed (no stage is read any
+        // more), publish the chunk count and complete one more phase of each stage
+        mma_commit(&S.dec_done);
+        bar_wait(&S.dec_done, 0);
+        // the loader has consumed every real phase once it waits for chunk Gd's
+        // (only then may one more completion land without skipping a phase it
+        // has not seen)
+        while (*reinterpret_cast<volatile int*>(&S.loader_g) != Gd) __nanosleep(64);
         *reinterpret_cast<volatile int*>(&S.dec_total) = Gd;
+        bar_arrive(&S.b_empty[Gd % kBStages]);
     } else if (DEC && warp == kLoadWarp && lane == 0) {
         // ---------------- codebook loader: chunk g + kBStages into the stage chunk g frees ----------------
         // (decoupled from the drains, which read the accumulators later; every
@@ -1046,16 +1059,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
         int G = 0;
         for (;;) {
             const int sg = G % kBStages;
-            // sleeps until the stage frees (no polling: this warp shares an SMSP
-            // with a blend pair); wakes now and then to see whether the decode ended
-            if (bar_wait_for(&S.b_empty[sg], (G / kBStages) & 1, 20000)) {
-                bar_expect_tx(&S.b_full[sg], kChunkBytes);
-                bulk_g2s(S.bring[sg], img + (size_t)((G + kBStages) % nchunk) * kChunkBytes, kChunkBytes, &S.b_full[sg]);
-                ++G;
-                continue;
-            }
+            // blocks until the stage frees (this warp shares an SMSP with a blend
+            // pair: no polling); after the last chunk the decode issuer completes
+            // this phase itself, with dec_total set
+            *reinterpret_cast<volatile int*>(&S.loader_g) = G;
+            bar_wait(&S.b_empty[sg], (G / kBStages) & 1);
             const int total = *reinterpret_cast<volatile int*>(&S.dec_total);
             if (total >= 0 && G >= total) break;
+            bar_expect_tx(&S.b_full[sg], kChunkBytes);
+            bulk_g2s(S.bring[sg], img + (size_t)((G + kBStages) % nchunk) * kChunkBytes, kChunkBytes, &S.b_full[sg]);
+            ++G;
         }
         // the loads of chunks G .. G + kBStages - 1 were never consumed: they land before exit
         for (int g = G; g < G + kBStages; ++g) bar_wait(&S.b_full[g % kBStages], (g / kBStages) & 1);
