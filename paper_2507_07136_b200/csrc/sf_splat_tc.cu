@@ -874,8 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                         box_zero = true;
                     }
                     if (lane == 0) {
-                        for (int g = 0; g < nchunk; ++g) {
-                            const int b = g / dchunks, c = g - b * dchunks;
+                        for (int g = 0, b = 0, c = 0; g < nchunk; ++g, c = (c + 1 == dchunks) ? (++b, 0) : c + 1) {
 #ifndef SF_NOSTORE  // experiment only: no feature stores
                             tma_store_4d(&fmap, wbox, c * kDecN, bx, by, b);
                             tma_store_4d(&fmap, wbox + kBoxBytes, c * kDecN + kBoxCols, bx, by, b);
@@ -885,8 +884,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     }
                     continue;
                 }
-                for (int g = 0; g < nchunk; ++g, ++Gd) {
-                    const int t = Gd & 1, b = g / dchunks, c = g - b * dchunks;
+                for (int g = 0, b = 0, c = 0; g < nchunk; ++g, ++Gd, c = (c + 1 == dchunks) ? (++b, 0) : c + 1) {
+                    const int t = Gd & 1;  // (b, c) = (level, chunk in level) of g, stepped without a division
                     if (lane == 0) SF_PROG(A, 5 + q, (uint32_t)it, 0x30000u | (uint32_t)Gd);
                     SF_TIMED(w1, bar_wait(&S.acc_full[t], (Gd >> 1) & 1));
                     if (q == 0 && lane == 0) SF_CSTAMP(A, Gd, 0);
@@ -1010,13 +1009,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                 bar_arrive(&S.slot_free[td & 1]);  // nothing to multiply: the slot is free now
                 continue;
             }
-            for (int cd = 0; cd < nchunk; ++cd, ++Gd) {
+            for (int cd = 0, b = 0, cl = 0; cd < nchunk; ++cd, ++Gd, cl = (cl + 1 == dchunks) ? (++b, 0) : cl + 1) {
                 const int s = Gd % kBStages, t = Gd & 1;
                 SF_TIMED(w1, bar_wait(&S.b_full[s], (Gd / kBStages) & 1));
                 if (Gd >= 2) SF_TIMED(w2, bar_wait(&S.acc_empty[t], ((Gd >> 1) - 1) & 1));
                 tc_after();
                 SF_CSTAMP(A, Gd, 4);
-                const int b = cd / dchunks;
                 const uint32_t d = tm + (uint32_t)(kAccCol0 + t * kDecN);
                 const uint64_t bd = bdesc0 + (uint64_t)((s * kChunkBytes) >> 4);
                 const uint32_t a0 = tm + (uint32_t)((td & 1) * kSlotCols + 64 * b);
