@@ -405,12 +405,17 @@ __global__ void __launch_bounds__(256, SF_EMIT_MINB) k_emit_pairs(int64_t N, con
         return row_keys ? r | (half_tile_flags(ht, tx * SF_TILE, ty * SF_TILE) << kEntryFlagShift) : r;
     };
     if (w * (int)a.h <= 64) {
+        // row by row over the hit mask (row-major bits, w per row): no division per hit
         unsigned long long mask = a.mask;
-        while (mask) {
-            const int bit = __ffsll((long long)mask) - 1;
-            mask &= mask - 1;
-            const int tx = a.tx0 + bit % w, ty = a.ty0 + bit / w;
-            emit_one(j++, ty * g.tiles_x + tx, tagged(tx, ty), a, offsets, base, cursor, entries);
+        const unsigned long long row_bits = w >= 64 ? ~0ull : (1ull << w) - 1ull;
+        for (int ty = a.ty0; mask; ++ty) {
+            unsigned long long rm = mask & row_bits;
+            mask = w >= 64 ? 0ull : mask >> w;
+            while (rm) {
+                const int tx = a.tx0 + __ffsll((long long)rm) - 1;
+                rm &= rm - 1;
+                emit_one(j++, ty * g.tiles_x + tx, tagged(tx, ty), a, offsets, base, cursor, entries);
+            }
         }
         return;
     }
