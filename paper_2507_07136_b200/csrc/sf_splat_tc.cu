@@ -65,6 +65,10 @@ constexpr int kDecWarp = 14;   // decode issuer (one thread)
 constexpr int kLoadWarp = 15;  // codebook chunk loader (one thread)
 constexpr int kStages = 3;
 constexpr int kBatch = 32;
+#ifndef SF_AG
+#define SF_AG 2
+#endif
+constexpr int kAG = SF_AG;  // alphas evaluated per group (the last group of a batch may run short)
 constexpr int kMaxLevels = 3;
 constexpr int kMaxCh = 64 * kMaxLevels;
 constexpr int kSlotCols = 192;
@@ -568,18 +572,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                     __syncwarp();
                     int c0 = 0;
 #pragma unroll 1
-                    for (uint32_t wm = wmask; wm; c0 += 8) {
-                        int jj[8];
+                    for (uint32_t wm = wmask; wm; c0 += kAG) {
+                        int jj[kAG];
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
+                        for (int u = 0; u < kAG; ++u) {
                             jj[u] = wm ? __ffs(wm) - 1 : -1;
                             wm &= wm - 1;
                         }
-                        float alv[8];
+                        float alv[kAG];
                         bool anyamb = false;
                         uint32_t amb = 0;
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
+                        for (int u = 0; u < kAG; ++u) {
                             const int j = jj[u] & 15;
                             bool gb = false;
                             alv[u] = blend_alpha_guarded(G[e0 + j], pxf, pyf, gsm[j], gb);
@@ -591,12 +595,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_splat_tc(BlendArgs A, const __g
                             // rare; unrolled so alv stays in registers (a rolled loop
                             // indexes it dynamically and spills it on the common path)
 #pragma unroll
-                            for (int u = 0; u < 8; ++u)
+                            for (int u = 0; u < kAG; ++u)
                                 if (amb & (1u << u))
                                     alv[u] = blend_alpha_exact(G[e0 + jj[u]], A.geom + S.row[s][e0 + jj[u]], pxd, pyd);
                         }
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
+                        for (int u = 0; u < kAG; ++u) {
                             if (c0 + u < 16) asc[(c0 + u) * 32 + lane] = alv[u];
                             if (jj[u] >= 0) P = fmaf(-alv[u], P, P);
                         }
