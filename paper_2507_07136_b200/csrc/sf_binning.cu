@@ -281,14 +281,17 @@ __global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t p
 // slot-positioned entries), pair total.
 // Also lists the tiles whose lists exceed kShortList entries (big[0] = count,
 // big[1..] = tile ids) for the long-list sorts, and those with kTinyList <
-// n <= kShortList in mid (same layout) for the mid-size sort.
+// n <= kMidList in mid, kMidList < n <= kShortList in mid4 (same layout) for
+// the mid-size sorts.
 constexpr int kShortList = 4096;
 constexpr int kTinyList = 2048;
+constexpr int kMidList = 3072;  // mid-size lists split at 3072 (into mid / mid4)
 __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t* __restrict__ counts,
                                                     uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ cursor,
                                                     int64_t pair_capacity, int64_t* stats,
-                                                    uint32_t* __restrict__ big, uint32_t* __restrict__ mid) {
+                                                    uint32_t* __restrict__ big, uint32_t* __restrict__ mid,
+                                                    uint32_t* __restrict__ mid4) {
     typedef cub::BlockScan<unsigned long long, 1024> Scan;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ unsigned long long carry;
@@ -296,6 +299,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
         carry = 0;
         big[0] = 0u;
         mid[0] = 0u;
+        mid4[0] = 0u;
     }
     __syncthreads();
     // 8 consecutive tiles per thread and pass: one block scan covers 8192 tiles
@@ -321,6 +325,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
                 offsets[t] = (uint32_t)ex;
                 cursor[t] = (uint32_t)(ex + c0[k]);
                 if (c[k] > (unsigned long long)kShortList) big[1 + atomicAdd(&big[0], 1u)] = (uint32_t)t;
+                else if (c[k] > (unsigned long long)kMidList) mid4[1 + atomicAdd(&mid4[0], 1u)] = (uint32_t)t;
                 else if (c[k] > (unsigned long long)kTinyList) mid[1 + atomicAdd(&mid[0], 1u)] = (uint32_t)t;
             }
             ex += c[k];
@@ -669,9 +674,6 @@ struct TileSortDepth {
     static constexpr size_t kSmem = (size_t)CAP * (8 + 4 + 2) + (size_t)(2 * CAP + 1) * 4;
 };
 
-__device__ __forceinline__ bool key_row_less(uint64_t ka, uint32_t ra, uint64_t kb, uint32_t rb) {
-    return ka < kb || (ka == kb && ra < rb);
-}
 
 template <int CAP, int NB, int NT>
 __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __restrict__ offsets,
@@ -679,10 +681,11 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
                                                     const uint64_t* __restrict__ row_keys,
                                                     uint8_t* __restrict__ flags);
 
-// NT threads per CTA: the mid-size and long lists use 512 (shared memory caps
-// the CTAs per SM, so more warps per CTA hide the key-gather latency)
-template <int CAP, int NB, int NT>
-__global__ void __launch_bounds__(NT) k_tile_sort_depth(const uint32_t* __restrict__ offsets,
+// NT threads per CTA: the mid-size and long lists use 384 / 512 (shared memory caps
+// the CTAs per SM, so more warps per CTA hide the key-gather latency); MINB
+// CTAs per SM bounds the registers so that the shared memory sets residency
+template <int CAP, int NB, int NT, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) k_tile_sort_depth(const uint32_t* __restrict__ offsets,
                                                          uint32_t* __restrict__ entries, int lo_exclusive,
                                                          const int64_t* __restrict__ stats,
                                                          const uint64_t* __restrict__ row_keys,
@@ -766,7 +769,8 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
     // bucket = (key - min) >> shift, the smallest shift that maps the span
     // below NB: monotone in the key, between NB / 2 and NB buckets used
     const uint64_t span = mx - kmin;
-    const int shift = max(0, 64 - __clzll((long long)span) - __ffs(NB) + 1);
+    constexpr int kLogNB = 31 - __builtin_clz((unsigned)NB);  // floor(log2 NB): NB need not be a power of two
+    const int shift = max(0, 64 - __clzll((long long)span) - kLogNB);
     auto bucket_of = [&](uint64_t k) { return (int)((k - kmin) >> shift); };
     for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cursor[bucket_of(keys[i])], 1u);
     __syncthreads();
@@ -806,9 +810,15 @@ __device__ __forceinline__ void tile_sort_depth_one(int t, const uint32_t* __res
         const int b = bucket_of(ki);
         const int q0 = (int)start[b], q1 = (int)start[b + 1];
         int r = q0;
+        // not unrolled, compare without branches: buckets hold ~2 entries, and
+        // nvcc's 8-way unroll with a fully unrolled remainder cost every warp
+        // ~330 instructions per pass whatever the trip count (ncu, config C)
+#pragma unroll 1
         for (int q = q0; q < q1; ++q) {
             const int j = order[q];
-            r += key_row_less(keys[j], rows[j] & kEntryRowMask, ki, ri) ? 1 : 0;
+            const uint64_t kj = keys[j];
+            const uint32_t rj = rows[j] & kEntryRowMask;
+            r += (int)((kj < ki) | ((kj == ki) & (rj < ri)));
         }
         e[r] = ri;
         flags[beg + r] = (uint8_t)(rows[i] >> kEntryFlagShift);
@@ -916,10 +926,11 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
     } else if (blocks) {
         k_count_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, row_keys, g, tile_counts, aux);
     }
-    uint32_t* big = tile_cursor + n_tiles;  // long-list tiles (tile_cursor holds 3 n_tiles + 2)
-    uint32_t* mid = big + n_tiles + 1;      // mid-size lists
+    uint32_t* big = tile_cursor + n_tiles;  // long-list tiles (tile_cursor holds 4 n_tiles + 3)
+    uint32_t* mid = big + n_tiles + 1;      // mid-size lists (2048, 3072]
+    uint32_t* mid4 = mid + n_tiles + 1;     // (3072, 4096]
     k_tile_scan<<<1, 1024, 0, st>>>(n_tiles, tile_counts, tile_offsets, tile_cursor, pair_capacity,
-                                    const_cast<int64_t*>(stats), big, mid);
+                                    const_cast<int64_t*>(stats), big, mid, mid4);
     if (blocks)
         k_emit_pairs<<<blocks, 256, 0, st>>>(n_items, stats, geom, row_keys, g, aux, tile_offsets, tile_cursor,
                                              entries, agg ? cta_base : nullptr, per);
@@ -927,19 +938,26 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
         // frame mode: each tile's rows into (depth, row) order -- the canonical
         // order, since scene rows are id-ordered; no global depth sort
         constexpr size_t s0 = TileSortDepth<2048>::kSmem, s1 = TileSortDepth<4096>::kSmem,
-                         s2 = TileSortDepth<8192>::kSmem;
-        ensure_smem_attr((const void*)k_tile_sort_depth<2048, 2048, 256>, s0);
+                         s2 = TileSortDepth<8192>::kSmem, s15 = TileSortDepth<3072>::kSmem;
+        ensure_smem_attr((const void*)k_tile_sort_depth<2048, 2048, 256, 4>, s0);
+        ensure_smem_attr((const void*)k_tile_sort_depth<3072, 3072, 384, 3>, s15);
         ensure_smem_attr((const void*)k_tile_sort_depth<4096, 4096, 512>, s1);
         ensure_smem_attr((const void*)k_tile_sort_depth<8192, 8192, 512>, s2);
         // one CTA per tile for the common lists (<= 2048 entries: 28 KB of
         // shared memory, 6 CTAs per SM); the longer ones by grids striding
         // over the tiles k_tile_scan listed
         const int sms = device_sm_count();
-        static_assert(kShortList == 4096 && kTinyList == 2048, "list-size classes");
-        k_tile_sort_depth<2048, 2048, 256><<<n_tiles, 256, s0, st>>>(tile_offsets, entries, 0, stats, row_keys, nullptr,
+        static_assert(kShortList == 4096 && kMidList == 3072 && kTinyList == 2048, "list-size classes");
+        k_tile_sort_depth<2048, 2048, 256, 4><<<n_tiles, 256, s0, st>>>(tile_offsets, entries, 0, stats, row_keys, nullptr,
                                                                 entry_flags);
-        k_tile_sort_depth<4096, 4096, 512><<<std::min(n_tiles, 3 * sms), 512, s1, st>>>(tile_offsets, entries, 2048, stats,
-                                                                                  row_keys, mid, entry_flags);
+        // the mid-size lists (2048, 4096]: the (2048, 3072] ones -- nearly all of them in
+        // dense views -- 3 CTAs per SM (71 KB each), the rest 2 per SM; each grid is
+        // exactly one resident wave striding over k_tile_scan's list (a second
+        // partial wave would double the slowest CTAs' tile count)
+        k_tile_sort_depth<3072, 3072, 384, 3><<<std::min(n_tiles, 3 * sms), 384, s15, st>>>(tile_offsets, entries, 2048,
+                                                                                      stats, row_keys, mid, entry_flags);
+        k_tile_sort_depth<4096, 4096, 512><<<std::min(n_tiles, 2 * sms), 512, s1, st>>>(tile_offsets, entries, 3072, stats,
+                                                                                  row_keys, mid4, entry_flags);
         k_tile_sort_depth<8192, 8192, 512><<<std::min(n_tiles, sms), 512, s2, st>>>(tile_offsets, entries, 4096, stats,
                                                                               row_keys, big, entry_flags);
         k_tile_sort_depth_large<<<std::min(n_tiles, sms), 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192,

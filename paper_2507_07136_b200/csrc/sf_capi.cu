@@ -141,7 +141,7 @@ static size_t carve_frame(void* base, size_t cap, int64_t G, int W, int H, int n
     ws->chan = c.take<unsigned char>((size_t)Gp * chan_rec_bytes(C));
     ws->tile_counts = c.take<uint32_t>(2 * n_tiles);
     ws->tile_offsets = c.take<uint32_t>(n_tiles + 1);
-    ws->tile_cursor = c.take<uint32_t>(3 * n_tiles + 2);  // + the long / mid-size list tile lists (launch_binning)
+    ws->tile_cursor = c.take<uint32_t>(4 * n_tiles + 3);  // + the long / two mid-size list tile lists (launch_binning)
     ws->entries = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
     ws->entry_flags = c.take<uint8_t>(pair_cap > 0 ? pair_cap : 1);
     ws->scratch = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
@@ -628,7 +628,7 @@ static size_t carve_bin(void* base, size_t cap, int64_t n, int W, int H, int64_t
     w->aux = c.take<BinAux>(np);
     w->cta_base = c.take<uint32_t>(bin_cta_base_elems(W, H));
     w->offsets = c.take<uint32_t>(n_tiles + 1);
-    w->cursor = c.take<uint32_t>(3 * n_tiles + 2);
+    w->cursor = c.take<uint32_t>(4 * n_tiles + 3);
     w->scratch = c.take<uint32_t>(pair_cap > 0 ? pair_cap : 1);
     return c.off;
 }
