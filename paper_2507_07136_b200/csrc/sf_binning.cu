@@ -943,25 +943,35 @@ void launch_binning(int64_t n_items, const int64_t* stats, const GeomRec* geom, 
         ensure_smem_attr((const void*)k_tile_sort_depth<3072, 3072, 384, 3>, s15);
         ensure_smem_attr((const void*)k_tile_sort_depth<4096, 4096, 512>, s1);
         ensure_smem_attr((const void*)k_tile_sort_depth<8192, 8192, 512>, s2);
-        // one CTA per tile for the common lists (<= 2048 entries: 28 KB of
-        // shared memory, 6 CTAs per SM); the longer ones by grids striding
-        // over the tiles k_tile_scan listed
         const int sms = device_sm_count();
         static_assert(kShortList == 4096 && kMidList == 3072 && kTinyList == 2048, "list-size classes");
-        k_tile_sort_depth<2048, 2048, 256, 4><<<n_tiles, 256, s0, st>>>(tile_offsets, entries, 0, stats, row_keys, nullptr,
-                                                                entry_flags);
-        // the mid-size lists (2048, 4096]: the (2048, 3072] ones -- nearly all of them in
-        // dense views -- 3 CTAs per SM (71 KB each), the rest 2 per SM; each grid is
+        // the classes touch disjoint tiles: the mid-size lists (2048, 4096] -- the bulk
+        // of the entries in dense views -- go first on a side stream, the <= 2048 lists
+        // on the frame's stream fill the SMs as the mid-size CTAs drain
+        SideStream* ss = side_stream(st);
+        cudaStream_t sm = st;
+        if (ss && cudaEventRecord(ss->fork, st) == cudaSuccess && cudaStreamWaitEvent(ss->s, ss->fork, 0) == cudaSuccess)
+            sm = ss->s;
+        // (2048, 3072]: 3 CTAs per SM (71 KB each), the rest 2 per SM; each grid is
         // exactly one resident wave striding over k_tile_scan's list (a second
         // partial wave would double the slowest CTAs' tile count)
-        k_tile_sort_depth<3072, 3072, 384, 3><<<std::min(n_tiles, 3 * sms), 384, s15, st>>>(tile_offsets, entries, 2048,
+        k_tile_sort_depth<3072, 3072, 384, 3><<<std::min(n_tiles, 3 * sms), 384, s15, sm>>>(tile_offsets, entries, 2048,
                                                                                       stats, row_keys, mid, entry_flags);
-        k_tile_sort_depth<4096, 4096, 512><<<std::min(n_tiles, 2 * sms), 512, s1, st>>>(tile_offsets, entries, 3072, stats,
+        k_tile_sort_depth<4096, 4096, 512><<<std::min(n_tiles, 2 * sms), 512, s1, sm>>>(tile_offsets, entries, 3072, stats,
                                                                                   row_keys, mid4, entry_flags);
+        // one CTA per tile for the common lists (<= 2048 entries: 28 KB of
+        // shared memory, 4 CTAs per SM); the long ones by grids striding over
+        // the tiles k_tile_scan listed
+        k_tile_sort_depth<2048, 2048, 256, 4><<<n_tiles, 256, s0, st>>>(tile_offsets, entries, 0, stats, row_keys, nullptr,
+                                                                entry_flags);
         k_tile_sort_depth<8192, 8192, 512><<<std::min(n_tiles, sms), 512, s2, st>>>(tile_offsets, entries, 4096, stats,
                                                                               row_keys, big, entry_flags);
         k_tile_sort_depth_large<<<std::min(n_tiles, sms), 256, 0, st>>>(tile_offsets, entries, sort_scratch, 8192,
                                                                         stats, row_keys, big, entry_flags);
+        if (sm != st) {
+            cudaEventRecord(ss->join, sm);
+            cudaStreamWaitEvent(st, ss->join, 0);
+        }
         return;
     }
     // sf_bin mode: unique ranks; most lists fit the shared-memory bucket sort

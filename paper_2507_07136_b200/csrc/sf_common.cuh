@@ -213,6 +213,13 @@ int ensure_smem_attr(const void* func, size_t bytes);
 // message for sf_last_error (sf_capi.cu)
 void set_error(const char* fmt, ...);
 int device_sm_count();
+// a side stream and fork / join events bound to (device, primary stream), for
+// independent kernels of one launcher to run concurrently; nullptr -> serial
+struct SideStream {
+    cudaStream_t s;
+    cudaEvent_t fork, join;
+};
+SideStream* side_stream(cudaStream_t primary);
 
 // ---------------- internal launchers (one .cu each) ----------------
 

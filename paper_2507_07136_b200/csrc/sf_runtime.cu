@@ -19,7 +19,24 @@ namespace {
 std::mutex g_attr_mu;
 std::map<std::pair<const void*, int>, size_t> g_attr;  // (kernel, device) -> dynamic smem limit set
 std::map<int, int> g_sms;                               // device -> SM count
+std::map<std::pair<int, cudaStream_t>, SideStream> g_side;  // (device, primary stream) -> side stream
 }  // namespace
+
+SideStream* side_stream(cudaStream_t primary) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_side.find({dev, primary});
+    if (it != g_side.end()) return &it->second;
+    SideStream ss{};
+    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return &(g_side[{dev, primary}] = ss);
+}
 
 int ensure_smem_attr(const void* func, size_t bytes) {
     int dev = 0;
