@@ -29,7 +29,12 @@ SideStream* side_stream(cudaStream_t primary) {
     auto it = g_side.find({dev, primary});
     if (it != g_side.end()) return &it->second;
     SideStream ss{};
-    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    int prio = 0;  // the primary's priority (a high-priority prepare stream stays high)
+    if (cudaStreamGetPriority(primary, &prio) != cudaSuccess) {
+        cudaGetLastError();
+        prio = 0;
+    }
+    if (cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, prio) != cudaSuccess) return nullptr;
     if (cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();

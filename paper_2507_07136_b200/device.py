@@ -511,7 +511,10 @@ class FramePipeline:
             e.pair_capacity = dscene.engine.pair_capacity
             e._plans = dscene.engine._plans  # the cached scatter plans are read-only
         self.outs = [e.allocate(W, H, levels, **alloc) for e in self.engines]
-        self.prep = torch.cuda.Stream()
+        # the prepare stream is the frame's critical path after the splat kernel (which
+        # holds every SM): at high priority its CTAs go first when the splat drains,
+        # and the previous frame's fixup / post fill the SMs it leaves idle
+        self.prep = torch.cuda.Stream(priority=-1)
         self.render = [torch.cuda.Stream(), torch.cuda.Stream()]
         self.k = 0
 
