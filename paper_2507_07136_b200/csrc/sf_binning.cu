@@ -286,6 +286,18 @@ __global__ void __launch_bounds__(512, 2) k_count_pairs_agg(int64_t N, int64_t p
 constexpr int kShortList = 4096;
 constexpr int kTinyList = 2048;
 constexpr int kMidList = 3072;  // mid-size lists split at 3072 (into mid / mid4)
+// warp-aggregated append of t to list (list[0] = count, list[1..] = items);
+// called by all 32 lanes of the warp
+__device__ __forceinline__ void list_append(uint32_t* list, bool take, uint32_t t) {
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(&list[0], (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (take) list[1 + base + __popc(m & ((1u << lane) - 1u))] = t;
+}
+
 __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t* __restrict__ counts,
                                                     uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ cursor,
@@ -324,10 +336,13 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int n_tiles, const uint32_t*
             if (t < n_tiles) {
                 offsets[t] = (uint32_t)ex;
                 cursor[t] = (uint32_t)(ex + c0[k]);
-                if (c[k] > (unsigned long long)kShortList) big[1 + atomicAdd(&big[0], 1u)] = (uint32_t)t;
-                else if (c[k] > (unsigned long long)kMidList) mid4[1 + atomicAdd(&mid4[0], 1u)] = (uint32_t)t;
-                else if (c[k] > (unsigned long long)kTinyList) mid[1 + atomicAdd(&mid[0], 1u)] = (uint32_t)t;
             }
+            // class lists: one atomic per warp and class (thousands of same-address
+            // atomics serialised in the L2 otherwise); list order is irrelevant
+            const unsigned long long n = t < n_tiles ? c[k] : 0ull;
+            list_append(big, n > (unsigned long long)kShortList, (uint32_t)t);
+            list_append(mid4, n > (unsigned long long)kMidList && n <= (unsigned long long)kShortList, (uint32_t)t);
+            list_append(mid, n > (unsigned long long)kTinyList && n <= (unsigned long long)kMidList, (uint32_t)t);
             ex += c[k];
         }
         __syncthreads();
